@@ -1,0 +1,168 @@
+/*
+ * mlora.h — C ABI of the B200-native BatchFusion multi-LoRA linear layer.
+ *
+ * This is the drop-in boundary for the hot path of ASPEN (arXiv 2312.02515)
+ * whose CPU reference lives in /root/reference/proj/include/fusim/lora.hpp and
+ * /root/reference/proj/src/lora.cpp.  Every entry point names the reference
+ * interface it replaces (file:line).  The reference is a C++ library; its C++
+ * API is reproduced on top of this ABI by include/fusim/lora.hpp (the façade,
+ * paper_2312_02515_b200/csrc/facade_lora.cpp), and Python binds it through
+ * ctypes (paper_2312_02515_b200/_native.py).
+ *
+ * Conventions:
+ *   - Plain pointers and sizes only.  Device pointers are caller-owned CUDA
+ *     device memory; host pointers are marked `host`.  Nothing allocates on a
+ *     hot call except the context's grow-only workspace.
+ *   - Errors are returned as mlora_status, never thrown across the boundary.
+ *     The status values mirror the reference exception taxonomy
+ *     (/root/reference/proj/include/fusim/errors.hpp:13-23) and every
+ *     precondition is checked on the host BEFORE any device work, exactly where
+ *     the reference checks it (lora.cpp:20-23, 62-70, 106-109, 115-131, 163-167).
+ *   - Calls on one context are ordered on the stream passed in; use one
+ *     context per GPU/thread (the reference is single-threaded and reentrant,
+ *     /root/reference/SPEC.md:161-162).
+ *   - Storage convention is the reference's: W0 is d x k (out x in), A_j is
+ *     r_j x k, B_j is d x r_j, all row-major (lora.hpp:16,36-37).  Fused rows
+ *     follow FusedBatch order: job order, then sequence order (lora.cpp:143-156).
+ *   - Device dtype: bf16 operands, fp32 accumulation, fp32 gradients/optimizer
+ *     state.  The reference has no scale; s_j = 1 reproduces it.
+ *
+ * Packed adapter layout ("cat" layout), owned by the caller:
+ *   R_pad = sum_j roundup(r_j, 16); job j owns columns [roff[j], roff[j+1]).
+ *   A_cat  : R_pad x k   (rows of job j = A_j, zero rows up to the padded rank)
+ *   B_cat  : d x R_pad   (cols of job j = B_j, zero cols up to the padded rank)
+ *   H_cat  : rows x R_pad, block-diagonal: H[t, roff[j]:roff[j]+r_j] = s_j X_t A_j^T
+ *            for t in job j's segment, 0 elsewhere (saved by fwd for bwd).
+ */
+#ifndef MLORA_H_
+#define MLORA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Mirrors fusim::Error subclasses (errors.hpp:13-23). */
+typedef enum mlora_status {
+    MLORA_OK = 0,
+    MLORA_USAGE = 1,   /* fusim::UsageError   — precondition violated       */
+    MLORA_SHAPE = 2,   /* fusim::ShapeError   — dimension mismatch          */
+    MLORA_ROUTING = 3, /* fusim::RoutingError — batch routed to no adapter  */
+    MLORA_NUMERIC = 4, /* fusim::NumericError — non-finite input            */
+    MLORA_STATE = 5,   /* fusim::StateError   — object in the wrong state   */
+    MLORA_CUDA = 6     /* device/runtime failure (no reference analogue)    */
+} mlora_status;
+
+typedef struct mlora_ctx mlora_ctx;
+typedef struct mlora_plan mlora_plan;
+
+/* Replaces fusim::FusedShape (lora.hpp:51-61). */
+typedef struct mlora_fused_shape {
+    int32_t max_len;
+    int64_t sequences;
+    int64_t total_tokens;   /* sequences * max_len  (ξ)   */
+    int64_t padding_tokens; /* Σ (max_len - len)    (ξ_p) */
+} mlora_fused_shape;
+
+const char* mlora_status_string(mlora_status s);
+/* Human-readable text of the last failing call on this context (or thread, for ctx==NULL). */
+const char* mlora_last_error(const mlora_ctx* ctx);
+/* ABI version, bumped on any signature change. */
+int32_t mlora_abi_version(void);
+
+/* ---------------------------------------------------------------- context */
+mlora_status mlora_ctx_create(int32_t device, mlora_ctx** out);
+mlora_status mlora_ctx_destroy(mlora_ctx* ctx);
+/* Number of SMs of the context's device (148 on B200). */
+int32_t mlora_ctx_num_sms(const mlora_ctx* ctx);
+/* Kernels launched through this context since creation (telemetry). */
+int64_t mlora_ctx_launch_count(const mlora_ctx* ctx);
+
+/* ---------------------------------------------------------------- accounting
+ * Replaces fusim::fused_shape (lora.hpp:63, lora.cpp:72-85).  Integer-exact.
+ * `lengths` (host) is the flattened per-group length list; groups do not
+ * matter for the result. */
+mlora_status mlora_fused_shape_of(const int32_t* lengths, int64_t n, mlora_fused_shape* out);
+
+/* Replaces fusim::count_launches (lora.hpp:97-106, lora.cpp:184-189):
+ * mode 0 = PerJob -> (4k, 0), mode 1 = Fused -> (2k, 2).  USAGE if k < 1. */
+mlora_status mlora_count_launches(int32_t num_jobs, int32_t mode, int64_t* small_launches,
+                                  int64_t* large_launches);
+
+/* ---------------------------------------------------------------- plan
+ * The segment layout of one fused batch: which rows belong to which job.
+ * Replaces the routing/mask role of fusim::FusedBatch (lora.hpp:65-82) for the
+ * kernels.  seg_offsets (host, J+1, non-decreasing, seg[0]=0) partitions the
+ * `rows = seg[J]` fused rows; ranks/scales (host, J) give r_j >= 1 and s_j.
+ * Builds the device tables (segment offsets, padded rank offsets, per-m-tile
+ * LoRA k-block ranges, per-chunk token ranges) with one H2D copy on `stream`. */
+mlora_status mlora_plan_create(mlora_ctx* ctx, int32_t num_jobs, const int64_t* seg_offsets,
+                               const int32_t* ranks, const float* scales, void* stream,
+                               mlora_plan** out);
+mlora_status mlora_plan_destroy(mlora_plan* plan);
+int64_t mlora_plan_rows(const mlora_plan* plan);
+int32_t mlora_plan_rank_padded(const mlora_plan* plan);
+/* host, J+1 entries */
+mlora_status mlora_plan_rank_offsets(const mlora_plan* plan, int32_t* roff_out);
+
+/* ---------------------------------------------------------------- forward
+ * Replaces fusim::fused_forward (lora.hpp:93-95, lora.cpp:160-182):
+ *   Y[rows, d] = X[rows, k] W0[d, k]^T + H_cat B_cat^T,  H_cat = s_j X_j A_j^T.
+ * Two tcgen05 launches: the rank-r down-projection (H, saved for backward)
+ * and the frozen-base GEMM whose LoRA k-blocks accumulate H B^T into the same
+ * TMEM tile.  SHAPE if d, k are not positive multiples of 8.
+ * X, W0, A_cat, B_cat, Y, H: bf16 device pointers (layouts above). */
+mlora_status mlora_linear_fwd(mlora_ctx* ctx, const mlora_plan* plan, int32_t d, int32_t k,
+                              const void* X, const void* W0, const void* A_cat, const void* B_cat,
+                              void* Y, void* H, void* stream);
+
+/* Backward of mlora_linear_fwd (no reference function; pinned by composing
+ * the reference primitives):
+ *   G_cat = s_j dY_j B_j          (rows x R_pad, bf16 scratch, caller-owned)
+ *   dX    = dY W0 + G_cat A_cat   (bf16, skipped when dX == NULL)
+ *   dA_cat = G_cat^T X            (fp32, R_pad x k, segmented over job rows)
+ *   dB_cat = dY^T H_cat           (fp32, d x R_pad, segmented over job rows) */
+mlora_status mlora_linear_bwd(mlora_ctx* ctx, const mlora_plan* plan, int32_t d, int32_t k,
+                              const void* dY, const void* X, const void* H, const void* W0,
+                              const void* A_cat, const void* B_cat, void* G, void* dX,
+                              float* dA_cat, float* dB_cat, void* stream);
+
+/* ---------------------------------------------------------------- adapters
+ * Pack per-job reference-layout adapters (device fp32: A_j r_j x k, B_j d x r_j)
+ * into the cat layout (fp32 master and bf16 operand copies; either output
+ * pointer may be NULL).  RoutingError semantics: a NULL A_j/B_j is ROUTING. */
+mlora_status mlora_pack_adapters(mlora_ctx* ctx, const mlora_plan* plan, int32_t d, int32_t k,
+                                 const float* const* A_ptrs, const float* const* B_ptrs,
+                                 float* A_cat_f32, float* B_cat_f32, void* A_cat_bf16,
+                                 void* B_cat_bf16, void* stream);
+
+/* One fused AdamW step over every adapter tensor of every projection
+ * (no reference function; parity unpinned).  Each group is a
+ * cat-layout tensor whose job of element (i, c) is given by its rows
+ * (layout 0, A_cat: row i in [roff[j], roff[j+1])) or columns (layout 1, B_cat).
+ * lr/step are per job (host arrays of J entries: the paper trains jobs with
+ * different learning rates).  Writes the fp32 master and, when
+ * p_bf16 != NULL, the bf16 operand copy used by the GEMMs. */
+typedef struct mlora_adam_group {
+    float* p;
+    const float* g;
+    float* m;
+    float* v;
+    void* p_bf16;
+    int64_t rows;
+    int64_t cols;
+    int32_t layout; /* 0: rows by job (A_cat), 1: cols by job (B_cat) */
+    int32_t _pad;
+} mlora_adam_group;
+
+mlora_status mlora_adam_step(mlora_ctx* ctx, const mlora_plan* plan, const mlora_adam_group* groups,
+                             int32_t num_groups, const float* lr, const int32_t* step, float beta1,
+                             float beta2, float eps, float weight_decay, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MLORA_H_ */

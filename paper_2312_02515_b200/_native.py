@@ -1,0 +1,108 @@
+"""ctypes binding of the C ABI in include/mlora.h (libmlora.so, built in-tree).
+
+This is the reference-side binding a Python maintainer would add:
+plain pointers and sizes, status codes mapped onto the fusim exception types.
+There is no fallback: if the shared library is missing the import fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+from . import errors
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libmlora.so")
+HEADER = os.path.join(os.path.dirname(_PKG), "include", "mlora.h")
+
+_lib: C.CDLL | None = None
+
+vp = C.c_void_p
+i32 = C.c_int32
+i64 = C.c_int64
+f32 = C.c_float
+
+
+class FusedShapeC(C.Structure):
+    _fields_ = [("max_len", i32), ("sequences", i64), ("total_tokens", i64), ("padding_tokens", i64)]
+
+
+class AdamGroupC(C.Structure):
+    _fields_ = [("p", vp), ("g", vp), ("m", vp), ("v", vp), ("p_bf16", vp), ("rows", i64),
+                ("cols", i64), ("layout", i32), ("_pad", i32)]
+
+
+_SIGS = {
+    "mlora_abi_version": (i32, []),
+    "mlora_status_string": (C.c_char_p, [i32]),
+    "mlora_last_error": (C.c_char_p, [vp]),
+    "mlora_ctx_create": (i32, [i32, C.POINTER(vp)]),
+    "mlora_ctx_destroy": (i32, [vp]),
+    "mlora_ctx_num_sms": (i32, [vp]),
+    "mlora_ctx_launch_count": (i64, [vp]),
+    "mlora_fused_shape_of": (i32, [C.POINTER(i32), i64, C.POINTER(FusedShapeC)]),
+    "mlora_count_launches": (i32, [i32, i32, C.POINTER(i64), C.POINTER(i64)]),
+    "mlora_plan_create": (i32, [vp, i32, C.POINTER(i64), C.POINTER(i32), C.POINTER(f32), vp, C.POINTER(vp)]),
+    "mlora_plan_destroy": (i32, [vp]),
+    "mlora_plan_rows": (i64, [vp]),
+    "mlora_plan_rank_padded": (i32, [vp]),
+    "mlora_plan_rank_offsets": (i32, [vp, C.POINTER(i32)]),
+    "mlora_linear_fwd": (i32, [vp, vp, i32, i32, vp, vp, vp, vp, vp, vp, vp]),
+    "mlora_linear_bwd": (i32, [vp, vp, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "mlora_pack_adapters": (i32, [vp, vp, i32, i32, C.POINTER(vp), C.POINTER(vp), vp, vp, vp, vp, vp]),
+    "mlora_adam_step": (i32, [vp, vp, C.POINTER(AdamGroupC), i32, C.POINTER(f32), C.POINTER(i32), f32, f32,
+                              f32, f32, vp]),
+}
+
+# Optional groups (present once the corresponding kernels are built).
+_OPTIONAL = {
+    "mlora_f64_fused_forward": (i32, [vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "mlora_masked_ce": (i32, [vp, vp, i64, i32, vp, vp, vp, vp, vp, vp, vp]),
+    "mlora_rmsnorm_fwd": (i32, [vp, i64, i32, vp, vp, f32, vp, vp, vp]),
+    "mlora_rmsnorm_bwd": (i32, [vp, i64, i32, vp, vp, vp, vp, vp, vp, vp]),
+    "mlora_rope_fwd": (i32, [vp, i64, i32, i32, vp, vp, f32, i32, vp]),
+    "mlora_rope_bwd": (i32, [vp, i64, i32, i32, vp, vp, f32, i32, vp]),
+}
+
+
+def exported_symbols() -> list[str]:
+    """Every function declared in include/mlora.h."""
+    with open(HEADER) as f:
+        text = f.read()
+    return sorted(set(re.findall(r"\b(mlora_[a-z0-9_]+)\s*\(", text)) - {"mlora_status"})
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `python -m paper_2312_02515_b200._build` "
+                "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in {**_SIGS}.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        for name, (res, args) in _OPTIONAL.items():
+            if hasattr(L, name):
+                fn = getattr(L, name)
+                fn.restype = res
+                fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def check(status: int, ctx=None) -> None:
+    if status == 0:
+        return
+    L = lib()
+    msg = L.mlora_last_error(ctx).decode() if ctx is not None else L.mlora_last_error(None).decode()
+    cls = errors.STATUS_TO_ERROR.get(status, errors.Error)
+    raise cls(msg or L.mlora_status_string(status).decode())
+
+
+def ptr(t) -> int | None:
+    """Device pointer of a torch tensor (None -> NULL)."""
+    return None if t is None else t.data_ptr()

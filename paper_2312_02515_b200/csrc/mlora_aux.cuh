@@ -1,0 +1,144 @@
+// mlora_aux.cuh — the HBM-bound helpers around the tcgen05 GEMMs:
+//   * split-partial reduction of the segmented dA/dB reductions,
+//   * packing of per-job reference-layout adapters into the cat layout,
+//   * one fused AdamW step over every adapter tensor with per-job lr/step.
+// All are grid-stride, float4-vectorised streaming kernels; their roofline is
+// HBM bandwidth (bytes per element stated next to each kernel).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+namespace mlora {
+
+constexpr int kMaxJobs = 128;
+constexpr int kMaxAdamGroups = 32;
+
+// out[i] = sum_s part[s * stride + i]   (fixed order: deterministic)
+// bytes/elem = 4 * nsplit (read) + 4 (write)
+__global__ void reduce_splits_kernel(const float4* __restrict__ part, float4* __restrict__ out,
+                                     long long n4, long long stride4, int nsplit) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
+         i += (long long)gridDim.x * blockDim.x) {
+        float4 a = part[i];
+        for (int s = 1; s < nsplit; ++s) {
+            const float4 b = part[s * stride4 + i];
+            a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+        }
+        out[i] = a;
+    }
+}
+
+struct PackArgs {
+    const float* A[kMaxJobs];
+    const float* B[kMaxJobs];
+    int roff[kMaxJobs + 1];
+    int rank[kMaxJobs];
+    int J, d, k, R_pad;
+    float* A_f32;
+    float* B_f32;
+    __nv_bfloat16* A_bf16;
+    __nv_bfloat16* B_bf16;
+};
+
+__device__ __forceinline__ int job_of_col(const int* roff, int J, int c) {
+    int lo = 0, hi = J - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (roff[mid] <= c) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+// A_cat (R_pad x k) then B_cat (d x R_pad), one element per thread-iteration.
+__global__ void pack_adapters_kernel(const __grid_constant__ PackArgs a) {
+    const long long nA = (long long)a.R_pad * a.k;
+    const long long nB = (long long)a.d * a.R_pad;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nA + nB;
+         e += (long long)gridDim.x * blockDim.x) {
+        float val;
+        if (e < nA) {
+            const int i = static_cast<int>(e / a.k);
+            const int c = static_cast<int>(e % a.k);
+            const int j = job_of_col(a.roff, a.J, i);
+            const int li = i - a.roff[j];
+            val = li < a.rank[j] ? a.A[j][(long long)li * a.k + c] : 0.f;
+            if (a.A_f32) a.A_f32[e] = val;
+            if (a.A_bf16) a.A_bf16[e] = __float2bfloat16_rn(val);
+        } else {
+            const long long f = e - nA;
+            const int row = static_cast<int>(f / a.R_pad);
+            const int c = static_cast<int>(f % a.R_pad);
+            const int j = job_of_col(a.roff, a.J, c);
+            const int lc = c - a.roff[j];
+            val = lc < a.rank[j] ? a.B[j][(long long)row * a.rank[j] + lc] : 0.f;
+            if (a.B_f32) a.B_f32[f] = val;
+            if (a.B_bf16) a.B_bf16[f] = __float2bfloat16_rn(val);
+        }
+    }
+}
+
+struct AdamGroupDev {
+    float* p;
+    const float* g;
+    float* m;
+    float* v;
+    __nv_bfloat16* pb;
+    long long rows, cols;
+    long long start4;  // first float4 index of this group in the flattened stream
+    int layout;
+};
+
+struct AdamArgs {
+    AdamGroupDev grp[kMaxAdamGroups];
+    int ngroups;
+    long long total4;
+    int roff[kMaxJobs + 1];
+    int J;
+    float lr[kMaxJobs];
+    float bc1[kMaxJobs];   // 1 - beta1^t_j
+    float bc2[kMaxJobs];   // 1 - beta2^t_j
+    float beta1, beta2, eps, wd;
+};
+
+// AdamW over all groups.  bytes/param: read p,g,m,v (16) + write p,m,v (12)
+// (+2 for the bf16 operand copy) = 30 B.
+__global__ void adam_kernel(const __grid_constant__ AdamArgs a) {
+    for (long long i4 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i4 < a.total4;
+         i4 += (long long)gridDim.x * blockDim.x) {
+        int gi = 0;
+        while (gi + 1 < a.ngroups && a.grp[gi + 1].start4 <= i4) ++gi;
+        const AdamGroupDev& G = a.grp[gi];
+        const long long e = (i4 - G.start4) * 4;  // element index within group
+        const long long row = e / G.cols;
+        const long long col = e % G.cols;
+        const int j = job_of_col(a.roff, a.J, static_cast<int>(G.layout == 0 ? row : col));
+        const float lr = a.lr[j], bc1 = a.bc1[j], bc2 = a.bc2[j];
+        float4 p = reinterpret_cast<float4*>(G.p)[e / 4];
+        const float4 g = reinterpret_cast<const float4*>(G.g)[e / 4];
+        float4 m = reinterpret_cast<float4*>(G.m)[e / 4];
+        float4 v = reinterpret_cast<float4*>(G.v)[e / 4];
+        float* pp = &p.x; const float* gg = &g.x; float* mm = &m.x; float* vv = &v.x;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            mm[u] = a.beta1 * mm[u] + (1.f - a.beta1) * gg[u];
+            vv[u] = a.beta2 * vv[u] + (1.f - a.beta2) * gg[u] * gg[u];
+            const float mh = mm[u] / bc1;
+            const float vh = vv[u] / bc2;
+            pp[u] -= lr * (mh / (sqrtf(vh) + a.eps) + a.wd * pp[u]);
+        }
+        reinterpret_cast<float4*>(G.p)[e / 4] = p;
+        reinterpret_cast<float4*>(G.m)[e / 4] = m;
+        reinterpret_cast<float4*>(G.v)[e / 4] = v;
+        if (G.pb) {
+            __nv_bfloat162 lo = __floats2bfloat162_rn(p.x, p.y);
+            __nv_bfloat162 hi = __floats2bfloat162_rn(p.z, p.w);
+            uint2 w;
+            w.x = *reinterpret_cast<uint32_t*>(&lo);
+            w.y = *reinterpret_cast<uint32_t*>(&hi);
+            reinterpret_cast<uint2*>(G.pb)[e / 4] = w;
+        }
+    }
+}
+
+}  // namespace mlora

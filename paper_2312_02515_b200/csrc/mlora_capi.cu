@@ -1,0 +1,669 @@
+// mlora_capi.cu — host side of the C ABI declared in include/mlora.h.
+//
+// Owns: the per-device context (TMA descriptor cache, grow-only workspace,
+// launch telemetry), the fused-batch plan (segment tables uploaded once per
+// step), and the launch logic of the tcgen05 kernels in mlora_gemm.cuh.
+// Every reference precondition is validated here, on the host, before any
+// device work.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/mlora.h"
+#include "mlora_aux.cuh"
+#include "mlora_gemm.cuh"
+
+using namespace mlora;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+constexpr int kMaxSplit = 8;
+constexpr int kBaseStages = 4;
+constexpr int kSmallStages = 4;
+
+using GemmLayoutBase = GemmSmem<256, kBaseStages>;
+using GemmLayoutSmall = GemmSmem<64, kSmallStages>;
+
+}  // namespace
+
+struct mlora_ctx {
+    int device = 0;
+    int num_sms = 0;
+    PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    std::map<std::tuple<const void*, uint64_t, uint64_t, uint64_t, uint32_t, uint32_t>, CUtensorMap> tmaps;
+    void* workspace = nullptr;
+    size_t workspace_bytes = 0;
+    long long launches = 0;
+    std::string last_error;
+};
+
+struct mlora_plan {
+    mlora_ctx* ctx = nullptr;
+    int J = 0;
+    int rows = 0;
+    int R_pad = 0;
+    int n_mblk = 0;
+    int n_chunks = 0;
+    std::vector<int> seg, roff, rank;
+    std::vector<float> scale;
+    std::vector<int> ext;                 // [n_mblk][2]
+    std::vector<int> down;                // [n_down][3]
+    int n_down = 0;
+    std::vector<int> chunk_kb;            // [n_chunks][2] token k-block range
+    int grad_off[kMaxSplit + 1] = {0};    // offset (ints) of the split-ns table
+    // device copies (one allocation)
+    void* dev = nullptr;
+    int* d_seg = nullptr;
+    int* d_roff = nullptr;
+    float* d_scale = nullptr;
+    int* d_ext = nullptr;
+    int* d_down = nullptr;
+    int* d_grad = nullptr;
+};
+
+namespace {
+
+mlora_status fail(mlora_ctx* ctx, mlora_status st, const std::string& msg) {
+    g_last_error = msg;
+    if (ctx) ctx->last_error = msg;
+    return st;
+}
+
+#define MLORA_CUDA_TRY(ctx, expr)                                                       \
+    do {                                                                                \
+        cudaError_t _e = (expr);                                                        \
+        if (_e != cudaSuccess)                                                          \
+            return fail(ctx, MLORA_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+inline int cdiv(long long a, long long b) { return static_cast<int>((a + b - 1) / b); }
+
+// 2-D bf16 tensor map, SWIZZLE_128B, OOB -> zero fill.
+mlora_status get_tmap(mlora_ctx* ctx, const void* ptr, uint64_t inner, uint64_t outer,
+                      uint64_t ld_elems, uint32_t box_inner, uint32_t box_outer, CUtensorMap* out) {
+    auto key = std::make_tuple(ptr, inner, outer, ld_elems, box_inner, box_outer);
+    auto it = ctx->tmaps.find(key);
+    if (it != ctx->tmaps.end()) {
+        *out = it->second;
+        return MLORA_OK;
+    }
+    if (reinterpret_cast<uintptr_t>(ptr) % 16 != 0)
+        return fail(ctx, MLORA_USAGE, "tensor base pointer must be 16-byte aligned");
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {inner, outer};
+    const cuuint64_t strides[1] = {ld_elems * 2};
+    const cuuint32_t box[2] = {box_inner, box_outer};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = ctx->encode(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims,
+                             strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        return fail(ctx, MLORA_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+    if (ctx->tmaps.size() > 4096) ctx->tmaps.clear();
+    ctx->tmaps.emplace(key, m);
+    *out = m;
+    return MLORA_OK;
+}
+
+mlora_status ensure_workspace(mlora_ctx* ctx, size_t bytes) {
+    if (bytes <= ctx->workspace_bytes) return MLORA_OK;
+    if (ctx->workspace) {
+        cudaDeviceSynchronize();
+        cudaFree(ctx->workspace);
+        ctx->workspace = nullptr;
+        ctx->workspace_bytes = 0;
+    }
+    MLORA_CUDA_TRY(ctx, cudaMalloc(&ctx->workspace, bytes));
+    ctx->workspace_bytes = bytes;
+    return MLORA_OK;
+}
+
+template <int MODE, int BN, int STAGES, bool A_MN, bool B_MN>
+mlora_status launch_gemm(mlora_ctx* ctx, const CUtensorMap& a0, const CUtensorMap& b0,
+                         const CUtensorMap& a1, const CUtensorMap& b1, const GemmParams& p,
+                         int ctas_per_sm, cudaStream_t stream) {
+    if (p.num_tiles <= 0) return MLORA_OK;
+    using L = GemmSmem<BN, STAGES>;
+    auto kern = mlora_gemm_kernel<MODE, BN, STAGES, A_MN, B_MN>;
+    static bool attr_done = false;  // per instantiation
+    if (!attr_done) {
+        MLORA_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 L::kDynBytes));
+        attr_done = true;
+    }
+    const int grid = std::min(p.num_tiles, ctx->num_sms * ctas_per_sm);
+    kern<<<grid, kNumThreads, L::kDynBytes, stream>>>(a0, b0, a1, b1, p);
+    MLORA_CUDA_TRY(ctx, cudaGetLastError());
+    ++ctx->launches;
+    return MLORA_OK;
+}
+
+mlora_status check_dims(mlora_ctx* ctx, const mlora_plan* plan, int d, int k) {
+    if (!ctx || !plan) return fail(ctx, MLORA_USAGE, "null context or plan");
+    if (plan->ctx != ctx) return fail(ctx, MLORA_USAGE, "plan belongs to another context");
+    if (d <= 0 || k <= 0 || d % 8 != 0 || k % 8 != 0)
+        return fail(ctx, MLORA_SHAPE, "d and k must be positive multiples of 8 (TMA 16-byte rows), got d=" +
+                                          std::to_string(d) + " k=" + std::to_string(k));
+    return MLORA_OK;
+}
+
+// Choose the token-split count of a segmented gradient reduction so that the
+// grid covers ~2 CTAs per SM.
+int choose_nsplit(const mlora_ctx* ctx, const mlora_plan* plan, int F) {
+    const int base = cdiv(F, kBM) * plan->n_chunks;
+    int ns = std::max(1, cdiv(2 * ctx->num_sms, std::max(base, 1)));
+    int max_len = 1;
+    for (int c = 0; c < plan->n_chunks; ++c)
+        max_len = std::max(max_len, plan->chunk_kb[2 * c + 1] - plan->chunk_kb[2 * c]);
+    ns = std::min(ns, std::max(1, max_len / 4));
+    return std::min(ns, kMaxSplit);
+}
+
+// Segmented reduction out = sum over the chunk token ranges (MODE_GRADT/GRAD).
+template <int MODE>
+mlora_status run_grad(mlora_ctx* ctx, const mlora_plan* plan, const CUtensorMap& ta,
+                      const CUtensorMap& tb, int F, float* out, cudaStream_t stream) {
+    const int ns = choose_nsplit(ctx, plan, F);
+    const long long nelem = (long long)F * plan->R_pad;
+    float* target = out;
+    if (ns > 1) {
+        mlora_status st = ensure_workspace(ctx, sizeof(float) * nelem * ns);
+        if (st != MLORA_OK) return st;
+        target = static_cast<float*>(ctx->workspace);
+    }
+    GemmParams p{};
+    p.M = F;
+    p.N = plan->R_pad;
+    p.n_mblk = cdiv(F, kBM);
+    p.nsplit = ns;
+    p.num_tiles = p.n_mblk * plan->n_chunks * ns;
+    p.out = target;
+    p.ldo = (MODE == MODE_GRADT) ? F : plan->R_pad;
+    p.split_stride = nelem;
+    p.grad_tab = plan->d_grad + plan->grad_off[ns];
+    p.seg = plan->d_seg;
+    p.roff = plan->d_roff;
+    p.scale = plan->d_scale;
+    p.num_jobs = plan->J;
+    mlora_status st = launch_gemm<MODE, 64, kSmallStages, true, true>(ctx, ta, tb, ta, tb, p, 2, stream);
+    if (st != MLORA_OK) return st;
+    if (ns > 1) {
+        const long long n4 = nelem / 4;
+        const int threads = 256;
+        const int blocks = static_cast<int>(std::min<long long>(cdiv(n4, threads), 4LL * ctx->num_sms));
+        reduce_splits_kernel<<<blocks, threads, 0, stream>>>(reinterpret_cast<const float4*>(target),
+                                                             reinterpret_cast<float4*>(out), n4, n4, ns);
+        MLORA_CUDA_TRY(ctx, cudaGetLastError());
+        ++ctx->launches;
+    }
+    return MLORA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t mlora_abi_version(void) { return 1; }
+
+const char* mlora_status_string(mlora_status s) {
+    switch (s) {
+        case MLORA_OK: return "ok";
+        case MLORA_USAGE: return "usage error";
+        case MLORA_SHAPE: return "shape error";
+        case MLORA_ROUTING: return "routing error";
+        case MLORA_NUMERIC: return "numeric error";
+        case MLORA_STATE: return "state error";
+        case MLORA_CUDA: return "cuda error";
+    }
+    return "unknown status";
+}
+
+const char* mlora_last_error(const mlora_ctx* ctx) {
+    return ctx ? ctx->last_error.c_str() : g_last_error.c_str();
+}
+
+mlora_status mlora_ctx_create(int32_t device, mlora_ctx** out) {
+    if (!out) return fail(nullptr, MLORA_USAGE, "out is null");
+    *out = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(nullptr, MLORA_CUDA, "no CUDA device available");
+    if (device < 0 || device >= ndev) return fail(nullptr, MLORA_USAGE, "device index out of range");
+    DeviceGuard g(device);
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess)
+        return fail(nullptr, MLORA_CUDA, "cudaGetDeviceProperties failed");
+    if (prop.major != 10)
+        return fail(nullptr, MLORA_CUDA, "mlora kernels are built for sm_100a (B200); device is sm_" +
+                                             std::to_string(prop.major) + std::to_string(prop.minor));
+    auto* ctx = new mlora_ctx();
+    ctx->device = device;
+    ctx->num_sms = prop.multiProcessorCount;
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn) {
+        delete ctx;
+        return fail(nullptr, MLORA_CUDA, "cuTensorMapEncodeTiled entry point unavailable");
+    }
+    ctx->encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    *out = ctx;
+    return MLORA_OK;
+}
+
+mlora_status mlora_ctx_destroy(mlora_ctx* ctx) {
+    if (!ctx) return MLORA_OK;
+    DeviceGuard g(ctx->device);
+    if (ctx->workspace) {
+        cudaDeviceSynchronize();
+        cudaFree(ctx->workspace);
+    }
+    delete ctx;
+    return MLORA_OK;
+}
+
+int32_t mlora_ctx_num_sms(const mlora_ctx* ctx) { return ctx ? ctx->num_sms : 0; }
+int64_t mlora_ctx_launch_count(const mlora_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+// lora.cpp:72-85: max_len over all lengths, sequences = count,
+// total = sequences * max_len, padding = total - Σ len.
+mlora_status mlora_fused_shape_of(const int32_t* lengths, int64_t n, mlora_fused_shape* out) {
+    if (!out || (n > 0 && !lengths)) return fail(nullptr, MLORA_USAGE, "null argument");
+    mlora_fused_shape s{0, 0, 0, 0};
+    long long real = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        s.max_len = std::max<int32_t>(s.max_len, lengths[i]);
+        ++s.sequences;
+        real += lengths[i];
+    }
+    s.total_tokens = s.sequences * s.max_len;
+    s.padding_tokens = s.total_tokens - real;
+    *out = s;
+    return MLORA_OK;
+}
+
+// lora.cpp:184-189
+mlora_status mlora_count_launches(int32_t num_jobs, int32_t mode, int64_t* small_launches,
+                                  int64_t* large_launches) {
+    if (num_jobs < 1) return fail(nullptr, MLORA_USAGE, "count_launches: need at least one job");
+    if (!small_launches || !large_launches) return fail(nullptr, MLORA_USAGE, "null argument");
+    if (mode != 0 && mode != 1) return fail(nullptr, MLORA_USAGE, "count_launches: bad mode");
+    const int64_t k = num_jobs;
+    *small_launches = mode == 0 ? 4 * k : 2 * k;
+    *large_launches = mode == 0 ? 0 : 2;
+    return MLORA_OK;
+}
+
+mlora_status mlora_plan_create(mlora_ctx* ctx, int32_t num_jobs, const int64_t* seg_offsets,
+                               const int32_t* ranks, const float* scales, void* stream,
+                               mlora_plan** out) {
+    if (!ctx || !out || !seg_offsets || !ranks) return fail(ctx, MLORA_USAGE, "null argument");
+    *out = nullptr;
+    if (num_jobs < 1 || num_jobs > kMaxJobs)
+        return fail(ctx, MLORA_USAGE, "num_jobs must be in [1, " + std::to_string(kMaxJobs) + "]");
+    if (seg_offsets[0] != 0) return fail(ctx, MLORA_USAGE, "seg_offsets[0] must be 0");
+    for (int j = 0; j < num_jobs; ++j) {
+        if (seg_offsets[j + 1] < seg_offsets[j])
+            return fail(ctx, MLORA_USAGE, "seg_offsets must be non-decreasing");
+        if (ranks[j] < 1) return fail(ctx, MLORA_USAGE, "adapter rank must be >= 1");
+        if (scales && !std::isfinite(scales[j])) return fail(ctx, MLORA_NUMERIC, "non-finite scale");
+    }
+    const long long rows = seg_offsets[num_jobs];
+    if (rows < 1) return fail(ctx, MLORA_USAGE, "fused batch has no rows");
+    if (rows > (1LL << 30)) return fail(ctx, MLORA_USAGE, "too many rows");
+    DeviceGuard g(ctx->device);
+
+    auto* p = new mlora_plan();
+    p->ctx = ctx;
+    p->J = num_jobs;
+    p->rows = static_cast<int>(rows);
+    p->seg.resize(num_jobs + 1);
+    p->roff.resize(num_jobs + 1);
+    p->rank.assign(ranks, ranks + num_jobs);
+    p->scale.resize(num_jobs);
+    p->roff[0] = 0;
+    for (int j = 0; j < num_jobs; ++j) {
+        p->seg[j] = static_cast<int>(seg_offsets[j]);
+        p->roff[j + 1] = p->roff[j] + ((ranks[j] + 15) / 16) * 16;
+        p->scale[j] = scales ? scales[j] : 1.0f;
+    }
+    p->seg[num_jobs] = static_cast<int>(rows);
+    p->R_pad = p->roff[num_jobs];
+    p->n_mblk = cdiv(rows, kBM);
+    p->n_chunks = cdiv(p->R_pad, kBK);
+
+    auto job_of_row = [&](int r) {
+        int j = static_cast<int>(std::upper_bound(p->seg.begin(), p->seg.end(), r) - p->seg.begin()) - 1;
+        return std::min(std::max(j, 0), num_jobs - 1);
+    };
+    // per m-block: the 64-col chunks (LoRA k-blocks) of the jobs present
+    p->ext.resize(2 * p->n_mblk);
+    for (int mb = 0; mb < p->n_mblk; ++mb) {
+        const int r0 = mb * kBM;
+        const int r1 = std::min<int>(r0 + kBM, p->rows) - 1;
+        const int ja = job_of_row(r0), jb = job_of_row(r1);
+        p->ext[2 * mb] = p->roff[ja] / kBK;
+        p->ext[2 * mb + 1] = cdiv(p->roff[jb + 1], kBK);
+        for (int c = p->ext[2 * mb]; c < p->ext[2 * mb + 1]; ++c) {
+            p->down.push_back(mb);
+            p->down.push_back(c);
+            p->down.push_back(c == p->ext[2 * mb] ? 1 : 0);
+        }
+    }
+    p->n_down = static_cast<int>(p->down.size() / 3);
+    // per chunk: union of the token segments of the jobs owning its columns
+    p->chunk_kb.resize(2 * p->n_chunks);
+    for (int c = 0; c < p->n_chunks; ++c) {
+        const int c0 = c * kBK, c1 = c0 + kBK;
+        int ja = -1, jb = -1;
+        for (int j = 0; j < num_jobs; ++j)
+            if (p->roff[j + 1] > c0 && p->roff[j] < c1) {
+                if (ja < 0) ja = j;
+                jb = j;
+            }
+        const int t0 = p->seg[ja], t1 = p->seg[jb + 1];
+        p->chunk_kb[2 * c] = t0 / kBK;
+        p->chunk_kb[2 * c + 1] = t1 > t0 ? cdiv(t1, kBK) : t0 / kBK;
+    }
+    std::vector<int> grad;
+    for (int ns = 1; ns <= kMaxSplit; ++ns) {
+        p->grad_off[ns] = static_cast<int>(grad.size());
+        for (int c = 0; c < p->n_chunks; ++c) {
+            const int a = p->chunk_kb[2 * c], b = p->chunk_kb[2 * c + 1];
+            const int len = b - a;
+            for (int s = 0; s < ns; ++s) {
+                grad.push_back(a + static_cast<int>((long long)len * s / ns));
+                grad.push_back(a + static_cast<int>((long long)len * (s + 1) / ns));
+            }
+        }
+    }
+    // one device buffer: seg | roff | scale | ext | down | grad
+    std::vector<int> blob;
+    auto append = [&](const std::vector<int>& v) {
+        const size_t off = blob.size();
+        blob.insert(blob.end(), v.begin(), v.end());
+        while (blob.size() % 4) blob.push_back(0);
+        return off;
+    };
+    std::vector<int> scale_bits(num_jobs);
+    std::memcpy(scale_bits.data(), p->scale.data(), sizeof(float) * num_jobs);
+    const size_t o_seg = append(p->seg), o_roff = append(p->roff), o_scale = append(scale_bits),
+                 o_ext = append(p->ext), o_down = append(p->down), o_grad = append(grad);
+    cudaError_t e = cudaMalloc(&p->dev, blob.size() * sizeof(int));
+    if (e != cudaSuccess) {
+        delete p;
+        return fail(ctx, MLORA_CUDA, std::string("cudaMalloc(plan): ") + cudaGetErrorString(e));
+    }
+    e = cudaMemcpyAsync(p->dev, blob.data(), blob.size() * sizeof(int), cudaMemcpyHostToDevice,
+                        static_cast<cudaStream_t>(stream));
+    if (e == cudaSuccess) e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) {
+        cudaFree(p->dev);
+        delete p;
+        return fail(ctx, MLORA_CUDA, std::string("plan upload: ") + cudaGetErrorString(e));
+    }
+    int* base = static_cast<int*>(p->dev);
+    p->d_seg = base + o_seg;
+    p->d_roff = base + o_roff;
+    p->d_scale = reinterpret_cast<float*>(base + o_scale);
+    p->d_ext = base + o_ext;
+    p->d_down = base + o_down;
+    p->d_grad = base + o_grad;
+    *out = p;
+    return MLORA_OK;
+}
+
+mlora_status mlora_plan_destroy(mlora_plan* plan) {
+    if (!plan) return MLORA_OK;
+    DeviceGuard g(plan->ctx->device);
+    if (plan->dev) {
+        cudaDeviceSynchronize();
+        cudaFree(plan->dev);
+    }
+    delete plan;
+    return MLORA_OK;
+}
+
+int64_t mlora_plan_rows(const mlora_plan* plan) { return plan ? plan->rows : 0; }
+int32_t mlora_plan_rank_padded(const mlora_plan* plan) { return plan ? plan->R_pad : 0; }
+mlora_status mlora_plan_rank_offsets(const mlora_plan* plan, int32_t* roff_out) {
+    if (!plan || !roff_out) return fail(nullptr, MLORA_USAGE, "null argument");
+    std::copy(plan->roff.begin(), plan->roff.end(), roff_out);
+    return MLORA_OK;
+}
+
+mlora_status mlora_linear_fwd(mlora_ctx* ctx, const mlora_plan* plan, int32_t d, int32_t k,
+                              const void* X, const void* W0, const void* A_cat, const void* B_cat,
+                              void* Y, void* H, void* stream) {
+    mlora_status st = check_dims(ctx, plan, d, k);
+    if (st != MLORA_OK) return st;
+    if (!X || !W0 || !A_cat || !B_cat || !Y || !H) return fail(ctx, MLORA_USAGE, "null tensor pointer");
+    DeviceGuard g(ctx->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int M = plan->rows, R = plan->R_pad;
+    CUtensorMap tX, tA, tW, tH, tB;
+    if ((st = get_tmap(ctx, X, k, M, k, 64, 128, &tX)) != MLORA_OK) return st;
+    if ((st = get_tmap(ctx, A_cat, k, R, k, 64, 64, &tA)) != MLORA_OK) return st;
+    if ((st = get_tmap(ctx, W0, k, d, k, 64, 256, &tW)) != MLORA_OK) return st;
+    if ((st = get_tmap(ctx, H, R, M, R, 64, 128, &tH)) != MLORA_OK) return st;
+    if ((st = get_tmap(ctx, B_cat, R, d, R, 64, 256, &tB)) != MLORA_OK) return st;
+
+    // (1) H = s_j X A_j^T, block-diagonal, bf16
+    GemmParams pd{};
+    pd.M = M;
+    pd.N = R;
+    pd.num_kb = cdiv(k, kBK);
+    pd.n_mblk = plan->n_mblk;
+    pd.num_tiles = plan->n_down;
+    pd.out = H;
+    pd.ldo = R;
+    pd.ext_tab = plan->d_ext;
+    pd.down_tab = plan->d_down;
+    pd.seg = plan->d_seg;
+    pd.roff = plan->d_roff;
+    pd.scale = plan->d_scale;
+    pd.num_jobs = plan->J;
+    st = launch_gemm<MODE_DOWN, 64, kSmallStages, false, false>(ctx, tX, tA, tX, tA, pd, 2, s);
+    if (st != MLORA_OK) return st;
+
+    // (2) Y = X W0^T + H B_cat^T
+    GemmParams pb{};
+    pb.M = M;
+    pb.N = d;
+    pb.num_kb = cdiv(k, kBK);
+    pb.n_mblk = plan->n_mblk;
+    pb.n_nblk = cdiv(d, 256);
+    pb.num_tiles = pb.n_mblk * pb.n_nblk;
+    pb.out = Y;
+    pb.ldo = d;
+    pb.ext_tab = plan->d_ext;
+    pb.seg = plan->d_seg;
+    pb.roff = plan->d_roff;
+    pb.scale = plan->d_scale;
+    pb.num_jobs = plan->J;
+    return launch_gemm<MODE_BASE, 256, kBaseStages, false, false>(ctx, tX, tW, tH, tB, pb, 1, s);
+}
+
+mlora_status mlora_linear_bwd(mlora_ctx* ctx, const mlora_plan* plan, int32_t d, int32_t k,
+                              const void* dY, const void* X, const void* H, const void* W0,
+                              const void* A_cat, const void* B_cat, void* G, void* dX,
+                              float* dA_cat, float* dB_cat, void* stream) {
+    mlora_status st = check_dims(ctx, plan, d, k);
+    if (st != MLORA_OK) return st;
+    if (!dY || !X || !H || !W0 || !A_cat || !B_cat || !G)
+        return fail(ctx, MLORA_USAGE, "null tensor pointer");
+    DeviceGuard g(ctx->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int M = plan->rows, R = plan->R_pad;
+
+    // (1) G = s_j dY B_j   (B operand B_cat viewed MN-major: n = rank col, k = d)
+    CUtensorMap tdY128, tBmn;
+    if ((st = get_tmap(ctx, dY, d, M, d, 64, 128, &tdY128)) != MLORA_OK) return st;
+    if ((st = get_tmap(ctx, B_cat, R, d, R, 64, 64, &tBmn)) != MLORA_OK) return st;
+    GemmParams pd{};
+    pd.M = M;
+    pd.N = R;
+    pd.num_kb = cdiv(d, kBK);
+    pd.n_mblk = plan->n_mblk;
+    pd.num_tiles = plan->n_down;
+    pd.out = G;
+    pd.ldo = R;
+    pd.ext_tab = plan->d_ext;
+    pd.down_tab = plan->d_down;
+    pd.seg = plan->d_seg;
+    pd.roff = plan->d_roff;
+    pd.scale = plan->d_scale;
+    pd.num_jobs = plan->J;
+    st = launch_gemm<MODE_DOWN, 64, kSmallStages, false, true>(ctx, tdY128, tBmn, tdY128, tBmn, pd, 2, s);
+    if (st != MLORA_OK) return st;
+
+    // (2) dX = dY W0 + G A_cat   (W0 and A_cat as MN-major B operands)
+    if (dX) {
+        CUtensorMap tWmn, tG128, tAmn;
+        if ((st = get_tmap(ctx, W0, k, d, k, 64, 64, &tWmn)) != MLORA_OK) return st;
+        if ((st = get_tmap(ctx, G, R, M, R, 64, 128, &tG128)) != MLORA_OK) return st;
+        if ((st = get_tmap(ctx, A_cat, k, R, k, 64, 64, &tAmn)) != MLORA_OK) return st;
+        GemmParams pb{};
+        pb.M = M;
+        pb.N = k;
+        pb.num_kb = cdiv(d, kBK);
+        pb.n_mblk = plan->n_mblk;
+        pb.n_nblk = cdiv(k, 256);
+        pb.num_tiles = pb.n_mblk * pb.n_nblk;
+        pb.out = dX;
+        pb.ldo = k;
+        pb.ext_tab = plan->d_ext;
+        pb.seg = plan->d_seg;
+        pb.roff = plan->d_roff;
+        pb.scale = plan->d_scale;
+        pb.num_jobs = plan->J;
+        st = launch_gemm<MODE_BASE, 256, kBaseStages, false, true>(ctx, tdY128, tWmn, tG128, tAmn, pb, 1, s);
+        if (st != MLORA_OK) return st;
+    }
+    // (3) dA_cat = G^T X over each chunk's token range  (stored R_pad x k)
+    if (dA_cat) {
+        CUtensorMap tXmn, tGmn;
+        if ((st = get_tmap(ctx, X, k, M, k, 64, 64, &tXmn)) != MLORA_OK) return st;
+        if ((st = get_tmap(ctx, G, R, M, R, 64, 64, &tGmn)) != MLORA_OK) return st;
+        st = run_grad<MODE_GRADT>(ctx, plan, tXmn, tGmn, k, dA_cat, s);
+        if (st != MLORA_OK) return st;
+    }
+    // (4) dB_cat = dY^T H over each chunk's token range  (stored d x R_pad)
+    if (dB_cat) {
+        CUtensorMap tdYmn, tHmn;
+        if ((st = get_tmap(ctx, dY, d, M, d, 64, 64, &tdYmn)) != MLORA_OK) return st;
+        if ((st = get_tmap(ctx, H, R, M, R, 64, 64, &tHmn)) != MLORA_OK) return st;
+        st = run_grad<MODE_GRAD>(ctx, plan, tdYmn, tHmn, d, dB_cat, s);
+        if (st != MLORA_OK) return st;
+    }
+    return MLORA_OK;
+}
+
+mlora_status mlora_pack_adapters(mlora_ctx* ctx, const mlora_plan* plan, int32_t d, int32_t k,
+                                 const float* const* A_ptrs, const float* const* B_ptrs,
+                                 float* A_cat_f32, float* B_cat_f32, void* A_cat_bf16,
+                                 void* B_cat_bf16, void* stream) {
+    mlora_status st = check_dims(ctx, plan, d, k);
+    if (st != MLORA_OK) return st;
+    if (!A_ptrs || !B_ptrs) return fail(ctx, MLORA_USAGE, "null pointer array");
+    PackArgs a{};
+    for (int j = 0; j < plan->J; ++j) {
+        if (!A_ptrs[j] || !B_ptrs[j])
+            return fail(ctx, MLORA_ROUTING, "no adapter for job " + std::to_string(j));
+        if (plan->rank[j] > std::min(d, k)) return fail(ctx, MLORA_USAGE, "adapter rank exceeds min(d, k)");
+        a.A[j] = A_ptrs[j];
+        a.B[j] = B_ptrs[j];
+        a.rank[j] = plan->rank[j];
+        a.roff[j] = plan->roff[j];
+    }
+    a.roff[plan->J] = plan->roff[plan->J];
+    a.J = plan->J;
+    a.d = d;
+    a.k = k;
+    a.R_pad = plan->R_pad;
+    a.A_f32 = A_cat_f32;
+    a.B_f32 = B_cat_f32;
+    a.A_bf16 = static_cast<__nv_bfloat16*>(A_cat_bf16);
+    a.B_bf16 = static_cast<__nv_bfloat16*>(B_cat_bf16);
+    DeviceGuard g(ctx->device);
+    const long long n = (long long)plan->R_pad * k + (long long)d * plan->R_pad;
+    const int blocks = static_cast<int>(std::min<long long>(cdiv(n, 256), 8LL * ctx->num_sms));
+    pack_adapters_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
+    MLORA_CUDA_TRY(ctx, cudaGetLastError());
+    ++ctx->launches;
+    return MLORA_OK;
+}
+
+mlora_status mlora_adam_step(mlora_ctx* ctx, const mlora_plan* plan, const mlora_adam_group* groups,
+                             int32_t num_groups, const float* lr, const int32_t* step, float beta1,
+                             float beta2, float eps, float weight_decay, void* stream) {
+    if (!ctx || !plan || (num_groups > 0 && !groups) || !lr || !step)
+        return fail(ctx, MLORA_USAGE, "null argument");
+    if (!(beta1 >= 0.f && beta1 < 1.f && beta2 >= 0.f && beta2 < 1.f && eps > 0.f))
+        return fail(ctx, MLORA_USAGE, "bad Adam hyper-parameters");
+    DeviceGuard g(ctx->device);
+    AdamArgs a{};
+    a.J = plan->J;
+    for (int j = 0; j <= plan->J; ++j) a.roff[j] = plan->roff[j];
+    for (int j = 0; j < plan->J; ++j) {
+        if (step[j] < 1) return fail(ctx, MLORA_USAGE, "Adam step must be >= 1");
+        if (!std::isfinite(lr[j])) return fail(ctx, MLORA_NUMERIC, "non-finite learning rate");
+        a.lr[j] = lr[j];
+        a.bc1[j] = static_cast<float>(1.0 - std::pow(static_cast<double>(beta1), step[j]));
+        a.bc2[j] = static_cast<float>(1.0 - std::pow(static_cast<double>(beta2), step[j]));
+    }
+    a.beta1 = beta1;
+    a.beta2 = beta2;
+    a.eps = eps;
+    a.wd = weight_decay;
+    for (int g0 = 0; g0 < num_groups; g0 += kMaxAdamGroups) {
+        const int ng = std::min(kMaxAdamGroups, num_groups - g0);
+        long long start4 = 0;
+        for (int i = 0; i < ng; ++i) {
+            const mlora_adam_group& G = groups[g0 + i];
+            if (!G.p || !G.g || !G.m || !G.v) return fail(ctx, MLORA_USAGE, "null Adam tensor");
+            if (G.cols % 4 != 0) return fail(ctx, MLORA_SHAPE, "Adam group cols must be a multiple of 4");
+            const long long bound = G.layout == 0 ? G.rows : G.cols;
+            if (bound != plan->R_pad) return fail(ctx, MLORA_SHAPE, "Adam group job axis must have R_pad entries");
+            a.grp[i] = AdamGroupDev{G.p, G.g, G.m, G.v, static_cast<__nv_bfloat16*>(G.p_bf16),
+                                    G.rows, G.cols, start4, G.layout};
+            start4 += G.rows * G.cols / 4;
+        }
+        a.ngroups = ng;
+        a.total4 = start4;
+        if (start4 == 0) continue;
+        const int blocks = static_cast<int>(std::min<long long>(cdiv(start4, 256), 8LL * ctx->num_sms));
+        adam_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
+        MLORA_CUDA_TRY(ctx, cudaGetLastError());
+        ++ctx->launches;
+    }
+    return MLORA_OK;
+}
+
+}  // extern "C"

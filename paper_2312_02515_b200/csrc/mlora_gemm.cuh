@@ -1,0 +1,379 @@
+// mlora_gemm.cuh — the one tcgen05 GEMM engine behind every multi-LoRA product.
+//
+// BatchFusion (ASPEN, arXiv 2312.02515, Eq. 1; reference fp64 loop in
+// /root/reference/proj/src/lora.cpp:160-182) computes, per job row-segment j,
+//     Y_j = X_j W0^T + (X_j A_j^T) B_j^T .
+// On B200 every term of the forward and backward is one of four tile programs
+// of the same persistent, warp-specialised kernel:
+//
+//   MODE_BASE : C[M,N]  = A0[M,K] B0[N,K]^T  (+ A1[M,R] B1[N,R]^T on the
+//               k-blocks of the jobs present in the m-tile)       -> bf16 C
+//               forward:  A0=X,  B0=W0 (K-major), A1=H_cat, B1=B_cat
+//               dX:       A0=dY, B0=W0 (MN-major), A1=G_cat, B1=A_cat (MN)
+//   MODE_DOWN : H_cat[M, 64-col chunk] = s_j * A0 B0^T, masked block-diagonal
+//               H = s X A_cat^T  (B0 = A_cat K-major)
+//               G = s dY B_cat   (B0 = B_cat MN-major)
+//   MODE_GRADT: dA_cat^T partials  [F, 64-col chunk] = X^T G_cat over the
+//               chunk's token range, stored transposed ([R_pad, F], fp32)
+//   MODE_GRAD : dB_cat partials    [F, 64-col chunk] = dY^T H_cat  ([F, R_pad])
+//
+// Roles (192 threads, 1 CTA per SM for BASE): warp 0 = TMA producer,
+// warp 1 = TMEM allocator + single-thread tcgen05.mma issuer, warps 2..5 =
+// epilogue (TMEM -> registers -> HBM).  Accumulators are double-buffered in
+// TMEM so the epilogue of tile i overlaps the MMAs of tile i+1.  Operands are
+// staged by TMA with 128-byte swizzle in a STAGES-deep mbarrier ring.
+#pragma once
+
+#include "sm100.cuh"
+
+namespace mlora {
+
+enum GemmMode : int { MODE_BASE = 0, MODE_DOWN = 1, MODE_GRADT = 2, MODE_GRAD = 3 };
+
+constexpr int kBM = 128;        // UMMA M (rows of the output tile)
+constexpr int kBK = 64;         // 64 bf16 = one 128 B swizzle row
+constexpr int kUmmaK = 16;      // K per tcgen05.mma kind::f16
+constexpr int kNumThreads = 192;
+
+struct GemmParams {
+    int M;             // valid output rows (tokens for BASE/DOWN, features for GRAD*)
+    int N;             // valid output cols (d for BASE, R_pad for DOWN/GRAD*)
+    int num_kb;        // main-segment k-blocks (BASE/DOWN)
+    int n_mblk;        // number of 128-row blocks
+    int n_nblk;        // number of BN-col blocks (BASE)
+    int num_tiles;
+    int nsplit;        // token splits (GRAD*)
+    void* out;         // output base
+    long long ldo;     // output leading dimension (elements)
+    long long split_stride;  // elements between split partials (GRAD*)
+    const int* ext_tab;   // [n_mblk][2]  extra (LoRA) k-block range per m-block
+    const int* down_tab;  // [num_tiles][3] (m_blk, chunk, flags) for MODE_DOWN
+    const int* grad_tab;  // [nchunks*nsplit][2] token k-block range
+    const int* seg;       // [J+1] row offsets of job segments
+    const int* roff;      // [J+1] padded rank column offsets
+    const float* scale;   // [J] per-job LoRA scale s_j
+    int num_jobs;
+};
+
+struct TileInfo {
+    int m0, n0;
+    int kb0, kb1;   // main segment k-blocks
+    int xb0, xb1;   // extra segment k-blocks
+    int aux;        // DOWN: flags; GRAD*: split index
+};
+
+template <int MODE, int BN>
+__device__ __forceinline__ TileInfo decode_tile(const GemmParams& p, int t) {
+    TileInfo ti;
+    if constexpr (MODE == MODE_BASE) {
+        const int mb = t % p.n_mblk;
+        const int nb = t / p.n_mblk;
+        ti.m0 = mb * kBM;
+        ti.n0 = nb * BN;
+        ti.kb0 = 0;
+        ti.kb1 = p.num_kb;
+        ti.xb0 = __ldg(p.ext_tab + 2 * mb);
+        ti.xb1 = __ldg(p.ext_tab + 2 * mb + 1);
+        ti.aux = 0;
+    } else if constexpr (MODE == MODE_DOWN) {
+        const int mb = __ldg(p.down_tab + 3 * t);
+        const int c = __ldg(p.down_tab + 3 * t + 1);
+        ti.aux = __ldg(p.down_tab + 3 * t + 2);
+        ti.m0 = mb * kBM;
+        ti.n0 = c * BN;
+        ti.kb0 = 0;
+        ti.kb1 = p.num_kb;
+        ti.xb0 = ti.xb1 = 0;
+    } else {
+        const int fb = t % p.n_mblk;
+        const int cs = t / p.n_mblk;  // chunk * nsplit + split
+        ti.m0 = fb * kBM;
+        ti.n0 = (cs / p.nsplit) * BN;
+        ti.kb0 = __ldg(p.grad_tab + 2 * cs);
+        ti.kb1 = __ldg(p.grad_tab + 2 * cs + 1);
+        ti.xb0 = ti.xb1 = 0;
+        ti.aux = cs % p.nsplit;
+    }
+    return ti;
+}
+
+template <int BN, int STAGES>
+struct GemmSmem {
+    static constexpr int kABytes = kBM * kBK * 2;
+    static constexpr int kBBytes = BN * kBK * 2;
+    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kBarOffset = STAGES * kStageBytes;
+    // full[S], empty[S], tmem_full[2], tmem_empty[2], tmem base slot
+    static constexpr int kBytes = kBarOffset + (2 * STAGES + 4) * 8 + 16;
+    static constexpr int kDynBytes = kBytes + 1024;  // manual 1 KB alignment slack
+};
+
+__device__ __forceinline__ int job_of_row(const int* seg, int num_jobs, int row) {
+    // largest j with seg[j] <= row (segments partition [0, M))
+    int lo = 0, hi = num_jobs - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (__ldg(seg + mid) <= row) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+template <int MODE, int BN, int STAGES, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(kNumThreads, 1)
+mlora_gemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmB0,
+                  const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1,
+                  const GemmParams p) {
+    using namespace sm100;
+    using L = GemmSmem<BN, STAGES>;
+    static_assert(BN % 64 == 0 && BN >= 64 && BN <= 256, "BN must be a multiple of 64 in [64,256]");
+    constexpr uint32_t kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
+                                 : (2 * BN <= 256) ? 256 : 512;
+    constexpr uint32_t kIdesc = idesc_bf16_f32(kBM, BN, A_MN, B_MN);
+
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw_addr = smem_u32(smem_raw);
+    const uint32_t base_addr = (raw_addr + 1023u) & ~1023u;
+    uint8_t* smem = smem_raw + (base_addr - raw_addr);
+    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + L::kBarOffset);
+    uint64_t* empty_bar = full_bar + STAGES;
+    uint64_t* tfull_bar = empty_bar + STAGES;
+    uint64_t* tempty_bar = tfull_bar + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+    const uint32_t warp = warp_id();
+    const uint32_t lane = threadIdx.x & 31;
+
+    if (warp == 0 && elect_one()) {
+        tma_prefetch_desc(&tmA0);
+        tma_prefetch_desc(&tmB0);
+        if constexpr (MODE == MODE_BASE) {
+            tma_prefetch_desc(&tmA1);
+            tma_prefetch_desc(&tmB1);
+        }
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(full_bar + s, 1);
+            mbar_init(empty_bar + s, 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(tfull_bar + a, 1);
+            mbar_init(tempty_bar + a, 128);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) {
+        tmem_alloc(tmem_slot, kTmemCols);
+        tmem_relinquish();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------ TMA producer
+        if (elect_one()) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+                const TileInfo ti = decode_tile<MODE, BN>(p, t);
+                const int nmain = ti.kb1 - ti.kb0;
+                const int nk = nmain + (ti.xb1 - ti.xb0);
+                for (int it = 0; it < nk; ++it) {
+                    mbar_wait(empty_bar + stage, phase ^ 1u);
+                    const bool ext = it >= nmain;
+                    const CUtensorMap* mA = ext ? &tmA1 : &tmA0;
+                    const CUtensorMap* mB = ext ? &tmB1 : &tmB0;
+                    const int kc = (ext ? (ti.xb0 + it - nmain) : (ti.kb0 + it)) * kBK;
+                    const uint32_t sA = base_addr + stage * L::kStageBytes;
+                    const uint32_t sB = sA + L::kABytes;
+                    uint64_t* bar = full_bar + stage;
+                    mbar_arrive_expect_tx(bar, L::kStageBytes);
+                    if constexpr (!A_MN) {
+                        tma_load_2d(sA, mA, bar, kc, ti.m0);
+                    } else {
+#pragma unroll
+                        for (int h = 0; h < kBM / 64; ++h)
+                            tma_load_2d(sA + h * 8192, mA, bar, ti.m0 + 64 * h, kc);
+                    }
+                    if constexpr (!B_MN) {
+                        tma_load_2d(sB, mB, bar, kc, ti.n0);
+                    } else {
+#pragma unroll
+                        for (int h = 0; h < BN / 64; ++h)
+                            tma_load_2d(sB + h * 8192, mB, bar, ti.n0 + 64 * h, kc);
+                    }
+                    if (++stage == STAGES) { stage = 0; phase ^= 1u; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------ MMA issuer
+        int stage = 0;
+        uint32_t phase = 0;
+        int local = 0;
+        for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++local) {
+            const TileInfo ti = decode_tile<MODE, BN>(p, t);
+            const int nk = (ti.kb1 - ti.kb0) + (ti.xb1 - ti.xb0);
+            const int acc = local & 1;
+            const uint32_t use = static_cast<uint32_t>(local >> 1);
+            mbar_wait(tempty_bar + acc, (use & 1u) ^ 1u);
+            tc_fence_after();
+            const uint32_t d_tmem = tmem_base + acc * BN;
+            for (int it = 0; it < nk; ++it) {
+                mbar_wait(full_bar + stage, phase);
+                tc_fence_after();
+                if (elect_one()) {
+                    const uint32_t sA = base_addr + stage * L::kStageBytes;
+                    const uint32_t sB = sA + L::kABytes;
+#pragma unroll
+                    for (int j = 0; j < kBK / kUmmaK; ++j) {
+                        const uint64_t ad = A_MN ? sdesc_sw128(sA + j * 2048, 8192, 1024)
+                                                 : sdesc_sw128(sA + j * 32, 16, 1024);
+                        const uint64_t bd = B_MN ? sdesc_sw128(sB + j * 2048, 8192, 1024)
+                                                 : sdesc_sw128(sB + j * 32, 16, 1024);
+                        mma_bf16(d_tmem, ad, bd, kIdesc, (it | j) != 0 ? 1u : 0u);
+                    }
+                    tc_commit(empty_bar + stage);
+                }
+                __syncwarp();
+                if (++stage == STAGES) { stage = 0; phase ^= 1u; }
+            }
+            if (elect_one()) tc_commit(tfull_bar + acc);
+            __syncwarp();
+        }
+    } else {
+        // ------------------------------------------------ epilogue (warps 2..5)
+        const uint32_t q = warp & 3;  // TMEM lane quarter this warp may access
+        const int rloc = static_cast<int>(q * 32 + lane);
+        int local = 0;
+        for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++local) {
+            const TileInfo ti = decode_tile<MODE, BN>(p, t);
+            const bool empty = (ti.kb1 - ti.kb0) + (ti.xb1 - ti.xb0) == 0;
+            const int acc = local & 1;
+            const uint32_t use = static_cast<uint32_t>(local >> 1);
+            mbar_wait(tfull_bar + acc, use & 1u);
+            tc_fence_after();
+            const uint32_t t_row = tmem_base + ((q * 32u) << 16) + acc * BN;
+            const int row = ti.m0 + rloc;
+            const bool row_ok = row < p.M;
+
+            if constexpr (MODE == MODE_BASE) {
+                __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out);
+#pragma unroll 1
+                for (int c = 0; c < BN / 32; ++c) {
+                    uint32_t v[32];
+                    tmem_ld32(t_row + c * 32, v);
+                    tmem_wait_ld();
+                    const int col = ti.n0 + c * 32;
+                    if (row_ok && col < p.N) {
+                        uint4* dst = reinterpret_cast<uint4*>(out + (long long)row * p.ldo + col);
+#pragma unroll
+                        for (int g = 0; g < 4; ++g) {
+                            if (col + 8 * g + 8 <= p.N) {
+                                uint4 w;
+                                w.x = pack_bf16x2(__uint_as_float(v[8 * g + 0]), __uint_as_float(v[8 * g + 1]));
+                                w.y = pack_bf16x2(__uint_as_float(v[8 * g + 2]), __uint_as_float(v[8 * g + 3]));
+                                w.z = pack_bf16x2(__uint_as_float(v[8 * g + 4]), __uint_as_float(v[8 * g + 5]));
+                                w.w = pack_bf16x2(__uint_as_float(v[8 * g + 6]), __uint_as_float(v[8 * g + 7]));
+                                dst[g] = w;
+                            }
+                        }
+                    }
+                }
+            } else if constexpr (MODE == MODE_DOWN) {
+                __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out);
+                int jr = 0, c_lo = 0, c_hi = 0;
+                float s = 0.f;
+                if (row_ok) {
+                    jr = job_of_row(p.seg, p.num_jobs, row);
+                    c_lo = __ldg(p.roff + jr);
+                    c_hi = __ldg(p.roff + jr + 1);
+                    s = __ldg(p.scale + jr);
+                }
+#pragma unroll 1
+                for (int c = 0; c < BN / 32; ++c) {
+                    uint32_t v[32];
+                    tmem_ld32(t_row + c * 32, v);
+                    tmem_wait_ld();
+                    const int col = ti.n0 + c * 32;
+                    if (row_ok) {
+                        uint4* dst = reinterpret_cast<uint4*>(out + (long long)row * p.ldo + col);
+#pragma unroll
+                        for (int g = 0; g < 4; ++g) {
+                            if (col + 8 * g + 8 > p.N) break;
+                            float f[8];
+#pragma unroll
+                            for (int e = 0; e < 8; ++e) {
+                                const int cc = col + 8 * g + e;
+                                f[e] = (cc >= c_lo && cc < c_hi) ? s * __uint_as_float(v[8 * g + e]) : 0.f;
+                            }
+                            uint4 w;
+                            w.x = pack_bf16x2(f[0], f[1]);
+                            w.y = pack_bf16x2(f[2], f[3]);
+                            w.z = pack_bf16x2(f[4], f[5]);
+                            w.w = pack_bf16x2(f[6], f[7]);
+                            dst[g] = w;
+                        }
+                    }
+                }
+                if ((ti.aux & 1) && row_ok) {
+                    // first chunk tile of this m-block: define every other column
+                    // of the row (zero) so H/G are fully block-diagonal in HBM.
+                    const int mb = ti.m0 / kBM;
+                    const int z0 = __ldg(p.ext_tab + 2 * mb) * kBK;
+                    const int z1 = __ldg(p.ext_tab + 2 * mb + 1) * kBK;
+                    uint4* rowp = reinterpret_cast<uint4*>(out + (long long)row * p.ldo);
+                    const uint4 zero = make_uint4(0, 0, 0, 0);
+                    for (int cc = 0; cc < p.N; cc += 8)
+                        if (cc < z0 || cc >= z1) rowp[cc / 8] = zero;
+                }
+            } else if constexpr (MODE == MODE_GRADT) {
+                float* out = static_cast<float*>(p.out) + (long long)ti.aux * p.split_stride;
+#pragma unroll 1
+                for (int c = 0; c < BN / 32; ++c) {
+                    uint32_t v[32];
+                    if (!empty) { tmem_ld32(t_row + c * 32, v); tmem_wait_ld(); }
+                    if (row_ok) {
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) {
+                            const int col = ti.n0 + c * 32 + e;
+                            if (col < p.N) out[(long long)col * p.ldo + row] = empty ? 0.f : __uint_as_float(v[e]);
+                        }
+                    }
+                }
+            } else {  // MODE_GRAD
+                float* out = static_cast<float*>(p.out) + (long long)ti.aux * p.split_stride;
+#pragma unroll 1
+                for (int c = 0; c < BN / 32; ++c) {
+                    uint32_t v[32];
+                    if (!empty) { tmem_ld32(t_row + c * 32, v); tmem_wait_ld(); }
+                    const int col = ti.n0 + c * 32;
+                    if (row_ok && col < p.N) {
+                        float4* dst = reinterpret_cast<float4*>(out + (long long)row * p.ldo + col);
+#pragma unroll
+                        for (int g = 0; g < 8; ++g) {
+                            if (col + 4 * g + 4 <= p.N) {
+                                float4 w;
+                                w.x = empty ? 0.f : __uint_as_float(v[4 * g + 0]);
+                                w.y = empty ? 0.f : __uint_as_float(v[4 * g + 1]);
+                                w.z = empty ? 0.f : __uint_as_float(v[4 * g + 2]);
+                                w.w = empty ? 0.f : __uint_as_float(v[4 * g + 3]);
+                                dst[g] = w;
+                            }
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(tempty_bar + acc);
+        }
+    }
+
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, kTmemCols);
+    }
+}
+
+}  // namespace mlora
