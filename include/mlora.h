@@ -79,6 +79,14 @@ mlora_status mlora_ctx_destroy(mlora_ctx* ctx);
 int32_t mlora_ctx_num_sms(const mlora_ctx* ctx);
 /* Kernels launched through this context since creation (telemetry). */
 int64_t mlora_ctx_launch_count(const mlora_ctx* ctx);
+/* Live per-kernel timing: while enabled, every launch is bracketed by CUDA
+ * events on its own stream.  profile_read synchronises on the recorded events
+ * and returns the accumulated launch count / device milliseconds of one kernel
+ * kind: 0 base GEMM (forward), 1 base GEMM (dX), 2 rank-r down-projection (H/G),
+ * 3 segmented dA/dB reduction, 4 split-reduce / pack / loss, 5 AdamW. */
+mlora_status mlora_ctx_set_profiling(mlora_ctx* ctx, int32_t enable);
+mlora_status mlora_ctx_profile_read(mlora_ctx* ctx, int32_t kind, int64_t* count, double* total_ms,
+                                    int32_t reset);
 
 /* ---------------------------------------------------------------- accounting
  * Replaces fusim::fused_shape (lora.hpp:63, lora.cpp:72-85).  Integer-exact.
@@ -160,6 +168,13 @@ typedef struct mlora_adam_group {
 mlora_status mlora_adam_step(mlora_ctx* ctx, const mlora_plan* plan, const mlora_adam_group* groups,
                              int32_t num_groups, const float* lr, const int32_t* step, float beta1,
                              float beta2, float eps, float weight_decay, void* stream);
+
+/* Per-job synthetic layer loss L_j = 1/2 sum_p sum_{t in job j} ||Y_p[t]||^2 over
+ * `num_tensors` bf16 tensors Y[p] (rows x cols[p]); loss: device fp32 [J].
+ * Deterministic (fixed-order two-level reduction).  Used by the trainer step:
+ * the reference's only runtime loss consumer is detect_stop (progress.cpp:90-124). */
+mlora_status mlora_segment_sumsq_loss(mlora_ctx* ctx, const mlora_plan* plan, const void* const* Y,
+                                      const int32_t* cols, int32_t num_tensors, float* loss, void* stream);
 
 #ifdef __cplusplus
 }

@@ -41,6 +41,8 @@ _SIGS = {
     "mlora_ctx_destroy": (i32, [vp]),
     "mlora_ctx_num_sms": (i32, [vp]),
     "mlora_ctx_launch_count": (i64, [vp]),
+    "mlora_ctx_set_profiling": (i32, [vp, i32]),
+    "mlora_ctx_profile_read": (i32, [vp, i32, C.POINTER(i64), C.POINTER(C.c_double), i32]),
     "mlora_fused_shape_of": (i32, [C.POINTER(i32), i64, C.POINTER(FusedShapeC)]),
     "mlora_count_launches": (i32, [i32, i32, C.POINTER(i64), C.POINTER(i64)]),
     "mlora_plan_create": (i32, [vp, i32, C.POINTER(i64), C.POINTER(i32), C.POINTER(f32), vp, C.POINTER(vp)]),
@@ -51,6 +53,7 @@ _SIGS = {
     "mlora_linear_fwd": (i32, [vp, vp, i32, i32, vp, vp, vp, vp, vp, vp, vp]),
     "mlora_linear_bwd": (i32, [vp, vp, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "mlora_pack_adapters": (i32, [vp, vp, i32, i32, C.POINTER(vp), C.POINTER(vp), vp, vp, vp, vp, vp]),
+    "mlora_segment_sumsq_loss": (i32, [vp, vp, C.POINTER(vp), C.POINTER(i32), i32, vp, vp]),
     "mlora_adam_step": (i32, [vp, vp, C.POINTER(AdamGroupC), i32, C.POINTER(f32), C.POINTER(i32), f32, f32,
                               f32, f32, vp]),
 }

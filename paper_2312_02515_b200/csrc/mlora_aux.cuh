@@ -141,4 +141,62 @@ __global__ void adam_kernel(const __grid_constant__ AdamArgs a) {
     }
 }
 
+// ---------------------------------------------------------------- per-job loss
+// Synthetic layer loss used by the bench/trainer step: L_j = 1/2 sum over the
+// projection outputs Y_p and job j's rows of ||y||^2 (so dL/dY_p = Y_p).
+// Deterministic two-level reduction: row sums (one warp per row), then a
+// fixed-order per-job block sum.  bytes/elem = 2 (bf16 read).
+constexpr int kMaxLossTensors = 16;
+struct SumsqArgs {
+    const __nv_bfloat16* y[kMaxLossTensors];
+    int cols[kMaxLossTensors];
+    int ntensors;
+    int rows;
+    float* row_acc;  // [rows]
+};
+
+__global__ void row_sumsq_kernel(const __grid_constant__ SumsqArgs a) {
+    const int warps = blockDim.x / 32;
+    const int lane = threadIdx.x & 31;
+    for (int row = blockIdx.x * warps + threadIdx.x / 32; row < a.rows; row += gridDim.x * warps) {
+        float acc = 0.f;
+        for (int t = 0; t < a.ntensors; ++t) {
+            const uint4* p = reinterpret_cast<const uint4*>(a.y[t] + (long long)row * a.cols[t]);
+            const int n8 = a.cols[t] / 8;
+            for (int i = lane; i < n8; i += 32) {
+                const uint4 w = p[i];
+                const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float2 f = __bfloat1622float2(h[e]);
+                    acc = fmaf(f.x, f.x, acc);
+                    acc = fmaf(f.y, f.y, acc);
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) a.row_acc[row] = acc;
+    }
+}
+
+__global__ void segment_loss_kernel(const float* __restrict__ row_acc, const int* __restrict__ seg,
+                                    float* __restrict__ loss) {
+    __shared__ float red[32];
+    const int j = blockIdx.x;
+    const int r0 = seg[j], r1 = seg[j + 1];
+    float acc = 0.f;
+    for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) acc += row_acc[r];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x / 32] = acc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        acc = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : 0.f;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (threadIdx.x == 0) loss[j] = 0.5f * acc;
+    }
+}
+
 }  // namespace mlora

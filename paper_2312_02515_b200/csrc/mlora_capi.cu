@@ -47,6 +47,13 @@ struct mlora_ctx {
     size_t workspace_bytes = 0;
     long long launches = 0;
     std::string last_error;
+    // optional live per-kernel timing: (kind, start, stop) event pairs recorded on
+    // the launch stream around every launch while profiling is on
+    bool profiling = false;
+    std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> prof_pending;
+    std::vector<cudaEvent_t> event_pool;
+    double prof_ms[8] = {0};
+    long long prof_count[8] = {0};
 };
 
 struct mlora_plan {
@@ -144,6 +151,39 @@ mlora_status ensure_workspace(mlora_ctx* ctx, size_t bytes) {
     return MLORA_OK;
 }
 
+cudaEvent_t pool_event(mlora_ctx* ctx) {
+    if (!ctx->event_pool.empty()) {
+        cudaEvent_t e = ctx->event_pool.back();
+        ctx->event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// Kernel kinds for the live profile: 0 base fwd, 1 base dX, 2 down (H/G), 3 grad (dA/dB),
+// 4 aux (reduce/pack/adam/loss).
+struct ProfScope {
+    mlora_ctx* ctx;
+    int kind;
+    cudaStream_t stream;
+    cudaEvent_t a = nullptr, b = nullptr;
+    ProfScope(mlora_ctx* c, int k, cudaStream_t s) : ctx(c), kind(k), stream(s) {
+        if (ctx->profiling) {
+            a = pool_event(ctx);
+            b = pool_event(ctx);
+            cudaEventRecord(a, stream);
+        }
+    }
+    ~ProfScope() {
+        if (a) {
+            cudaEventRecord(b, stream);
+            ctx->prof_pending.emplace_back(kind, a, b);
+        }
+    }
+};
+
 template <int MODE, int BN, int STAGES, bool A_MN, bool B_MN>
 mlora_status launch_gemm(mlora_ctx* ctx, const CUtensorMap& a0, const CUtensorMap& b0,
                          const CUtensorMap& a1, const CUtensorMap& b1, const GemmParams& p,
@@ -158,6 +198,7 @@ mlora_status launch_gemm(mlora_ctx* ctx, const CUtensorMap& a0, const CUtensorMa
         attr_done = true;
     }
     const int grid = std::min(p.num_tiles, ctx->num_sms * ctas_per_sm);
+    ProfScope ps(ctx, MODE == MODE_BASE ? (B_MN ? 1 : 0) : MODE == MODE_DOWN ? 2 : 3, stream);
     kern<<<grid, kNumThreads, L::kDynBytes, stream>>>(a0, b0, a1, b1, p);
     MLORA_CUDA_TRY(ctx, cudaGetLastError());
     ++ctx->launches;
@@ -217,6 +258,7 @@ mlora_status run_grad(mlora_ctx* ctx, const mlora_plan* plan, const CUtensorMap&
         const long long n4 = nelem / 4;
         const int threads = 256;
         const int blocks = static_cast<int>(std::min<long long>(cdiv(n4, threads), 4LL * ctx->num_sms));
+        ProfScope ps(ctx, 4, stream);
         reduce_splits_kernel<<<blocks, threads, 0, stream>>>(reinterpret_cast<const float4*>(target),
                                                              reinterpret_cast<float4*>(out), n4, n4, ns);
         MLORA_CUDA_TRY(ctx, cudaGetLastError());
@@ -284,11 +326,44 @@ mlora_status mlora_ctx_destroy(mlora_ctx* ctx) {
         cudaDeviceSynchronize();
         cudaFree(ctx->workspace);
     }
+    for (auto& t : ctx->prof_pending) {
+        cudaEventDestroy(std::get<1>(t));
+        cudaEventDestroy(std::get<2>(t));
+    }
+    for (auto e : ctx->event_pool) cudaEventDestroy(e);
     delete ctx;
     return MLORA_OK;
 }
 
 int32_t mlora_ctx_num_sms(const mlora_ctx* ctx) { return ctx ? ctx->num_sms : 0; }
+
+mlora_status mlora_ctx_set_profiling(mlora_ctx* ctx, int32_t enable) {
+    if (!ctx) return fail(nullptr, MLORA_USAGE, "null context");
+    ctx->profiling = enable != 0;
+    return MLORA_OK;
+}
+
+mlora_status mlora_ctx_profile_read(mlora_ctx* ctx, int32_t kind, int64_t* count, double* total_ms,
+                                    int32_t reset) {
+    if (!ctx || !count || !total_ms || kind < 0 || kind >= 8) return fail(ctx, MLORA_USAGE, "bad argument");
+    DeviceGuard g(ctx->device);
+    for (auto& t : ctx->prof_pending) {
+        cudaEvent_t a = std::get<1>(t), b = std::get<2>(t);
+        MLORA_CUDA_TRY(ctx, cudaEventSynchronize(b));
+        float ms = 0.f;
+        MLORA_CUDA_TRY(ctx, cudaEventElapsedTime(&ms, a, b));
+        ctx->prof_ms[std::get<0>(t)] += ms;
+        ctx->prof_count[std::get<0>(t)] += 1;
+        ctx->event_pool.push_back(a);
+        ctx->event_pool.push_back(b);
+    }
+    ctx->prof_pending.clear();
+    *count = ctx->prof_count[kind];
+    *total_ms = ctx->prof_ms[kind];
+    if (reset)
+        for (int i = 0; i < 8; ++i) ctx->prof_ms[i] = 0, ctx->prof_count[i] = 0;
+    return MLORA_OK;
+}
 int64_t mlora_ctx_launch_count(const mlora_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
 // lora.cpp:72-85: max_len over all lengths, sequences = count,
@@ -614,6 +689,7 @@ mlora_status mlora_pack_adapters(mlora_ctx* ctx, const mlora_plan* plan, int32_t
     DeviceGuard g(ctx->device);
     const long long n = (long long)plan->R_pad * k + (long long)d * plan->R_pad;
     const int blocks = static_cast<int>(std::min<long long>(cdiv(n, 256), 8LL * ctx->num_sms));
+    ProfScope ps(ctx, 4, static_cast<cudaStream_t>(stream));
     pack_adapters_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
     MLORA_CUDA_TRY(ctx, cudaGetLastError());
     ++ctx->launches;
@@ -659,10 +735,40 @@ mlora_status mlora_adam_step(mlora_ctx* ctx, const mlora_plan* plan, const mlora
         a.total4 = start4;
         if (start4 == 0) continue;
         const int blocks = static_cast<int>(std::min<long long>(cdiv(start4, 256), 8LL * ctx->num_sms));
+        ProfScope ps(ctx, 5, static_cast<cudaStream_t>(stream));
         adam_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
         MLORA_CUDA_TRY(ctx, cudaGetLastError());
         ++ctx->launches;
     }
+    return MLORA_OK;
+}
+
+mlora_status mlora_segment_sumsq_loss(mlora_ctx* ctx, const mlora_plan* plan, const void* const* Y,
+                                      const int32_t* cols, int32_t num_tensors, float* loss, void* stream) {
+    if (!ctx || !plan || !Y || !cols || !loss) return fail(ctx, MLORA_USAGE, "null argument");
+    if (num_tensors < 1 || num_tensors > kMaxLossTensors)
+        return fail(ctx, MLORA_USAGE, "num_tensors out of range");
+    SumsqArgs a{};
+    for (int t = 0; t < num_tensors; ++t) {
+        if (!Y[t] || cols[t] <= 0 || cols[t] % 8 != 0)
+            return fail(ctx, MLORA_SHAPE, "loss tensors need cols that are positive multiples of 8");
+        a.y[t] = static_cast<const __nv_bfloat16*>(Y[t]);
+        a.cols[t] = cols[t];
+    }
+    a.ntensors = num_tensors;
+    a.rows = plan->rows;
+    DeviceGuard g(ctx->device);
+    mlora_status st = ensure_workspace(ctx, sizeof(float) * plan->rows);
+    if (st != MLORA_OK) return st;
+    a.row_acc = static_cast<float*>(ctx->workspace);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int blocks = std::min(cdiv(plan->rows, 8), 8 * ctx->num_sms);
+    ProfScope ps(ctx, 4, s);
+    row_sumsq_kernel<<<blocks, 256, 0, s>>>(a);
+    MLORA_CUDA_TRY(ctx, cudaGetLastError());
+    segment_loss_kernel<<<plan->J, 1024, 0, s>>>(a.row_acc, plan->d_seg, loss);
+    MLORA_CUDA_TRY(ctx, cudaGetLastError());
+    ctx->launches += 2;
     return MLORA_OK;
 }
 

@@ -64,6 +64,23 @@ class Context:
     def launches(self) -> int:
         return N.lib().mlora_ctx_launch_count(self._h)
 
+    KERNEL_KINDS = {0: "base_fwd", 1: "base_dx", 2: "down", 3: "grad", 4: "aux", 5: "adam"}
+
+    def set_profiling(self, enable: bool) -> None:
+        N.check(N.lib().mlora_ctx_set_profiling(self._h, 1 if enable else 0), self._h)
+
+    def profile(self, reset: bool = False) -> dict:
+        """{kind: (launches, total device ms)} of the live per-kernel timing."""
+        out = {}
+        names = list(self.KERNEL_KINDS.items())
+        for i, (kind, name) in enumerate(names):
+            cnt, ms = N.i64(), C.c_double()
+            last = i == len(names) - 1
+            N.check(N.lib().mlora_ctx_profile_read(self._h, kind, C.byref(cnt), C.byref(ms),
+                                                   1 if (reset and last) else 0), self._h)
+            out[name] = (cnt.value, ms.value)
+        return out
+
     def close(self) -> None:
         if getattr(self, "_h", None):
             N.lib().mlora_ctx_destroy(self._h)

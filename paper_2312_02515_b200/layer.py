@@ -1,0 +1,148 @@
+"""One fused multi-LoRA training step over the LoRA'd projections of a transformer layer.
+
+This is the executor that slots in at the reference simulator's fused-iteration
+hook (/root/reference/proj/src/sim.cpp:163-191): given the fused batch's
+segment layout (which rows belong to which job, from the MinPad packer) it runs
+every projection's forward, the per-job loss, every backward and one per-job-lr
+AdamW update — all on device, all through the C ABI, with no per-job launches.
+
+Step semantics (stated in DESIGN.md §Measurement): the layer's hidden state x
+feeds q, k, v, gate, up; o consumes v's output and down consumes up's output
+(attention / SiLU-gating are outside the hot path).  The per-job loss is
+L_j = 1/2 sum_p ||Y_p[rows of j]||^2, so dL/dY_p = Y_p (every projection's
+backward is exact for this loss with its input detached).  FLOPs per effective
+token per projection: 4dk + 6 r (d + k).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import torch
+
+from . import _native as N
+from . import fused as F
+
+# (name, d_out, k_in, input source)
+LLAMA7B = [("q", 4096, 4096, "x"), ("k", 4096, 4096, "x"), ("v", 4096, 4096, "x"), ("o", 4096, 4096, "v"),
+           ("gate", 11008, 4096, "x"), ("up", 11008, 4096, "x"), ("down", 4096, 11008, "up")]
+LLAMA13B = [("q", 5120, 5120, "x"), ("k", 5120, 5120, "x"), ("v", 5120, 5120, "x"), ("o", 5120, 5120, "v"),
+            ("gate", 13824, 5120, "x"), ("up", 13824, 5120, "x"), ("down", 5120, 13824, "up")]
+# ChatGLM2-6B: multi-query attention -> fused qkv 4096 -> 4096 + 2*2*128 = 4608; h->4h is the fused
+# gate/up (2 x 13696 = 27392); 4h->h 13696 -> 4096.
+CHATGLM2_6B = [("qkv", 4608, 4096, "x"), ("dense", 4096, 4096, "x"), ("h_to_4h", 27392, 4096, "x"),
+               ("4h_to_h", 4096, 13696, "h_to_4h_half")]
+TINY = [("q", 256, 256, "x"), ("k", 256, 256, "x"), ("v", 256, 256, "x"), ("o", 256, 256, "v"),
+        ("gate", 688, 256, "x"), ("up", 688, 256, "x"), ("down", 256, 688, "up")]
+
+SHAPES = {"llama7b": LLAMA7B, "llama13b": LLAMA13B, "chatglm2_6b": CHATGLM2_6B, "tiny": TINY}
+
+
+def flops_per_token(shapes, rank: int) -> int:
+    """Algorithmic fwd+bwd FLOPs per effective token for one job of rank r (frozen W0)."""
+    return sum(4 * d * k + 6 * rank * (d + k) for _, d, k, _ in shapes)
+
+
+@dataclass
+class Projection:
+    name: str
+    d: int
+    k: int
+    src: str
+    W0: torch.Tensor                   # bf16 [d, k] frozen base weight (replicated)
+    A: F.AdamState                     # A_cat fp32 master [R_pad, k] (+ bf16 copy)
+    B: F.AdamState                     # B_cat fp32 master [d, R_pad] (+ bf16 copy)
+    dA: torch.Tensor                   # fp32 [R_pad, k]
+    dB: torch.Tensor                   # fp32 [d, R_pad]
+    Y: torch.Tensor                    # bf16 [rows, d]
+    H: torch.Tensor                    # bf16 [rows, R_pad]
+    G: torch.Tensor                    # bf16 [rows, R_pad]
+    dX: torch.Tensor                   # bf16 [rows, k]
+
+
+class FusedLoraLayer:
+    """All adapters of J jobs on one layer's projections, cat layout, on one GPU."""
+
+    def __init__(self, ctx: F.Context, shapes, ranks, scales, lrs, rows: int, seed: int = 0,
+                 W0: dict | None = None, lora_init: str = "random"):
+        self.ctx = ctx
+        self.shapes = shapes
+        self.ranks = list(ranks)
+        self.scales = list(scales)
+        self.lrs = list(lrs)
+        self.J = len(ranks)
+        self.rows = rows
+        self.step_count = [0] * self.J
+        dev = ctx.device
+        # plan with a placeholder layout; set_layout() installs the real one
+        self.plan = F.Plan(ctx, [0] * self.J + [rows], ranks, scales)
+        R = self.plan.rank_padded
+        g = torch.Generator(device="cpu").manual_seed(seed)
+        self.proj: list[Projection] = []
+        for name, d, k, src in shapes:
+            if W0 is not None and name in W0:
+                w = W0[name]
+            else:
+                w = ((torch.rand(d, k, generator=g) * 2 - 1) / k ** 0.5).to(torch.bfloat16).to(dev)
+            As, Bs = [], []
+            for r in ranks:
+                As.append(((torch.rand(r, k, generator=g) * 2 - 1) / k ** 0.5).to(dev))
+                if lora_init == "zero_b":   # standard LoRA init: B = 0
+                    Bs.append(torch.zeros(d, r, device=dev))
+                else:
+                    Bs.append(((torch.rand(d, r, generator=g) * 2 - 1) / r ** 0.5).to(dev))
+            A32, B32, A16, B16 = F.pack_adapters(ctx, self.plan, d, k, As, Bs)
+            self.proj.append(Projection(
+                name, d, k, src, w, F.AdamState.of(A32, A16, 0), F.AdamState.of(B32, B16, 1),
+                torch.zeros(R, k, device=dev), torch.zeros(d, R, device=dev),
+                torch.empty(rows, d, dtype=torch.bfloat16, device=dev),
+                torch.empty(rows, R, dtype=torch.bfloat16, device=dev),
+                torch.empty(rows, R, dtype=torch.bfloat16, device=dev),
+                torch.empty(rows, k, dtype=torch.bfloat16, device=dev)))
+        self.loss = torch.zeros(self.J, dtype=torch.float32, device=dev)
+        ys = (N.vp * len(self.proj))(*[p.Y.data_ptr() for p in self.proj])
+        self._loss_ptrs = ys
+        self._loss_cols = (N.i32 * len(self.proj))(*[p.d for p in self.proj])
+
+    def set_layout(self, seg_offsets) -> None:
+        """Install the segment layout of the next fused batch (rows must equal self.rows)."""
+        if int(seg_offsets[-1]) != self.rows:
+            raise ValueError("layout rows must equal the layer's row capacity")
+        self.plan = F.Plan(self.ctx, seg_offsets, self.ranks, self.scales)
+
+    def _input(self, src: str, x: torch.Tensor) -> torch.Tensor:
+        if src == "x":
+            return x
+        if src == "h_to_4h_half":
+            p = next(q for q in self.proj if q.name == "h_to_4h")
+            # first half of the fused gate/up output (stand-in for the gated act.)
+            return p.Y[:, : p.d // 2].contiguous() if p.d // 2 != p.Y.shape[1] else p.Y
+        return next(q for q in self.proj if q.name == src).Y
+
+    def forward_backward(self, x: torch.Tensor, stream=None) -> torch.Tensor:
+        ctx, plan = self.ctx, self.plan
+        inputs = []
+        for p in self.proj:
+            xin = self._input(p.src, x)
+            inputs.append(xin)
+            F.linear_fwd(ctx, plan, xin, p.W0, p.A.p_bf16, p.B.p_bf16, p.Y, p.H, stream=stream)
+        N.check(N.lib().mlora_segment_sumsq_loss(ctx.handle, plan.handle, self._loss_ptrs, self._loss_cols,
+                                                 len(self.proj), self.loss.data_ptr(),
+                                                 F._stream_handle(stream)), ctx.handle)
+        for p, xin in zip(reversed(self.proj), reversed(inputs)):
+            F.linear_bwd(ctx, plan, p.Y, xin, p.H, p.W0, p.A.p_bf16, p.B.p_bf16, need_dX=True, dX=p.dX,
+                         dA_cat=p.dA, dB_cat=p.dB, G=p.G, stream=stream)
+        return self.loss
+
+    def optimizer_step(self, stream=None) -> None:
+        self.step_count = [s + 1 for s in self.step_count]
+        states, grads = [], []
+        for p in self.proj:
+            states += [p.A, p.B]
+            grads += [p.dA, p.dB]
+        F.adam_step(self.ctx, self.plan, states, grads, self.lrs, self.step_count, stream=stream)
+
+    def step(self, x: torch.Tensor, stream=None) -> torch.Tensor:
+        loss = self.forward_backward(x, stream)
+        self.optimizer_step(stream)
+        return loss
