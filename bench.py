@@ -325,7 +325,7 @@ def main():
         "step_tflops": step_tflops, "step_frac_of_peak": step_tflops / peak,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                     "kernel": "mlora_gemm_kernel<MODE_BASE,256> forward (X W0^T + H B^T)",
+                     "kernel": "mlora_base_pair_kernel (cta_group::2, 256x256 tile) forward: X W0^T + H B^T",
                      "peak_kind": ("sustained" if use_sustained else "burst") + " bf16, " + peaks["source"],
                      "launches": cnt, "avg_launch_us": 1e3 * ms / cnt if cnt else None},
         "kernel_time_share": kernel_share,

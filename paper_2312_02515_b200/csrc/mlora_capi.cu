@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -65,7 +66,9 @@ struct mlora_plan {
     int n_chunks = 0;
     std::vector<int> seg, roff, rank;
     std::vector<float> scale;
-    std::vector<int> ext;                 // [n_mblk][2]
+    std::vector<int> ext;                 // [n_mblk][2]   (128-row m-blocks)
+    std::vector<int> ext256;              // [n_mblk256][2] (256-row m-blocks of the CTA-pair kernel)
+    int n_mblk256 = 0;
     std::vector<int> down;                // [n_down][3]
     int n_down = 0;
     std::vector<int> chunk_kb;            // [n_chunks][2] token k-block range
@@ -76,6 +79,7 @@ struct mlora_plan {
     int* d_roff = nullptr;
     float* d_scale = nullptr;
     int* d_ext = nullptr;
+    int* d_ext256 = nullptr;
     int* d_down = nullptr;
     int* d_grad = nullptr;
 };
@@ -203,6 +207,82 @@ mlora_status launch_gemm(mlora_ctx* ctx, const CUtensorMap& a0, const CUtensorMa
     MLORA_CUDA_TRY(ctx, cudaGetLastError());
     ++ctx->launches;
     return MLORA_OK;
+}
+
+bool use_pair_kernel() {
+    static const bool pair = [] {
+        const char* e = std::getenv("MLORA_BASE_KERNEL");
+        return !(e && std::string(e) == "single");
+    }();
+    return pair;
+}
+
+constexpr int kPairStages = 6;
+
+template <bool B_MN>
+mlora_status launch_base_pair(mlora_ctx* ctx, const CUtensorMap& a0, const CUtensorMap& b0,
+                              const CUtensorMap& a1, const CUtensorMap& b1, const GemmParams& p,
+                              cudaStream_t stream) {
+    if (p.num_tiles <= 0) return MLORA_OK;
+    using L = PairSmem<kPairStages>;
+    auto kern = mlora_base_pair_kernel<kPairStages, B_MN>;
+    static bool attr_done = false;
+    if (!attr_done) {
+        MLORA_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 L::kDynBytes));
+        attr_done = true;
+    }
+    const int clusters = std::min(p.num_tiles, ctx->num_sms / 2);
+    ProfScope ps(ctx, B_MN ? 1 : 0, stream);
+    kern<<<2 * clusters, kNumThreads, L::kDynBytes, stream>>>(a0, b0, a1, b1, p);
+    MLORA_CUDA_TRY(ctx, cudaGetLastError());
+    ++ctx->launches;
+    return MLORA_OK;
+}
+
+// Frozen-base GEMM + LoRA k-blocks (forward: B_MN=false; dX: B_MN=true).
+template <bool B_MN>
+mlora_status run_base(mlora_ctx* ctx, const mlora_plan* plan, const void* A0, int64_t lda0, int K0,
+                      const void* B0, const void* A1, const void* B1, int R, int N, void* out,
+                      cudaStream_t s) {
+    const bool pair = use_pair_kernel();
+    const int M = plan->rows;
+    const uint32_t bbox = pair ? 128 : 256;  // K-major B rows staged per CTA
+    CUtensorMap tA0, tB0, tA1, tB1;
+    mlora_status st;
+    if ((st = get_tmap(ctx, A0, K0, M, lda0, 64, 128, &tA0)) != MLORA_OK) return st;
+    if ((st = get_tmap(ctx, A1, R, M, R, 64, 128, &tA1)) != MLORA_OK) return st;
+    if (!B_MN) {
+        // B0 = W0 [N=d, K0=k], B1 = B_cat [N=d, R]
+        if ((st = get_tmap(ctx, B0, K0, N, K0, 64, bbox, &tB0)) != MLORA_OK) return st;
+        if ((st = get_tmap(ctx, B1, R, N, R, 64, bbox, &tB1)) != MLORA_OK) return st;
+    } else {
+        // B0 = W0 [K0=d, N=k] (n contiguous), B1 = A_cat [R, N=k]
+        if ((st = get_tmap(ctx, B0, N, K0, N, 64, 64, &tB0)) != MLORA_OK) return st;
+        if ((st = get_tmap(ctx, B1, N, R, N, 64, 64, &tB1)) != MLORA_OK) return st;
+    }
+    GemmParams pb{};
+    pb.M = M;
+    pb.N = N;
+    pb.num_kb = cdiv(K0, kBK);
+    pb.out = out;
+    pb.ldo = N;
+    pb.seg = plan->d_seg;
+    pb.roff = plan->d_roff;
+    pb.scale = plan->d_scale;
+    pb.num_jobs = plan->J;
+    if (pair) {
+        pb.n_mblk = plan->n_mblk256;
+        pb.n_nblk = cdiv(N, kPairBN);
+        pb.num_tiles = pb.n_mblk * pb.n_nblk;
+        pb.ext_tab = plan->d_ext256;
+        return launch_base_pair<B_MN>(ctx, tA0, tB0, tA1, tB1, pb, s);
+    }
+    pb.n_mblk = plan->n_mblk;
+    pb.n_nblk = cdiv(N, 256);
+    pb.num_tiles = pb.n_mblk * pb.n_nblk;
+    pb.ext_tab = plan->d_ext;
+    return launch_gemm<MODE_BASE, 256, kBaseStages, false, B_MN>(ctx, tA0, tB0, tA1, tB1, pb, 1, s);
 }
 
 mlora_status check_dims(mlora_ctx* ctx, const mlora_plan* plan, int d, int k) {
@@ -452,6 +532,15 @@ mlora_status mlora_plan_create(mlora_ctx* ctx, int32_t num_jobs, const int64_t* 
         }
     }
     p->n_down = static_cast<int>(p->down.size() / 3);
+    p->n_mblk256 = cdiv(rows, kPairBM);
+    p->ext256.resize(2 * p->n_mblk256);
+    for (int mb = 0; mb < p->n_mblk256; ++mb) {
+        const int r0 = mb * kPairBM;
+        const int r1 = std::min<int>(r0 + kPairBM, p->rows) - 1;
+        const int ja = job_of_row(r0), jb = job_of_row(r1);
+        p->ext256[2 * mb] = p->roff[ja] / kBK;
+        p->ext256[2 * mb + 1] = cdiv(p->roff[jb + 1], kBK);
+    }
     // per chunk: union of the token segments of the jobs owning its columns
     p->chunk_kb.resize(2 * p->n_chunks);
     for (int c = 0; c < p->n_chunks; ++c) {
@@ -489,7 +578,8 @@ mlora_status mlora_plan_create(mlora_ctx* ctx, int32_t num_jobs, const int64_t* 
     std::vector<int> scale_bits(num_jobs);
     std::memcpy(scale_bits.data(), p->scale.data(), sizeof(float) * num_jobs);
     const size_t o_seg = append(p->seg), o_roff = append(p->roff), o_scale = append(scale_bits),
-                 o_ext = append(p->ext), o_down = append(p->down), o_grad = append(grad);
+                 o_ext = append(p->ext), o_ext256 = append(p->ext256), o_down = append(p->down),
+                 o_grad = append(grad);
     cudaError_t e = cudaMalloc(&p->dev, blob.size() * sizeof(int));
     if (e != cudaSuccess) {
         delete p;
@@ -508,6 +598,7 @@ mlora_status mlora_plan_create(mlora_ctx* ctx, int32_t num_jobs, const int64_t* 
     p->d_roff = base + o_roff;
     p->d_scale = reinterpret_cast<float*>(base + o_scale);
     p->d_ext = base + o_ext;
+    p->d_ext256 = base + o_ext256;
     p->d_down = base + o_down;
     p->d_grad = base + o_grad;
     *out = p;
@@ -542,12 +633,9 @@ mlora_status mlora_linear_fwd(mlora_ctx* ctx, const mlora_plan* plan, int32_t d,
     DeviceGuard g(ctx->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int M = plan->rows, R = plan->R_pad;
-    CUtensorMap tX, tA, tW, tH, tB;
+    CUtensorMap tX, tA;
     if ((st = get_tmap(ctx, X, k, M, k, 64, 128, &tX)) != MLORA_OK) return st;
     if ((st = get_tmap(ctx, A_cat, k, R, k, 64, 64, &tA)) != MLORA_OK) return st;
-    if ((st = get_tmap(ctx, W0, k, d, k, 64, 256, &tW)) != MLORA_OK) return st;
-    if ((st = get_tmap(ctx, H, R, M, R, 64, 128, &tH)) != MLORA_OK) return st;
-    if ((st = get_tmap(ctx, B_cat, R, d, R, 64, 256, &tB)) != MLORA_OK) return st;
 
     // (1) H = s_j X A_j^T, block-diagonal, bf16
     GemmParams pd{};
@@ -568,21 +656,7 @@ mlora_status mlora_linear_fwd(mlora_ctx* ctx, const mlora_plan* plan, int32_t d,
     if (st != MLORA_OK) return st;
 
     // (2) Y = X W0^T + H B_cat^T
-    GemmParams pb{};
-    pb.M = M;
-    pb.N = d;
-    pb.num_kb = cdiv(k, kBK);
-    pb.n_mblk = plan->n_mblk;
-    pb.n_nblk = cdiv(d, 256);
-    pb.num_tiles = pb.n_mblk * pb.n_nblk;
-    pb.out = Y;
-    pb.ldo = d;
-    pb.ext_tab = plan->d_ext;
-    pb.seg = plan->d_seg;
-    pb.roff = plan->d_roff;
-    pb.scale = plan->d_scale;
-    pb.num_jobs = plan->J;
-    return launch_gemm<MODE_BASE, 256, kBaseStages, false, false>(ctx, tX, tW, tH, tB, pb, 1, s);
+    return run_base<false>(ctx, plan, X, k, k, W0, H, B_cat, R, d, Y, s);
 }
 
 mlora_status mlora_linear_bwd(mlora_ctx* ctx, const mlora_plan* plan, int32_t d, int32_t k,
@@ -620,25 +694,7 @@ mlora_status mlora_linear_bwd(mlora_ctx* ctx, const mlora_plan* plan, int32_t d,
 
     // (2) dX = dY W0 + G A_cat   (W0 and A_cat as MN-major B operands)
     if (dX) {
-        CUtensorMap tWmn, tG128, tAmn;
-        if ((st = get_tmap(ctx, W0, k, d, k, 64, 64, &tWmn)) != MLORA_OK) return st;
-        if ((st = get_tmap(ctx, G, R, M, R, 64, 128, &tG128)) != MLORA_OK) return st;
-        if ((st = get_tmap(ctx, A_cat, k, R, k, 64, 64, &tAmn)) != MLORA_OK) return st;
-        GemmParams pb{};
-        pb.M = M;
-        pb.N = k;
-        pb.num_kb = cdiv(d, kBK);
-        pb.n_mblk = plan->n_mblk;
-        pb.n_nblk = cdiv(k, 256);
-        pb.num_tiles = pb.n_mblk * pb.n_nblk;
-        pb.out = dX;
-        pb.ldo = k;
-        pb.ext_tab = plan->d_ext;
-        pb.seg = plan->d_seg;
-        pb.roff = plan->d_roff;
-        pb.scale = plan->d_scale;
-        pb.num_jobs = plan->J;
-        st = launch_gemm<MODE_BASE, 256, kBaseStages, false, true>(ctx, tdY128, tWmn, tG128, tAmn, pb, 1, s);
+        st = run_base<true>(ctx, plan, dY, d, d, W0, G, A_cat, R, k, dX, s);
         if (st != MLORA_OK) return st;
     }
     // (3) dA_cat = G^T X over each chunk's token range  (stored R_pad x k)

@@ -376,4 +376,198 @@ mlora_gemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constan
     }
 }
 
+// ============================================================================
+// MODE_BASE on a CTA pair (cta_group::2): one 256 x 256 output tile per
+// cluster, UMMA M=256 N=256.  CTA r of the pair stages A rows [m0+128r, +128)
+// and B rows [n0+128r, +128) (half of the N tile) in its own smem; the leader
+// CTA issues every tcgen05.mma for the pair, each CTA's TMEM holds its own 128
+// accumulator rows.  Per SM this halves the B-operand TMA/L2 traffic of the
+// 1-CTA kernel (32 KB per 64-deep k-block instead of 48 KB) and leaves room for
+// a 6-stage ring, i.e. ~2.5k cycles of load lookahead.
+// ============================================================================
+constexpr int kPairBM = 256;
+constexpr int kPairBN = 256;
+
+template <int STAGES>
+struct PairSmem {
+    static constexpr int kABytes = 128 * kBK * 2;   // this CTA's A rows
+    static constexpr int kBBytes = 128 * kBK * 2;   // this CTA's half of the B tile
+    static constexpr int kStageBytes = kABytes + kBBytes;
+    static constexpr int kBarOffset = STAGES * kStageBytes;
+    static constexpr int kBytes = kBarOffset + (2 * STAGES + 4) * 8 + 16;
+    static constexpr int kDynBytes = kBytes + 1024;
+};
+
+template <int STAGES, bool B_MN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
+mlora_base_pair_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmB0,
+                       const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1,
+                       const GemmParams p) {
+    using namespace sm100;
+    using L = PairSmem<STAGES>;
+    constexpr uint32_t kTmemCols = 512;  // 2 x 256 fp32 accumulator columns
+    constexpr uint32_t kIdesc = idesc_bf16_f32(kPairBM, kPairBN, false, B_MN);
+
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw_addr = smem_u32(smem_raw);
+    const uint32_t base_addr = (raw_addr + 1023u) & ~1023u;
+    uint8_t* smem = smem_raw + (base_addr - raw_addr);
+    uint64_t* full_bar = reinterpret_cast<uint64_t*>(smem + L::kBarOffset);
+    uint64_t* empty_bar = full_bar + STAGES;
+    uint64_t* tfull_bar = empty_bar + STAGES;
+    uint64_t* tempty_bar = tfull_bar + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+
+    const uint32_t warp = warp_id();
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t cta = cluster_ctarank();
+    const bool leader = cta == 0;
+    const int cluster_id = blockIdx.x >> 1;
+    const int nclusters = gridDim.x >> 1;
+
+    if (warp == 0 && elect_one()) {
+        tma_prefetch_desc(&tmA0);
+        tma_prefetch_desc(&tmB0);
+        tma_prefetch_desc(&tmA1);
+        tma_prefetch_desc(&tmB1);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(full_bar + s, 1);    // leader producer's arrive.expect_tx
+            mbar_init(empty_bar + s, 1);   // leader MMA's multicast commit
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(tfull_bar + a, 1);   // leader MMA's multicast commit
+            mbar_init(tempty_bar + a, 8);  // 4 epilogue warps x 2 CTAs (leader copy used)
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) {
+        tmem_alloc_2cta(tmem_slot, kTmemCols);
+        tmem_relinquish_2cta();
+    }
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------ TMA producer (both CTAs)
+        if (elect_one()) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = cluster_id; t < p.num_tiles; t += nclusters) {
+                const int mb = t % p.n_mblk;
+                const int nb = t / p.n_mblk;
+                const int m0 = mb * kPairBM + static_cast<int>(cta) * 128;
+                const int n0 = nb * kPairBN + static_cast<int>(cta) * 128;
+                const int xb0 = __ldg(p.ext_tab + 2 * mb), xb1 = __ldg(p.ext_tab + 2 * mb + 1);
+                const int nmain = p.num_kb;
+                const int nk = nmain + (xb1 - xb0);
+                for (int it = 0; it < nk; ++it) {
+                    mbar_wait(empty_bar + stage, phase ^ 1u);
+                    const bool ext = it >= nmain;
+                    const CUtensorMap* mA = ext ? &tmA1 : &tmA0;
+                    const CUtensorMap* mB = ext ? &tmB1 : &tmB0;
+                    const int kc = (ext ? (xb0 + it - nmain) : it) * kBK;
+                    const uint32_t sA = base_addr + stage * L::kStageBytes;
+                    const uint32_t sB = sA + L::kABytes;
+                    const uint32_t lbar = smem_u32(full_bar + stage) & kPeerBitMask;
+                    if (leader) mbar_arrive_expect_tx(full_bar + stage, 2 * L::kStageBytes);
+                    tma_load_2d_2sm(sA, mA, lbar, kc, m0);
+                    if constexpr (!B_MN) {
+                        tma_load_2d_2sm(sB, mB, lbar, kc, n0);
+                    } else {
+                        tma_load_2d_2sm(sB, mB, lbar, n0, kc);
+                        tma_load_2d_2sm(sB + 8192, mB, lbar, n0 + 64, kc);
+                    }
+                    if (++stage == STAGES) { stage = 0; phase ^= 1u; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------ MMA issuer (leader CTA only)
+        if (leader) {
+            int stage = 0;
+            uint32_t phase = 0;
+            int local = 0;
+            for (int t = cluster_id; t < p.num_tiles; t += nclusters, ++local) {
+                const int mb = t % p.n_mblk;
+                const int nk = p.num_kb + (__ldg(p.ext_tab + 2 * mb + 1) - __ldg(p.ext_tab + 2 * mb));
+                const int acc = local & 1;
+                const uint32_t use = static_cast<uint32_t>(local >> 1);
+                mbar_wait(tempty_bar + acc, (use & 1u) ^ 1u);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * kPairBN;
+                for (int it = 0; it < nk; ++it) {
+                    mbar_wait(full_bar + stage, phase);
+                    tc_fence_after();
+                    if (elect_one()) {
+                        const uint32_t sA = base_addr + stage * L::kStageBytes;
+                        const uint32_t sB = sA + L::kABytes;
+#pragma unroll
+                        for (int j = 0; j < kBK / kUmmaK; ++j) {
+                            const uint64_t ad = sdesc_sw128(sA + j * 32, 16, 1024);
+                            const uint64_t bd = B_MN ? sdesc_sw128(sB + j * 2048, 8192, 1024)
+                                                     : sdesc_sw128(sB + j * 32, 16, 1024);
+                            mma_bf16_2cta(d_tmem, ad, bd, kIdesc, (it | j) != 0 ? 1u : 0u);
+                        }
+                        tc_commit_2cta_mc(empty_bar + stage, 0x3);
+                    }
+                    __syncwarp();
+                    if (++stage == STAGES) { stage = 0; phase ^= 1u; }
+                }
+                if (elect_one()) tc_commit_2cta_mc(tfull_bar + acc, 0x3);
+                __syncwarp();
+            }
+        }
+    } else {
+        // ------------------------------------------------ epilogue (warps 2..5, both CTAs)
+        const uint32_t q = warp & 3;
+        const int rloc = static_cast<int>(cta * 128 + q * 32 + lane);
+        __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out);
+        int local = 0;
+        for (int t = cluster_id; t < p.num_tiles; t += nclusters, ++local) {
+            const int mb = t % p.n_mblk;
+            const int nb = t / p.n_mblk;
+            const int acc = local & 1;
+            const uint32_t use = static_cast<uint32_t>(local >> 1);
+            mbar_wait(tfull_bar + acc, use & 1u);
+            tc_fence_after();
+            const uint32_t t_row = tmem_base + ((q * 32u) << 16) + acc * kPairBN;
+            const int row = mb * kPairBM + rloc;
+            const bool row_ok = row < p.M;
+#pragma unroll 1
+            for (int c = 0; c < kPairBN / 32; ++c) {
+                uint32_t v[32];
+                tmem_ld32(t_row + c * 32, v);
+                tmem_wait_ld();
+                const int col = nb * kPairBN + c * 32;
+                if (row_ok && col < p.N) {
+                    uint4* dst = reinterpret_cast<uint4*>(out + (long long)row * p.ldo + col);
+#pragma unroll
+                    for (int g = 0; g < 4; ++g) {
+                        if (col + 8 * g + 8 <= p.N) {
+                            uint4 w;
+                            w.x = pack_bf16x2(__uint_as_float(v[8 * g + 0]), __uint_as_float(v[8 * g + 1]));
+                            w.y = pack_bf16x2(__uint_as_float(v[8 * g + 2]), __uint_as_float(v[8 * g + 3]));
+                            w.z = pack_bf16x2(__uint_as_float(v[8 * g + 4]), __uint_as_float(v[8 * g + 5]));
+                            w.w = pack_bf16x2(__uint_as_float(v[8 * g + 6]), __uint_as_float(v[8 * g + 7]));
+                            dst[g] = w;
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(tempty_bar + acc), 0));
+        }
+    }
+
+    __syncthreads();
+    cluster_sync();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc_2cta(tmem_base, kTmemCols);
+    }
+}
+
 }  // namespace mlora
