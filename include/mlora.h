@@ -169,6 +169,18 @@ mlora_status mlora_adam_step(mlora_ctx* ctx, const mlora_plan* plan, const mlora
                              int32_t num_groups, const float* lr, const int32_t* step, float beta1,
                              float beta2, float eps, float weight_decay, void* stream);
 
+/* ---------------------------------------------------------------- fp64 path
+ * Device fp64 GEMM with the reference's exact per-element operation order
+ * (lora.cpp:19-34: k ascending, a_ik == 0 terms skipped, product and sum
+ * rounded separately), so results are bitwise equal to fusim::matmul.
+ * C[M,N] = op(A)[M,K] op(B)[K,N]; op(A)(i,k) = transA ? A[k*lda+i] : A[i*lda+k].
+ * All pointers device fp64.  Used by the fusim::* C++ façade (fp64 API). */
+mlora_status mlora_f64_gemm(int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, int32_t transA,
+                            const double* B, int64_t ldb, int32_t transB, double* C, int64_t ldc,
+                            void* stream);
+/* c = a + b elementwise (lora.cpp:36-42), device fp64. */
+mlora_status mlora_f64_add(int64_t n, const double* a, const double* b, double* c, void* stream);
+
 /* Per-job synthetic layer loss L_j = 1/2 sum_p sum_{t in job j} ||Y_p[t]||^2 over
  * `num_tensors` bf16 tensors Y[p] (rows x cols[p]); loss: device fp32 [J].
  * Deterministic (fixed-order two-level reduction).  Used by the trainer step:

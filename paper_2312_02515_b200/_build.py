@@ -57,15 +57,25 @@ def build_facade(force: bool = False) -> str | None:
     deps = srcs + [LIB_MLORA] + ([os.path.join(fdir, h) for h in os.listdir(fdir)] if os.path.isdir(fdir) else [])
     if not force and _newer(LIB_FACADE, deps):
         return LIB_FACADE
-    cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-I", inc, "-o", LIB_FACADE, *srcs,
-           "-L", PKG, "-lmlora", "-Wl,-rpath,$ORIGIN"]
+    cuda = os.path.dirname(os.path.dirname(NVCC))
+    cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-I", inc, "-I", os.path.join(cuda, "include"),
+           "-o", LIB_FACADE, *srcs, "-L", PKG, "-lmlora", "-Wl,-rpath,$ORIGIN",
+           "-L", os.path.join(cuda, "lib64"), "-lcudart_static", "-ldl", "-lrt", "-lpthread"]
     _run(cmd)
     return LIB_FACADE
+
+
+def build_cpp_tests() -> None:
+    """The reference's own unit suites compiled against the façade (needs /root/reference)."""
+    script = os.path.join(ROOT, "tests", "cpp", "build.sh")
+    if os.path.exists(script):
+        _run(["bash", script])
 
 
 def build_all(force: bool = False) -> None:
     build_mlora(force)
     build_facade(force)
+    build_cpp_tests()
 
 
 if __name__ == "__main__":
