@@ -10,9 +10,15 @@ REF="${REF:-/root/reference/proj/tests}"
 PKG="$ROOT/paper_2312_02515_b200"
 OUT="$HERE/build"
 mkdir -p "$OUT"
-[ -d "$REF" ] || { echo "reference tests not present ($REF); using prebuilt binaries" >&2; exit 0; }
+if [ -d "$REF" ]; then
 for t in test_lora test_batch_select test_workload; do
   g++ -std=c++20 -O1 -I "$HERE" -I "$ROOT/include" -o "$OUT/$t" "$REF/$t.cpp" "$HERE/main.cpp" \
       -L "$PKG" -lfusim_b200 -lmlora -Wl,-rpath,"$PKG"
 done
+else
+  echo "reference tests not present ($REF); reference suites not rebuilt" >&2
+fi
+# façade-only driver (no reference sources needed)
+g++ -std=c++20 -O1 -I "$ROOT/include" -o "$OUT/facade_forward_io" "$HERE/facade_forward_io.cpp" \
+    -L "$PKG" -lfusim_b200 -lmlora -Wl,-rpath,"$PKG"
 echo "built: $(ls "$OUT")"

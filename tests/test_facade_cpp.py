@@ -43,6 +43,35 @@ def test_reference_workload_suite_on_facade():
 
 
 @pytest.mark.gpu
+def test_facade_fused_forward_bitwise_equals_reference_gpu():
+    """fusim::fused_forward on the façade (device fp64, reference operation
+    order) reproduces the reference's own outputs (tests/golden/, produced by
+    the reference sources) BIT FOR BIT on all 66 golden instances."""
+    import numpy as np
+
+    from oracle.golden import unpack_case
+    z = np.load(os.path.join(HERE, "golden", "lora_ref.npz"))
+    keys = [str(k) for k in z["_index_forward"]]
+    buf = [np.array([len(keys)], np.int32).tobytes()]
+    for key in keys:
+        W0, ranks, As, Bs, seqs = unpack_case(z, key)
+        d, k = W0.shape
+        buf.append(np.array([d, k, len(ranks), *ranks, len(seqs), *[j for j, _ in seqs],
+                             *[x.shape[0] for _, x in seqs]], np.int32).tobytes())
+        buf += [np.ascontiguousarray(W0).tobytes(), z[key + "A_all"].tobytes(), z[key + "B_all"].tobytes(),
+                z[key + "X_all"].tobytes()]
+    r = subprocess.run([_binary("facade_forward_io")], input=b"".join(buf), capture_output=True, timeout=600)
+    assert r.returncode == 0, r.stderr.decode()
+    got = np.frombuffer(r.stdout, np.float64)
+    off = 0
+    for key in keys:
+        ref_out = z[key + "out"].ravel()
+        assert np.array_equal(got[off:off + ref_out.size].view(np.uint64), ref_out.view(np.uint64)), key
+        off += ref_out.size
+    assert off == got.size
+
+
+@pytest.mark.gpu
 def test_reference_lora_suite_on_facade_gpu():
     # all 15 cases of test_lora.cpp, including "fused forward equals per-job
     # forward on real tokens" (100 trials, < 1e-9) and the BITWISE padding-
