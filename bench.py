@@ -246,10 +246,8 @@ def main():
         layer.step(x)
     barrier()
 
-    # ---------------- device-resident timed region
+    # ---------------- device-resident timed region (headline `value`)
     sampler = ClockSampler(dev)
-    ctx.profile(reset=True)
-    ctx.set_profiling(True)
     launches0 = ctx.launches
     sampler.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -260,13 +258,27 @@ def main():
     e1.record(stream)
     barrier()
     clocks = sampler.stop()
-    ctx.set_profiling(False)
     launches = ctx.launches - launches0
-    prof = ctx.profile(reset=True)
     ms_total = max_over_ranks(e0.elapsed_time(e1))
     ms_step = ms_total / args.steps
     eff_tokens = rows * world  # δ = 0: every fused row is a real token
     value = eff_tokens * args.steps / (ms_total / 1e3)
+
+    # ---------------- per-kernel live timing: the same K steps again with every launch
+    # bracketed by CUDA events on its own stream (mlora_ctx_set_profiling).  Kept out of
+    # the headline pass because events between launches defeat the PDL prologue overlap.
+    ctx.profile(reset=True)
+    ctx.set_profiling(True)
+    barrier()
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    for _ in range(args.steps):
+        layer.step(x)
+    p1.record(stream)
+    barrier()
+    ctx.set_profiling(False)
+    prof = ctx.profile(reset=True)
+    prof_ms_total = p0.elapsed_time(p1)
 
     # ---------------- end-to-end through the public API with host buffers
     barrier()
@@ -298,6 +310,7 @@ def main():
     fpt = flops_per_token(shapes, cfg["ranks"][0])
     step_tflops = value * fpt / 1e12
     kernel_share = {k: round(v[1] / max(sum(x[1] for x in prof.values()), 1e-9), 4) for k, v in prof.items()}
+    kernel_ms_per_step = {k: round(v[1] / args.steps, 4) for k, v in prof.items()}
 
     if rank != 0:
         dist.destroy_process_group() if world > 1 else None
@@ -329,6 +342,8 @@ def main():
                      "peak_kind": ("sustained" if use_sustained else "burst") + " bf16, " + peaks["source"],
                      "launches": cnt, "avg_launch_us": 1e3 * ms / cnt if cnt else None},
         "kernel_time_share": kernel_share,
+        "kernel_ms_per_step": kernel_ms_per_step,
+        "profiled_pass_ms_per_step": prof_ms_total / args.steps,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": x_host.numel() * 2,
                 "d2h_bytes_per_step": J * 4, "ms_per_step": e2e_ms / args.steps},
         "gpu_launches": launches,

@@ -18,6 +18,8 @@ constexpr int kMaxAdamGroups = 32;
 // bytes/elem = 4 * nsplit (read) + 4 (write)
 __global__ void reduce_splits_kernel(const float4* __restrict__ part, float4* __restrict__ out,
                                      long long n4, long long stride4, int nsplit) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
          i += (long long)gridDim.x * blockDim.x) {
         float4 a = part[i];
@@ -52,6 +54,8 @@ __device__ __forceinline__ int job_of_col(const int* roff, int J, int c) {
 
 // A_cat (R_pad x k) then B_cat (d x R_pad), one element per thread-iteration.
 __global__ void pack_adapters_kernel(const __grid_constant__ PackArgs a) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const long long nA = (long long)a.R_pad * a.k;
     const long long nB = (long long)a.d * a.R_pad;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nA + nB;
@@ -104,6 +108,8 @@ struct AdamArgs {
 // AdamW over all groups.  bytes/param: read p,g,m,v (16) + write p,m,v (12)
 // (+2 for the bf16 operand copy) = 30 B.
 __global__ void adam_kernel(const __grid_constant__ AdamArgs a) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     for (long long i4 = blockIdx.x * (long long)blockDim.x + threadIdx.x; i4 < a.total4;
          i4 += (long long)gridDim.x * blockDim.x) {
         int gi = 0;
@@ -156,6 +162,8 @@ struct SumsqArgs {
 };
 
 __global__ void row_sumsq_kernel(const __grid_constant__ SumsqArgs a) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int warps = blockDim.x / 32;
     const int lane = threadIdx.x & 31;
     for (int row = blockIdx.x * warps + threadIdx.x / 32; row < a.rows; row += gridDim.x * warps) {
@@ -182,6 +190,8 @@ __global__ void row_sumsq_kernel(const __grid_constant__ SumsqArgs a) {
 
 __global__ void segment_loss_kernel(const float* __restrict__ row_acc, const int* __restrict__ seg,
                                     float* __restrict__ loss) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     __shared__ float red[32];
     const int j = blockIdx.x;
     const int r0 = seg[j], r1 = seg[j + 1];

@@ -18,6 +18,7 @@
 #include <mutex>
 #include <string>
 #include <tuple>
+#include <utility>
 #include <vector>
 
 #include "../../include/mlora.h"
@@ -155,6 +156,42 @@ mlora_status ensure_workspace(mlora_ctx* ctx, size_t bytes) {
     return MLORA_OK;
 }
 
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("MLORA_PDL");
+        return !(e && std::string(e) == "0");
+    }();
+    return on;
+}
+
+// Every kernel goes through cudaLaunchKernelEx with programmatic stream
+// serialisation (PDL): the next kernel's prologue overlaps this one's tail; the
+// kernels themselves griddepcontrol.wait before their first global access.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                     unsigned cluster_x, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[2];
+    unsigned n = 0;
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    ++n;
+    if (cluster_x > 1) {
+        attr[n].id = cudaLaunchAttributeClusterDimension;
+        attr[n].val.clusterDim.x = cluster_x;
+        attr[n].val.clusterDim.y = 1;
+        attr[n].val.clusterDim.z = 1;
+        ++n;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = n;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 cudaEvent_t pool_event(mlora_ctx* ctx) {
     if (!ctx->event_pool.empty()) {
         cudaEvent_t e = ctx->event_pool.back();
@@ -203,8 +240,7 @@ mlora_status launch_gemm(mlora_ctx* ctx, const CUtensorMap& a0, const CUtensorMa
     }
     const int grid = std::min(p.num_tiles, ctx->num_sms * ctas_per_sm);
     ProfScope ps(ctx, MODE == MODE_BASE ? (B_MN ? 1 : 0) : MODE == MODE_DOWN ? 2 : 3, stream);
-    kern<<<grid, kNumThreads, L::kDynBytes, stream>>>(a0, b0, a1, b1, p);
-    MLORA_CUDA_TRY(ctx, cudaGetLastError());
+    MLORA_CUDA_TRY(ctx, launch_k(kern, dim3(grid), dim3(kNumThreads), L::kDynBytes, stream, 1, a0, b0, a1, b1, p));
     ++ctx->launches;
     return MLORA_OK;
 }
@@ -234,8 +270,8 @@ mlora_status launch_base_pair(mlora_ctx* ctx, const CUtensorMap& a0, const CUten
     }
     const int clusters = std::min(p.num_tiles, ctx->num_sms / 2);
     ProfScope ps(ctx, B_MN ? 1 : 0, stream);
-    kern<<<2 * clusters, kNumThreads, L::kDynBytes, stream>>>(a0, b0, a1, b1, p);
-    MLORA_CUDA_TRY(ctx, cudaGetLastError());
+    MLORA_CUDA_TRY(ctx, launch_k(kern, dim3(2 * clusters), dim3(kNumThreads), L::kDynBytes, stream, 1, a0, b0,
+                                 a1, b1, p));
     ++ctx->launches;
     return MLORA_OK;
 }
@@ -283,6 +319,36 @@ mlora_status run_base(mlora_ctx* ctx, const mlora_plan* plan, const void* A0, in
     pb.num_tiles = pb.n_mblk * pb.n_nblk;
     pb.ext_tab = plan->d_ext;
     return launch_gemm<MODE_BASE, 256, kBaseStages, false, B_MN>(ctx, tA0, tB0, tA1, tB1, pb, 1, s);
+}
+
+constexpr int kDownStages = 6;
+
+// MODE_DOWN with the K range split across a CTA pair (cluster of 2, DSMEM reduce).
+template <bool B_MN>
+mlora_status launch_down_ksplit(mlora_ctx* ctx, const CUtensorMap& a0, const CUtensorMap& b0,
+                                const GemmParams& p, cudaStream_t stream) {
+    if (p.num_tiles <= 0) return MLORA_OK;
+    using L = GemmSmem<64, kDownStages, 2>;
+    auto kern = mlora_gemm_kernel<MODE_DOWN, 64, kDownStages, false, B_MN, 2>;
+    static bool attr_done = false;
+    if (!attr_done) {
+        MLORA_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 L::kDynBytes));
+        attr_done = true;
+    }
+    ProfScope ps(ctx, 2, stream);
+    MLORA_CUDA_TRY(ctx, launch_k(kern, dim3(2 * std::min(p.num_tiles, ctx->num_sms / 2)), dim3(kNumThreads),
+                                 L::kDynBytes, stream, 2, a0, b0, a0, b0, p));
+    ++ctx->launches;
+    return MLORA_OK;
+}
+
+bool use_down_ksplit() {
+    static const bool on = [] {
+        const char* e = std::getenv("MLORA_DOWN_KERNEL");
+        return !(e && std::string(e) == "single");
+    }();
+    return on;
 }
 
 mlora_status check_dims(mlora_ctx* ctx, const mlora_plan* plan, int d, int k) {
@@ -339,9 +405,9 @@ mlora_status run_grad(mlora_ctx* ctx, const mlora_plan* plan, const CUtensorMap&
         const int threads = 256;
         const int blocks = static_cast<int>(std::min<long long>(cdiv(n4, threads), 4LL * ctx->num_sms));
         ProfScope ps(ctx, 4, stream);
-        reduce_splits_kernel<<<blocks, threads, 0, stream>>>(reinterpret_cast<const float4*>(target),
-                                                             reinterpret_cast<float4*>(out), n4, n4, ns);
-        MLORA_CUDA_TRY(ctx, cudaGetLastError());
+        MLORA_CUDA_TRY(ctx, launch_k(reduce_splits_kernel, dim3(blocks), dim3(threads), 0, stream, 1,
+                                     reinterpret_cast<const float4*>(target), reinterpret_cast<float4*>(out), n4,
+                                     n4, ns));
         ++ctx->launches;
     }
     return MLORA_OK;
@@ -652,7 +718,8 @@ mlora_status mlora_linear_fwd(mlora_ctx* ctx, const mlora_plan* plan, int32_t d,
     pd.roff = plan->d_roff;
     pd.scale = plan->d_scale;
     pd.num_jobs = plan->J;
-    st = launch_gemm<MODE_DOWN, 64, kSmallStages, false, false>(ctx, tX, tA, tX, tA, pd, 2, s);
+    st = use_down_ksplit() ? launch_down_ksplit<false>(ctx, tX, tA, pd, s)
+                           : launch_gemm<MODE_DOWN, 64, kSmallStages, false, false>(ctx, tX, tA, tX, tA, pd, 2, s);
     if (st != MLORA_OK) return st;
 
     // (2) Y = X W0^T + H B_cat^T
@@ -689,7 +756,8 @@ mlora_status mlora_linear_bwd(mlora_ctx* ctx, const mlora_plan* plan, int32_t d,
     pd.roff = plan->d_roff;
     pd.scale = plan->d_scale;
     pd.num_jobs = plan->J;
-    st = launch_gemm<MODE_DOWN, 64, kSmallStages, false, true>(ctx, tdY128, tBmn, tdY128, tBmn, pd, 2, s);
+    st = use_down_ksplit() ? launch_down_ksplit<true>(ctx, tdY128, tBmn, pd, s)
+                           : launch_gemm<MODE_DOWN, 64, kSmallStages, false, true>(ctx, tdY128, tBmn, tdY128, tBmn, pd, 2, s);
     if (st != MLORA_OK) return st;
 
     // (2) dX = dY W0 + G A_cat   (W0 and A_cat as MN-major B operands)
@@ -746,8 +814,8 @@ mlora_status mlora_pack_adapters(mlora_ctx* ctx, const mlora_plan* plan, int32_t
     const long long n = (long long)plan->R_pad * k + (long long)d * plan->R_pad;
     const int blocks = static_cast<int>(std::min<long long>(cdiv(n, 256), 8LL * ctx->num_sms));
     ProfScope ps(ctx, 4, static_cast<cudaStream_t>(stream));
-    pack_adapters_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
-    MLORA_CUDA_TRY(ctx, cudaGetLastError());
+    MLORA_CUDA_TRY(ctx, launch_k(pack_adapters_kernel, dim3(blocks), dim3(256), 0,
+                                 static_cast<cudaStream_t>(stream), 1, a));
     ++ctx->launches;
     return MLORA_OK;
 }
@@ -792,8 +860,8 @@ mlora_status mlora_adam_step(mlora_ctx* ctx, const mlora_plan* plan, const mlora
         if (start4 == 0) continue;
         const int blocks = static_cast<int>(std::min<long long>(cdiv(start4, 256), 8LL * ctx->num_sms));
         ProfScope ps(ctx, 5, static_cast<cudaStream_t>(stream));
-        adam_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
-        MLORA_CUDA_TRY(ctx, cudaGetLastError());
+        MLORA_CUDA_TRY(ctx, launch_k(adam_kernel, dim3(blocks), dim3(256), 0, static_cast<cudaStream_t>(stream), 1,
+                                     a));
         ++ctx->launches;
     }
     return MLORA_OK;
@@ -820,10 +888,9 @@ mlora_status mlora_segment_sumsq_loss(mlora_ctx* ctx, const mlora_plan* plan, co
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int blocks = std::min(cdiv(plan->rows, 8), 8 * ctx->num_sms);
     ProfScope ps(ctx, 4, s);
-    row_sumsq_kernel<<<blocks, 256, 0, s>>>(a);
-    MLORA_CUDA_TRY(ctx, cudaGetLastError());
-    segment_loss_kernel<<<plan->J, 1024, 0, s>>>(a.row_acc, plan->d_seg, loss);
-    MLORA_CUDA_TRY(ctx, cudaGetLastError());
+    MLORA_CUDA_TRY(ctx, launch_k(row_sumsq_kernel, dim3(blocks), dim3(256), 0, s, 1, a));
+    MLORA_CUDA_TRY(ctx, launch_k(segment_loss_kernel, dim3(plan->J), dim3(1024), 0, s, 1,
+                                 static_cast<const float*>(a.row_acc), static_cast<const int*>(plan->d_seg), loss));
     ctx->launches += 2;
     return MLORA_OK;
 }

@@ -97,14 +97,17 @@ __device__ __forceinline__ TileInfo decode_tile(const GemmParams& p, int t) {
     return ti;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int KSPLIT = 1>
 struct GemmSmem {
     static constexpr int kABytes = kBM * kBK * 2;
     static constexpr int kBBytes = BN * kBK * 2;
     static constexpr int kStageBytes = kABytes + kBBytes;
-    static constexpr int kBarOffset = STAGES * kStageBytes;
-    // full[S], empty[S], tmem_full[2], tmem_empty[2], tmem base slot
-    static constexpr int kBytes = kBarOffset + (2 * STAGES + 4) * 8 + 16;
+    // K-split across a CTA pair: the follower's fp32 partial tile lands here (DSMEM)
+    static constexpr int kPartOffset = STAGES * kStageBytes;
+    static constexpr int kPartBytes = KSPLIT == 2 ? kBM * BN * 4 : 0;
+    static constexpr int kBarOffset = kPartOffset + kPartBytes;
+    // full[S], empty[S], tmem_full[2], tmem_empty[2], part_full, part_empty, tmem base slot
+    static constexpr int kBytes = kBarOffset + (2 * STAGES + 6) * 8 + 16;
     static constexpr int kDynBytes = kBytes + 1024;  // manual 1 KB alignment slack
 };
 
@@ -118,13 +121,19 @@ __device__ __forceinline__ int job_of_row(const int* seg, int num_jobs, int row)
     return lo;
 }
 
-template <int MODE, int BN, int STAGES, bool A_MN, bool B_MN>
+// KSPLIT = 2 (MODE_DOWN): launched in clusters of 2; CTA r of the pair reduces
+// the r-th half of the K range into its own TMEM, the follower ships its fp32
+// partial tile to the leader's smem over DSMEM and the leader adds it in a fixed
+// order (deterministic) before the masked/scaled store.  Doubles the CTAs that
+// stream the HBM-bound operand and halves the bytes each must keep in flight.
+template <int MODE, int BN, int STAGES, bool A_MN, bool B_MN, int KSPLIT = 1>
 __global__ void __launch_bounds__(kNumThreads, 1)
 mlora_gemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmB0,
                   const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1,
                   const GemmParams p) {
     using namespace sm100;
-    using L = GemmSmem<BN, STAGES>;
+    using L = GemmSmem<BN, STAGES, KSPLIT>;
+    static_assert(KSPLIT == 1 || (KSPLIT == 2 && MODE == MODE_DOWN && BN == 64), "K split: DOWN, BN=64 only");
     static_assert(BN % 64 == 0 && BN >= 64 && BN <= 256, "BN must be a multiple of 64 in [64,256]");
     constexpr uint32_t kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
                                  : (2 * BN <= 256) ? 256 : 512;
@@ -138,10 +147,24 @@ mlora_gemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constan
     uint64_t* empty_bar = full_bar + STAGES;
     uint64_t* tfull_bar = empty_bar + STAGES;
     uint64_t* tempty_bar = tfull_bar + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty_bar + 2);
+    uint64_t* pfull_bar = tempty_bar + 2;
+    uint64_t* pempty_bar = pfull_bar + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pempty_bar + 1);
 
     const uint32_t warp = warp_id();
     const uint32_t lane = threadIdx.x & 31;
+    const uint32_t krank = KSPLIT == 2 ? cluster_ctarank() : 0u;
+    const int t_first = static_cast<int>(blockIdx.x) / KSPLIT;
+    const int t_step = static_cast<int>(gridDim.x) / KSPLIT;
+    // this CTA's tile program: for a K-split pair, its half of the main k-blocks
+    auto tile_of = [&](int t) {
+        TileInfo ti = decode_tile<MODE, BN>(p, t);
+        if constexpr (KSPLIT == 2) {
+            const int mid = ti.kb0 + (ti.kb1 - ti.kb0) / 2;
+            if (krank == 0) ti.kb1 = mid; else ti.kb0 = mid;
+        }
+        return ti;
+    };
 
     if (warp == 0 && elect_one()) {
         tma_prefetch_desc(&tmA0);
@@ -158,6 +181,8 @@ mlora_gemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constan
             mbar_init(tfull_bar + a, 1);
             mbar_init(tempty_bar + a, 128);
         }
+        mbar_init(pfull_bar, 4);   // follower's 4 epilogue warps (K split)
+        mbar_init(pempty_bar, 4);  // leader's 4 epilogue warps (K split)
         fence_barrier_init();
     }
     if (warp == 1) {
@@ -165,17 +190,19 @@ mlora_gemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constan
         tmem_relinquish();
     }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (KSPLIT == 2) cluster_sync(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    griddep_launch_dependents();
+    griddep_wait();  // predecessor's results visible; everything above overlapped its tail
 
     if (warp == 0) {
         // ------------------------------------------------ TMA producer
         if (elect_one()) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-                const TileInfo ti = decode_tile<MODE, BN>(p, t);
+            for (int t = t_first; t < p.num_tiles; t += t_step) {
+                const TileInfo ti = tile_of(t);
                 const int nmain = ti.kb1 - ti.kb0;
                 const int nk = nmain + (ti.xb1 - ti.xb0);
                 for (int it = 0; it < nk; ++it) {
@@ -211,8 +238,8 @@ mlora_gemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constan
         int stage = 0;
         uint32_t phase = 0;
         int local = 0;
-        for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++local) {
-            const TileInfo ti = decode_tile<MODE, BN>(p, t);
+        for (int t = t_first; t < p.num_tiles; t += t_step, ++local) {
+            const TileInfo ti = tile_of(t);
             const int nk = (ti.kb1 - ti.kb0) + (ti.xb1 - ti.xb0);
             const int acc = local & 1;
             const uint32_t use = static_cast<uint32_t>(local >> 1);
@@ -246,8 +273,8 @@ mlora_gemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constan
         const uint32_t q = warp & 3;  // TMEM lane quarter this warp may access
         const int rloc = static_cast<int>(q * 32 + lane);
         int local = 0;
-        for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x, ++local) {
-            const TileInfo ti = decode_tile<MODE, BN>(p, t);
+        for (int t = t_first; t < p.num_tiles; t += t_step, ++local) {
+            const TileInfo ti = tile_of(t);
             const bool empty = (ti.kb1 - ti.kb0) + (ti.xb1 - ti.xb0) == 0;
             const int acc = local & 1;
             const uint32_t use = static_cast<uint32_t>(local >> 1);
@@ -282,50 +309,73 @@ mlora_gemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constan
                 }
             } else if constexpr (MODE == MODE_DOWN) {
                 __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out);
-                int jr = 0, c_lo = 0, c_hi = 0;
-                float s = 0.f;
-                if (row_ok) {
-                    jr = job_of_row(p.seg, p.num_jobs, row);
-                    c_lo = __ldg(p.roff + jr);
-                    c_hi = __ldg(p.roff + jr + 1);
-                    s = __ldg(p.scale + jr);
-                }
-#pragma unroll 1
+                float accv[BN];
+#pragma unroll
                 for (int c = 0; c < BN / 32; ++c) {
                     uint32_t v[32];
-                    tmem_ld32(t_row + c * 32, v);
-                    tmem_wait_ld();
-                    const int col = ti.n0 + c * 32;
-                    if (row_ok) {
-                        uint4* dst = reinterpret_cast<uint4*>(out + (long long)row * p.ldo + col);
+                    if (!empty) { tmem_ld32(t_row + c * 32, v); tmem_wait_ld(); }
 #pragma unroll
-                        for (int g = 0; g < 4; ++g) {
-                            if (col + 8 * g + 8 > p.N) break;
-                            float f[8];
+                    for (int e = 0; e < 32; ++e) accv[c * 32 + e] = empty ? 0.f : __uint_as_float(v[e]);
+                }
+                bool store = true;
+                if constexpr (KSPLIT == 2) {
+                    // partial tile layout [BN/4][128 rows][4]: a warp moves 512 contiguous bytes per float4
+                    float4* part = reinterpret_cast<float4*>(smem + L::kPartOffset);
+                    if (krank == 1) {
+                        mbar_wait(pempty_bar, (static_cast<uint32_t>(local) & 1u) ^ 1u);
 #pragma unroll
-                            for (int e = 0; e < 8; ++e) {
-                                const int cc = col + 8 * g + e;
-                                f[e] = (cc >= c_lo && cc < c_hi) ? s * __uint_as_float(v[8 * g + e]) : 0.f;
-                            }
-                            uint4 w;
-                            w.x = pack_bf16x2(f[0], f[1]);
-                            w.y = pack_bf16x2(f[2], f[3]);
-                            w.z = pack_bf16x2(f[4], f[5]);
-                            w.w = pack_bf16x2(f[6], f[7]);
-                            dst[g] = w;
+                        for (int g = 0; g < BN / 4; ++g)
+                            st_cluster_v4(mapa_shared(smem_u32(part + g * kBM + rloc), 0),
+                                          make_float4(accv[4 * g], accv[4 * g + 1], accv[4 * g + 2], accv[4 * g + 3]));
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(pfull_bar), 0));
+                        store = false;
+                    } else {
+                        mbar_wait_cluster(pfull_bar, static_cast<uint32_t>(local) & 1u);
+#pragma unroll
+                        for (int g = 0; g < BN / 4; ++g) {
+                            const float4 q4 = part[g * kBM + rloc];
+                            accv[4 * g] += q4.x;
+                            accv[4 * g + 1] += q4.y;
+                            accv[4 * g + 2] += q4.z;
+                            accv[4 * g + 3] += q4.w;
                         }
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(pempty_bar), 1));
                     }
                 }
-                if ((ti.aux & 1) && row_ok) {
-                    // first chunk tile of this m-block: define every other column
-                    // of the row (zero) so H/G are fully block-diagonal in HBM.
-                    const int mb = ti.m0 / kBM;
-                    const int z0 = __ldg(p.ext_tab + 2 * mb) * kBK;
-                    const int z1 = __ldg(p.ext_tab + 2 * mb + 1) * kBK;
-                    uint4* rowp = reinterpret_cast<uint4*>(out + (long long)row * p.ldo);
-                    const uint4 zero = make_uint4(0, 0, 0, 0);
-                    for (int cc = 0; cc < p.N; cc += 8)
-                        if (cc < z0 || cc >= z1) rowp[cc / 8] = zero;
+                if (store && row_ok) {
+                    const int jr = job_of_row(p.seg, p.num_jobs, row);
+                    const int c_lo = __ldg(p.roff + jr), c_hi = __ldg(p.roff + jr + 1);
+                    const float s = __ldg(p.scale + jr);
+                    uint4* dst = reinterpret_cast<uint4*>(out + (long long)row * p.ldo + ti.n0);
+#pragma unroll
+                    for (int g = 0; g < BN / 8; ++g) {
+                        if (ti.n0 + 8 * g + 8 > p.N) break;
+                        float f[8];
+#pragma unroll
+                        for (int e = 0; e < 8; ++e) {
+                            const int cc = ti.n0 + 8 * g + e;
+                            f[e] = (cc >= c_lo && cc < c_hi) ? s * accv[8 * g + e] : 0.f;
+                        }
+                        uint4 w;
+                        w.x = pack_bf16x2(f[0], f[1]);
+                        w.y = pack_bf16x2(f[2], f[3]);
+                        w.z = pack_bf16x2(f[4], f[5]);
+                        w.w = pack_bf16x2(f[6], f[7]);
+                        dst[g] = w;
+                    }
+                    if (ti.aux & 1) {
+                        // first chunk tile of this m-block: define every other column
+                        // of the row (zero) so H/G are fully block-diagonal in HBM.
+                        const int mb = ti.m0 / kBM;
+                        const int z0 = __ldg(p.ext_tab + 2 * mb) * kBK;
+                        const int z1 = __ldg(p.ext_tab + 2 * mb + 1) * kBK;
+                        uint4* rowp = reinterpret_cast<uint4*>(out + (long long)row * p.ldo);
+                        const uint4 zero = make_uint4(0, 0, 0, 0);
+                        for (int cc = 0; cc < p.N; cc += 8)
+                            if (cc < z0 || cc >= z1) rowp[cc / 8] = zero;
+                    }
                 }
             } else if constexpr (MODE == MODE_GRADT) {
                 float* out = static_cast<float*>(p.out) + (long long)ti.aux * p.split_stride;
@@ -370,6 +420,7 @@ mlora_gemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constan
     }
 
     __syncthreads();
+    if constexpr (KSPLIT == 2) cluster_sync();  // no DSMEM traffic may target an exited CTA
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc(tmem_base, kTmemCols);
@@ -448,6 +499,8 @@ mlora_base_pair_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_co
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    griddep_launch_dependents();
+    griddep_wait();  // predecessor's results visible; everything above overlapped its tail
 
     if (warp == 0) {
         // ------------------------------------------------ TMA producer (both CTAs)
