@@ -126,6 +126,18 @@ mlora_status mlora_linear_fwd(mlora_ctx* ctx, const mlora_plan* plan, int32_t d,
                               const void* X, const void* W0, const void* A_cat, const void* B_cat,
                               void* Y, void* H, void* stream);
 
+/* As mlora_linear_fwd, and (row_sq != NULL) the forward GEMM's epilogue also
+ * writes, per 256-column block nb of Y, row_sq[nb * rows + t] = sum over the
+ * block's columns of bf16(Y[t, c])^2 — the layer loss without re-reading Y.
+ * row_sq holds mlora_rowsq_blocks(d) * rows floats. */
+mlora_status mlora_linear_fwd_ex(mlora_ctx* ctx, const mlora_plan* plan, int32_t d, int32_t k,
+                                 const void* X, const void* W0, const void* A_cat, const void* B_cat,
+                                 void* Y, void* H, float* row_sq, void* stream);
+int32_t mlora_rowsq_blocks(int32_t d);
+/* loss[j] = 1/2 sum over tensors t, blocks and job j's rows of row_sq[t] (fixed order). */
+mlora_status mlora_loss_from_rowsq(mlora_ctx* ctx, const mlora_plan* plan, const float* const* row_sq,
+                                   const int32_t* d, int32_t num_tensors, float* loss, void* stream);
+
 /* Backward of mlora_linear_fwd (no reference function; pinned by composing
  * the reference primitives):
  *   G_cat = s_j dY_j B_j          (rows x R_pad, bf16 scratch, caller-owned)

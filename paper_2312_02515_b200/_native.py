@@ -51,6 +51,9 @@ _SIGS = {
     "mlora_plan_rank_padded": (i32, [vp]),
     "mlora_plan_rank_offsets": (i32, [vp, C.POINTER(i32)]),
     "mlora_linear_fwd": (i32, [vp, vp, i32, i32, vp, vp, vp, vp, vp, vp, vp]),
+    "mlora_linear_fwd_ex": (i32, [vp, vp, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "mlora_rowsq_blocks": (i32, [i32]),
+    "mlora_loss_from_rowsq": (i32, [vp, vp, C.POINTER(vp), C.POINTER(i32), i32, vp, vp]),
     "mlora_linear_bwd": (i32, [vp, vp, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "mlora_pack_adapters": (i32, [vp, vp, i32, i32, C.POINTER(vp), C.POINTER(vp), vp, vp, vp, vp, vp]),
     "mlora_segment_sumsq_loss": (i32, [vp, vp, C.POINTER(vp), C.POINTER(i32), i32, vp, vp]),

@@ -209,4 +209,26 @@ __global__ void segment_loss_kernel(const float* __restrict__ row_acc, const int
     }
 }
 
+// Per-job loss from the row partials the forward GEMM epilogue wrote:
+// loss[j] = 1/2 sum_t sum_nb sum_{rows of j} row_sq_t[nb][row], fixed order.
+struct RowSqArgs {
+    const float* part[kMaxLossTensors];
+    int nblk[kMaxLossTensors];
+    int ntensors;
+    int rows;
+};
+
+// step 1 (grid over rows, coalesced): row_acc[r] = sum_t sum_nb row_sq_t[nb][r]
+__global__ void rowsq_rows_kernel(const __grid_constant__ RowSqArgs a, float* __restrict__ row_acc) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < a.rows; r += gridDim.x * blockDim.x) {
+        float rs = 0.f;
+        for (int t = 0; t < a.ntensors; ++t)
+            for (int nb = 0; nb < a.nblk[t]; ++nb) rs += a.part[t][(long long)nb * a.rows + r];
+        row_acc[r] = rs;
+    }
+}
+// step 2: segment_loss_kernel (fixed-order per-job block sum of row_acc)
+
 }  // namespace mlora

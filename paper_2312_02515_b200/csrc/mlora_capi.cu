@@ -280,7 +280,7 @@ mlora_status launch_base_pair(mlora_ctx* ctx, const CUtensorMap& a0, const CUten
 template <bool B_MN>
 mlora_status run_base(mlora_ctx* ctx, const mlora_plan* plan, const void* A0, int64_t lda0, int K0,
                       const void* B0, const void* A1, const void* B1, int R, int N, void* out,
-                      cudaStream_t s) {
+                      cudaStream_t s, float* row_sq = nullptr) {
     const bool pair = use_pair_kernel();
     const int M = plan->rows;
     const uint32_t bbox = pair ? 128 : 256;  // K-major B rows staged per CTA
@@ -307,6 +307,8 @@ mlora_status run_base(mlora_ctx* ctx, const mlora_plan* plan, const void* A0, in
     pb.roff = plan->d_roff;
     pb.scale = plan->d_scale;
     pb.num_jobs = plan->J;
+    pb.row_sq = row_sq;
+    if (row_sq && !pair) return fail(ctx, MLORA_USAGE, "fused row sums need the CTA-pair base kernel");
     if (pair) {
         pb.n_mblk = plan->n_mblk256;
         pb.n_nblk = cdiv(N, kPairBN);
@@ -401,6 +403,7 @@ mlora_status run_grad(mlora_ctx* ctx, const mlora_plan* plan, const CUtensorMap&
     mlora_status st = launch_gemm<MODE, 64, kSmallStages, true, true>(ctx, ta, tb, ta, tb, p, 2, stream);
     if (st != MLORA_OK) return st;
     if (ns > 1) {
+        // fixed-order sum of the token-split partials (deterministic, no atomics)
         const long long n4 = nelem / 4;
         const int threads = 256;
         const int blocks = static_cast<int>(std::min<long long>(cdiv(n4, threads), 4LL * ctx->num_sms));
@@ -690,9 +693,9 @@ mlora_status mlora_plan_rank_offsets(const mlora_plan* plan, int32_t* roff_out) 
     return MLORA_OK;
 }
 
-mlora_status mlora_linear_fwd(mlora_ctx* ctx, const mlora_plan* plan, int32_t d, int32_t k,
-                              const void* X, const void* W0, const void* A_cat, const void* B_cat,
-                              void* Y, void* H, void* stream) {
+mlora_status mlora_linear_fwd_ex(mlora_ctx* ctx, const mlora_plan* plan, int32_t d, int32_t k,
+                                 const void* X, const void* W0, const void* A_cat, const void* B_cat,
+                                 void* Y, void* H, float* row_sq, void* stream) {
     mlora_status st = check_dims(ctx, plan, d, k);
     if (st != MLORA_OK) return st;
     if (!X || !W0 || !A_cat || !B_cat || !Y || !H) return fail(ctx, MLORA_USAGE, "null tensor pointer");
@@ -723,7 +726,41 @@ mlora_status mlora_linear_fwd(mlora_ctx* ctx, const mlora_plan* plan, int32_t d,
     if (st != MLORA_OK) return st;
 
     // (2) Y = X W0^T + H B_cat^T
-    return run_base<false>(ctx, plan, X, k, k, W0, H, B_cat, R, d, Y, s);
+    return run_base<false>(ctx, plan, X, k, k, W0, H, B_cat, R, d, Y, s, row_sq);
+}
+
+mlora_status mlora_linear_fwd(mlora_ctx* ctx, const mlora_plan* plan, int32_t d, int32_t k,
+                              const void* X, const void* W0, const void* A_cat, const void* B_cat,
+                              void* Y, void* H, void* stream) {
+    return mlora_linear_fwd_ex(ctx, plan, d, k, X, W0, A_cat, B_cat, Y, H, nullptr, stream);
+}
+
+int32_t mlora_rowsq_blocks(int32_t d) { return cdiv(d, kPairBN); }
+
+mlora_status mlora_loss_from_rowsq(mlora_ctx* ctx, const mlora_plan* plan, const float* const* row_sq,
+                                   const int32_t* d, int32_t num_tensors, float* loss, void* stream) {
+    if (!ctx || !plan || !row_sq || !d || !loss) return fail(ctx, MLORA_USAGE, "null argument");
+    if (num_tensors < 1 || num_tensors > kMaxLossTensors) return fail(ctx, MLORA_USAGE, "num_tensors out of range");
+    RowSqArgs a{};
+    for (int t = 0; t < num_tensors; ++t) {
+        if (!row_sq[t] || d[t] <= 0) return fail(ctx, MLORA_USAGE, "bad row-sum tensor");
+        a.part[t] = row_sq[t];
+        a.nblk[t] = cdiv(d[t], kPairBN);
+    }
+    a.ntensors = num_tensors;
+    a.rows = plan->rows;
+    DeviceGuard g(ctx->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    mlora_status st = ensure_workspace(ctx, sizeof(float) * plan->rows);
+    if (st != MLORA_OK) return st;
+    float* row_acc = static_cast<float*>(ctx->workspace);
+    ProfScope ps(ctx, 4, s);
+    MLORA_CUDA_TRY(ctx, launch_k(rowsq_rows_kernel, dim3(std::min(cdiv(plan->rows, 256), 4 * ctx->num_sms)),
+                                 dim3(256), 0, s, 1, a, row_acc));
+    MLORA_CUDA_TRY(ctx, launch_k(segment_loss_kernel, dim3(plan->J), dim3(1024), 0, s, 1,
+                                 static_cast<const float*>(row_acc), static_cast<const int*>(plan->d_seg), loss));
+    ctx->launches += 2;
+    return MLORA_OK;
 }
 
 mlora_status mlora_linear_bwd(mlora_ctx* ctx, const mlora_plan* plan, int32_t d, int32_t k,

@@ -49,6 +49,7 @@ struct GemmParams {
     const int* ext_tab;   // [n_mblk][2]  extra (LoRA) k-block range per m-block
     const int* down_tab;  // [num_tiles][3] (m_blk, chunk, flags) for MODE_DOWN
     const int* grad_tab;  // [nchunks*nsplit][2] token k-block range
+    float* row_sq;        // BASE (pair) optional: [n_nblk][M] sum over the tile's columns of bf16(Y)^2
     const int* seg;       // [J+1] row offsets of job segments
     const int* roff;      // [J+1] padded rank column offsets
     const float* scale;   // [J] per-job LoRA scale s_j
@@ -588,6 +589,7 @@ mlora_base_pair_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_co
             const uint32_t t_row = tmem_base + ((q * 32u) << 16) + acc * kPairBN;
             const int row = mb * kPairBM + rloc;
             const bool row_ok = row < p.M;
+            float sq = 0.f;  // fused loss: sum of squares of the stored (bf16-rounded) outputs
 #pragma unroll 1
             for (int c = 0; c < kPairBN / 32; ++c) {
                 uint32_t v[32];
@@ -599,16 +601,20 @@ mlora_base_pair_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_co
 #pragma unroll
                     for (int g = 0; g < 4; ++g) {
                         if (col + 8 * g + 8 <= p.N) {
-                            uint4 w;
-                            w.x = pack_bf16x2(__uint_as_float(v[8 * g + 0]), __uint_as_float(v[8 * g + 1]));
-                            w.y = pack_bf16x2(__uint_as_float(v[8 * g + 2]), __uint_as_float(v[8 * g + 3]));
-                            w.z = pack_bf16x2(__uint_as_float(v[8 * g + 4]), __uint_as_float(v[8 * g + 5]));
-                            w.w = pack_bf16x2(__uint_as_float(v[8 * g + 6]), __uint_as_float(v[8 * g + 7]));
-                            dst[g] = w;
+                            uint32_t w[4];
+#pragma unroll
+                            for (int h = 0; h < 4; ++h) {
+                                w[h] = pack_bf16x2(__uint_as_float(v[8 * g + 2 * h]), __uint_as_float(v[8 * g + 2 * h + 1]));
+                                const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[h]));
+                                sq = fmaf(f.x, f.x, sq);
+                                sq = fmaf(f.y, f.y, sq);
+                            }
+                            dst[g] = make_uint4(w[0], w[1], w[2], w[3]);
                         }
                     }
                 }
             }
+            if (p.row_sq && row_ok) p.row_sq[(long long)nb * p.M + row] = sq;
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(tempty_bar + acc), 0));

@@ -142,8 +142,10 @@ class Plan:
 
 def linear_fwd(ctx: Context, plan: Plan, X: torch.Tensor, W0: torch.Tensor, A_cat: torch.Tensor,
                B_cat: torch.Tensor, Y: torch.Tensor | None = None, H: torch.Tensor | None = None,
-               stream=None):
-    """Y = X W0^T + s_j (X_j A_j^T) B_j^T on packed rows; returns (Y, H)."""
+               row_sq: torch.Tensor | None = None, stream=None):
+    """Y = X W0^T + s_j (X_j A_j^T) B_j^T on packed rows; returns (Y, H).
+    row_sq (optional, fp32 [mlora_rowsq_blocks(d), rows]) receives the fused
+    per-row sums of squares of Y from the GEMM epilogue."""
     d, k = W0.shape
     M, R = plan.rows, plan.rank_padded
     _require_cuda(X, "X", torch.bfloat16, (M, k))
@@ -156,8 +158,11 @@ def linear_fwd(ctx: Context, plan: Plan, X: torch.Tensor, W0: torch.Tensor, A_ca
         H = torch.empty((M, R), dtype=torch.bfloat16, device=X.device)
     _require_cuda(Y, "Y", torch.bfloat16, (M, d))
     _require_cuda(H, "H", torch.bfloat16, (M, R))
-    N.check(N.lib().mlora_linear_fwd(ctx.handle, plan.handle, d, k, N.ptr(X), N.ptr(W0), N.ptr(A_cat),
-                                     N.ptr(B_cat), N.ptr(Y), N.ptr(H), _stream_handle(stream)), ctx.handle)
+    if row_sq is not None:
+        _require_cuda(row_sq, "row_sq", torch.float32, (N.lib().mlora_rowsq_blocks(d), M))
+    N.check(N.lib().mlora_linear_fwd_ex(ctx.handle, plan.handle, d, k, N.ptr(X), N.ptr(W0), N.ptr(A_cat),
+                                        N.ptr(B_cat), N.ptr(Y), N.ptr(H), N.ptr(row_sq), _stream_handle(stream)),
+            ctx.handle)
     return Y, H
 
 

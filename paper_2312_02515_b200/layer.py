@@ -58,6 +58,7 @@ class Projection:
     H: torch.Tensor                    # bf16 [rows, R_pad]
     G: torch.Tensor                    # bf16 [rows, R_pad]
     dX: torch.Tensor                   # bf16 [rows, k]
+    row_sq: torch.Tensor               # fp32 [ceil(d/256), rows] fused-loss row partials
 
 
 class FusedLoraLayer:
@@ -98,11 +99,11 @@ class FusedLoraLayer:
                 torch.empty(rows, d, dtype=torch.bfloat16, device=dev),
                 torch.empty(rows, R, dtype=torch.bfloat16, device=dev),
                 torch.empty(rows, R, dtype=torch.bfloat16, device=dev),
-                torch.empty(rows, k, dtype=torch.bfloat16, device=dev)))
+                torch.empty(rows, k, dtype=torch.bfloat16, device=dev),
+                torch.empty(N.lib().mlora_rowsq_blocks(d), rows, dtype=torch.float32, device=dev)))
         self.loss = torch.zeros(self.J, dtype=torch.float32, device=dev)
-        ys = (N.vp * len(self.proj))(*[p.Y.data_ptr() for p in self.proj])
-        self._loss_ptrs = ys
-        self._loss_cols = (N.i32 * len(self.proj))(*[p.d for p in self.proj])
+        self._rowsq_ptrs = (N.vp * len(self.proj))(*[p.row_sq.data_ptr() for p in self.proj])
+        self._rowsq_d = (N.i32 * len(self.proj))(*[p.d for p in self.proj])
 
     def set_layout(self, seg_offsets) -> None:
         """Install the segment layout of the next fused batch (rows must equal self.rows)."""
@@ -125,10 +126,11 @@ class FusedLoraLayer:
         for p in self.proj:
             xin = self._input(p.src, x)
             inputs.append(xin)
-            F.linear_fwd(ctx, plan, xin, p.W0, p.A.p_bf16, p.B.p_bf16, p.Y, p.H, stream=stream)
-        N.check(N.lib().mlora_segment_sumsq_loss(ctx.handle, plan.handle, self._loss_ptrs, self._loss_cols,
-                                                 len(self.proj), self.loss.data_ptr(),
-                                                 F._stream_handle(stream)), ctx.handle)
+            F.linear_fwd(ctx, plan, xin, p.W0, p.A.p_bf16, p.B.p_bf16, p.Y, p.H, row_sq=p.row_sq, stream=stream)
+        # per-job loss from the row sums the forward GEMM epilogues produced (no re-read of Y)
+        N.check(N.lib().mlora_loss_from_rowsq(ctx.handle, plan.handle, self._rowsq_ptrs, self._rowsq_d,
+                                              len(self.proj), self.loss.data_ptr(),
+                                              F._stream_handle(stream)), ctx.handle)
         for p, xin in zip(reversed(self.proj), reversed(inputs)):
             F.linear_bwd(ctx, plan, p.Y, xin, p.H, p.W0, p.A.p_bf16, p.B.p_bf16, need_dX=True, dX=p.dX,
                          dA_cat=p.dA, dB_cat=p.dB, G=p.G, stream=stream)
