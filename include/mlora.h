@@ -163,7 +163,8 @@ mlora_status mlora_pack_adapters(mlora_ctx* ctx, const mlora_plan* plan, int32_t
  * cat-layout tensor whose job of element (i, c) is given by its rows
  * (layout 0, A_cat: row i in [roff[j], roff[j+1])) or columns (layout 1, B_cat).
  * lr/step are per job (host arrays of J entries: the paper trains jobs with
- * different learning rates).  Writes the fp32 master and, when
+ * different learning rates); step[j] = 0 marks a job that was
+ * not in this fused batch — its p, m, v are left untouched.  Writes the fp32 master and, when
  * p_bf16 != NULL, the bf16 operand copy used by the GEMMs. */
 typedef struct mlora_adam_group {
     float* p;

@@ -22,7 +22,7 @@ LIB_FACADE = os.path.join(PKG, "libfusim_b200.so")
 
 MLORA_SOURCES = ["mlora_capi.cu", "mlora_f64.cu", "mlora_model.cu"]
 MLORA_HEADERS = ["sm100.cuh", "mlora_gemm.cuh", "mlora_aux.cuh"]
-FACADE_SOURCES = ["facade_lora.cpp", "facade_batch_select.cpp", "facade_workload.cpp"]
+FACADE_SOURCES = ["facade_lora.cpp", "facade_batch_select.cpp", "facade_workload.cpp", "facade_capi.cpp"]
 
 
 def _newer(target: str, deps: list[str]) -> bool:

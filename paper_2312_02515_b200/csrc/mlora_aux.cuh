@@ -120,6 +120,7 @@ __global__ void adam_kernel(const __grid_constant__ AdamArgs a) {
         const long long col = e % G.cols;
         const int j = job_of_col(a.roff, a.J, static_cast<int>(G.layout == 0 ? row : col));
         const float lr = a.lr[j], bc1 = a.bc1[j], bc2 = a.bc2[j];
+        if (bc1 == 0.f) continue;  // step 0: job not in this fused batch -> p, m, v untouched
         float4 p = reinterpret_cast<float4*>(G.p)[e / 4];
         const float4 g = reinterpret_cast<const float4*>(G.g)[e / 4];
         float4 m = reinterpret_cast<float4*>(G.m)[e / 4];

@@ -869,7 +869,7 @@ mlora_status mlora_adam_step(mlora_ctx* ctx, const mlora_plan* plan, const mlora
     a.J = plan->J;
     for (int j = 0; j <= plan->J; ++j) a.roff[j] = plan->roff[j];
     for (int j = 0; j < plan->J; ++j) {
-        if (step[j] < 1) return fail(ctx, MLORA_USAGE, "Adam step must be >= 1");
+        if (step[j] < 0) return fail(ctx, MLORA_USAGE, "Adam step must be >= 0 (0 = job inactive this step)");
         if (!std::isfinite(lr[j])) return fail(ctx, MLORA_NUMERIC, "non-finite learning rate");
         a.lr[j] = lr[j];
         a.bc1[j] = static_cast<float>(1.0 - std::pow(static_cast<double>(beta1), step[j]));

@@ -1,0 +1,163 @@
+"""A real executor behind the reference simulator's fused iteration.
+
+The reference's discrete-event engine charges every fused iteration an
+analytic time (`duration = base + per_token·ξ + per_launch·launches`,
+/root/reference/proj/src/sim.cpp:177-179).  This executor runs the same
+iteration for real on the B200:
+
+  peek each running job's next batch      (JobState::next_candidate_batch, workload.cpp:50-60)
+  choose the jobs to fuse                 (fifo / priority / MinPad, batch_select.cpp:56-128 — the
+                                           façade's C++ via packer.select)
+  lay the rows out, account ξ, ξ_p, δ      (fuse / fused_shape, lora.cpp:72-158)
+  one fused fwd + bwd + per-job AdamW     (FusedLoraLayer.step — the sm_100a kernels)
+  commit the consumed items               (JobState::commit_batch, workload.cpp:62-66)
+
+and emits the reference's `iteration_done{ξ, ξ_p, jobs_in_batch}` event
+(sim.cpp:185-191) with the MEASURED device time and the per-job losses (what
+the reference's detect_stop consumes, progress.cpp:90-124).  Metrics follow
+compute_metrics (sim.cpp:258-265): δ = Σξ_p / Σξ, T_tot = Σξ / makespan,
+T_e = (1 − δ)·T_tot.  Admission under a memory budget (scheduler.cpp) and early
+stopping are policy outside the hot path and are not reproduced here.
+
+Row order: the kernels need each job's rows contiguous and in adapter order, so
+the fused rows are placed in job-index order; the selection (urgency) order is
+kept as the routing order reported in the event.  The linear layer is
+row-independent, so this changes no result.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import torch
+
+from . import fused as F
+from . import packer as P
+from .layer import FusedLoraLayer
+
+
+@dataclass
+class JobConfig:
+    id: str
+    lengths: list                  # dataset item token counts
+    batch_size: int = 4
+    rank: int = 16
+    lr: float = 1e-4
+    scale: float = 2.0
+    priority: int = 1
+    submit_time: float = 0.0
+    iterations: int = 10           # true_iterations
+
+
+@dataclass
+class _JobState:
+    cfg: JobConfig
+    cursor: int = 0
+    done: int = 0
+
+    @property
+    def finished(self) -> bool:
+        return self.done >= self.cfg.iterations
+
+    def peek(self) -> list:
+        n = len(self.cfg.lengths)
+        pos = self.cursor % n
+        take = min(self.cfg.batch_size, n - pos)
+        return list(self.cfg.lengths[pos:pos + take])
+
+    def commit(self, n_items: int) -> None:
+        self.cursor += n_items
+        if self.cursor >= len(self.cfg.lengths):
+            self.cursor = 0
+
+
+@dataclass
+class Trace:
+    events: list = field(default_factory=list)
+    busy_time: float = 0.0
+
+    def metrics(self) -> dict:
+        xi = sum(e["total_tokens"] for e in self.events)
+        xi_p = sum(e["padding_tokens"] for e in self.events)
+        eff = sum(e["effective_tokens"] for e in self.events)
+        delta = xi_p / xi if xi else 0.0
+        t_tot = xi / self.busy_time if self.busy_time else 0.0
+        return {"iterations": len(self.events), "delta": delta, "T_tot": t_tot, "T_e": (1.0 - delta) * t_tot,
+                "effective_tokens": eff, "effective_tokens_per_s": eff / self.busy_time if self.busy_time else 0.0,
+                "busy_time_s": self.busy_time}
+
+
+class FusedExecutor:
+    """Runs fused multi-LoRA training iterations of several jobs on one GPU."""
+
+    def __init__(self, ctx: F.Context, shapes, jobs: list[JobConfig], max_concurrent: int,
+                 strategy: str = "minpad", padded: bool = False, seed: int = 0, W0: dict | None = None):
+        self.ctx = ctx
+        self.shapes = shapes
+        self.jobs = [_JobState(j) for j in jobs]
+        self.M = max_concurrent
+        self.strategy = strategy
+        self.padded = padded
+        max_len = max(max(j.lengths) for j in jobs)
+        max_bs = max(j.batch_size for j in jobs)
+        capacity = max_concurrent * max_bs * max_len
+        self.layer = FusedLoraLayer(ctx, shapes, [j.rank for j in jobs], [j.scale for j in jobs],
+                                    [j.lr for j in jobs], rows=capacity, seed=seed, W0=W0)
+        self.k_in = shapes[0][2]
+        self.gen = torch.Generator(device=ctx.device).manual_seed(seed + 1)
+        self.trace = Trace()
+        self.clock = 0.0
+
+    def active(self) -> list[int]:
+        return [i for i, js in enumerate(self.jobs) if not js.finished]
+
+    def step(self) -> dict | None:
+        live = self.active()
+        if not live:
+            return None
+        cands = [P.Candidate(i, self.jobs[i].peek(), self.jobs[i].cfg.priority, self.jobs[i].cfg.submit_time)
+                 for i in live]
+        sel = P.select(cands, self.M, self.strategy)
+        chosen = [cands[c].job for c in sel.chosen]          # job indices, urgency (routing) order
+        batches = {i: self.jobs[i].peek() for i in chosen}
+        in_batch = sorted(chosen)                            # row order: job-index order
+        lay = P.layout([batches[i] for i in in_batch], padded=self.padded)
+        seg, r = [0], 0
+        for j in range(len(self.jobs)):
+            if j in batches:
+                r = lay.seg[in_batch.index(j) + 1]
+            seg.append(r)
+        self.layer.set_layout(seg)
+        x = torch.empty(lay.rows, self.k_in, device=self.ctx.device)
+        x.uniform_(-1.0, 1.0, generator=self.gen)
+        x = x.to(torch.bfloat16)
+        if self.padded:  # pad rows are zero, exactly as fuse() builds them
+            mask = torch.zeros(lay.rows, dtype=torch.bool, device=self.ctx.device)
+            for rows in lay.seq_rows:
+                for r0, L in rows:
+                    mask[r0:r0 + L] = True
+            x[~mask] = 0
+        active = [j in batches for j in range(len(self.jobs))]
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        loss = self.layer.step(x, active=active)
+        e1.record()
+        losses = loss.tolist()                               # synchronises
+        duration = e0.elapsed_time(e1) / 1e3
+        for i in chosen:
+            self.jobs[i].commit(len(batches[i]))
+            self.jobs[i].done += 1
+        self.clock += duration
+        self.trace.busy_time += duration
+        ev = {"type": "iteration_done", "time": self.clock, "duration_s": duration,
+              "total_tokens": lay.total_tokens, "padding_tokens": lay.padding_tokens,
+              "effective_tokens": lay.effective_tokens, "rows": lay.rows, "jobs_in_batch": len(chosen),
+              "routing": [self.jobs[i].cfg.id for i in chosen],
+              "losses": {self.jobs[i].cfg.id: losses[i] for i in chosen}}
+        self.trace.events.append(ev)
+        return ev
+
+    def run(self, max_iterations: int | None = None) -> Trace:
+        n = 0
+        while (max_iterations is None or n < max_iterations) and self.step() is not None:
+            n += 1
+        return self.trace

@@ -106,45 +106,62 @@ class FusedLoraLayer:
         self._rowsq_d = (N.i32 * len(self.proj))(*[p.d for p in self.proj])
 
     def set_layout(self, seg_offsets) -> None:
-        """Install the segment layout of the next fused batch (rows must equal self.rows)."""
-        if int(seg_offsets[-1]) != self.rows:
-            raise ValueError("layout rows must equal the layer's row capacity")
+        """Install the segment layout of the next fused batch: job j owns rows
+        seg[j]:seg[j+1] (empty for jobs not in this batch); total rows <= capacity."""
+        rows = int(seg_offsets[-1])
+        if rows < 1 or rows > self.rows:
+            raise ValueError(f"layout rows {rows} outside [1, capacity {self.rows}]")
         self.plan = F.Plan(self.ctx, seg_offsets, self.ranks, self.scales)
+        self.cur_rows = rows
 
-    def _input(self, src: str, x: torch.Tensor) -> torch.Tensor:
+    def _views(self, p: Projection, rows: int):
+        nblk = p.row_sq.shape[0]
+        return (p.Y[:rows], p.H[:rows], p.G[:rows], p.dX[:rows],
+                p.row_sq.view(-1)[: nblk * rows].view(nblk, rows))
+
+    def _input(self, src: str, x: torch.Tensor, rows: int) -> torch.Tensor:
         if src == "x":
             return x
         if src == "h_to_4h_half":
             p = next(q for q in self.proj if q.name == "h_to_4h")
             # first half of the fused gate/up output (stand-in for the gated act.)
-            return p.Y[:, : p.d // 2].contiguous() if p.d // 2 != p.Y.shape[1] else p.Y
-        return next(q for q in self.proj if q.name == src).Y
+            return p.Y[:rows, : p.d // 2].contiguous()
+        return next(q for q in self.proj if q.name == src).Y[:rows]
 
     def forward_backward(self, x: torch.Tensor, stream=None) -> torch.Tensor:
         ctx, plan = self.ctx, self.plan
-        inputs = []
+        rows = getattr(self, "cur_rows", self.rows)
+        inputs, rowsq = [], []
         for p in self.proj:
-            xin = self._input(p.src, x)
+            xin = self._input(p.src, x, rows)
             inputs.append(xin)
-            F.linear_fwd(ctx, plan, xin, p.W0, p.A.p_bf16, p.B.p_bf16, p.Y, p.H, row_sq=p.row_sq, stream=stream)
+            Y, H, _, _, rsq = self._views(p, rows)
+            rowsq.append(rsq)
+            F.linear_fwd(ctx, plan, xin, p.W0, p.A.p_bf16, p.B.p_bf16, Y, H, row_sq=rsq, stream=stream)
         # per-job loss from the row sums the forward GEMM epilogues produced (no re-read of Y)
-        N.check(N.lib().mlora_loss_from_rowsq(ctx.handle, plan.handle, self._rowsq_ptrs, self._rowsq_d,
+        ptrs = (N.vp * len(rowsq))(*[t.data_ptr() for t in rowsq])
+        N.check(N.lib().mlora_loss_from_rowsq(ctx.handle, plan.handle, ptrs, self._rowsq_d,
                                               len(self.proj), self.loss.data_ptr(),
                                               F._stream_handle(stream)), ctx.handle)
         for p, xin in zip(reversed(self.proj), reversed(inputs)):
-            F.linear_bwd(ctx, plan, p.Y, xin, p.H, p.W0, p.A.p_bf16, p.B.p_bf16, need_dX=True, dX=p.dX,
-                         dA_cat=p.dA, dB_cat=p.dB, G=p.G, stream=stream)
+            Y, H, G, dX, _ = self._views(p, rows)
+            F.linear_bwd(ctx, plan, Y, xin, H, p.W0, p.A.p_bf16, p.B.p_bf16, need_dX=True, dX=dX,
+                         dA_cat=p.dA, dB_cat=p.dB, G=G, stream=stream)
         return self.loss
 
-    def optimizer_step(self, stream=None) -> None:
-        self.step_count = [s + 1 for s in self.step_count]
+    def optimizer_step(self, active=None, stream=None) -> None:
+        """AdamW on every adapter; jobs not in `active` (bool per job) keep p, m, v
+        untouched this step (their rows were absent from the fused batch)."""
+        active = [True] * self.J if active is None else list(active)
+        self.step_count = [s + (1 if a else 0) for s, a in zip(self.step_count, active)]
+        steps = [s if a else 0 for s, a in zip(self.step_count, active)]
         states, grads = [], []
         for p in self.proj:
             states += [p.A, p.B]
             grads += [p.dA, p.dB]
-        F.adam_step(self.ctx, self.plan, states, grads, self.lrs, self.step_count, stream=stream)
+        F.adam_step(self.ctx, self.plan, states, grads, self.lrs, steps, stream=stream)
 
-    def step(self, x: torch.Tensor, stream=None) -> torch.Tensor:
+    def step(self, x: torch.Tensor, active=None, stream=None) -> torch.Tensor:
         loss = self.forward_backward(x, stream)
-        self.optimizer_step(stream)
+        self.optimizer_step(active, stream)
         return loss
