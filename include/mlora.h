@@ -194,6 +194,31 @@ mlora_status mlora_f64_gemm(int64_t M, int64_t N, int64_t K, const double* A, in
 /* c = a + b elementwise (lora.cpp:36-42), device fp64. */
 mlora_status mlora_f64_add(int64_t n, const double* a, const double* b, double* c, void* stream);
 
+/* ---------------------------------------------------------------- model kernels (K4, K5)
+ * No reference counterpart (the reference model is analytic): parity unpinned,
+ * checked against fp64 restatements.  All device pointers; deterministic.
+ *
+ * Padding-masked cross-entropy over the fused batch (C4: V = 65024):
+ *   row_loss[t] = logsumexp(logits[t]) - logits[t, labels[t]]   (0 where mask[t] == 0)
+ *   loss[j]     = mean of row_loss over job j's real rows (seg_dev: device J+1 offsets)
+ *   dlogits[t]  = (softmax(logits[t]) - onehot(labels[t])) / n_j  (0 on pad rows), optional
+ * mask may be NULL (every row real).  row_loss: rows floats, inv_count: J floats (scratch). */
+mlora_status mlora_masked_ce(int32_t num_jobs, const int32_t* seg_dev, int64_t rows, int32_t V, const void* logits,
+                             const int32_t* labels, const uint8_t* mask, float* row_loss, float* loss,
+                             float* inv_count, void* dlogits, void* stream);
+/* RMSNorm: y = x * rstd * w, rstd = 1 / sqrt(mean(x^2) + eps) (bf16 x, w, y; fp32 rstd). */
+mlora_status mlora_rmsnorm_fwd(int64_t rows, int32_t h, const void* x, const void* w, float eps, void* y,
+                               float* rstd, void* stream);
+/* dx = rstd (g - xhat mean(g xhat)), g = dy w; dw = sum_rows dy xhat (fp32, fixed-order
+ * reduction through workspace[ceil(rows / rows_per_block) * h]). */
+mlora_status mlora_rmsnorm_bwd(int64_t rows, int32_t h, const void* dy, const void* x, const void* w,
+                               const float* rstd, void* dx, float* dw, float* workspace, int32_t rows_per_block,
+                               void* stream);
+/* Rotary embedding on [rows, heads, head_dim] bf16 (rotate-half pairing), angle
+ * pos[row] * base^(-2i/head_dim); inverse = 1 applies the transpose (backward). */
+mlora_status mlora_rope(int64_t rows, int32_t heads, int32_t head_dim, const void* x, void* y, const int32_t* pos,
+                        float base, int32_t inverse, void* stream);
+
 /* Per-job synthetic layer loss L_j = 1/2 sum_p sum_{t in job j} ||Y_p[t]||^2 over
  * `num_tensors` bf16 tensors Y[p] (rows x cols[p]); loss: device fp32 [J].
  * Deterministic (fixed-order two-level reduction).  Used by the trainer step:

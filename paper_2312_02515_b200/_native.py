@@ -63,12 +63,12 @@ _SIGS = {
 
 # Optional groups (present once the corresponding kernels are built).
 _OPTIONAL = {
-    "mlora_f64_fused_forward": (i32, [vp, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp]),
-    "mlora_masked_ce": (i32, [vp, vp, i64, i32, vp, vp, vp, vp, vp, vp, vp]),
-    "mlora_rmsnorm_fwd": (i32, [vp, i64, i32, vp, vp, f32, vp, vp, vp]),
-    "mlora_rmsnorm_bwd": (i32, [vp, i64, i32, vp, vp, vp, vp, vp, vp, vp]),
-    "mlora_rope_fwd": (i32, [vp, i64, i32, i32, vp, vp, f32, i32, vp]),
-    "mlora_rope_bwd": (i32, [vp, i64, i32, i32, vp, vp, f32, i32, vp]),
+    "mlora_f64_gemm": (i32, [i64, i64, i64, vp, i64, i32, vp, i64, i32, vp, i64, vp]),
+    "mlora_f64_add": (i32, [i64, vp, vp, vp, vp]),
+    "mlora_masked_ce": (i32, [i32, vp, i64, i32, vp, vp, vp, vp, vp, vp, vp, vp]),
+    "mlora_rmsnorm_fwd": (i32, [i64, i32, vp, vp, f32, vp, vp, vp]),
+    "mlora_rmsnorm_bwd": (i32, [i64, i32, vp, vp, vp, vp, vp, vp, vp, i32, vp]),
+    "mlora_rope": (i32, [i64, i32, i32, vp, vp, vp, f32, i32, vp]),
 }
 
 

@@ -1,0 +1,301 @@
+// mlora_model.cu — the small HBM-bound kernels around the LoRA linears
+// (north star item 4): padding-masked cross-entropy with
+// per-job mean loss, RMSNorm forward/backward, rotary embedding.
+//
+// The reference has none of these (its model is analytic), so their semantics
+// are "parity unpinned": they are checked against fp64 numpy restatements in
+// tests/test_gpu_model.py.  All reductions are deterministic (fixed order, no
+// float atomics).  Roofline: HBM bandwidth; bytes per row are stated per kernel.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+
+#include "../../include/mlora.h"
+
+namespace {
+
+__device__ __forceinline__ void pdl_prologue() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+template <typename T>
+__device__ __forceinline__ T block_reduce(T v, T* red, bool is_max) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const T u = __shfl_xor_sync(0xffffffffu, v, o);
+        v = is_max ? (u > v ? u : v) : v + u;
+    }
+    __syncthreads();
+    if (lane == 0) red[w] = v;
+    __syncthreads();
+    if (w == 0) {
+        v = lane < (int)(blockDim.x >> 5) ? red[lane] : (is_max ? -INFINITY : T(0));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const T u = __shfl_xor_sync(0xffffffffu, v, o);
+            v = is_max ? (u > v ? u : v) : v + u;
+        }
+        if (lane == 0) red[0] = v;
+    }
+    __syncthreads();
+    return red[0];
+}
+
+// ---------------------------------------------------------------- masked CE
+// One CTA per row.  The row (V bf16) is read from HBM once into shared memory,
+// max / sum-exp are reduced from smem, then dlogits = (softmax - onehot) / n_j
+// is written (0 for pad rows).  bytes/row: 2V read + 2V write.
+__global__ void masked_ce_kernel(const __nv_bfloat16* __restrict__ logits, int V, const int* __restrict__ labels,
+                                 const uint8_t* __restrict__ mask, const int* __restrict__ seg, int J,
+                                 float* __restrict__ row_loss, __nv_bfloat16* __restrict__ dlogits) {
+    pdl_prologue();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __nv_bfloat16* srow = reinterpret_cast<__nv_bfloat16*>(smem_raw);
+    __shared__ float red[32];
+    const int row = blockIdx.x;
+    const bool real = mask == nullptr || mask[row] != 0;
+    const __nv_bfloat16* src = logits + (long long)row * V;
+    // stage the row (16-byte vectors when aligned)
+    float mx = -INFINITY;
+    if ((V & 7) == 0) {
+        const uint4* s4 = reinterpret_cast<const uint4*>(src);
+        uint4* d4 = reinterpret_cast<uint4*>(srow);
+        for (int i = threadIdx.x; i < V / 8; i += blockDim.x) {
+            const uint4 w = s4[i];
+            d4[i] = w;
+            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float2 f = __bfloat1622float2(h[e]);
+                mx = fmaxf(mx, fmaxf(f.x, f.y));
+            }
+        }
+    } else {
+        for (int i = threadIdx.x; i < V; i += blockDim.x) {
+            srow[i] = src[i];
+            mx = fmaxf(mx, __bfloat162float(src[i]));
+        }
+    }
+    mx = block_reduce(mx, red, true);
+    float se = 0.f;
+    for (int i = threadIdx.x; i < V; i += blockDim.x) se += __expf(__bfloat162float(srow[i]) - mx);
+    se = block_reduce(se, red, false);
+    const float lse = mx + __logf(se);
+    const int label = labels[row];
+    if (threadIdx.x == 0) row_loss[row] = real ? lse - __bfloat162float(srow[label]) : 0.f;
+    if (dlogits) {
+        // per-row gradient of the row loss; the per-job mean's 1/n_j is applied by
+        // scale_rows_kernel once segment_mean_kernel has counted the real rows
+        __nv_bfloat16* dst = dlogits + (long long)row * V;
+        const float keep = real ? 1.f : 0.f;
+        for (int i = threadIdx.x; i < V; i += blockDim.x) {
+            const float p = __expf(__bfloat162float(srow[i]) - lse);
+            dst[i] = __float2bfloat16_rn(keep * (p - (i == label ? 1.f : 0.f)));
+        }
+    }
+    (void)seg;
+    (void)J;
+}
+
+// loss[j] = sum of row_loss over job j's real rows / max(1, #real rows): fixed order.
+__global__ void segment_mean_kernel(const float* __restrict__ row_loss, const uint8_t* __restrict__ mask,
+                                    const int* __restrict__ seg, float* __restrict__ loss,
+                                    float* __restrict__ inv_count) {
+    pdl_prologue();
+    __shared__ float red[32];
+    const int j = blockIdx.x;
+    float acc = 0.f, cnt = 0.f;
+    for (int r = seg[j] + threadIdx.x; r < seg[j + 1]; r += blockDim.x) {
+        acc += row_loss[r];
+        cnt += (mask == nullptr || mask[r]) ? 1.f : 0.f;
+    }
+    acc = block_reduce(acc, red, false);
+    cnt = block_reduce(cnt, red, false);
+    if (threadIdx.x == 0) {
+        loss[j] = cnt > 0.f ? acc / cnt : 0.f;
+        if (inv_count) inv_count[j] = cnt > 0.f ? 1.f / cnt : 0.f;
+    }
+}
+
+// dlogits of job j's rows *= 1/n_j  (so dlogits = d mean_j / d logits)
+__global__ void scale_rows_kernel(__nv_bfloat16* __restrict__ d, long long V, const int* __restrict__ seg, int J,
+                                  const float* __restrict__ inv_count) {
+    pdl_prologue();
+    const int row = blockIdx.x;
+    int j = 0;
+    for (int t = 1; t < J; ++t)
+        if (seg[t] <= row) j = t;
+    const float s = inv_count[j];
+    __nv_bfloat16* p = d + row * V;
+    for (long long i = threadIdx.x; i < V; i += blockDim.x) p[i] = __float2bfloat16_rn(s * __bfloat162float(p[i]));
+}
+
+// ---------------------------------------------------------------- RMSNorm
+// y = x * rstd * w, rstd = 1/sqrt(mean(x^2) + eps).  One CTA per row.
+// bytes/row: 2h read + 2h write (+ w from L2).
+__global__ void rmsnorm_fwd_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w, int h,
+                                   float eps, __nv_bfloat16* __restrict__ y, float* __restrict__ rstd) {
+    pdl_prologue();
+    __shared__ float red[32];
+    const __nv_bfloat16* xr = x + (long long)blockIdx.x * h;
+    float ss = 0.f;
+    for (int i = threadIdx.x; i < h; i += blockDim.x) {
+        const float v = __bfloat162float(xr[i]);
+        ss = fmaf(v, v, ss);
+    }
+    ss = block_reduce(ss, red, false);
+    const float r = rsqrtf(ss / h + eps);
+    if (threadIdx.x == 0) rstd[blockIdx.x] = r;
+    __nv_bfloat16* yr = y + (long long)blockIdx.x * h;
+    for (int i = threadIdx.x; i < h; i += blockDim.x)
+        yr[i] = __float2bfloat16_rn(__bfloat162float(xr[i]) * r * __bfloat162float(w[i]));
+}
+
+// dx = rstd * (g - xhat * mean(g * xhat)), g = dy * w; dw partials per row block (deterministic).
+__global__ void rmsnorm_bwd_kernel(const __nv_bfloat16* __restrict__ dy, const __nv_bfloat16* __restrict__ x,
+                                   const __nv_bfloat16* __restrict__ w, const float* __restrict__ rstd, int rows,
+                                   int h, __nv_bfloat16* __restrict__ dx, float* __restrict__ dw_part,
+                                   int rows_per_block) {
+    pdl_prologue();
+    __shared__ float red[32];
+    const int r0 = blockIdx.x * rows_per_block;
+    const int r1 = min(rows, r0 + rows_per_block);
+    // dw partial for this block's rows: each thread owns columns i, i + blockDim, ...
+    for (int i = threadIdx.x; i < h; i += blockDim.x) dw_part[(long long)blockIdx.x * h + i] = 0.f;
+    for (int row = r0; row < r1; ++row) {
+        const __nv_bfloat16* xr = x + (long long)row * h;
+        const __nv_bfloat16* gr = dy + (long long)row * h;
+        const float r = rstd[row];
+        float dot = 0.f;
+        for (int i = threadIdx.x; i < h; i += blockDim.x)
+            dot += __bfloat162float(gr[i]) * __bfloat162float(w[i]) * __bfloat162float(xr[i]) * r;
+        dot = block_reduce(dot, red, false) / h;
+        for (int i = threadIdx.x; i < h; i += blockDim.x) {
+            const float xh = __bfloat162float(xr[i]) * r;
+            const float g = __bfloat162float(gr[i]) * __bfloat162float(w[i]);
+            dx[(long long)row * h + i] = __float2bfloat16_rn(r * (g - xh * dot));
+            dw_part[(long long)blockIdx.x * h + i] += __bfloat162float(gr[i]) * xh;
+        }
+    }
+}
+
+__global__ void column_sum_kernel(const float* __restrict__ part, int nblk, int h, float* __restrict__ out) {
+    pdl_prologue();
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < h; i += gridDim.x * blockDim.x) {
+        float s = 0.f;
+        for (int b = 0; b < nblk; ++b) s += part[(long long)b * h + i];
+        out[i] = s;
+    }
+}
+
+// ---------------------------------------------------------------- RoPE
+// x, y: [rows, heads, head_dim] bf16; rotate-half pairing (i, i + head_dim/2)
+// by angle pos * base^(-2i/head_dim); inverse = 1 rotates by -angle (backward).
+__global__ void rope_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y,
+                            const int* __restrict__ pos, int heads, int hd, float base, int inverse) {
+    pdl_prologue();
+    const int row = blockIdx.x;
+    const int half = hd / 2;
+    const float p = static_cast<float>(pos[row]);
+    for (int e = threadIdx.x; e < heads * half; e += blockDim.x) {
+        const int hh = e / half, i = e % half;
+        const float inv_freq = exp2f(-(2.f * i / hd) * log2f(base));
+        float sn, cs;
+        sincosf(p * inv_freq, &sn, &cs);
+        if (inverse) sn = -sn;
+        const long long o = ((long long)row * heads + hh) * hd;
+        const float a = __bfloat162float(x[o + i]), b = __bfloat162float(x[o + i + half]);
+        y[o + i] = __float2bfloat16_rn(a * cs - b * sn);
+        y[o + i + half] = __float2bfloat16_rn(b * cs + a * sn);
+    }
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, void* stream, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = g;
+    cfg.blockDim = b;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = static_cast<cudaStream_t>(stream);
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr.val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, args...);
+}
+
+}  // namespace
+
+extern "C" {
+
+mlora_status mlora_masked_ce(int32_t num_jobs, const int32_t* seg_dev, int64_t rows, int32_t V, const void* logits,
+                             const int32_t* labels, const uint8_t* mask, float* row_loss, float* loss,
+                             float* inv_count, void* dlogits, void* stream) {
+    if (rows < 1 || V < 1 || num_jobs < 1 || !seg_dev || !logits || !labels || !row_loss || !loss || !inv_count)
+        return MLORA_USAGE;
+    const size_t smem = static_cast<size_t>(V) * 2;
+    if (smem > 200 * 1024) return MLORA_SHAPE;
+    if (cudaFuncSetAttribute(masked_ce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem)) != cudaSuccess)
+        return MLORA_CUDA;
+    auto* d = static_cast<__nv_bfloat16*>(dlogits);
+    if (launch(masked_ce_kernel, dim3(static_cast<unsigned>(rows)), dim3(512), smem, stream,
+               static_cast<const __nv_bfloat16*>(logits), static_cast<int>(V), labels, mask,
+               static_cast<const int*>(seg_dev), static_cast<int>(num_jobs), row_loss, d) != cudaSuccess)
+        return MLORA_CUDA;
+    if (launch(segment_mean_kernel, dim3(num_jobs), dim3(1024), 0, stream, static_cast<const float*>(row_loss), mask,
+               static_cast<const int*>(seg_dev), loss, inv_count) != cudaSuccess)
+        return MLORA_CUDA;
+    if (d && launch(scale_rows_kernel, dim3(static_cast<unsigned>(rows)), dim3(256), 0, stream, d,
+                    static_cast<long long>(V), static_cast<const int*>(seg_dev), static_cast<int>(num_jobs),
+                    static_cast<const float*>(inv_count)) != cudaSuccess)
+        return MLORA_CUDA;
+    return MLORA_OK;
+}
+
+mlora_status mlora_rmsnorm_fwd(int64_t rows, int32_t h, const void* x, const void* w, float eps, void* y,
+                               float* rstd, void* stream) {
+    if (rows < 1 || h < 1 || !x || !w || !y || !rstd) return MLORA_USAGE;
+    if (!(eps > 0.f)) return MLORA_USAGE;
+    return launch(rmsnorm_fwd_kernel, dim3(static_cast<unsigned>(rows)), dim3(256), 0, stream,
+                  static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(w), static_cast<int>(h),
+                  eps, static_cast<__nv_bfloat16*>(y), rstd) == cudaSuccess
+               ? MLORA_OK
+               : MLORA_CUDA;
+}
+
+mlora_status mlora_rmsnorm_bwd(int64_t rows, int32_t h, const void* dy, const void* x, const void* w,
+                               const float* rstd, void* dx, float* dw, float* workspace, int32_t rows_per_block,
+                               void* stream) {
+    if (rows < 1 || h < 1 || !dy || !x || !w || !rstd || !dx || !dw || !workspace || rows_per_block < 1)
+        return MLORA_USAGE;
+    const int nblk = static_cast<int>((rows + rows_per_block - 1) / rows_per_block);
+    if (launch(rmsnorm_bwd_kernel, dim3(nblk), dim3(256), 0, stream, static_cast<const __nv_bfloat16*>(dy),
+               static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(w), rstd,
+               static_cast<int>(rows), static_cast<int>(h), static_cast<__nv_bfloat16*>(dx), workspace,
+               static_cast<int>(rows_per_block)) != cudaSuccess)
+        return MLORA_CUDA;
+    return launch(column_sum_kernel, dim3((h + 255) / 256), dim3(256), 0, stream, static_cast<const float*>(workspace),
+                  nblk, static_cast<int>(h), dw) == cudaSuccess
+               ? MLORA_OK
+               : MLORA_CUDA;
+}
+
+mlora_status mlora_rope(int64_t rows, int32_t heads, int32_t head_dim, const void* x, void* y, const int32_t* pos,
+                        float base, int32_t inverse, void* stream) {
+    if (rows < 1 || heads < 1 || head_dim < 2 || (head_dim & 1) || !x || !y || !pos || !(base > 1.f))
+        return MLORA_USAGE;
+    return launch(rope_kernel, dim3(static_cast<unsigned>(rows)), dim3(256), 0, stream,
+                  static_cast<const __nv_bfloat16*>(x), static_cast<__nv_bfloat16*>(y), pos, static_cast<int>(heads),
+                  static_cast<int>(head_dim), base, static_cast<int>(inverse)) == cudaSuccess
+               ? MLORA_OK
+               : MLORA_CUDA;
+}
+
+}  // extern "C"
