@@ -202,13 +202,20 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
+    from paper_2312_02515_b200 import parallel as PL
+
     shapes = SHAPES[cfg["shapes"]]
-    J = len(cfg["ranks"])
     per_job = cfg["seqs"] * cfg["seq_len"]
+    # adapter-parallel weak scaling: 4 jobs per GPU (32 jobs at N=8, C5), partitioned by LPT
+    all_ranks = cfg["ranks"] * world
+    all_lrs = cfg["lrs"] * world
+    mine = PL.partition_jobs([per_job] * len(all_ranks), world)[rank]
+    ranks_l, lrs_l = [all_ranks[j] for j in mine], [all_lrs[j] for j in mine]
+    J = len(mine)
     rows = J * per_job
     seg = [j * per_job for j in range(J + 1)]
 
-    # frozen base weights: created on rank 0, replicated with one NCCL broadcast per tensor
+    # frozen base weights: created on rank 0, replicated once (NCCL broadcast over NVLink)
     g = torch.Generator(device="cpu").manual_seed(1234)
     W0 = {}
     for name, d, k, _ in shapes:
@@ -216,13 +223,11 @@ def main():
             W0[name] = ((torch.rand(d, k, generator=g) * 2 - 1) / k ** 0.5).to(torch.bfloat16).to(dev)
         else:
             W0[name] = torch.empty(d, k, dtype=torch.bfloat16, device=dev)
-    if world > 1:
-        for name in W0:
-            dist.broadcast(W0[name], src=0)
-        torch.cuda.synchronize()
+    PL.broadcast_base_weights(W0, src=0)
+    torch.cuda.synchronize()
 
     ctx = F.Context(dev)
-    layer = FusedLoraLayer(ctx, shapes, cfg["ranks"], [2.0] * J, cfg["lrs"], rows, seed=1000 + rank, W0=W0)
+    layer = FusedLoraLayer(ctx, shapes, ranks_l, [2.0] * J, lrs_l, rows, seed=1000 + rank, W0=W0)
     layer.set_layout(seg)
     xg = torch.Generator(device="cpu").manual_seed(77 + rank)
     x_host = (torch.rand(rows, shapes[0][2], generator=xg) * 2 - 1).to(torch.bfloat16).pin_memory()
@@ -236,11 +241,7 @@ def main():
             dist.barrier()
 
     def max_over_ranks(v: float) -> float:
-        if world == 1:
-            return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return PL.max_over_ranks(v, device=dev)
 
     for _ in range(max(args.warmup, 3)):
         layer.step(x)
@@ -261,7 +262,7 @@ def main():
     launches = ctx.launches - launches0
     ms_total = max_over_ranks(e0.elapsed_time(e1))
     ms_step = ms_total / args.steps
-    eff_tokens = rows * world  # δ = 0: every fused row is a real token
+    eff_tokens = int(PL.sum_over_ranks(rows, device=dev))  # δ = 0: every fused row is a real token
     value = eff_tokens * args.steps / (ms_total / 1e3)
 
     # ---------------- per-kernel live timing: the same K steps again with every launch
@@ -297,7 +298,7 @@ def main():
     # ---------------- roofline of the dominant kernel (base GEMM, forward)
     peaks = load_peaks()
     cnt, ms = prof["base_fwd"]
-    r_sum = sum(cfg["ranks"])
+    r_sum = sum(ranks_l)
     fl_fwd = sum(2 * rows * d * k + 2 * per_job * d * r_sum for _, d, k, _ in shapes)  # per step
     achieved = (fl_fwd * args.steps) / (ms / 1e3) / 1e12 if ms > 0 else None
     use_sustained = ms_total > 1000.0
