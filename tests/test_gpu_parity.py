@@ -293,3 +293,22 @@ def test_error_conventions(F, ctx):
         F.Plan(ctx, [0, 10], [0])                # rank < 1
     with pytest.raises(E.RoutingError):
         F.pack_adapters(ctx, plan, 64, 64, [], [])
+
+
+def test_pipelined_trainer_matches_sequential_steps(F, ctx):
+    """The public host-batch API (double-buffered H2D on a copy stream, async D2H
+    of losses) produces bitwise the same per-step losses as plain steps."""
+    from paper_2312_02515_b200.layer import TINY, FusedLoraLayer
+    from paper_2312_02515_b200.trainer import PipelinedTrainer
+    seg = [0, 100, 256]
+    mk = lambda: FusedLoraLayer(ctx, TINY, [8, 16], [1.0, 2.0], [1e-2, 5e-3], rows=256, seed=4)
+    a, b = mk(), mk()
+    a.set_layout(seg)
+    b.set_layout(seg)
+    g = torch.Generator().manual_seed(5)
+    xs = [bf(torch.rand(256, 256, generator=g) * 2 - 1).pin_memory() for _ in range(4)]
+    want = [a.step(x.to(ctx.device)).clone() for x in xs]
+    losses = torch.empty(4, 2, dtype=torch.float32).pin_memory()
+    PipelinedTrainer(b, 256, 256).run(xs, losses)
+    torch.cuda.synchronize()
+    assert torch.equal(torch.stack(want).cpu(), losses)
