@@ -149,6 +149,33 @@ mlora_status mlora_linear_bwd(mlora_ctx* ctx, const mlora_plan* plan, int32_t d,
                               const void* A_cat, const void* B_cat, void* G, void* dX,
                               float* dA_cat, float* dB_cat, void* stream);
 
+/* ---------------------------------------------------------------- layer-level building blocks
+ * The same kernels as mlora_linear_fwd/bwd, exposed per op so a layer issues
+ * each HBM-bound op ONCE for all of its projections (grouped launch: one
+ * problem per projection, up to 8 per launch) — launch count per layer step is
+ * independent of the number of projections as well as of the number of jobs.
+ *
+ * down_group, forward (backward = 0):  out_i = H_i = s_j in_i A_cat_i^T  (in_i: X_i [rows, width_i],
+ *                                      adapter_i: A_cat_i [R_pad, width_i])
+ * down_group, backward (backward = 1): out_i = G_i = s_j in_i B_cat_i    (in_i: dY_i [rows, width_i = d_i],
+ *                                      adapter_i: B_cat_i [d_i, R_pad]) */
+mlora_status mlora_down_group(mlora_ctx* ctx, const mlora_plan* plan, int32_t n, int32_t backward,
+                              const int32_t* width, const void* const* in, const void* const* adapter,
+                              void* const* out, void* stream);
+/* Y = X W0^T + H B_cat^T (CTA-pair tcgen05 GEMM; optional fused row sums, see _ex). */
+mlora_status mlora_base_fwd(mlora_ctx* ctx, const mlora_plan* plan, int32_t d, int32_t k, const void* X,
+                            const void* W0, const void* H, const void* B_cat, void* Y, float* row_sq,
+                            void* stream);
+/* dX = dY W0 + G A_cat. */
+mlora_status mlora_base_dx(mlora_ctx* ctx, const mlora_plan* plan, int32_t d, int32_t k, const void* dY,
+                           const void* W0, const void* G, const void* A_cat, void* dX, void* stream);
+/* dA_cat_i = G_i^T X_i and dB_cat_i = dY_i^T H_i for n projections (two grouped launches + at most one
+ * grouped fixed-order split reduction). */
+mlora_status mlora_grad_group(mlora_ctx* ctx, const mlora_plan* plan, int32_t n, const int32_t* d,
+                              const int32_t* k, const void* const* X, const void* const* dY,
+                              const void* const* H, const void* const* G, float* const* dA_cat,
+                              float* const* dB_cat, void* stream);
+
 /* ---------------------------------------------------------------- adapters
  * Pack per-job reference-layout adapters (device fp32: A_j r_j x k, B_j d x r_j)
  * into the cat layout (fp32 master and bf16 operand copies; either output

@@ -54,6 +54,11 @@ _SIGS = {
     "mlora_linear_fwd_ex": (i32, [vp, vp, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp]),
     "mlora_rowsq_blocks": (i32, [i32]),
     "mlora_loss_from_rowsq": (i32, [vp, vp, C.POINTER(vp), C.POINTER(i32), i32, vp, vp]),
+    "mlora_down_group": (i32, [vp, vp, i32, i32, C.POINTER(i32), C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), vp]),
+    "mlora_base_fwd": (i32, [vp, vp, i32, i32, vp, vp, vp, vp, vp, vp, vp]),
+    "mlora_base_dx": (i32, [vp, vp, i32, i32, vp, vp, vp, vp, vp, vp]),
+    "mlora_grad_group": (i32, [vp, vp, i32, C.POINTER(i32), C.POINTER(i32), C.POINTER(vp), C.POINTER(vp),
+                               C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), vp]),
     "mlora_linear_bwd": (i32, [vp, vp, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
     "mlora_pack_adapters": (i32, [vp, vp, i32, i32, C.POINTER(vp), C.POINTER(vp), vp, vp, vp, vp, vp]),
     "mlora_segment_sumsq_loss": (i32, [vp, vp, C.POINTER(vp), C.POINTER(i32), i32, vp, vp]),

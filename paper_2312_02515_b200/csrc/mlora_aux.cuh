@@ -31,6 +31,38 @@ __global__ void reduce_splits_kernel(const float4* __restrict__ part, float4* __
     }
 }
 
+// Grouped version: several gradients' split partials in one launch.
+// part_i = [nsplit][n4_i] float4; out_i[e] = sum_s part_i[s][e] (fixed order).
+struct ReduceGroupArgs {
+    struct Item {
+        const float4* part;
+        float4* out;
+        long long n4;
+        long long start4;  // first element of this item in the flattened index space
+    } item[8];
+    int n;
+    int nsplit;
+    long long total4;
+};
+
+__global__ void reduce_splits_group_kernel(const __grid_constant__ ReduceGroupArgs a) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < a.total4;
+         i += (long long)gridDim.x * blockDim.x) {
+        int g = 0;
+        while (g + 1 < a.n && a.item[g + 1].start4 <= i) ++g;
+        const ReduceGroupArgs::Item& it = a.item[g];
+        const long long e = i - it.start4;
+        float4 acc = it.part[e];
+        for (int s = 1; s < a.nsplit; ++s) {
+            const float4 b = it.part[s * it.n4 + e];
+            acc.x += b.x; acc.y += b.y; acc.z += b.z; acc.w += b.w;
+        }
+        it.out[e] = acc;
+    }
+}
+
 struct PackArgs {
     const float* A[kMaxJobs];
     const float* B[kMaxJobs];

@@ -225,27 +225,48 @@ struct ProfScope {
     }
 };
 
-template <int MODE, int BN, int STAGES, bool A_MN, bool B_MN>
-mlora_status launch_gemm(mlora_ctx* ctx, const CUtensorMap& a0, const CUtensorMap& b0,
-                         const CUtensorMap& a1, const CUtensorMap& b1, const GemmParams& p,
-                         int ctas_per_sm, cudaStream_t stream) {
-    if (p.num_tiles <= 0) return MLORA_OK;
-    using L = GemmSmem<BN, STAGES>;
-    auto kern = mlora_gemm_kernel<MODE, BN, STAGES, A_MN, B_MN>;
+constexpr int kGroupMax = 8;  // problems per grouped launch (a transformer layer has <= 7 LoRA'd projections)
+
+// Accumulates the problems of one (possibly grouped) launch.
+template <int NP>
+struct ProblemSet {
+    GemmProblemSet<NP> ps{};
+    bool add(const CUtensorMap& a0, const CUtensorMap& b0, const CUtensorMap& a1, const CUtensorMap& b1,
+             const GemmParams& p) {
+        if (ps.nprobs >= NP) return false;
+        GemmProblem& g = ps.prob[ps.nprobs++];
+        g.tmA0 = a0;
+        g.tmB0 = b0;
+        g.tmA1 = a1;
+        g.tmB1 = b1;
+        g.p = p;
+        g.tile_begin = ps.total_tiles;
+        ps.total_tiles += p.num_tiles;
+        return true;
+    }
+};
+
+// One launch of the 1-CTA (KSPLIT=1) or K-split-pair (KSPLIT=2) tcgen05 kernel over a problem set.
+template <int MODE, int BN, int STAGES, bool A_MN, bool B_MN, int KSPLIT, int NP>
+mlora_status launch_gemm(mlora_ctx* ctx, const ProblemSet<NP>& set, int ctas_per_sm, cudaStream_t stream) {
+    if (set.ps.total_tiles <= 0) return MLORA_OK;
+    using L = GemmSmem<BN, STAGES, KSPLIT>;
+    auto kern = mlora_gemm_kernel<MODE, BN, STAGES, A_MN, B_MN, KSPLIT, NP>;
     static bool attr_done = false;  // per instantiation
     if (!attr_done) {
         MLORA_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  L::kDynBytes));
         attr_done = true;
     }
-    const int grid = std::min(p.num_tiles, ctx->num_sms * ctas_per_sm);
+    const int units = std::min(set.ps.total_tiles, ctx->num_sms * ctas_per_sm / KSPLIT);
     ProfScope ps(ctx, MODE == MODE_BASE ? (B_MN ? 1 : 0) : MODE == MODE_DOWN ? 2 : 3, stream);
-    MLORA_CUDA_TRY(ctx, launch_k(kern, dim3(grid), dim3(kNumThreads), L::kDynBytes, stream, 1, a0, b0, a1, b1, p));
+    MLORA_CUDA_TRY(ctx, launch_k(kern, dim3(units * KSPLIT), dim3(kNumThreads), L::kDynBytes, stream, KSPLIT,
+                                 set.ps));
     ++ctx->launches;
     return MLORA_OK;
 }
 
-bool use_pair_kernel() {
+bool use_pair_kernel() {  // MLORA_BASE_KERNEL=single selects the 1-CTA variant (A/B measurements)
     static const bool pair = [] {
         const char* e = std::getenv("MLORA_BASE_KERNEL");
         return !(e && std::string(e) == "single");
@@ -320,37 +341,52 @@ mlora_status run_base(mlora_ctx* ctx, const mlora_plan* plan, const void* A0, in
     pb.n_nblk = cdiv(N, 256);
     pb.num_tiles = pb.n_mblk * pb.n_nblk;
     pb.ext_tab = plan->d_ext;
-    return launch_gemm<MODE_BASE, 256, kBaseStages, false, B_MN>(ctx, tA0, tB0, tA1, tB1, pb, 1, s);
+    ProblemSet<1> set;
+    set.add(tA0, tB0, tA1, tB1, pb);
+    return launch_gemm<MODE_BASE, 256, kBaseStages, false, B_MN, 1, 1>(ctx, set, 1, s);
 }
 
 constexpr int kDownStages = 6;
 
-// MODE_DOWN with the K range split across a CTA pair (cluster of 2, DSMEM reduce).
+// Rank-r down-projections of n projections in ONE launch (K split across CTA
+// pairs, DSMEM reduction):  out_i = s_j in_i Bop_i^T, block-diagonal.
+//   forward (B_MN=false): in = X_i [rows, K_i], Bop = A_cat_i [R, K_i]  -> H_i
+//   backward (B_MN=true): in = dY_i [rows, K_i = d_i], Bop = B_cat_i [K_i, R] -> G_i
 template <bool B_MN>
-mlora_status launch_down_ksplit(mlora_ctx* ctx, const CUtensorMap& a0, const CUtensorMap& b0,
-                                const GemmParams& p, cudaStream_t stream) {
-    if (p.num_tiles <= 0) return MLORA_OK;
-    using L = GemmSmem<64, kDownStages, 2>;
-    auto kern = mlora_gemm_kernel<MODE_DOWN, 64, kDownStages, false, B_MN, 2>;
-    static bool attr_done = false;
-    if (!attr_done) {
-        MLORA_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 L::kDynBytes));
-        attr_done = true;
+mlora_status run_down_group(mlora_ctx* ctx, const mlora_plan* plan, int n, const int32_t* K,
+                            const void* const* in, const void* const* bop, void* const* out, cudaStream_t s) {
+    const int M = plan->rows, R = plan->R_pad;
+    for (int i0 = 0; i0 < n; i0 += kGroupMax) {
+        ProblemSet<kGroupMax> set;
+        for (int i = i0; i < std::min(n, i0 + kGroupMax); ++i) {
+            if (!in[i] || !bop[i] || !out[i]) return fail(ctx, MLORA_USAGE, "null tensor pointer");
+            if (K[i] <= 0 || K[i] % 8) return fail(ctx, MLORA_SHAPE, "down-projection width must be a positive multiple of 8");
+            CUtensorMap tA, tB;
+            mlora_status st;
+            if ((st = get_tmap(ctx, in[i], K[i], M, K[i], 64, 128, &tA)) != MLORA_OK) return st;
+            if (!B_MN) st = get_tmap(ctx, bop[i], K[i], R, K[i], 64, 64, &tB);   // A_cat [R, K] K-major
+            else st = get_tmap(ctx, bop[i], R, K[i], R, 64, 64, &tB);            // B_cat [K, R] MN-major
+            if (st != MLORA_OK) return st;
+            GemmParams p{};
+            p.M = M;
+            p.N = R;
+            p.num_kb = cdiv(K[i], kBK);
+            p.n_mblk = plan->n_mblk;
+            p.num_tiles = plan->n_down;
+            p.out = out[i];
+            p.ldo = R;
+            p.ext_tab = plan->d_ext;
+            p.down_tab = plan->d_down;
+            p.seg = plan->d_seg;
+            p.roff = plan->d_roff;
+            p.scale = plan->d_scale;
+            p.num_jobs = plan->J;
+            set.add(tA, tB, tA, tB, p);
+        }
+        mlora_status st = launch_gemm<MODE_DOWN, 64, kDownStages, false, B_MN, 2, kGroupMax>(ctx, set, 1, s);
+        if (st != MLORA_OK) return st;
     }
-    ProfScope ps(ctx, 2, stream);
-    MLORA_CUDA_TRY(ctx, launch_k(kern, dim3(2 * std::min(p.num_tiles, ctx->num_sms / 2)), dim3(kNumThreads),
-                                 L::kDynBytes, stream, 2, a0, b0, a0, b0, p));
-    ++ctx->launches;
     return MLORA_OK;
-}
-
-bool use_down_ksplit() {
-    static const bool on = [] {
-        const char* e = std::getenv("MLORA_DOWN_KERNEL");
-        return !(e && std::string(e) == "single");
-    }();
-    return on;
 }
 
 mlora_status check_dims(mlora_ctx* ctx, const mlora_plan* plan, int d, int k) {
@@ -362,56 +398,75 @@ mlora_status check_dims(mlora_ctx* ctx, const mlora_plan* plan, int d, int k) {
     return MLORA_OK;
 }
 
-// Choose the token-split count of a segmented gradient reduction so that the
-// grid covers ~2 CTAs per SM.
-int choose_nsplit(const mlora_ctx* ctx, const mlora_plan* plan, int F) {
-    const int base = cdiv(F, kBM) * plan->n_chunks;
-    int ns = std::max(1, cdiv(2 * ctx->num_sms, std::max(base, 1)));
+// Segmented gradient reductions of n projections in one launch:
+//   MODE_GRADT: dA_cat_i [R, F_i=k_i] = G_i^T X_i   (a = X_i, b = G_i)
+//   MODE_GRAD : dB_cat_i [F_i=d_i, R] = dY_i^T H_i  (a = dY_i, b = H_i)
+// each 64-column rank chunk reduced over its jobs' token range only.  The token
+// range is split (same split count for the whole group) only as far as needed
+// to give ~2 CTAs per SM; split partials are summed in a fixed order by one
+// grouped reduce launch (deterministic, no atomics).
+template <int MODE>
+mlora_status run_grad_group(mlora_ctx* ctx, const mlora_plan* plan, int n, const int32_t* F,
+                            const void* const* a, const void* const* b, float* const* out, cudaStream_t s) {
+    const int M = plan->rows, R = plan->R_pad;
+    long long base = 0;
+    for (int i = 0; i < n; ++i) {
+        if (!a[i] || !b[i] || !out[i]) return fail(ctx, MLORA_USAGE, "null tensor pointer");
+        if (F[i] <= 0 || F[i] % 8) return fail(ctx, MLORA_SHAPE, "gradient width must be a positive multiple of 8");
+        base += (long long)cdiv(F[i], kBM) * plan->n_chunks;
+    }
+    int ns = static_cast<int>(std::max<long long>(1, (2LL * ctx->num_sms + base - 1) / std::max<long long>(base, 1)));
     int max_len = 1;
     for (int c = 0; c < plan->n_chunks; ++c)
         max_len = std::max(max_len, plan->chunk_kb[2 * c + 1] - plan->chunk_kb[2 * c]);
-    ns = std::min(ns, std::max(1, max_len / 4));
-    return std::min(ns, kMaxSplit);
-}
-
-// Segmented reduction out = sum over the chunk token ranges (MODE_GRADT/GRAD).
-template <int MODE>
-mlora_status run_grad(mlora_ctx* ctx, const mlora_plan* plan, const CUtensorMap& ta,
-                      const CUtensorMap& tb, int F, float* out, cudaStream_t stream) {
-    const int ns = choose_nsplit(ctx, plan, F);
-    const long long nelem = (long long)F * plan->R_pad;
-    float* target = out;
+    ns = std::min({ns, std::max(1, max_len / 4), kMaxSplit});
+    std::vector<long long> part_off(n + 1, 0);
+    for (int i = 0; i < n; ++i) part_off[i + 1] = part_off[i] + (ns > 1 ? (long long)ns * F[i] * R : 0);
     if (ns > 1) {
-        mlora_status st = ensure_workspace(ctx, sizeof(float) * nelem * ns);
+        mlora_status st = ensure_workspace(ctx, sizeof(float) * part_off[n]);
         if (st != MLORA_OK) return st;
-        target = static_cast<float*>(ctx->workspace);
     }
-    GemmParams p{};
-    p.M = F;
-    p.N = plan->R_pad;
-    p.n_mblk = cdiv(F, kBM);
-    p.nsplit = ns;
-    p.num_tiles = p.n_mblk * plan->n_chunks * ns;
-    p.out = target;
-    p.ldo = (MODE == MODE_GRADT) ? F : plan->R_pad;
-    p.split_stride = nelem;
-    p.grad_tab = plan->d_grad + plan->grad_off[ns];
-    p.seg = plan->d_seg;
-    p.roff = plan->d_roff;
-    p.scale = plan->d_scale;
-    p.num_jobs = plan->J;
-    mlora_status st = launch_gemm<MODE, 64, kSmallStages, true, true>(ctx, ta, tb, ta, tb, p, 2, stream);
-    if (st != MLORA_OK) return st;
-    if (ns > 1) {
-        // fixed-order sum of the token-split partials (deterministic, no atomics)
-        const long long n4 = nelem / 4;
-        const int threads = 256;
-        const int blocks = static_cast<int>(std::min<long long>(cdiv(n4, threads), 4LL * ctx->num_sms));
-        ProfScope ps(ctx, 4, stream);
-        MLORA_CUDA_TRY(ctx, launch_k(reduce_splits_kernel, dim3(blocks), dim3(threads), 0, stream, 1,
-                                     reinterpret_cast<const float4*>(target), reinterpret_cast<float4*>(out), n4,
-                                     n4, ns));
-        ++ctx->launches;
+    float* ws = static_cast<float*>(ctx->workspace);
+    for (int i0 = 0; i0 < n; i0 += kGroupMax) {
+        ProblemSet<kGroupMax> set;
+        ReduceGroupArgs red{};
+        for (int i = i0; i < std::min(n, i0 + kGroupMax); ++i) {
+            CUtensorMap tA, tB;
+            mlora_status st;
+            if ((st = get_tmap(ctx, a[i], F[i], M, F[i], 64, 64, &tA)) != MLORA_OK) return st;  // MN-major
+            if ((st = get_tmap(ctx, b[i], R, M, R, 64, 64, &tB)) != MLORA_OK) return st;        // MN-major
+            const long long nelem = (long long)F[i] * R;
+            GemmParams p{};
+            p.M = F[i];
+            p.N = R;
+            p.n_mblk = cdiv(F[i], kBM);
+            p.nsplit = ns;
+            p.num_tiles = p.n_mblk * plan->n_chunks * ns;
+            p.out = ns > 1 ? static_cast<void*>(ws + part_off[i]) : static_cast<void*>(out[i]);
+            p.ldo = (MODE == MODE_GRADT) ? F[i] : R;
+            p.split_stride = nelem;
+            p.grad_tab = plan->d_grad + plan->grad_off[ns];
+            p.seg = plan->d_seg;
+            p.roff = plan->d_roff;
+            p.scale = plan->d_scale;
+            p.num_jobs = plan->J;
+            set.add(tA, tB, tA, tB, p);
+            ReduceGroupArgs::Item& it = red.item[red.n++];
+            it.part = reinterpret_cast<const float4*>(ws + part_off[i]);
+            it.out = reinterpret_cast<float4*>(out[i]);
+            it.n4 = nelem / 4;
+            it.start4 = red.total4;
+            red.total4 += it.n4;
+        }
+        mlora_status st = launch_gemm<MODE, 64, kSmallStages, true, true, 1, kGroupMax>(ctx, set, 2, s);
+        if (st != MLORA_OK) return st;
+        if (ns > 1) {
+            red.nsplit = ns;
+            const int blocks = static_cast<int>(std::min<long long>(cdiv(red.total4, 256), 8LL * ctx->num_sms));
+            ProfScope ps(ctx, 4, s);
+            MLORA_CUDA_TRY(ctx, launch_k(reduce_splits_group_kernel, dim3(blocks), dim3(256), 0, s, 1, red));
+            ++ctx->launches;
+        }
     }
     return MLORA_OK;
 }
@@ -701,32 +756,13 @@ mlora_status mlora_linear_fwd_ex(mlora_ctx* ctx, const mlora_plan* plan, int32_t
     if (!X || !W0 || !A_cat || !B_cat || !Y || !H) return fail(ctx, MLORA_USAGE, "null tensor pointer");
     DeviceGuard g(ctx->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const int M = plan->rows, R = plan->R_pad;
-    CUtensorMap tX, tA;
-    if ((st = get_tmap(ctx, X, k, M, k, 64, 128, &tX)) != MLORA_OK) return st;
-    if ((st = get_tmap(ctx, A_cat, k, R, k, 64, 64, &tA)) != MLORA_OK) return st;
-
     // (1) H = s_j X A_j^T, block-diagonal, bf16
-    GemmParams pd{};
-    pd.M = M;
-    pd.N = R;
-    pd.num_kb = cdiv(k, kBK);
-    pd.n_mblk = plan->n_mblk;
-    pd.num_tiles = plan->n_down;
-    pd.out = H;
-    pd.ldo = R;
-    pd.ext_tab = plan->d_ext;
-    pd.down_tab = plan->d_down;
-    pd.seg = plan->d_seg;
-    pd.roff = plan->d_roff;
-    pd.scale = plan->d_scale;
-    pd.num_jobs = plan->J;
-    st = use_down_ksplit() ? launch_down_ksplit<false>(ctx, tX, tA, pd, s)
-                           : launch_gemm<MODE_DOWN, 64, kSmallStages, false, false>(ctx, tX, tA, tX, tA, pd, 2, s);
+    const int32_t kk = k;
+    void* hh = H;
+    st = run_down_group<false>(ctx, plan, 1, &kk, &X, &A_cat, &hh, s);
     if (st != MLORA_OK) return st;
-
     // (2) Y = X W0^T + H B_cat^T
-    return run_base<false>(ctx, plan, X, k, k, W0, H, B_cat, R, d, Y, s, row_sq);
+    return run_base<false>(ctx, plan, X, k, k, W0, H, B_cat, plan->R_pad, d, Y, s, row_sq);
 }
 
 mlora_status mlora_linear_fwd(mlora_ctx* ctx, const mlora_plan* plan, int32_t d, int32_t k,
@@ -773,52 +809,75 @@ mlora_status mlora_linear_bwd(mlora_ctx* ctx, const mlora_plan* plan, int32_t d,
         return fail(ctx, MLORA_USAGE, "null tensor pointer");
     DeviceGuard g(ctx->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const int M = plan->rows, R = plan->R_pad;
-
+    const int32_t dd = d, kk = k;
+    void* gg = G;
     // (1) G = s_j dY B_j   (B operand B_cat viewed MN-major: n = rank col, k = d)
-    CUtensorMap tdY128, tBmn;
-    if ((st = get_tmap(ctx, dY, d, M, d, 64, 128, &tdY128)) != MLORA_OK) return st;
-    if ((st = get_tmap(ctx, B_cat, R, d, R, 64, 64, &tBmn)) != MLORA_OK) return st;
-    GemmParams pd{};
-    pd.M = M;
-    pd.N = R;
-    pd.num_kb = cdiv(d, kBK);
-    pd.n_mblk = plan->n_mblk;
-    pd.num_tiles = plan->n_down;
-    pd.out = G;
-    pd.ldo = R;
-    pd.ext_tab = plan->d_ext;
-    pd.down_tab = plan->d_down;
-    pd.seg = plan->d_seg;
-    pd.roff = plan->d_roff;
-    pd.scale = plan->d_scale;
-    pd.num_jobs = plan->J;
-    st = use_down_ksplit() ? launch_down_ksplit<true>(ctx, tdY128, tBmn, pd, s)
-                           : launch_gemm<MODE_DOWN, 64, kSmallStages, false, true>(ctx, tdY128, tBmn, tdY128, tBmn, pd, 2, s);
+    st = run_down_group<true>(ctx, plan, 1, &dd, &dY, &B_cat, &gg, s);
     if (st != MLORA_OK) return st;
-
     // (2) dX = dY W0 + G A_cat   (W0 and A_cat as MN-major B operands)
     if (dX) {
-        st = run_base<true>(ctx, plan, dY, d, d, W0, G, A_cat, R, k, dX, s);
+        st = run_base<true>(ctx, plan, dY, d, d, W0, G, A_cat, plan->R_pad, k, dX, s);
         if (st != MLORA_OK) return st;
     }
     // (3) dA_cat = G^T X over each chunk's token range  (stored R_pad x k)
     if (dA_cat) {
-        CUtensorMap tXmn, tGmn;
-        if ((st = get_tmap(ctx, X, k, M, k, 64, 64, &tXmn)) != MLORA_OK) return st;
-        if ((st = get_tmap(ctx, G, R, M, R, 64, 64, &tGmn)) != MLORA_OK) return st;
-        st = run_grad<MODE_GRADT>(ctx, plan, tXmn, tGmn, k, dA_cat, s);
+        const void* gc = G;
+        st = run_grad_group<MODE_GRADT>(ctx, plan, 1, &kk, &X, &gc, &dA_cat, s);
         if (st != MLORA_OK) return st;
     }
     // (4) dB_cat = dY^T H over each chunk's token range  (stored d x R_pad)
     if (dB_cat) {
-        CUtensorMap tdYmn, tHmn;
-        if ((st = get_tmap(ctx, dY, d, M, d, 64, 64, &tdYmn)) != MLORA_OK) return st;
-        if ((st = get_tmap(ctx, H, R, M, R, 64, 64, &tHmn)) != MLORA_OK) return st;
-        st = run_grad<MODE_GRAD>(ctx, plan, tdYmn, tHmn, d, dB_cat, s);
+        st = run_grad_group<MODE_GRAD>(ctx, plan, 1, &dd, &dY, &H, &dB_cat, s);
         if (st != MLORA_OK) return st;
     }
     return MLORA_OK;
+}
+
+// ---------------------------------------------------------------- layer-level grouped entry points
+mlora_status mlora_down_group(mlora_ctx* ctx, const mlora_plan* plan, int32_t n, int32_t backward,
+                              const int32_t* width, const void* const* in, const void* const* adapter,
+                              void* const* out, void* stream) {
+    if (!ctx || !plan || n < 0 || (n > 0 && (!width || !in || !adapter || !out)))
+        return fail(ctx, MLORA_USAGE, "null argument");
+    if (plan->ctx != ctx) return fail(ctx, MLORA_USAGE, "plan belongs to another context");
+    DeviceGuard g(ctx->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    return backward ? run_down_group<true>(ctx, plan, n, width, in, adapter, out, s)
+                    : run_down_group<false>(ctx, plan, n, width, in, adapter, out, s);
+}
+
+mlora_status mlora_base_fwd(mlora_ctx* ctx, const mlora_plan* plan, int32_t d, int32_t k, const void* X,
+                            const void* W0, const void* H, const void* B_cat, void* Y, float* row_sq,
+                            void* stream) {
+    mlora_status st = check_dims(ctx, plan, d, k);
+    if (st != MLORA_OK) return st;
+    if (!X || !W0 || !H || !B_cat || !Y) return fail(ctx, MLORA_USAGE, "null tensor pointer");
+    DeviceGuard g(ctx->device);
+    return run_base<false>(ctx, plan, X, k, k, W0, H, B_cat, plan->R_pad, d, Y, static_cast<cudaStream_t>(stream),
+                           row_sq);
+}
+
+mlora_status mlora_base_dx(mlora_ctx* ctx, const mlora_plan* plan, int32_t d, int32_t k, const void* dY,
+                           const void* W0, const void* G, const void* A_cat, void* dX, void* stream) {
+    mlora_status st = check_dims(ctx, plan, d, k);
+    if (st != MLORA_OK) return st;
+    if (!dY || !W0 || !G || !A_cat || !dX) return fail(ctx, MLORA_USAGE, "null tensor pointer");
+    DeviceGuard g(ctx->device);
+    return run_base<true>(ctx, plan, dY, d, d, W0, G, A_cat, plan->R_pad, k, dX, static_cast<cudaStream_t>(stream));
+}
+
+mlora_status mlora_grad_group(mlora_ctx* ctx, const mlora_plan* plan, int32_t n, const int32_t* d,
+                              const int32_t* k, const void* const* X, const void* const* dY,
+                              const void* const* H, const void* const* G, float* const* dA_cat,
+                              float* const* dB_cat, void* stream) {
+    if (!ctx || !plan || n < 0 || (n > 0 && (!d || !k || !X || !dY || !H || !G || !dA_cat || !dB_cat)))
+        return fail(ctx, MLORA_USAGE, "null argument");
+    if (plan->ctx != ctx) return fail(ctx, MLORA_USAGE, "plan belongs to another context");
+    DeviceGuard g(ctx->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    mlora_status st = run_grad_group<MODE_GRADT>(ctx, plan, n, k, X, G, dA_cat, s);
+    if (st != MLORA_OK) return st;
+    return run_grad_group<MODE_GRAD>(ctx, plan, n, d, dY, H, dB_cat, s);
 }
 
 mlora_status mlora_pack_adapters(mlora_ctx* ctx, const mlora_plan* plan, int32_t d, int32_t k,

@@ -122,16 +122,33 @@ __device__ __forceinline__ int job_of_row(const int* seg, int num_jobs, int row)
     return lo;
 }
 
+// One GEMM problem of a (possibly grouped) launch: its operand tensor maps, its
+// parameters and the global index of its first tile.  A launch carries up to NP
+// problems by value in the kernel's parameter space (__grid_constant__), so one
+// launch serves e.g. the rank-r down-projections of every projection of a layer:
+// the ~12 us fixed cost of an HBM-bound launch (pipeline fill, TMEM/barrier
+// setup, tail) is paid once per layer instead of once per projection.
+struct alignas(64) GemmProblem {
+    CUtensorMap tmA0, tmB0, tmA1, tmB1;
+    GemmParams p;
+    int tile_begin;
+};
+
+template <int NP>
+struct GemmProblemSet {
+    GemmProblem prob[NP];
+    int nprobs;
+    int total_tiles;
+};
+
 // KSPLIT = 2 (MODE_DOWN): launched in clusters of 2; CTA r of the pair reduces
 // the r-th half of the K range into its own TMEM, the follower ships its fp32
 // partial tile to the leader's smem over DSMEM and the leader adds it in a fixed
 // order (deterministic) before the masked/scaled store.  Doubles the CTAs that
 // stream the HBM-bound operand and halves the bytes each must keep in flight.
-template <int MODE, int BN, int STAGES, bool A_MN, bool B_MN, int KSPLIT = 1>
+template <int MODE, int BN, int STAGES, bool A_MN, bool B_MN, int KSPLIT = 1, int NP = 1>
 __global__ void __launch_bounds__(kNumThreads, 1)
-mlora_gemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmB0,
-                  const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1,
-                  const GemmParams p) {
+mlora_gemm_kernel(const __grid_constant__ GemmProblemSet<NP> ps) {
     using namespace sm100;
     using L = GemmSmem<BN, STAGES, KSPLIT>;
     static_assert(KSPLIT == 1 || (KSPLIT == 2 && MODE == MODE_DOWN && BN == 64), "K split: DOWN, BN=64 only");
@@ -157,22 +174,31 @@ mlora_gemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constan
     const uint32_t krank = KSPLIT == 2 ? cluster_ctarank() : 0u;
     const int t_first = static_cast<int>(blockIdx.x) / KSPLIT;
     const int t_step = static_cast<int>(gridDim.x) / KSPLIT;
+    // problem owning global tile t (problems are few and tiles visited in order)
+    auto find = [&](int t) {
+        int pi = 0;
+        while (pi + 1 < ps.nprobs && ps.prob[pi + 1].tile_begin <= t) ++pi;
+        return pi;
+    };
     // this CTA's tile program: for a K-split pair, its half of the main k-blocks
-    auto tile_of = [&](int t) {
-        TileInfo ti = decode_tile<MODE, BN>(p, t);
+    auto tile_of = [&](int pi, int t) {
+        TileInfo ti = decode_tile<MODE, BN>(ps.prob[pi].p, t - ps.prob[pi].tile_begin);
         if constexpr (KSPLIT == 2) {
             const int mid = ti.kb0 + (ti.kb1 - ti.kb0) / 2;
             if (krank == 0) ti.kb1 = mid; else ti.kb0 = mid;
         }
         return ti;
     };
+    const int num_tiles = ps.total_tiles;
 
     if (warp == 0 && elect_one()) {
-        tma_prefetch_desc(&tmA0);
-        tma_prefetch_desc(&tmB0);
-        if constexpr (MODE == MODE_BASE) {
-            tma_prefetch_desc(&tmA1);
-            tma_prefetch_desc(&tmB1);
+        for (int pi = 0; pi < ps.nprobs; ++pi) {
+            tma_prefetch_desc(&ps.prob[pi].tmA0);
+            tma_prefetch_desc(&ps.prob[pi].tmB0);
+            if constexpr (MODE == MODE_BASE) {
+                tma_prefetch_desc(&ps.prob[pi].tmA1);
+                tma_prefetch_desc(&ps.prob[pi].tmB1);
+            }
         }
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(full_bar + s, 1);
@@ -202,15 +228,17 @@ mlora_gemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constan
         if (elect_one()) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = t_first; t < p.num_tiles; t += t_step) {
-                const TileInfo ti = tile_of(t);
+            for (int t = t_first; t < num_tiles; t += t_step) {
+                const int pi = find(t);
+                const GemmProblem& P = ps.prob[pi];
+                const TileInfo ti = tile_of(pi, t);
                 const int nmain = ti.kb1 - ti.kb0;
                 const int nk = nmain + (ti.xb1 - ti.xb0);
                 for (int it = 0; it < nk; ++it) {
                     mbar_wait(empty_bar + stage, phase ^ 1u);
                     const bool ext = it >= nmain;
-                    const CUtensorMap* mA = ext ? &tmA1 : &tmA0;
-                    const CUtensorMap* mB = ext ? &tmB1 : &tmB0;
+                    const CUtensorMap* mA = ext ? &P.tmA1 : &P.tmA0;
+                    const CUtensorMap* mB = ext ? &P.tmB1 : &P.tmB0;
                     const int kc = (ext ? (ti.xb0 + it - nmain) : (ti.kb0 + it)) * kBK;
                     const uint32_t sA = base_addr + stage * L::kStageBytes;
                     const uint32_t sB = sA + L::kABytes;
@@ -239,8 +267,8 @@ mlora_gemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constan
         int stage = 0;
         uint32_t phase = 0;
         int local = 0;
-        for (int t = t_first; t < p.num_tiles; t += t_step, ++local) {
-            const TileInfo ti = tile_of(t);
+        for (int t = t_first; t < num_tiles; t += t_step, ++local) {
+            const TileInfo ti = tile_of(find(t), t);
             const int nk = (ti.kb1 - ti.kb0) + (ti.xb1 - ti.xb0);
             const int acc = local & 1;
             const uint32_t use = static_cast<uint32_t>(local >> 1);
@@ -274,8 +302,10 @@ mlora_gemm_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constan
         const uint32_t q = warp & 3;  // TMEM lane quarter this warp may access
         const int rloc = static_cast<int>(q * 32 + lane);
         int local = 0;
-        for (int t = t_first; t < p.num_tiles; t += t_step, ++local) {
-            const TileInfo ti = tile_of(t);
+        for (int t = t_first; t < num_tiles; t += t_step, ++local) {
+            const int pi = find(t);
+            const GemmParams& p = ps.prob[pi].p;
+            const TileInfo ti = tile_of(pi, t);
             const bool empty = (ti.kb1 - ti.kb0) + (ti.xb1 - ti.xb0) == 0;
             const int acc = local & 1;
             const uint32_t use = static_cast<uint32_t>(local >> 1);

@@ -129,24 +129,61 @@ class FusedLoraLayer:
         return next(q for q in self.proj if q.name == src).Y[:rows]
 
     def forward_backward(self, x: torch.Tensor, stream=None) -> torch.Tensor:
+        """Grouped schedule: every HBM-bound op is issued once for all projections
+        whose inputs are ready (mlora_down_group / mlora_grad_group), the tensor-
+        bound base GEMMs once per projection.  LLaMA layer: 2 forward down-group
+        launches, 7 base GEMMs, loss, 1 backward down-group, 7 dX GEMMs, 1 grad group."""
         ctx, plan = self.ctx, self.plan
+        L, s = N.lib(), F._stream_handle(stream)
         rows = getattr(self, "cur_rows", self.rows)
-        inputs, rowsq = [], []
-        for p in self.proj:
-            xin = self._input(p.src, x, rows)
-            inputs.append(xin)
-            Y, H, _, _, rsq = self._views(p, rows)
-            rowsq.append(rsq)
-            F.linear_fwd(ctx, plan, xin, p.W0, p.A.p_bf16, p.B.p_bf16, Y, H, row_sq=rsq, stream=stream)
-        # per-job loss from the row sums the forward GEMM epilogues produced (no re-read of Y)
-        ptrs = (N.vp * len(rowsq))(*[t.data_ptr() for t in rowsq])
-        N.check(N.lib().mlora_loss_from_rowsq(ctx.handle, plan.handle, ptrs, self._rowsq_d,
-                                              len(self.proj), self.loss.data_ptr(),
-                                              F._stream_handle(stream)), ctx.handle)
-        for p, xin in zip(reversed(self.proj), reversed(inputs)):
-            Y, H, G, dX, _ = self._views(p, rows)
-            F.linear_bwd(ctx, plan, Y, xin, H, p.W0, p.A.p_bf16, p.B.p_bf16, need_dX=True, dX=dX,
-                         dA_cat=p.dA, dB_cat=p.dB, G=G, stream=stream)
+        views = [self._views(p, rows) for p in self.proj]
+        inputs: dict[int, torch.Tensor] = {}
+        done: set[str] = set()
+        # ---- forward, in dependency waves
+        while len(done) < len(self.proj):
+            source = lambda src: None if src == "x" else ("h_to_4h" if src == "h_to_4h_half" else src)
+            wave = [i for i, p in enumerate(self.proj)
+                    if p.name not in done and (source(p.src) is None or source(p.src) in done)]
+            if not wave:
+                raise RuntimeError("projection inputs form a cycle")
+            for i in wave:
+                inputs[i] = self._input(self.proj[i].src, x, rows)
+            n = len(wave)
+            N.check(L.mlora_down_group(ctx.handle, plan.handle, n, 0,
+                                       (N.i32 * n)(*[self.proj[i].k for i in wave]),
+                                       (N.vp * n)(*[inputs[i].data_ptr() for i in wave]),
+                                       (N.vp * n)(*[self.proj[i].A.p_bf16.data_ptr() for i in wave]),
+                                       (N.vp * n)(*[views[i][1].data_ptr() for i in wave]), s), ctx.handle)
+            for i in wave:
+                p = self.proj[i]
+                Y, H, _, _, rsq = views[i]
+                N.check(L.mlora_base_fwd(ctx.handle, plan.handle, p.d, p.k, inputs[i].data_ptr(), p.W0.data_ptr(),
+                                         H.data_ptr(), p.B.p_bf16.data_ptr(), Y.data_ptr(), rsq.data_ptr(), s),
+                        ctx.handle)
+                done.add(p.name)
+        # ---- per-job loss from the row sums the forward GEMM epilogues produced (no re-read of Y)
+        n = len(self.proj)
+        ptrs = (N.vp * n)(*[v[4].data_ptr() for v in views])
+        N.check(L.mlora_loss_from_rowsq(ctx.handle, plan.handle, ptrs, self._rowsq_d, n, self.loss.data_ptr(), s),
+                ctx.handle)
+        # ---- backward: dL/dY_p = Y_p for every projection
+        N.check(L.mlora_down_group(ctx.handle, plan.handle, n, 1, (N.i32 * n)(*[p.d for p in self.proj]),
+                                   (N.vp * n)(*[v[0].data_ptr() for v in views]),
+                                   (N.vp * n)(*[p.B.p_bf16.data_ptr() for p in self.proj]),
+                                   (N.vp * n)(*[v[2].data_ptr() for v in views]), s), ctx.handle)
+        for i in reversed(range(n)):
+            p = self.proj[i]
+            Y, _, G, dX, _ = views[i]
+            N.check(L.mlora_base_dx(ctx.handle, plan.handle, p.d, p.k, Y.data_ptr(), p.W0.data_ptr(), G.data_ptr(),
+                                    p.A.p_bf16.data_ptr(), dX.data_ptr(), s), ctx.handle)
+        N.check(L.mlora_grad_group(ctx.handle, plan.handle, n, (N.i32 * n)(*[p.d for p in self.proj]),
+                                   (N.i32 * n)(*[p.k for p in self.proj]),
+                                   (N.vp * n)(*[inputs[i].data_ptr() for i in range(n)]),
+                                   (N.vp * n)(*[v[0].data_ptr() for v in views]),
+                                   (N.vp * n)(*[v[1].data_ptr() for v in views]),
+                                   (N.vp * n)(*[v[2].data_ptr() for v in views]),
+                                   (N.vp * n)(*[p.dA.data_ptr() for p in self.proj]),
+                                   (N.vp * n)(*[p.dB.data_ptr() for p in self.proj]), s), ctx.handle)
         return self.loss
 
     def optimizer_step(self, active=None, stream=None) -> None:
