@@ -331,6 +331,14 @@ mlora_status run_base(mlora_ctx* ctx, const mlora_plan* plan, const void* A0, in
     pb.row_sq = row_sq;
     if (row_sq && !pair) return fail(ctx, MLORA_USAGE, "fused row sums need the CTA-pair base kernel");
     if (pair) {
+        // super-row of m-blocks whose A slab (~32 MB) stays L2-resident while all of B streams past it
+        static const int raster_env = [] {
+            const char* e = std::getenv("MLORA_RASTER");
+            return e ? std::atoi(e) : -1;
+        }();
+        const long long slab = (long long)kPairBM * K0 * 2;
+        pb.raster_group = raster_env >= 0 ? raster_env
+                                          : static_cast<int>(std::max<long long>(1, (32LL << 20) / slab));
         pb.n_mblk = plan->n_mblk256;
         pb.n_nblk = cdiv(N, kPairBN);
         pb.num_tiles = pb.n_mblk * pb.n_nblk;

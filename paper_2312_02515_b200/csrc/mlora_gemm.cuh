@@ -50,6 +50,7 @@ struct GemmParams {
     const int* down_tab;  // [num_tiles][3] (m_blk, chunk, flags) for MODE_DOWN
     const int* grad_tab;  // [nchunks*nsplit][2] token k-block range
     float* row_sq;        // BASE (pair) optional: [n_nblk][M] sum over the tile's columns of bf16(Y)^2
+    int raster_group;     // BASE (pair): m-blocks per raster super-row (<= 0: plain m-fastest)
     const int* seg;       // [J+1] row offsets of job segments
     const int* roff;      // [J+1] padded rank column offsets
     const float* scale;   // [J] per-job LoRA scale s_j
@@ -470,6 +471,18 @@ mlora_gemm_kernel(const __grid_constant__ GemmProblemSet<NP> ps) {
 constexpr int kPairBM = 256;
 constexpr int kPairBN = 256;
 
+// Grouped raster: tiles walk super-rows of `group_m` m-blocks (m fastest inside a
+// super-row) so the A rows of a super-row stay L2-resident while every n-block
+// of B streams past them; group_m <= 0 means plain m-fastest order.
+__device__ __forceinline__ void pair_tile_coords(const GemmParams& p, int t, int& mb, int& nb) {
+    const int gm = p.raster_group > 0 ? p.raster_group : p.n_mblk;
+    const int per_group = gm * p.n_nblk;
+    const int g = t / per_group, r = t - g * per_group;
+    const int rows_in_group = min(gm, p.n_mblk - g * gm);
+    mb = g * gm + r % rows_in_group;
+    nb = r / rows_in_group;
+}
+
 template <int STAGES>
 struct PairSmem {
     static constexpr int kABytes = 128 * kBK * 2;   // this CTA's A rows
@@ -539,8 +552,8 @@ mlora_base_pair_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_co
             int stage = 0;
             uint32_t phase = 0;
             for (int t = cluster_id; t < p.num_tiles; t += nclusters) {
-                const int mb = t % p.n_mblk;
-                const int nb = t / p.n_mblk;
+                int mb, nb;
+                pair_tile_coords(p, t, mb, nb);
                 const int m0 = mb * kPairBM + static_cast<int>(cta) * 128;
                 const int n0 = nb * kPairBN + static_cast<int>(cta) * 128;
                 const int xb0 = __ldg(p.ext_tab + 2 * mb), xb1 = __ldg(p.ext_tab + 2 * mb + 1);
@@ -574,7 +587,8 @@ mlora_base_pair_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_co
             uint32_t phase = 0;
             int local = 0;
             for (int t = cluster_id; t < p.num_tiles; t += nclusters, ++local) {
-                const int mb = t % p.n_mblk;
+                int mb, nb;
+                pair_tile_coords(p, t, mb, nb);
                 const int nk = p.num_kb + (__ldg(p.ext_tab + 2 * mb + 1) - __ldg(p.ext_tab + 2 * mb));
                 const int acc = local & 1;
                 const uint32_t use = static_cast<uint32_t>(local >> 1);
@@ -610,8 +624,8 @@ mlora_base_pair_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_co
         __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out);
         int local = 0;
         for (int t = cluster_id; t < p.num_tiles; t += nclusters, ++local) {
-            const int mb = t % p.n_mblk;
-            const int nb = t / p.n_mblk;
+            int mb, nb;
+            pair_tile_coords(p, t, mb, nb);
             const int acc = local & 1;
             const uint32_t use = static_cast<uint32_t>(local >> 1);
             mbar_wait(tfull_bar + acc, use & 1u);
