@@ -391,6 +391,7 @@ mlora_status run_down_group(mlora_ctx* ctx, const mlora_plan* plan, int n, const
             p.num_jobs = plan->J;
             set.add(tA, tB, tA, tB, p);
         }
+        set.ps.interleave = 1;  // equal tile counts; projections sharing an input read it together
         mlora_status st = launch_gemm<MODE_DOWN, 64, kDownStages, false, B_MN, 2, kGroupMax>(ctx, set, 1, s);
         if (st != MLORA_OK) return st;
     }

@@ -140,6 +140,10 @@ struct GemmProblemSet {
     GemmProblem prob[NP];
     int nprobs;
     int total_tiles;
+    // 1: all problems have the same tile count and tile t is tile t / nprobs of
+    // problem t % nprobs, so problems reading the same operand rows (e.g. the
+    // projections fed by one hidden state) run them concurrently and share L2.
+    int interleave;
 };
 
 // KSPLIT = 2 (MODE_DOWN): launched in clusters of 2; CTA r of the pair reduces
@@ -177,13 +181,15 @@ mlora_gemm_kernel(const __grid_constant__ GemmProblemSet<NP> ps) {
     const int t_step = static_cast<int>(gridDim.x) / KSPLIT;
     // problem owning global tile t (problems are few and tiles visited in order)
     auto find = [&](int t) {
+        if (ps.interleave) return t % ps.nprobs;
         int pi = 0;
         while (pi + 1 < ps.nprobs && ps.prob[pi + 1].tile_begin <= t) ++pi;
         return pi;
     };
     // this CTA's tile program: for a K-split pair, its half of the main k-blocks
     auto tile_of = [&](int pi, int t) {
-        TileInfo ti = decode_tile<MODE, BN>(ps.prob[pi].p, t - ps.prob[pi].tile_begin);
+        const int local_t = ps.interleave ? t / ps.nprobs : t - ps.prob[pi].tile_begin;
+        TileInfo ti = decode_tile<MODE, BN>(ps.prob[pi].p, local_t);
         if constexpr (KSPLIT == 2) {
             const int mid = ti.kb0 + (ti.kb1 - ti.kb0) / 2;
             if (krank == 0) ti.kb1 = mid; else ti.kb0 = mid;
