@@ -232,7 +232,6 @@ def main():
     xg = torch.Generator(device="cpu").manual_seed(77 + rank)
     x_host = (torch.rand(rows, shapes[0][2], generator=xg) * 2 - 1).to(torch.bfloat16).pin_memory()
     x = x_host.to(dev)
-    loss_host = torch.empty(J, dtype=torch.float32).pin_memory()
     stream = torch.cuda.current_stream()
 
     def barrier():

@@ -248,8 +248,10 @@ mlora_status mlora_rope(int64_t rows, int32_t heads, int32_t head_dim, const voi
 
 /* Per-job synthetic layer loss L_j = 1/2 sum_p sum_{t in job j} ||Y_p[t]||^2 over
  * `num_tensors` bf16 tensors Y[p] (rows x cols[p]); loss: device fp32 [J].
- * Deterministic (fixed-order two-level reduction).  Used by the trainer step:
- * the reference's only runtime loss consumer is detect_stop (progress.cpp:90-124). */
+ * Deterministic (fixed-order two-level reduction).  Unfused form of the loss the
+ * trainer step takes from the forward GEMM epilogues (mlora_linear_fwd_ex +
+ * mlora_loss_from_rowsq); the reference's only runtime loss consumer is
+ * detect_stop (progress.cpp:90-124). */
 mlora_status mlora_segment_sumsq_loss(mlora_ctx* ctx, const mlora_plan* plan, const void* const* Y,
                                       const int32_t* cols, int32_t num_tensors, float* loss, void* stream);
 

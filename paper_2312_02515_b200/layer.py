@@ -102,7 +102,6 @@ class FusedLoraLayer:
                 torch.empty(rows, k, dtype=torch.bfloat16, device=dev),
                 torch.empty(N.lib().mlora_rowsq_blocks(d), rows, dtype=torch.float32, device=dev)))
         self.loss = torch.zeros(self.J, dtype=torch.float32, device=dev)
-        self._rowsq_ptrs = (N.vp * len(self.proj))(*[p.row_sq.data_ptr() for p in self.proj])
         self._rowsq_d = (N.i32 * len(self.proj))(*[p.d for p in self.proj])
 
     def set_layout(self, seg_offsets) -> None:

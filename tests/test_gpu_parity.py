@@ -270,6 +270,15 @@ def test_layer_step_loss_and_progress(F, ctx):
     # per-job loss = 1/2 sum over projections of ||Y||^2 on the job's rows (oracle on the step's own Y)
     want = [0.5 * sum(float((p.Y[seg[j]:seg[j + 1]].double() ** 2).sum()) for p in layer.proj) for j in range(2)]
     assert np.allclose(l0.cpu().numpy(), want, rtol=1e-4)
+    # the unfused loss entry point (reads Y back) agrees with the GEMM-epilogue row sums
+    from paper_2312_02515_b200 import _native as N
+    n = len(layer.proj)
+    alt = torch.zeros(2, dtype=torch.float32, device=ctx.device)
+    N.check(N.lib().mlora_segment_sumsq_loss(ctx.handle, layer.plan.handle,
+                                             (N.vp * n)(*[p.Y.data_ptr() for p in layer.proj]),
+                                             (N.i32 * n)(*[p.d for p in layer.proj]), n, alt.data_ptr(),
+                                             torch.cuda.current_stream().cuda_stream), ctx.handle)
+    assert np.allclose(alt.cpu().numpy(), want, rtol=1e-4)
     for _ in range(5):
         l1 = layer.step(x).clone()
     torch.cuda.synchronize()
