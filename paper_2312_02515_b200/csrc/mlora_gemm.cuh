@@ -365,6 +365,8 @@ mlora_gemm_kernel(const __grid_constant__ GemmProblemSet<NP> ps) {
                         for (int g = 0; g < BN / 4; ++g)
                             st_cluster_v4(mapa_shared(smem_u32(part + g * kBM + rloc), 0),
                                           make_float4(accv[4 * g], accv[4 * g + 1], accv[4 * g + 2], accv[4 * g + 3]));
+                        // every lane orders its DSMEM stores at cluster scope before lane 0's release-arrive
+                        asm volatile("fence.acq_rel.cluster;" ::: "memory");
                         __syncwarp();
                         if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(pfull_bar), 0));
                         store = false;
@@ -378,6 +380,8 @@ mlora_gemm_kernel(const __grid_constant__ GemmProblemSet<NP> ps) {
                             accv[4 * g + 2] += q4.z;
                             accv[4 * g + 3] += q4.w;
                         }
+                        // reads of the partial buffer complete before the follower may overwrite it
+                        asm volatile("fence.acq_rel.cluster;" ::: "memory");
                         __syncwarp();
                         if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(pempty_bar), 1));
                     }
