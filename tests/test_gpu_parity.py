@@ -321,3 +321,37 @@ def test_pipelined_trainer_matches_sequential_steps(F, ctx):
     PipelinedTrainer(b, 256, 256).run(xs, losses)
     torch.cuda.synchronize()
     assert torch.equal(torch.stack(want).cpu(), losses)
+
+
+@pytest.mark.parametrize("J", [1, 4, 8])
+def test_launch_count_independent_of_jobs(F, ctx, J):
+    """§8f launch-count validation.  The paper's fused scheme needs 2k small + 2
+    large launches per linear (count_launches, lora.cpp:184-189; per-job: 4k); the
+    B200 path issues 2 per linear forward (down-projection + base GEMM) and a fixed
+    number per layer step, whatever the number of fused jobs k."""
+    import ctypes as C
+    from paper_2312_02515_b200 import _native as N
+    from paper_2312_02515_b200.layer import TINY, FusedLoraLayer
+    rows = 64 * J
+    seg = [64 * j for j in range(J + 1)]
+    plan = F.Plan(ctx, seg, [8] * J, [1.0] * J)
+    X = torch.zeros(rows, 256, dtype=torch.bfloat16, device=ctx.device)
+    W = torch.zeros(256, 256, dtype=torch.bfloat16, device=ctx.device)
+    A = torch.zeros(plan.rank_padded, 256, dtype=torch.bfloat16, device=ctx.device)
+    B = torch.zeros(256, plan.rank_padded, dtype=torch.bfloat16, device=ctx.device)
+    n0 = ctx.launches
+    F.linear_fwd(ctx, plan, X, W, A, B)
+    assert ctx.launches - n0 == 2
+    s, l = C.c_int64(), C.c_int64()
+    N.check(N.lib().mlora_count_launches(J, 1, C.byref(s), C.byref(l)))
+    assert s.value + l.value == 2 * J + 2          # the reference's analytic fused count
+    layer = FusedLoraLayer(ctx, TINY, [8] * J, [1.0] * J, [1e-3] * J, rows=rows, seed=J)
+    layer.set_layout(seg)
+    layer.step(X)
+    n1 = ctx.launches
+    layer.step(X)
+    per_step = ctx.launches - n1
+    assert per_step <= 24, per_step                 # 7 projections, fwd + loss + bwd + AdamW
+    test_launch_count_independent_of_jobs.counts = getattr(test_launch_count_independent_of_jobs, "counts", set())
+    test_launch_count_independent_of_jobs.counts.add(per_step)
+    assert len(test_launch_count_independent_of_jobs.counts) == 1  # identical for every J
