@@ -109,6 +109,11 @@ mlora_status mlora_count_launches(int32_t num_jobs, int32_t mode, int64_t* small
 mlora_status mlora_plan_create(mlora_ctx* ctx, int32_t num_jobs, const int64_t* seg_offsets,
                                const int32_t* ranks, const float* scales, void* stream,
                                mlora_plan** out);
+/* Re-point an existing plan (same jobs, ranks and scales) at the next fused
+ * batch's segment layout.  Stream-ordered and non-blocking: the tables go up
+ * through pinned staging on `stream`, so kernels already enqueued there still
+ * read the previous layout and the host can pack step t+1 while step t runs. */
+mlora_status mlora_plan_update(mlora_plan* plan, const int64_t* seg_offsets, void* stream);
 mlora_status mlora_plan_destroy(mlora_plan* plan);
 int64_t mlora_plan_rows(const mlora_plan* plan);
 int32_t mlora_plan_rank_padded(const mlora_plan* plan);

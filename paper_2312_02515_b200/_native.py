@@ -47,6 +47,7 @@ _SIGS = {
     "mlora_count_launches": (i32, [i32, i32, C.POINTER(i64), C.POINTER(i64)]),
     "mlora_plan_create": (i32, [vp, i32, C.POINTER(i64), C.POINTER(i32), C.POINTER(f32), vp, C.POINTER(vp)]),
     "mlora_plan_destroy": (i32, [vp]),
+    "mlora_plan_update": (i32, [vp, C.POINTER(i64), vp]),
     "mlora_plan_rows": (i64, [vp]),
     "mlora_plan_rank_padded": (i32, [vp]),
     "mlora_plan_rank_offsets": (i32, [vp, C.POINTER(i32)]),

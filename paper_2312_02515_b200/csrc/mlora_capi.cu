@@ -74,8 +74,12 @@ struct mlora_plan {
     int n_down = 0;
     std::vector<int> chunk_kb;            // [n_chunks][2] token k-block range
     int grad_off[kMaxSplit + 1] = {0};    // offset (ints) of the split-ns table
-    // device copies (one allocation)
+    // device copies (one allocation, grow-only) and the pinned staging of their upload
     void* dev = nullptr;
+    size_t dev_bytes = 0;
+    void* staging = nullptr;
+    size_t staging_bytes = 0;
+    cudaEvent_t staging_done = nullptr;
     int* d_seg = nullptr;
     int* d_roff = nullptr;
     float* d_scale = nullptr;
@@ -608,50 +612,37 @@ mlora_status mlora_count_launches(int32_t num_jobs, int32_t mode, int64_t* small
     return MLORA_OK;
 }
 
-mlora_status mlora_plan_create(mlora_ctx* ctx, int32_t num_jobs, const int64_t* seg_offsets,
-                               const int32_t* ranks, const float* scales, void* stream,
-                               mlora_plan** out) {
-    if (!ctx || !out || !seg_offsets || !ranks) return fail(ctx, MLORA_USAGE, "null argument");
-    *out = nullptr;
-    if (num_jobs < 1 || num_jobs > kMaxJobs)
-        return fail(ctx, MLORA_USAGE, "num_jobs must be in [1, " + std::to_string(kMaxJobs) + "]");
-    if (seg_offsets[0] != 0) return fail(ctx, MLORA_USAGE, "seg_offsets[0] must be 0");
-    for (int j = 0; j < num_jobs; ++j) {
-        if (seg_offsets[j + 1] < seg_offsets[j])
-            return fail(ctx, MLORA_USAGE, "seg_offsets must be non-decreasing");
-        if (ranks[j] < 1) return fail(ctx, MLORA_USAGE, "adapter rank must be >= 1");
-        if (scales && !std::isfinite(scales[j])) return fail(ctx, MLORA_NUMERIC, "non-finite scale");
-    }
-    const long long rows = seg_offsets[num_jobs];
-    if (rows < 1) return fail(ctx, MLORA_USAGE, "fused batch has no rows");
-    if (rows > (1LL << 30)) return fail(ctx, MLORA_USAGE, "too many rows");
-    DeviceGuard g(ctx->device);
+}  // extern "C"
 
-    auto* p = new mlora_plan();
-    p->ctx = ctx;
-    p->J = num_jobs;
+namespace {
+
+mlora_status check_segments(mlora_ctx* ctx, int32_t num_jobs, const int64_t* seg_offsets) {
+    if (!seg_offsets) return fail(ctx, MLORA_USAGE, "null argument");
+    if (seg_offsets[0] != 0) return fail(ctx, MLORA_USAGE, "seg_offsets[0] must be 0");
+    for (int j = 0; j < num_jobs; ++j)
+        if (seg_offsets[j + 1] < seg_offsets[j]) return fail(ctx, MLORA_USAGE, "seg_offsets must be non-decreasing");
+    if (seg_offsets[num_jobs] < 1) return fail(ctx, MLORA_USAGE, "fused batch has no rows");
+    if (seg_offsets[num_jobs] > (1LL << 30)) return fail(ctx, MLORA_USAGE, "too many rows");
+    return MLORA_OK;
+}
+
+// Host tables of a segment layout (ranks/roff/scale already set) -> one blob:
+// seg | roff | scale | ext | ext256 | down | grad, with the section offsets.
+std::vector<int> build_tables(mlora_plan* p, const int64_t* seg_offsets, size_t off[7]) {
+    const int J = p->J;
+    const long long rows = seg_offsets[J];
     p->rows = static_cast<int>(rows);
-    p->seg.resize(num_jobs + 1);
-    p->roff.resize(num_jobs + 1);
-    p->rank.assign(ranks, ranks + num_jobs);
-    p->scale.resize(num_jobs);
-    p->roff[0] = 0;
-    for (int j = 0; j < num_jobs; ++j) {
-        p->seg[j] = static_cast<int>(seg_offsets[j]);
-        p->roff[j + 1] = p->roff[j] + ((ranks[j] + 15) / 16) * 16;
-        p->scale[j] = scales ? scales[j] : 1.0f;
-    }
-    p->seg[num_jobs] = static_cast<int>(rows);
-    p->R_pad = p->roff[num_jobs];
+    p->seg.assign(J + 1, 0);
+    for (int j = 0; j <= J; ++j) p->seg[j] = static_cast<int>(seg_offsets[j]);
     p->n_mblk = cdiv(rows, kBM);
     p->n_chunks = cdiv(p->R_pad, kBK);
-
     auto job_of_row = [&](int r) {
         int j = static_cast<int>(std::upper_bound(p->seg.begin(), p->seg.end(), r) - p->seg.begin()) - 1;
-        return std::min(std::max(j, 0), num_jobs - 1);
+        return std::min(std::max(j, 0), J - 1);
     };
     // per m-block: the 64-col chunks (LoRA k-blocks) of the jobs present
-    p->ext.resize(2 * p->n_mblk);
+    p->ext.assign(2 * p->n_mblk, 0);
+    p->down.clear();
     for (int mb = 0; mb < p->n_mblk; ++mb) {
         const int r0 = mb * kBM;
         const int r1 = std::min<int>(r0 + kBM, p->rows) - 1;
@@ -666,7 +657,7 @@ mlora_status mlora_plan_create(mlora_ctx* ctx, int32_t num_jobs, const int64_t* 
     }
     p->n_down = static_cast<int>(p->down.size() / 3);
     p->n_mblk256 = cdiv(rows, kPairBM);
-    p->ext256.resize(2 * p->n_mblk256);
+    p->ext256.assign(2 * p->n_mblk256, 0);
     for (int mb = 0; mb < p->n_mblk256; ++mb) {
         const int r0 = mb * kPairBM;
         const int r1 = std::min<int>(r0 + kPairBM, p->rows) - 1;
@@ -675,11 +666,11 @@ mlora_status mlora_plan_create(mlora_ctx* ctx, int32_t num_jobs, const int64_t* 
         p->ext256[2 * mb + 1] = cdiv(p->roff[jb + 1], kBK);
     }
     // per chunk: union of the token segments of the jobs owning its columns
-    p->chunk_kb.resize(2 * p->n_chunks);
+    p->chunk_kb.assign(2 * p->n_chunks, 0);
     for (int c = 0; c < p->n_chunks; ++c) {
         const int c0 = c * kBK, c1 = c0 + kBK;
         int ja = -1, jb = -1;
-        for (int j = 0; j < num_jobs; ++j)
+        for (int j = 0; j < J; ++j)
             if (p->roff[j + 1] > c0 && p->roff[j] < c1) {
                 if (ja < 0) ja = j;
                 jb = j;
@@ -700,52 +691,126 @@ mlora_status mlora_plan_create(mlora_ctx* ctx, int32_t num_jobs, const int64_t* 
             }
         }
     }
-    // one device buffer: seg | roff | scale | ext | down | grad
     std::vector<int> blob;
     auto append = [&](const std::vector<int>& v) {
-        const size_t off = blob.size();
+        const size_t o = blob.size();
         blob.insert(blob.end(), v.begin(), v.end());
         while (blob.size() % 4) blob.push_back(0);
-        return off;
+        return o;
     };
-    std::vector<int> scale_bits(num_jobs);
-    std::memcpy(scale_bits.data(), p->scale.data(), sizeof(float) * num_jobs);
-    const size_t o_seg = append(p->seg), o_roff = append(p->roff), o_scale = append(scale_bits),
-                 o_ext = append(p->ext), o_ext256 = append(p->ext256), o_down = append(p->down),
-                 o_grad = append(grad);
-    cudaError_t e = cudaMalloc(&p->dev, blob.size() * sizeof(int));
-    if (e != cudaSuccess) {
-        delete p;
-        return fail(ctx, MLORA_CUDA, std::string("cudaMalloc(plan): ") + cudaGetErrorString(e));
+    std::vector<int> scale_bits(J);
+    std::memcpy(scale_bits.data(), p->scale.data(), sizeof(float) * J);
+    off[0] = append(p->seg);
+    off[1] = append(p->roff);
+    off[2] = append(scale_bits);
+    off[3] = append(p->ext);
+    off[4] = append(p->ext256);
+    off[5] = append(p->down);
+    off[6] = append(grad);
+    return blob;
+}
+
+// Stream-ordered upload: pinned staging + cudaMemcpyAsync, device buffer grown with
+// cudaMallocAsync/cudaFreeAsync.  Kernels already enqueued on `stream` still see the
+// old tables (the copy runs after them); nothing blocks the host.
+mlora_status upload_tables(mlora_plan* p, const std::vector<int>& blob, const size_t off[7], cudaStream_t s) {
+    mlora_ctx* ctx = p->ctx;
+    const size_t bytes = blob.size() * sizeof(int);
+    if (p->staging_done) MLORA_CUDA_TRY(ctx, cudaEventSynchronize(p->staging_done));  // staging reusable
+    if (bytes > p->staging_bytes) {
+        if (p->staging) cudaFreeHost(p->staging);
+        p->staging = nullptr;
+        MLORA_CUDA_TRY(ctx, cudaMallocHost(&p->staging, 2 * bytes));
+        p->staging_bytes = 2 * bytes;
     }
-    e = cudaMemcpyAsync(p->dev, blob.data(), blob.size() * sizeof(int), cudaMemcpyHostToDevice,
-                        static_cast<cudaStream_t>(stream));
-    if (e == cudaSuccess) e = cudaStreamSynchronize(static_cast<cudaStream_t>(stream));
-    if (e != cudaSuccess) {
-        cudaFree(p->dev);
-        delete p;
-        return fail(ctx, MLORA_CUDA, std::string("plan upload: ") + cudaGetErrorString(e));
+    if (bytes > p->dev_bytes) {
+        if (p->dev) MLORA_CUDA_TRY(ctx, cudaFreeAsync(p->dev, s));
+        p->dev = nullptr;
+        MLORA_CUDA_TRY(ctx, cudaMallocAsync(&p->dev, 2 * bytes, s));
+        p->dev_bytes = 2 * bytes;
     }
+    std::memcpy(p->staging, blob.data(), bytes);
+    MLORA_CUDA_TRY(ctx, cudaMemcpyAsync(p->dev, p->staging, bytes, cudaMemcpyHostToDevice, s));
+    if (!p->staging_done) MLORA_CUDA_TRY(ctx, cudaEventCreateWithFlags(&p->staging_done, cudaEventDisableTiming));
+    MLORA_CUDA_TRY(ctx, cudaEventRecord(p->staging_done, s));
     int* base = static_cast<int*>(p->dev);
-    p->d_seg = base + o_seg;
-    p->d_roff = base + o_roff;
-    p->d_scale = reinterpret_cast<float*>(base + o_scale);
-    p->d_ext = base + o_ext;
-    p->d_ext256 = base + o_ext256;
-    p->d_down = base + o_down;
-    p->d_grad = base + o_grad;
+    p->d_seg = base + off[0];
+    p->d_roff = base + off[1];
+    p->d_scale = reinterpret_cast<float*>(base + off[2]);
+    p->d_ext = base + off[3];
+    p->d_ext256 = base + off[4];
+    p->d_down = base + off[5];
+    p->d_grad = base + off[6];
+    return MLORA_OK;
+}
+
+void release_plan(mlora_plan* p) {
+    if (p->dev) {
+        cudaDeviceSynchronize();
+        cudaFree(p->dev);
+    }
+    if (p->staging_done) cudaEventDestroy(p->staging_done);
+    if (p->staging) cudaFreeHost(p->staging);
+    delete p;
+}
+
+}  // namespace
+
+extern "C" {
+
+mlora_status mlora_plan_create(mlora_ctx* ctx, int32_t num_jobs, const int64_t* seg_offsets,
+                               const int32_t* ranks, const float* scales, void* stream,
+                               mlora_plan** out) {
+    if (!ctx || !out || !seg_offsets || !ranks) return fail(ctx, MLORA_USAGE, "null argument");
+    *out = nullptr;
+    if (num_jobs < 1 || num_jobs > kMaxJobs)
+        return fail(ctx, MLORA_USAGE, "num_jobs must be in [1, " + std::to_string(kMaxJobs) + "]");
+    mlora_status st = check_segments(ctx, num_jobs, seg_offsets);
+    if (st != MLORA_OK) return st;
+    for (int j = 0; j < num_jobs; ++j) {
+        if (ranks[j] < 1) return fail(ctx, MLORA_USAGE, "adapter rank must be >= 1");
+        if (scales && !std::isfinite(scales[j])) return fail(ctx, MLORA_NUMERIC, "non-finite scale");
+    }
+    DeviceGuard g(ctx->device);
+    auto* p = new mlora_plan();
+    p->ctx = ctx;
+    p->J = num_jobs;
+    p->roff.assign(num_jobs + 1, 0);
+    p->rank.assign(ranks, ranks + num_jobs);
+    p->scale.resize(num_jobs);
+    for (int j = 0; j < num_jobs; ++j) {
+        p->roff[j + 1] = p->roff[j] + ((ranks[j] + 15) / 16) * 16;
+        p->scale[j] = scales ? scales[j] : 1.0f;
+    }
+    p->R_pad = p->roff[num_jobs];
+    size_t off[7];
+    const std::vector<int> blob = build_tables(p, seg_offsets, off);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    st = upload_tables(p, blob, off, s);
+    if (st == MLORA_OK && cudaStreamSynchronize(s) != cudaSuccess) st = fail(ctx, MLORA_CUDA, "plan upload failed");
+    if (st != MLORA_OK) {
+        release_plan(p);
+        return st;
+    }
     *out = p;
     return MLORA_OK;
+}
+
+mlora_status mlora_plan_update(mlora_plan* plan, const int64_t* seg_offsets, void* stream) {
+    if (!plan) return fail(nullptr, MLORA_USAGE, "null plan");
+    mlora_ctx* ctx = plan->ctx;
+    mlora_status st = check_segments(ctx, plan->J, seg_offsets);
+    if (st != MLORA_OK) return st;
+    DeviceGuard g(ctx->device);
+    size_t off[7];
+    const std::vector<int> blob = build_tables(plan, seg_offsets, off);
+    return upload_tables(plan, blob, off, static_cast<cudaStream_t>(stream));
 }
 
 mlora_status mlora_plan_destroy(mlora_plan* plan) {
     if (!plan) return MLORA_OK;
     DeviceGuard g(plan->ctx->device);
-    if (plan->dev) {
-        cudaDeviceSynchronize();
-        cudaFree(plan->dev);
-    }
-    delete plan;
+    release_plan(plan);
     return MLORA_OK;
 }
 

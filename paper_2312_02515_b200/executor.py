@@ -90,13 +90,15 @@ class FusedExecutor:
     """Runs fused multi-LoRA training iterations of several jobs on one GPU."""
 
     def __init__(self, ctx: F.Context, shapes, jobs: list[JobConfig], max_concurrent: int,
-                 strategy: str = "minpad", padded: bool = False, seed: int = 0, W0: dict | None = None):
+                 strategy: str = "minpad", padded: bool = False, seed: int = 0, W0: dict | None = None,
+                 pipelined: bool = True):
         self.ctx = ctx
         self.shapes = shapes
         self.jobs = [_JobState(j) for j in jobs]
         self.M = max_concurrent
         self.strategy = strategy
         self.padded = padded
+        self.pipelined = pipelined
         max_len = max(max(j.lengths) for j in jobs)
         max_bs = max(j.batch_size for j in jobs)
         capacity = max_concurrent * max_bs * max_len
@@ -106,14 +108,36 @@ class FusedExecutor:
         self.gen = torch.Generator(device=ctx.device).manual_seed(seed + 1)
         self.trace = Trace()
         self.clock = 0.0
+        self._pending = None  # the enqueued step whose time/losses have not been collected yet
+        self._loss_host = [torch.empty(len(jobs), dtype=torch.float32).pin_memory() for _ in range(2)]
+        self._slot = 0
 
     def active(self) -> list[int]:
         return [i for i, js in enumerate(self.jobs) if not js.finished]
 
+    def _collect(self) -> dict | None:
+        """Finish the pending step: wait for its end event, read its device time and
+        its per-job losses (copied D2H into pinned memory when it was enqueued)."""
+        if self._pending is None:
+            return None
+        pend, self._pending = self._pending, None
+        pend["e1"].synchronize()
+        duration = pend["e0"].elapsed_time(pend["e1"]) / 1e3
+        losses = pend["loss"].tolist()
+        self.clock += duration
+        self.trace.busy_time += duration
+        ev = {"type": "iteration_done", "time": self.clock, "duration_s": duration, **pend["meta"],
+              "losses": {self.jobs[i].cfg.id: losses[i] for i in pend["chosen"]}}
+        self.trace.events.append(ev)
+        return ev
+
     def step(self) -> dict | None:
+        """Select, pack and enqueue the next fused iteration.  Pipelined (default):
+        returns the PREVIOUS iteration's event, so the host packing of step t+1
+        overlaps the device executing step t; `flush()` collects the last one."""
         live = self.active()
         if not live:
-            return None
+            return self._collect()
         cands = [P.Candidate(i, self.jobs[i].peek(), self.jobs[i].cfg.priority, self.jobs[i].cfg.submit_time)
                  for i in live]
         sel = P.select(cands, self.M, self.strategy)
@@ -126,38 +150,43 @@ class FusedExecutor:
             if j in batches:
                 r = lay.seg[in_batch.index(j) + 1]
             seg.append(r)
-        self.layer.set_layout(seg)
+        self.layer.set_layout(seg)                           # stream-ordered plan update, no host sync
         x = torch.empty(lay.rows, self.k_in, device=self.ctx.device)
         x.uniform_(-1.0, 1.0, generator=self.gen)
         x = x.to(torch.bfloat16)
         if self.padded:  # pad rows are zero, exactly as fuse() builds them
-            mask = torch.zeros(lay.rows, dtype=torch.bool, device=self.ctx.device)
+            mask = torch.zeros(lay.rows, dtype=torch.bool)
             for rows in lay.seq_rows:
                 for r0, L in rows:
                     mask[r0:r0 + L] = True
-            x[~mask] = 0
+            x[~mask.to(self.ctx.device, non_blocking=True)] = 0
         active = [j in batches for j in range(len(self.jobs))]
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        slot = self._loss_host[self._slot]
+        self._slot ^= 1
         e0.record()
         loss = self.layer.step(x, active=active)
+        slot.copy_(loss, non_blocking=True)                  # D2H of this step's per-job losses
         e1.record()
-        losses = loss.tolist()                               # synchronises
-        duration = e0.elapsed_time(e1) / 1e3
+        prev = self._collect()                               # step t-1 (normally finished already)
         for i in chosen:
             self.jobs[i].commit(len(batches[i]))
             self.jobs[i].done += 1
-        self.clock += duration
-        self.trace.busy_time += duration
-        ev = {"type": "iteration_done", "time": self.clock, "duration_s": duration,
-              "total_tokens": lay.total_tokens, "padding_tokens": lay.padding_tokens,
-              "effective_tokens": lay.effective_tokens, "rows": lay.rows, "jobs_in_batch": len(chosen),
-              "routing": [self.jobs[i].cfg.id for i in chosen],
-              "losses": {self.jobs[i].cfg.id: losses[i] for i in chosen}}
-        self.trace.events.append(ev)
-        return ev
+        self._pending = {"e0": e0, "e1": e1, "loss": slot, "chosen": chosen,
+                         "meta": {"total_tokens": lay.total_tokens, "padding_tokens": lay.padding_tokens,
+                                  "effective_tokens": lay.effective_tokens, "rows": lay.rows,
+                                  "jobs_in_batch": len(chosen), "routing": [self.jobs[i].cfg.id for i in chosen]}}
+        if not self.pipelined:
+            return self._collect()
+        return prev
+
+    def flush(self) -> dict | None:
+        return self._collect()
 
     def run(self, max_iterations: int | None = None) -> Trace:
         n = 0
-        while (max_iterations is None or n < max_iterations) and self.step() is not None:
+        while (max_iterations is None or n < max_iterations) and self.active():
+            self.step()
             n += 1
+        self.flush()
         return self.trace

@@ -128,6 +128,18 @@ class Plan:
     def handle(self):
         return self._h
 
+    def update(self, seg_offsets, stream=None) -> None:
+        """Next fused batch's segment layout (same jobs/ranks/scales): stream-ordered,
+        no host sync, no allocation in steady state (mlora_plan_update)."""
+        if len(seg_offsets) != self.num_jobs + 1:
+            raise errors.UsageError("seg_offsets must have num_jobs+1 entries")
+        seg = [int(x) for x in seg_offsets]
+        with torch.cuda.device(self.ctx.device):
+            N.check(N.lib().mlora_plan_update(self._h, (N.i64 * len(seg))(*seg), _stream_handle(stream)),
+                    self.ctx.handle)
+        self.seg = seg
+        self.rows = int(N.lib().mlora_plan_rows(self._h))
+
     def close(self) -> None:
         if getattr(self, "_h", None):
             N.lib().mlora_plan_destroy(self._h)

@@ -110,7 +110,7 @@ class FusedLoraLayer:
         rows = int(seg_offsets[-1])
         if rows < 1 or rows > self.rows:
             raise ValueError(f"layout rows {rows} outside [1, capacity {self.rows}]")
-        self.plan = F.Plan(self.ctx, seg_offsets, self.ranks, self.scales)
+        self.plan.update(seg_offsets)  # stream-ordered, no host sync
         self.cur_rows = rows
 
     def _views(self, p: Projection, rows: int):

@@ -35,7 +35,8 @@ def test_executor_replays_reference_selection(padded):
 
     ctx = F.Context(0)
     jobs = make_jobs(X, packer)
-    ex = X.FusedExecutor(ctx, TINY, jobs, max_concurrent=3, strategy="minpad", padded=padded, seed=3)
+    ex = X.FusedExecutor(ctx, TINY, jobs, max_concurrent=3, strategy="minpad", padded=padded, seed=3,
+                         pipelined=False)
     # oracle replay state
     cursors = [0] * len(jobs)
     done = [0] * len(jobs)
@@ -74,3 +75,26 @@ def test_executor_replays_reference_selection(padded):
     assert m["T_e"] == pytest.approx((1 - m["delta"]) * xi / m["busy_time_s"])
     assert m["iterations"] == len(ex.trace.events) and m["effective_tokens"] == xi - xi_p
     assert np.isfinite(m["effective_tokens_per_s"]) and m["effective_tokens_per_s"] > 0
+
+
+def test_pipelined_executor_matches_synchronous():
+    """Pipelined host packing (step t+1 selected and enqueued while step t runs,
+    plan updates stream-ordered) yields the identical trace: same selections and
+    accounting, bitwise-identical per-job losses."""
+    from paper_2312_02515_b200 import executor as X
+    from paper_2312_02515_b200 import fused as F
+    from paper_2312_02515_b200 import packer
+    from paper_2312_02515_b200.layer import TINY
+
+    ctx = F.Context(0)
+    traces = []
+    for pipelined in (False, True):
+        ex = X.FusedExecutor(ctx, TINY, make_jobs(X, packer), max_concurrent=3, strategy="minpad", seed=9,
+                             pipelined=pipelined)
+        traces.append(ex.run())
+    a, b = traces
+    assert len(a.events) == len(b.events) > 0
+    for ea, eb in zip(a.events, b.events):
+        for key in ("total_tokens", "padding_tokens", "effective_tokens", "rows", "routing"):
+            assert ea[key] == eb[key]
+        assert ea["losses"] == eb["losses"]

@@ -43,6 +43,7 @@ def main():
             ex = X.FusedExecutor(ctx, LLAMA13B, jobs(iters), max_concurrent=4, strategy=strategy, padded=padded,
                                  seed=5, W0=W0)
             ex.step()  # warm-up iteration (kernel attributes, tensor maps)
+            ex.flush()
             ex.trace = X.Trace()
             trace = ex.run()
             m = trace.metrics()
