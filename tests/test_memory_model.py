@@ -39,9 +39,9 @@ def test_reference_fit_of_b200_memory_samples():
               mem.ctypes.data_as(C.POINTER(C.c_double)), 0, out) == 0
     b0, b1, b2, rmse = list(out)
     t = bs.astype(np.float64) * seq
-    A = np.stack([np.ones_like(t), t, t * t], 1)
+    A = np.stack([np.ones_like(t), t, t * seq], 1)  # Eq. 6 features (1, Bt*Ln, Bt*Ln^2)
     want, *_ = np.linalg.lstsq(A, mem, rcond=None)
     assert np.allclose([b0, b1, b2], want, rtol=1e-6, atol=1e-12)
     assert rmse < 0.005
     # activations scale linearly with tokens on this path (no attention): beta2 ~ 0
-    assert abs(b2) * (8 * 1024) ** 2 < 0.01 and b1 > 0
+    assert abs(b2) * 8 * 1024 ** 2 < 0.01 and b1 > 0

@@ -48,8 +48,9 @@ def main(out_csv):
         for bs, L, m in rows_out:
             w.writerow([bs, L, f"{m:.6f}"])
     t = np.array([bs * L for bs, L, _ in rows_out], np.float64)
+    Ln = np.array([L for _, L, _ in rows_out], np.float64)
     M = np.array([m for _, _, m in rows_out])
-    A = np.stack([np.ones_like(t), t, t * t], 1)
+    A = np.stack([np.ones_like(t), t, t * Ln], 1)  # Eq. 6: (1, Bt*Ln, Bt*Ln^2)
     beta, *_ = np.linalg.lstsq(A, M, rcond=None)
     rmse = float(np.sqrt(np.mean((A @ beta - M) ** 2)))
     print(f"samples={len(rows_out)} beta0={beta[0]:.6g} GB beta1={beta[1]:.6g} GB/token beta2={beta[2]:.6g} "
