@@ -196,11 +196,19 @@ def main():
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    # one process per GPU.  (MLORA_BENCH_SHARE_GPU=1 folds ranks onto the visible
+    # devices and uses gloo — only to exercise the multi-rank logic on a 1-GPU box.)
+    share = os.environ.get("MLORA_BENCH_SHARE_GPU") == "1"
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if share:
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     from paper_2312_02515_b200 import parallel as PL
 
