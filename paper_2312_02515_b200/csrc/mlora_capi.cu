@@ -24,6 +24,7 @@
 #include "../../include/mlora.h"
 #include "mlora_aux.cuh"
 #include "mlora_gemm.cuh"
+#include "mlora_quad.cuh"
 
 using namespace mlora;
 
@@ -70,6 +71,8 @@ struct mlora_plan {
     std::vector<int> ext;                 // [n_mblk][2]   (128-row m-blocks)
     std::vector<int> ext256;              // [n_mblk256][2] (256-row m-blocks of the CTA-pair kernel)
     int n_mblk256 = 0;
+    std::vector<int> ext512;              // [n_mblk512][2] (512-row m-blocks of the 4-CTA kernel)
+    int n_mblk512 = 0;
     std::vector<int> down;                // [n_down][3]
     int n_down = 0;
     std::vector<int> chunk_kb;            // [n_chunks][2] token k-block range
@@ -85,6 +88,7 @@ struct mlora_plan {
     float* d_scale = nullptr;
     int* d_ext = nullptr;
     int* d_ext256 = nullptr;
+    int* d_ext512 = nullptr;
     int* d_down = nullptr;
     int* d_grad = nullptr;
 };
@@ -270,13 +274,60 @@ mlora_status launch_gemm(mlora_ctx* ctx, const ProblemSet<NP>& set, int ctas_per
     return MLORA_OK;
 }
 
-bool use_pair_kernel() {  // MLORA_BASE_KERNEL=single selects the 1-CTA variant (A/B measurements)
-    static const bool pair = [] {
+// MLORA_BASE_KERNEL: "pair" (default, CTA pair), "quad" (two pairs sharing the
+// weight tile by TMA multicast), "single" (1-CTA variant) — A/B measurement knob.
+int base_kernel_variant() {
+    static const int v = [] {
         const char* e = std::getenv("MLORA_BASE_KERNEL");
-        return !(e && std::string(e) == "single");
+        if (!e) return 1;
+        const std::string s(e);
+        return s == "single" ? 0 : s == "quad" ? 2 : 1;
     }();
-    return pair;
+    return v;
 }
+
+constexpr int kQuadStages = 6;
+
+template <bool B_MN>
+mlora_status launch_base_quad(mlora_ctx* ctx, const CUtensorMap& a0, const CUtensorMap& b0,
+                              const CUtensorMap& a1, const CUtensorMap& b1, const GemmParams& p,
+                              cudaStream_t stream) {
+    if (p.num_tiles <= 0) return MLORA_OK;
+    using L = PairSmem<kQuadStages>;
+    auto kern = mlora_base_quad_kernel<kQuadStages, B_MN>;
+    static bool attr_done = false;
+    if (!attr_done) {
+        MLORA_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 L::kDynBytes));
+        attr_done = true;
+    }
+    // clusters of 4 pack into fewer SMs than pairs do (GPC granularity): size the
+    // persistent grid by the hardware's co-resident cluster count, not num_sms / 4
+    static int max_clusters = 0;
+    if (!max_clusters) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(4 * (ctx->num_sms / 4));
+        cfg.blockDim = dim3(kNumThreads);
+        cfg.dynamicSmemBytes = L::kDynBytes;
+        cudaLaunchAttribute attr;
+        attr.id = cudaLaunchAttributeClusterDimension;
+        attr.val.clusterDim.x = 4;
+        attr.val.clusterDim.y = 1;
+        attr.val.clusterDim.z = 1;
+        cfg.attrs = &attr;
+        cfg.numAttrs = 1;
+        MLORA_CUDA_TRY(ctx, cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg));
+        if (max_clusters < 1) max_clusters = 1;
+    }
+    const int clusters = std::min(p.num_tiles, max_clusters);
+    ProfScope ps(ctx, B_MN ? 1 : 0, stream);
+    MLORA_CUDA_TRY(ctx, launch_k(kern, dim3(4 * clusters), dim3(kNumThreads), L::kDynBytes, stream, 4, a0, b0,
+                                 a1, b1, p));
+    ++ctx->launches;
+    return MLORA_OK;
+}
+
+bool use_pair_kernel() { return base_kernel_variant() != 0; }
 
 constexpr int kPairStages = 6;
 
@@ -307,8 +358,9 @@ mlora_status run_base(mlora_ctx* ctx, const mlora_plan* plan, const void* A0, in
                       const void* B0, const void* A1, const void* B1, int R, int N, void* out,
                       cudaStream_t s, float* row_sq = nullptr) {
     const bool pair = use_pair_kernel();
+    const bool quad = base_kernel_variant() == 2;
     const int M = plan->rows;
-    const uint32_t bbox = pair ? 128 : 256;  // K-major B rows staged per CTA
+    const uint32_t bbox = quad ? 64 : pair ? 128 : 256;  // K-major B rows staged per TMA box
     CUtensorMap tA0, tB0, tA1, tB1;
     mlora_status st;
     if ((st = get_tmap(ctx, A0, K0, M, lda0, 64, 128, &tA0)) != MLORA_OK) return st;
@@ -340,9 +392,16 @@ mlora_status run_base(mlora_ctx* ctx, const mlora_plan* plan, const void* A0, in
             const char* e = std::getenv("MLORA_RASTER");
             return e ? std::atoi(e) : -1;
         }();
-        const long long slab = (long long)kPairBM * K0 * 2;
+        const long long slab = (long long)(quad ? kQuadBM : kPairBM) * K0 * 2;
         pb.raster_group = raster_env >= 0 ? raster_env
                                           : static_cast<int>(std::max<long long>(1, (32LL << 20) / slab));
+        if (quad) {
+            pb.n_mblk = plan->n_mblk512;
+            pb.n_nblk = cdiv(N, kPairBN);
+            pb.num_tiles = pb.n_mblk * pb.n_nblk;
+            pb.ext_tab = plan->d_ext512;
+            return launch_base_quad<B_MN>(ctx, tA0, tB0, tA1, tB1, pb, s);
+        }
         pb.n_mblk = plan->n_mblk256;
         pb.n_nblk = cdiv(N, kPairBN);
         pb.num_tiles = pb.n_mblk * pb.n_nblk;
@@ -628,7 +687,7 @@ mlora_status check_segments(mlora_ctx* ctx, int32_t num_jobs, const int64_t* seg
 
 // Host tables of a segment layout (ranks/roff/scale already set) -> one blob:
 // seg | roff | scale | ext | ext256 | down | grad, with the section offsets.
-std::vector<int> build_tables(mlora_plan* p, const int64_t* seg_offsets, size_t off[7]) {
+std::vector<int> build_tables(mlora_plan* p, const int64_t* seg_offsets, size_t off[8]) {
     const int J = p->J;
     const long long rows = seg_offsets[J];
     p->rows = static_cast<int>(rows);
@@ -664,6 +723,15 @@ std::vector<int> build_tables(mlora_plan* p, const int64_t* seg_offsets, size_t 
         const int ja = job_of_row(r0), jb = job_of_row(r1);
         p->ext256[2 * mb] = p->roff[ja] / kBK;
         p->ext256[2 * mb + 1] = cdiv(p->roff[jb + 1], kBK);
+    }
+    p->n_mblk512 = cdiv(rows, kQuadBM);
+    p->ext512.assign(2 * p->n_mblk512, 0);
+    for (int mb = 0; mb < p->n_mblk512; ++mb) {
+        const int r0 = mb * kQuadBM;
+        const int r1 = std::min<int>(r0 + kQuadBM, p->rows) - 1;
+        const int ja = job_of_row(r0), jb = job_of_row(r1);
+        p->ext512[2 * mb] = p->roff[ja] / kBK;
+        p->ext512[2 * mb + 1] = cdiv(p->roff[jb + 1], kBK);
     }
     // per chunk: union of the token segments of the jobs owning its columns
     p->chunk_kb.assign(2 * p->n_chunks, 0);
@@ -707,13 +775,14 @@ std::vector<int> build_tables(mlora_plan* p, const int64_t* seg_offsets, size_t 
     off[4] = append(p->ext256);
     off[5] = append(p->down);
     off[6] = append(grad);
+    off[7] = append(p->ext512);
     return blob;
 }
 
 // Stream-ordered upload: pinned staging + cudaMemcpyAsync, device buffer grown with
 // cudaMallocAsync/cudaFreeAsync.  Kernels already enqueued on `stream` still see the
 // old tables (the copy runs after them); nothing blocks the host.
-mlora_status upload_tables(mlora_plan* p, const std::vector<int>& blob, const size_t off[7], cudaStream_t s) {
+mlora_status upload_tables(mlora_plan* p, const std::vector<int>& blob, const size_t off[8], cudaStream_t s) {
     mlora_ctx* ctx = p->ctx;
     const size_t bytes = blob.size() * sizeof(int);
     if (p->staging_done) MLORA_CUDA_TRY(ctx, cudaEventSynchronize(p->staging_done));  // staging reusable
@@ -741,6 +810,7 @@ mlora_status upload_tables(mlora_plan* p, const std::vector<int>& blob, const si
     p->d_ext256 = base + off[4];
     p->d_down = base + off[5];
     p->d_grad = base + off[6];
+    p->d_ext512 = base + off[7];
     return MLORA_OK;
 }
 
@@ -783,7 +853,7 @@ mlora_status mlora_plan_create(mlora_ctx* ctx, int32_t num_jobs, const int64_t* 
         p->scale[j] = scales ? scales[j] : 1.0f;
     }
     p->R_pad = p->roff[num_jobs];
-    size_t off[7];
+    size_t off[8];
     const std::vector<int> blob = build_tables(p, seg_offsets, off);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     st = upload_tables(p, blob, off, s);
@@ -802,7 +872,7 @@ mlora_status mlora_plan_update(mlora_plan* plan, const int64_t* seg_offsets, voi
     mlora_status st = check_segments(ctx, plan->J, seg_offsets);
     if (st != MLORA_OK) return st;
     DeviceGuard g(ctx->device);
-    size_t off[7];
+    size_t off[8];
     const std::vector<int> blob = build_tables(plan, seg_offsets, off);
     return upload_tables(plan, blob, off, static_cast<cudaStream_t>(stream));
 }
