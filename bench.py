@@ -106,10 +106,18 @@ class ClockSampler(threading.Thread):
 
 
 # ----------------------------------------------------------------------------- reference CPU arm
-def reference_sample(cfg, seq_len=64, seed=1):
-    """Pre-marshalled reference fused_forward calls: one per projection of the layer,
-    each over the fused sample (J jobs x 1 sequence x seq_len tokens).  Forward only:
-    the reference has no backward."""
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def reference_sample(cfg, seq_len=64, seed=1, replicas=1):
+    """Pre-marshalled reference fused_forward calls: `replicas` independent fused
+    samples (J jobs x 1 sequence x seq_len tokens each) per projection of the
+    layer, all sharing that projection's frozen W0.  Forward only: the reference
+    has no backward."""
     import numpy as np
     from oracle import ref
     from paper_2312_02515_b200.layer import SHAPES
@@ -122,25 +130,33 @@ def reference_sample(cfg, seq_len=64, seed=1):
         del W0
         As = [rng.uniform(-1, 1, (r, k)) for r in cfg["ranks"]]
         Bs = [rng.uniform(-1, 1, (d, r)) for r in cfg["ranks"]]
-        seqs = [(j, rng.uniform(-1, 1, (seq_len, k))) for j in range(J)]
-        calls.append(ref.FusedCall(w, cfg["ranks"], As, Bs, seqs))
-    return calls, J * seq_len
+        for _ in range(replicas):
+            seqs = [(j, rng.uniform(-1, 1, (seq_len, k))) for j in range(J)]
+            calls.append(ref.FusedCall(w, cfg["ranks"], As, Bs, seqs))
+    return calls, J * seq_len * replicas
 
 
-def time_reference(cfg, steps, warmup, seq_len=64):
-    """Runs the reference's fused_forward for every projection of the layer in
-    parallel host threads (the reference is single-threaded and reentrant)."""
+def time_reference(cfg, steps, warmup, seq_len=64, budget_s=None):
+    """Runs the reference's fused_forward on every host core: each step is
+    `replicas` independent fused samples per projection of the layer, one
+    single-threaded (reentrant) reference call per host thread.  With budget_s,
+    stops taking timed steps once the budget is spent (at least one)."""
     from concurrent.futures import ThreadPoolExecutor
     from oracle import ref
     if not ref.available():
         ref.build()
     if not ref.available():
         return None
-    calls, tokens = reference_sample(cfg, seq_len)
-    threads = min(len(calls), os.cpu_count() or 1)
+    nproj = len(__import__("paper_2312_02515_b200.layer", fromlist=["SHAPES"]).SHAPES[cfg["shapes"]])
+    replicas = max(1, min(8, host_threads() // nproj))
+    calls, tokens = reference_sample(cfg, seq_len, replicas=replicas)
+    threads = min(len(calls), host_threads())
     times = []
+    t_start = time.perf_counter()
     with ThreadPoolExecutor(threads) as ex:
         for i in range(warmup + steps):
+            if budget_s is not None and times and time.perf_counter() - t_start > budget_s:
+                break
             t0 = time.perf_counter()
             list(ex.map(lambda c: c(), calls))
             dt = time.perf_counter() - t0
@@ -148,10 +164,11 @@ def time_reference(cfg, steps, warmup, seq_len=64):
                 times.append(dt)
     total = sum(times)
     return dict(value=tokens * len(times) / total, unit=UNIT, cores=threads, kind="reference",
-                sample=f"reference fusim::fused_forward (fp64, forward only) on {len(calls)} LLaMA-7B projections x "
-                       f"{len(cfg['ranks'])} jobs x 1 seq x {seq_len} tokens = {tokens} effective tokens per step, "
-                       f"one host thread per projection; {len(times)} timed steps, {total:.1f} s",
-                ms_per_step=1e3 * total / len(times))
+                sample=f"reference fusim::fused_forward (fp64, forward only): {replicas} fused sample(s) of "
+                       f"{len(cfg['ranks'])} jobs x 1 seq x {seq_len} tokens per LLaMA-7B projection x {nproj} "
+                       f"projections = {tokens} effective tokens per step, {len(calls)} concurrent reference calls "
+                       f"on {threads} host threads ({host_threads()} available); {len(times)} timed steps, {total:.1f} s",
+                ms_per_step=1e3 * total / len(times), steps_run=len(times))
 
 
 def run_reference_arm(args, cfg):
@@ -160,14 +177,15 @@ def run_reference_arm(args, cfg):
         return 0
     steps = max(1, args.steps)
     warmup = max(0, args.warmup)
-    r = time_reference(cfg, steps, warmup)
+    # the reference CPU path takes ~10 s per step: bound the arm to a few minutes
+    r = time_reference(cfg, steps, warmup, budget_s=float(os.environ.get("MLORA_REF_BUDGET_S", "180")))
     if r is None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libfusim_ref.so not built and "
                           "/root/reference absent"}))
         return 0
     line = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": args.gpus,
-            "steps": steps, "warmup": warmup, "ms_per_step": r["ms_per_step"], "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "steps": r["steps_run"], "requested_steps": steps, "warmup": warmup, "ms_per_step": r["ms_per_step"],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg["workload"] + " [reference CPU sample: see cpu_baseline.sample]"},
             "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
