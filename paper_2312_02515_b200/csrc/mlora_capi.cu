@@ -427,9 +427,21 @@ template <bool B_MN>
 mlora_status run_down_group(mlora_ctx* ctx, const mlora_plan* plan, int n, const int32_t* K,
                             const void* const* in, const void* const* bop, void* const* out, cudaStream_t s) {
     const int M = plan->rows, R = plan->R_pad;
+    // Tile order.  Equal widths: interleave the problems tile by tile, so the
+    // projections fed by one hidden state stream it concurrently and share L2.
+    // Mixed widths: problems back to back, widest first — interleaving would hand
+    // each cluster tiles of a single problem whenever the cluster count is a
+    // multiple of the problem count (74 clusters, 2 problems: one half of the
+    // grid gets every 11008-wide tile), a 2.7x load imbalance.
+    std::vector<int> order(n);
+    for (int i = 0; i < n; ++i) order[i] = i;
+    bool same_k = true;
+    for (int i = 1; i < n; ++i) same_k = same_k && K[i] == K[0];
+    if (!same_k) std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return K[x] > K[y]; });
     for (int i0 = 0; i0 < n; i0 += kGroupMax) {
         ProblemSet<kGroupMax> set;
-        for (int i = i0; i < std::min(n, i0 + kGroupMax); ++i) {
+        for (int oi = i0; oi < std::min(n, i0 + kGroupMax); ++oi) {
+            const int i = order[oi];
             if (!in[i] || !bop[i] || !out[i]) return fail(ctx, MLORA_USAGE, "null tensor pointer");
             if (K[i] <= 0 || K[i] % 8) return fail(ctx, MLORA_SHAPE, "down-projection width must be a positive multiple of 8");
             CUtensorMap tA, tB;
@@ -454,7 +466,7 @@ mlora_status run_down_group(mlora_ctx* ctx, const mlora_plan* plan, int n, const
             p.num_jobs = plan->J;
             set.add(tA, tB, tA, tB, p);
         }
-        set.ps.interleave = 1;  // equal tile counts; projections sharing an input read it together
+        set.ps.interleave = same_k ? 1 : 0;
         mlora_status st = launch_gemm<MODE_DOWN, 64, kDownStages, false, B_MN, 2, kGroupMax>(ctx, set, 1, s);
         if (st != MLORA_OK) return st;
     }
