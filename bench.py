@@ -249,10 +249,12 @@ def main():
             W0[name] = ((torch.rand(d, k, generator=g) * 2 - 1) / k ** 0.5).to(torch.bfloat16).to(dev)
         else:
             W0[name] = torch.empty(d, k, dtype=torch.bfloat16, device=dev)
-    PL.broadcast_base_weights(W0, src=0)
+    ctx = F.Context(dev)
+    # one GPU per rank: the native communicator (libmlora.so -> NCCL), all W0 in one group
+    comm = PL.NativeComm(ctx) if world > 1 and not share else None
+    PL.broadcast_base_weights(W0, src=0, comm=comm)
     torch.cuda.synchronize()
 
-    ctx = F.Context(dev)
     layer = FusedLoraLayer(ctx, shapes, ranks_l, [2.0] * J, lrs_l, rows, seed=1000 + rank, W0=W0)
     layer.set_layout(seg)
     xg = torch.Generator(device="cpu").manual_seed(77 + rank)
@@ -361,7 +363,7 @@ def main():
         "config": {"workload": cfg["workload"], "jobs_per_gpu": J, "ranks": cfg["ranks"], "lrs": cfg["lrs"],
                    "tokens_per_step_per_gpu": rows, "effective_tokens_per_step_per_gpu": rows,
                    "padding_ratio": 0.0, "parallelism": f"adapter-parallel (jobs partitioned) x{world}, "
-                   "W0 replicated by one NCCL broadcast at init",
+                   "W0 replicated once at init (mlora_broadcast_base: one NCCL group)",
                    "l2": "no flush; per-step working set (7 projections' W0 = 0.39 GB + activations) > 126 MB L2",
                    "flops_per_token": fpt},
         "step_tflops": step_tflops, "step_frac_of_peak": step_tflops / peak,

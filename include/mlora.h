@@ -260,6 +260,37 @@ mlora_status mlora_rope(int64_t rows, int32_t heads, int32_t head_dim, const voi
 mlora_status mlora_segment_sumsq_loss(mlora_ctx* ctx, const mlora_plan* plan, const void* const* Y,
                                       const int32_t* cols, int32_t num_tensors, float* loss, void* stream);
 
+/* ---------------------------------------------------------------- multi-GPU
+ * Adapter-parallel: jobs are partitioned across GPUs (one process and one
+ * context per GPU); the frozen base weights are replicated ONCE at start-up and
+ * the steady-state step has no collective.  The reference has no multi-GPU
+ * runtime (its simulator models one device, sim.hpp:16-31; its batches are
+ * routed per job, lora.cpp:165-167, which is what makes the job partition
+ * exact).  NCCL is loaded at first use (dlopen "libnccl.so.2", override with
+ * MLORA_NCCL_LIBRARY); without it these calls return MLORA_CUDA and every other
+ * entry point is unaffected.
+ *
+ * Start-up: rank 0 calls mlora_comm_unique_id and ships the id bytes to the
+ * other ranks over any out-of-band channel; every rank then calls
+ * mlora_comm_create with its own context (the communicator is bound to the
+ * context's device). */
+typedef struct mlora_comm mlora_comm;
+int32_t mlora_comm_id_bytes(void); /* 128 */
+mlora_status mlora_comm_nccl_version(int32_t* version /* host */);
+mlora_status mlora_comm_unique_id(uint8_t* id /* host, mlora_comm_id_bytes() bytes */);
+mlora_status mlora_comm_create(mlora_ctx* ctx, const uint8_t* id /* host */, int32_t nranks, int32_t rank,
+                               mlora_comm** out);
+mlora_status mlora_comm_destroy(mlora_comm* comm);
+int32_t mlora_comm_rank(const mlora_comm* comm);
+int32_t mlora_comm_size(const mlora_comm* comm);
+/* Replicate n device buffers (e.g. every W0 of the model) from `root` to all
+ * ranks in place, as ONE NCCL group (pipelined over NVLink/NVSwitch).
+ * Stream-ordered on `stream`; USAGE on a bad root / null buffer / negative size. */
+mlora_status mlora_broadcast_base(mlora_comm* comm, int32_t n, void* const* ptrs, const int64_t* bytes,
+                                  int32_t root, void* stream);
+/* In-place fp32 sum over ranks (per-job metric aggregation; not on the step path). */
+mlora_status mlora_comm_sum_f32(mlora_comm* comm, float* buf, int64_t count, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -20,8 +20,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 LIB_MLORA = os.path.join(PKG, "libmlora.so")
 LIB_FACADE = os.path.join(PKG, "libfusim_b200.so")
 
-MLORA_SOURCES = ["mlora_capi.cu", "mlora_f64.cu", "mlora_model.cu"]
-MLORA_HEADERS = ["sm100.cuh", "mlora_gemm.cuh", "mlora_aux.cuh"]
+MLORA_SOURCES = ["mlora_capi.cu", "mlora_f64.cu", "mlora_model.cu", "mlora_comm.cpp"]
+MLORA_HEADERS = ["sm100.cuh", "mlora_gemm.cuh", "mlora_aux.cuh", "mlora_quad.cuh"]
 FACADE_SOURCES = ["facade_lora.cpp", "facade_batch_select.cpp", "facade_workload.cpp", "facade_capi.cpp"]
 
 
@@ -43,7 +43,7 @@ def build_mlora(force: bool = False) -> str:
     if not force and _newer(LIB_MLORA, deps):
         return LIB_MLORA
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-shared",
-           "-cudart", "static", "-I", os.path.join(ROOT, "include"), "-o", LIB_MLORA, *srcs]
+           "-cudart", "static", "-I", os.path.join(ROOT, "include"), "-o", LIB_MLORA, *srcs, "-ldl"]
     _run(cmd)
     return LIB_MLORA
 

@@ -75,6 +75,16 @@ _OPTIONAL = {
     "mlora_rmsnorm_fwd": (i32, [i64, i32, vp, vp, f32, vp, vp, vp]),
     "mlora_rmsnorm_bwd": (i32, [i64, i32, vp, vp, vp, vp, vp, vp, vp, i32, vp]),
     "mlora_rope": (i32, [i64, i32, i32, vp, vp, vp, f32, i32, vp]),
+    # multi-GPU boundary (NCCL resolved at first use)
+    "mlora_comm_id_bytes": (i32, []),
+    "mlora_comm_nccl_version": (i32, [C.POINTER(i32)]),
+    "mlora_comm_unique_id": (i32, [vp]),
+    "mlora_comm_create": (i32, [vp, vp, i32, i32, C.POINTER(vp)]),
+    "mlora_comm_destroy": (i32, [vp]),
+    "mlora_comm_rank": (i32, [vp]),
+    "mlora_comm_size": (i32, [vp]),
+    "mlora_broadcast_base": (i32, [vp, i32, C.POINTER(vp), C.POINTER(i64), i32, vp]),
+    "mlora_comm_sum_f32": (i32, [vp, vp, i64, vp]),
 }
 
 

@@ -557,6 +557,12 @@ mlora_status run_grad_group(mlora_ctx* ctx, const mlora_plan* plan, int n, const
 
 }  // namespace
 
+// Bridge for the other translation units of libmlora.so (mlora_comm.cpp).
+namespace mlora_internal {
+mlora_status set_error(mlora_ctx* ctx, mlora_status st, const std::string& msg) { return fail(ctx, st, msg); }
+int ctx_device(const mlora_ctx* ctx) { return ctx->device; }
+}  // namespace mlora_internal
+
 extern "C" {
 
 int32_t mlora_abi_version(void) { return 1; }

@@ -82,3 +82,23 @@ def test_no_gpu_context_fails_loudly(lib):
     h = N.vp()
     with pytest.raises(E.CudaError):
         N.check(lib.mlora_ctx_create(0, C.byref(h)))
+
+
+def test_comm_host_entry_points(lib):
+    """The native multi-GPU boundary resolves NCCL at run time; its host-only
+    calls (version, unique id) work without a GPU, and argument errors map to
+    the reference's UsageError before any NCCL/CUDA work."""
+    v = N.i32()
+    N.check(lib.mlora_comm_nccl_version(C.byref(v)))
+    assert v.value >= 21800  # NCCL >= 2.18 (ncclGroup + in-place broadcast semantics)
+    assert lib.mlora_comm_id_bytes() == 128
+    a, b = (C.c_uint8 * 128)(), (C.c_uint8 * 128)()
+    N.check(lib.mlora_comm_unique_id(C.cast(a, C.c_void_p)))
+    N.check(lib.mlora_comm_unique_id(C.cast(b, C.c_void_p)))
+    assert bytes(a) != bytes(b)  # fresh rendezvous id each call
+    with pytest.raises(E.UsageError):
+        N.check(lib.mlora_comm_unique_id(None))
+    with pytest.raises(E.UsageError):
+        N.check(lib.mlora_broadcast_base(None, 0, None, None, 0, None))
+    assert lib.mlora_comm_rank(None) == -1 and lib.mlora_comm_size(None) == -1
+    assert lib.mlora_comm_destroy(None) == 0

@@ -42,7 +42,11 @@ def _worker(rank, world, port, out):
         dist.all_gather_object(gathered, parts)
         mx = PL.max_over_ranks(10.0 * (rank + 1))
         tot = PL.sum_over_ranks(float(len(parts[rank])))
-        out[rank] = (ok, gathered, mx, tot, parts)
+        # the native communicator's rendezvous: rank 0's NCCL id reaches every rank
+        cid = PL.comm_rendezvous_id()
+        ids = [None] * world
+        dist.all_gather_object(ids, cid)
+        out[rank] = (ok, gathered, mx, tot, parts, ids)
     finally:
         dist.destroy_process_group()
 
@@ -55,7 +59,8 @@ def test_world2_broadcast_partition_and_timing():
     mp.spawn(_worker, args=(world, _free_port(), out), nprocs=world, join=True)
     assert set(out.keys()) == {0, 1}
     for r in range(world):
-        ok, gathered, mx, tot, parts = out[r]
+        ok, gathered, mx, tot, parts, ids = out[r]
+        assert len(ids[0]) == 128 and ids[0] == ids[1] and any(ids[0])  # one shared NCCL id
         assert ok, f"rank {r} did not receive rank 0's base weights"
         assert gathered[0] == gathered[1] == parts     # identical, independently computed partitions
         assert mx == 20.0                                # max over ranks
