@@ -226,6 +226,23 @@ mlora_status mlora_f64_gemm(int64_t M, int64_t N, int64_t K, const double* A, in
 /* c = a + b elementwise (lora.cpp:36-42), device fp64. */
 mlora_status mlora_f64_add(int64_t n, const double* a, const double* b, double* c, void* stream);
 
+/* Non-finite guard, between the loss and the backward.  For every job j with a
+ * non-finite loss[j] (device fp32 [J]), zero its rows seg[j]..seg[j+1] of each
+ * bf16 row-major tensor (rows x cols[t]), normally the backward's dY.  The fused
+ * reductions multiply a job's dY rows by the exact zeros the other jobs' columns
+ * of H_cat hold (dB = dY^T H), and 0 * inf = NaN: without the guard a job whose
+ * activations overflow would poison every co-scheduled job.  The reference
+ * computes each sequence separately (lora.cpp:168-181), so this is what keeps
+ * the jobs independent, as it requires.  The diverged job keeps its non-finite
+ * loss, which is what detect_stop (progress.cpp:90-124) consumes; its gradient
+ * for this step is zero (skip-on-overflow, as in loss-scaled mixed precision).
+ * Pass every tensor the backward reads (dY, the saved H_cat, each projection's
+ * input X; up to 32): a NaN left in any of them meets the structural zeros of
+ * the other jobs' columns.  One launch; in the all-finite case it reads J floats. */
+mlora_status mlora_zero_nonfinite_rows(mlora_ctx* ctx, const mlora_plan* plan, const float* loss,
+                                       void* const* tensors, const int32_t* cols, int32_t num_tensors,
+                                       void* stream);
+
 /* ---------------------------------------------------------------- model kernels (K4, K5)
  * No reference counterpart (the reference model is analytic): parity unpinned,
  * checked against fp64 restatements.  All device pointers; deterministic.

@@ -176,6 +176,20 @@ def batch_trace(items, batch_size, rounds):
     return res, cur.value
 
 
+def detect_stop(losses, accuracies=(), patience=3):
+    """fusim::detect_stop (progress.cpp:90-124): None or (iteration, cause),
+    cause in {"nan_loss", "accuracy_decline"}."""
+    l, lp = _d(losses or [0.0])
+    a, ap = _d(accuracies or [0.0])
+    it, cause = C.c_int(), C.c_int()
+    rc = lib().ref_detect_stop(len(losses), lp, len(accuracies), ap, patience, C.byref(it), C.byref(cause))
+    if rc == 9:
+        raise RuntimeError("reference detect_stop failed")
+    if rc == 0:
+        return None
+    return it.value, ("nan_loss", "accuracy_decline", "completed")[cause.value]
+
+
 class Weights:
     """A frozen W0 marshalled once into a reference fusim::Matrix (for timing)."""
 

@@ -221,6 +221,37 @@ __global__ void row_sumsq_kernel(const __grid_constant__ SumsqArgs a) {
     }
 }
 
+// Non-finite guard: every job whose loss is not finite gets its rows of each
+// tensor zeroed (the backward's dY), so no inf/NaN reaches the structural
+// zeros the fused reductions multiply it by (other jobs' columns of H_cat in
+// dB = dY^T H) — 0 * inf would poison co-scheduled jobs.  Grid (J, ysplit);
+// the common all-finite case reads J floats and exits.
+constexpr int kMaxGuardTensors = 32;
+struct GuardArgs {
+    __nv_bfloat16* t[kMaxGuardTensors];
+    int cols[kMaxGuardTensors];
+    int ntensors;
+    const int* seg;     // device, J+1
+    const float* loss;  // device, J
+};
+
+__global__ void zero_nonfinite_rows_kernel(const __grid_constant__ GuardArgs a) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int j = blockIdx.x;
+    if (isfinite(a.loss[j])) return;
+    const int r0 = a.seg[j], r1 = a.seg[j + 1];
+    const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+    for (int t = 0; t < a.ntensors; ++t) {
+        const int n8 = a.cols[t] / 8;
+        const long long total = (long long)(r1 - r0) * n8;
+        uint4* base = reinterpret_cast<uint4*>(a.t[t] + (long long)r0 * a.cols[t]);
+        for (long long i = (long long)blockIdx.y * blockDim.x + threadIdx.x; i < total;
+             i += (long long)gridDim.y * blockDim.x)
+            base[i] = z;
+    }
+}
+
 __global__ void segment_loss_kernel(const float* __restrict__ row_acc, const int* __restrict__ seg,
                                     float* __restrict__ loss) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");

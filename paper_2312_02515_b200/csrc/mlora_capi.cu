@@ -1153,4 +1153,29 @@ mlora_status mlora_segment_sumsq_loss(mlora_ctx* ctx, const mlora_plan* plan, co
     return MLORA_OK;
 }
 
+mlora_status mlora_zero_nonfinite_rows(mlora_ctx* ctx, const mlora_plan* plan, const float* loss,
+                                       void* const* tensors, const int32_t* cols, int32_t num_tensors,
+                                       void* stream) {
+    if (!ctx || !plan || !loss || !tensors || !cols) return fail(ctx, MLORA_USAGE, "null argument");
+    if (num_tensors < 1 || num_tensors > kMaxGuardTensors) return fail(ctx, MLORA_USAGE, "num_tensors out of range");
+    GuardArgs a{};
+    for (int t = 0; t < num_tensors; ++t) {
+        if (!tensors[t] || cols[t] <= 0 || cols[t] % 8 != 0)
+            return fail(ctx, MLORA_SHAPE, "guarded tensors need cols that are positive multiples of 8");
+        if (reinterpret_cast<uintptr_t>(tensors[t]) % 16 != 0)
+            return fail(ctx, MLORA_USAGE, "tensor base pointer must be 16-byte aligned");
+        a.t[t] = static_cast<__nv_bfloat16*>(tensors[t]);
+        a.cols[t] = cols[t];
+    }
+    a.ntensors = num_tensors;
+    a.seg = plan->d_seg;
+    a.loss = loss;
+    DeviceGuard g(ctx->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    ProfScope ps(ctx, 4, s);
+    MLORA_CUDA_TRY(ctx, launch_k(zero_nonfinite_rows_kernel, dim3(plan->J, 16), dim3(256), 0, s, 1, a));
+    ++ctx->launches;
+    return MLORA_OK;
+}
+
 }  // extern "C"

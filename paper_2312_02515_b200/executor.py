@@ -16,8 +16,21 @@ and emits the reference's `iteration_done{ξ, ξ_p, jobs_in_batch}` event
 (sim.cpp:185-191) with the MEASURED device time and the per-job losses (what
 the reference's detect_stop consumes, progress.cpp:90-124).  Metrics follow
 compute_metrics (sim.cpp:258-265): δ = Σξ_p / Σξ, T_tot = Σξ / makespan,
-T_e = (1 − δ)·T_tot.  Admission under a memory budget (scheduler.cpp) and early
-stopping are policy outside the hot path and are not reproduced here.
+T_e = (1 − δ)·T_tot.  Admission under a memory budget (scheduler.cpp) is policy
+outside the hot path and is not reproduced here.
+
+Early stopping (`early_stopping=True`) applies the reference's rule,
+detect_stop (progress.cpp:90-124, restated below), to the REAL per-job losses
+(and to accuracies from an optional `accuracy_fn`).  It is checked where the
+reference's stream_stop checks it (sim.cpp:85-101): a job stops once its event's
+iteration is <= the iterations it has done.  The job then leaves the candidate
+set, and a `job_stopped` record is appended to `Trace.stops` (the reference's
+scheduler.on_stop_event).  A job stopped for a non-finite loss is also
+quarantined (FusedLoraLayer.quarantine): its bf16 operand copies are zeroed, so
+its NaN adapter cannot reach the shared rank k-blocks of other jobs' tiles.  Pipelined, a step's losses are read while the next
+step is already queued, so a stop seen in step t's losses takes effect from
+step t+2.  With `pipelined=False` it takes effect from step t+1, as in the
+reference.
 
 Row order: the kernels need each job's rows contiguous and in adapter order, so
 the fused rows are placed in job-index order; the selection (urgency) order is
@@ -26,6 +39,7 @@ row-independent, so this changes no result.
 """
 from __future__ import annotations
 
+import math
 from dataclasses import dataclass, field
 
 import torch
@@ -33,6 +47,32 @@ import torch
 from . import fused as F
 from . import packer as P
 from .layer import FusedLoraLayer
+
+
+def detect_stop(losses, accuracies=(), patience: int = 3):
+    """fusim::detect_stop (progress.cpp:90-124): the first non-finite loss stops
+    the job at that (1-based) iteration; `patience` consecutive accuracy values
+    not above the best so far stop it at the last of them; the earlier event
+    wins and a tie goes to the NaN stop.  Returns None or (iteration, cause)."""
+    nan_ev = None
+    for i, v in enumerate(losses):
+        if not math.isfinite(v):
+            nan_ev = (i + 1, "nan_loss")
+            break
+    dec_ev = None
+    if len(accuracies) > 0 and patience >= 1:
+        best, streak = accuracies[0], 0
+        for i in range(1, len(accuracies)):
+            if accuracies[i] <= best:
+                streak += 1
+                if streak == patience:
+                    dec_ev = (i + 1, "accuracy_decline")
+                    break
+            else:
+                best, streak = accuracies[i], 0
+    if nan_ev and dec_ev:
+        return nan_ev if nan_ev[0] <= dec_ev[0] else dec_ev
+    return nan_ev or dec_ev
 
 
 @dataclass
@@ -53,10 +93,13 @@ class _JobState:
     cfg: JobConfig
     cursor: int = 0
     done: int = 0
+    losses: list = field(default_factory=list)      # one per completed iteration
+    accuracies: list = field(default_factory=list)
+    stopped: str | None = None                      # stop cause once early-stopped
 
     @property
     def finished(self) -> bool:
-        return self.done >= self.cfg.iterations
+        return self.stopped is not None or self.done >= self.cfg.iterations
 
     def peek(self) -> list:
         n = len(self.cfg.lengths)
@@ -73,6 +116,7 @@ class _JobState:
 @dataclass
 class Trace:
     events: list = field(default_factory=list)
+    stops: list = field(default_factory=list)       # job_stopped records (early stopping)
     busy_time: float = 0.0
 
     def metrics(self) -> dict:
@@ -91,8 +135,12 @@ class FusedExecutor:
 
     def __init__(self, ctx: F.Context, shapes, jobs: list[JobConfig], max_concurrent: int,
                  strategy: str = "minpad", padded: bool = False, seed: int = 0, W0: dict | None = None,
-                 pipelined: bool = True):
+                 pipelined: bool = True, early_stopping: bool = False, patience: int = 3,
+                 accuracy_fn=None):
         self.ctx = ctx
+        self.early_stopping = early_stopping
+        self.patience = patience
+        self.accuracy_fn = accuracy_fn  # (job_id, iteration, loss) -> accuracy or None
         self.shapes = shapes
         self.jobs = [_JobState(j) for j in jobs]
         self.M = max_concurrent
@@ -129,6 +177,22 @@ class FusedExecutor:
         ev = {"type": "iteration_done", "time": self.clock, "duration_s": duration, **pend["meta"],
               "losses": {self.jobs[i].cfg.id: losses[i] for i in pend["chosen"]}}
         self.trace.events.append(ev)
+        for i in pend["chosen"]:
+            js = self.jobs[i]
+            js.losses.append(losses[i])
+            if self.accuracy_fn is not None:
+                acc = self.accuracy_fn(js.cfg.id, len(js.losses), losses[i])
+                if acc is not None:
+                    js.accuracies.append(float(acc))
+            if self.early_stopping and js.stopped is None:
+                stop = detect_stop(js.losses, js.accuracies, self.patience)
+                if stop is not None and stop[0] <= len(js.losses):
+                    js.stopped = stop[1]
+                    if stop[1] == "nan_loss":
+                        self.layer.quarantine(i)  # a non-finite adapter must not reach other jobs' tiles
+                    self.trace.stops.append({"type": "job_stopped", "time": self.clock, "job": js.cfg.id,
+                                             "iteration": stop[0], "cause": stop[1],
+                                             "iterations_done": js.done})
         return ev
 
     def step(self) -> dict | None:

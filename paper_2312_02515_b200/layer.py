@@ -113,6 +113,19 @@ class FusedLoraLayer:
         self.plan.update(seg_offsets)  # stream-ordered, no host sync
         self.cur_rows = rows
 
+    def quarantine(self, job: int) -> None:
+        """Zero job `job`'s bf16 operand copies (its rows of every A_cat, its
+        columns of every B_cat), stream-ordered.  The fused kernels rely on
+        structural zeros: the other jobs' rows of H_cat / G_cat are exactly 0
+        and multiply this job's adapter inside a shared 64-column rank k-block.
+        0 * NaN is NaN, so a diverged adapter could poison its neighbours.  The
+        executor calls this when early stopping retires a job with a
+        non-finite loss.  Its fp32 masters and moments are kept for inspection."""
+        r0, r1 = self.plan.rank_offsets[job], self.plan.rank_offsets[job + 1]
+        for p in self.proj:
+            p.A.p_bf16[r0:r1].zero_()
+            p.B.p_bf16[:, r0:r1].zero_()
+
     def _views(self, p: Projection, rows: int):
         nblk = p.row_sq.shape[0]
         return (p.Y[:rows], p.H[:rows], p.G[:rows], p.dX[:rows],
@@ -131,7 +144,8 @@ class FusedLoraLayer:
         """Grouped schedule: every HBM-bound op is issued once for all projections
         whose inputs are ready (mlora_down_group / mlora_grad_group), the tensor-
         bound base GEMMs once per projection.  LLaMA layer: 2 forward down-group
-        launches, 7 base GEMMs, loss, 1 backward down-group, 7 dX GEMMs, 1 grad group."""
+        launches, 7 base GEMMs, loss, non-finite guard, 1 backward down-group, 7 dX GEMMs,
+        1 grad group."""
         ctx, plan = self.ctx, self.plan
         L, s = N.lib(), F._stream_handle(stream)
         rows = getattr(self, "cur_rows", self.rows)
@@ -164,6 +178,22 @@ class FusedLoraLayer:
         n = len(self.proj)
         ptrs = (N.vp * n)(*[v[4].data_ptr() for v in views])
         N.check(L.mlora_loss_from_rowsq(ctx.handle, plan.handle, ptrs, self._rowsq_d, n, self.loss.data_ptr(), s),
+                ctx.handle)
+        # ---- a job whose loss is not finite contributes a zero gradient: its rows of
+        # every tensor the backward reads — dY (= Y here), the saved H and every
+        # projection input X — are zeroed.  No inf/NaN then meets the structural
+        # zeros of other jobs' columns (dB = dY^T H, dA = G^T X), and the job's own
+        # gradient is exactly 0, so its adapter stays finite and cannot leak into
+        # its neighbours' forward tiles either.  (The caller's x rows of that job
+        # are zeroed in place.)
+        guard = {}
+        for i, v in enumerate(views):
+            guard[v[0].data_ptr()] = self.proj[i].d
+            guard[v[1].data_ptr()] = self.plan.rank_padded
+            guard[inputs[i].data_ptr()] = inputs[i].shape[1]
+        ng = len(guard)
+        N.check(L.mlora_zero_nonfinite_rows(ctx.handle, plan.handle, self.loss.data_ptr(),
+                                            (N.vp * ng)(*guard.keys()), (N.i32 * ng)(*guard.values()), ng, s),
                 ctx.handle)
         # ---- backward: dL/dY_p = Y_p for every projection
         N.check(L.mlora_down_group(ctx.handle, plan.handle, n, 1, (N.i32 * n)(*[p.d for p in self.proj]),

@@ -98,3 +98,101 @@ def test_pipelined_executor_matches_synchronous():
         for key in ("total_tokens", "padding_tokens", "effective_tokens", "rows", "routing"):
             assert ea[key] == eb[key]
         assert ea["losses"] == eb["losses"]
+
+
+@pytest.mark.parametrize("pipelined", [False, True])
+def test_executor_early_stopping_on_real_losses(pipelined):
+    """detect_stop (progress.cpp:90-124) on the device's real per-job losses: a
+    job driven to overflow by a huge learning rate stops on its first
+    non-finite loss, a job whose accuracy stream declines stops after
+    `patience` evaluations, and both leave the fused batch while the others
+    train to completion."""
+    from paper_2312_02515_b200 import executor as X
+    from paper_2312_02515_b200 import fused as F
+    from paper_2312_02515_b200.layer import TINY
+
+    ctx = F.Context(0)
+    jobs = [X.JobConfig(id=f"job{j}", lengths=[24, 40, 16, 32], batch_size=2, rank=8,
+                        lr=(1e30 if j == 1 else 1e-3), submit_time=float(j), iterations=7) for j in range(4)]
+    acc = lambda job, it, loss: 1.0 / it if job == "job2" else float(it)  # noqa: E731
+    ex = X.FusedExecutor(ctx, TINY, jobs, max_concurrent=4, seed=11, pipelined=pipelined,
+                         early_stopping=True, patience=2, accuracy_fn=acc)
+    trace = ex.run()
+    stops = {s["job"]: s for s in trace.stops}
+    assert set(stops) == {"job1", "job2"}, trace.stops
+    assert stops["job1"]["cause"] == "nan_loss" and stops["job2"]["cause"] == "accuracy_decline"
+    assert stops["job2"]["iteration"] == 3  # accuracies 1, 1/2, 1/3 with patience 2
+    losses = {j.id: [e["losses"][j.id] for e in trace.events if j.id in e["losses"]] for j in jobs}
+    assert X.detect_stop(losses["job1"]) == (stops["job1"]["iteration"], "nan_loss")
+    assert all(math.isfinite(v) for v in losses["job0"] + losses["job3"])
+    lag = 1 if pipelined else 0  # pipelined: the stop is seen while the next step is queued
+    for jid in ("job1", "job2"):
+        ran = sum(1 for e in trace.events if jid in e["routing"])
+        assert ran == stops[jid]["iteration"] + lag, (jid, ran, stops[jid])
+    for jid in ("job0", "job3"):
+        assert sum(1 for e in trace.events if jid in e["routing"]) == 7
+    r = ex.layer.plan.rank_offsets
+    for p in ex.layer.proj:  # the surviving jobs' adapters never saw the diverged one
+        for j in (0, 3):
+            assert torch.isfinite(p.A.p[r[j]:r[j + 1]]).all() and torch.isfinite(p.B.p[:, r[j]:r[j + 1]]).all()
+
+
+def test_quarantined_nan_adapter_cannot_reach_other_jobs():
+    """A job whose adapter went NaN and was retired (quarantined, absent from
+    the batch) leaves every output of the other jobs bitwise identical to a run
+    where it never diverged — Y, per-job loss, dX, dA, dB."""
+    from paper_2312_02515_b200 import fused as F
+    from paper_2312_02515_b200.layer import TINY, FusedLoraLayer
+
+    ctx = F.Context(0)
+    seg = [0, 96, 96, 200]  # job 1 absent from this batch
+    outs = []
+    for poison in (False, True):
+        layer = FusedLoraLayer(ctx, TINY, [8, 8, 16], [2.0] * 3, [1e-3] * 3, rows=200, seed=21)
+        layer.set_layout(seg)
+        if poison:
+            r = layer.plan.rank_offsets
+            for p in layer.proj:
+                p.A.p_bf16[r[1]:r[2]] = float("nan")
+                p.B.p_bf16[:, r[1]:r[2]] = float("nan")
+            layer.quarantine(1)
+        x = torch.Generator(device="cpu").manual_seed(4)
+        x = (torch.rand(200, TINY[0][2], generator=x) * 2 - 1).to(torch.bfloat16).cuda()
+        loss = layer.forward_backward(x).clone()
+        torch.cuda.synchronize()
+        outs.append((loss, [(p.Y[:200].clone(), p.dX[:200].clone(), p.dA.clone(), p.dB.clone()) for p in layer.proj],
+                     layer.plan.rank_offsets))
+    (l0, t0, r), (l1, t1, _) = outs
+    assert torch.equal(l0[[0, 2]], l1[[0, 2]])
+    keep = [c for j in (0, 2) for c in range(r[j], r[j + 1])]
+    for (y0, dx0, da0, db0), (y1, dx1, da1, db1) in zip(t0, t1):
+        assert torch.equal(y0, y1) and torch.equal(dx0, dx1)
+        assert torch.equal(da0[keep], da1[keep]) and torch.equal(db0[:, keep], db1[:, keep])
+
+
+def test_diverged_job_leaves_other_jobs_bitwise_unchanged():
+    """Without early stopping: a job driven to overflow (lr 1e30) reports a
+    non-finite loss every step from its divergence on, while every other job's
+    per-step loss is bitwise identical to a run in which it never diverged —
+    the per-job independence of the reference (lora.cpp:168-181 computes every
+    sequence with its own adapter), kept by mlora_zero_nonfinite_rows."""
+    from paper_2312_02515_b200 import fused as F
+    from paper_2312_02515_b200.layer import TINY, FusedLoraLayer
+
+    ctx = F.Context(0)
+    seg = [0, 72, 144, 216, 288]
+    runs = []
+    for lr1 in (1e-3, 1e30):
+        layer = FusedLoraLayer(ctx, TINY, [8] * 4, [2.0] * 4, [1e-3, lr1, 1e-3, 1e-3], rows=288, seed=11)
+        layer.set_layout(seg)
+        g = torch.Generator(device="cpu").manual_seed(3)
+        losses = []
+        for _ in range(5):
+            x = ((torch.rand(288, TINY[0][2], generator=g) * 2 - 1).to(torch.bfloat16)).cuda()
+            losses.append(layer.step(x).clone())
+        torch.cuda.synchronize()
+        runs.append(torch.stack(losses).cpu())
+    calm, wild = runs
+    assert torch.isfinite(calm).all()
+    assert not torch.isfinite(wild[1:, 1]).any()            # diverged from step 2 on
+    assert torch.equal(calm[:, [0, 2, 3]], wild[:, [0, 2, 3]])  # the others never noticed
