@@ -25,6 +25,7 @@
 #include "mlora_aux.cuh"
 #include "mlora_gemm.cuh"
 #include "mlora_quad.cuh"
+#include "mlora_down_multi.cuh"
 
 using namespace mlora;
 
@@ -419,6 +420,72 @@ mlora_status run_base(mlora_ctx* ctx, const mlora_plan* plan, const void* A0, in
 
 constexpr int kDownStages = 6;
 
+// MLORA_DOWN_MULTI=0 sends shared-input forward down-projections through the
+// grouped per-projection kernel instead (A/B measurement knob).
+bool down_multi_enabled() {
+    static const bool v = [] {
+        const char* e = std::getenv("MLORA_DOWN_MULTI");
+        return !(e && std::string(e) == "0");
+    }();
+    return v;
+}
+
+// Pipeline depth of the shared-input kernel: as deep as 227 KB of shared memory
+// allows (stage = x tile + NB adapter tiles; the K-split partials reuse the ring).
+constexpr int down_multi_stages(int nb) { return nb <= 2 ? 6 : nb == 3 ? 5 : 4; }
+
+template <int NB>
+mlora_status launch_down_multi(mlora_ctx* ctx, const mlora_plan* plan, int K, const void* x,
+                               const void* const* bop, void* const* out, cudaStream_t s) {
+    constexpr int STAGES = down_multi_stages(NB);
+    using L = DownMultiSmem<NB, STAGES>;
+    static_assert(L::kDynBytes <= 232448, "shared memory budget");
+    const int M = plan->rows, R = plan->R_pad;
+    DownMultiArgs<NB> a{};
+    mlora_status st;
+    if ((st = get_tmap(ctx, x, K, M, K, 64, 128, &a.tmA)) != MLORA_OK) return st;
+    for (int b = 0; b < NB; ++b) {
+        if ((st = get_tmap(ctx, bop[b], K, R, K, 64, 64, &a.tmB[b])) != MLORA_OK) return st;
+        a.out[b] = out[b];
+    }
+    GemmParams& p = a.p;
+    p.M = M;
+    p.N = R;
+    p.num_kb = cdiv(K, kBK);
+    p.n_mblk = plan->n_mblk;
+    p.num_tiles = plan->n_down;
+    p.ldo = R;
+    p.ext_tab = plan->d_ext;
+    p.down_tab = plan->d_down;
+    p.seg = plan->d_seg;
+    p.roff = plan->d_roff;
+    p.scale = plan->d_scale;
+    p.num_jobs = plan->J;
+    if (p.num_tiles <= 0) return MLORA_OK;
+    auto kern = mlora_down_multi_kernel<NB, STAGES>;
+    static bool attr_done = false;
+    if (!attr_done) {
+        MLORA_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kDynBytes));
+        attr_done = true;
+    }
+    const int clusters = std::min(p.num_tiles, ctx->num_sms / 2);
+    ProfScope ps(ctx, 2, s);
+    MLORA_CUDA_TRY(ctx, launch_k(kern, dim3(2 * clusters), dim3(kNumThreads), L::kDynBytes, s, 2, a));
+    ++ctx->launches;
+    return MLORA_OK;
+}
+
+mlora_status launch_down_multi_n(mlora_ctx* ctx, const mlora_plan* plan, int nb, int K, const void* x,
+                                 const void* const* bop, void* const* out, cudaStream_t s) {
+    switch (nb) {
+        case 2: return launch_down_multi<2>(ctx, plan, K, x, bop, out, s);
+        case 3: return launch_down_multi<3>(ctx, plan, K, x, bop, out, s);
+        case 4: return launch_down_multi<4>(ctx, plan, K, x, bop, out, s);
+        case 5: return launch_down_multi<5>(ctx, plan, K, x, bop, out, s);
+        default: return fail(ctx, MLORA_USAGE, "shared-input group size out of range");
+    }
+}
+
 // Rank-r down-projections of n projections in ONE launch (K split across CTA
 // pairs, DSMEM reduction):  out_i = s_j in_i Bop_i^T, block-diagonal.
 //   forward (B_MN=false): in = X_i [rows, K_i], Bop = A_cat_i [R, K_i]  -> H_i
@@ -427,23 +494,57 @@ template <bool B_MN>
 mlora_status run_down_group(mlora_ctx* ctx, const mlora_plan* plan, int n, const int32_t* K,
                             const void* const* in, const void* const* bop, void* const* out, cudaStream_t s) {
     const int M = plan->rows, R = plan->R_pad;
-    // Tile order.  Equal widths: interleave the problems tile by tile, so the
-    // projections fed by one hidden state stream it concurrently and share L2.
-    // Mixed widths: problems back to back, widest first — interleaving would hand
-    // each cluster tiles of a single problem whenever the cluster count is a
-    // multiple of the problem count (74 clusters, 2 problems: one half of the
-    // grid gets every 11008-wide tile), a 2.7x load imbalance.
-    std::vector<int> order(n);
-    for (int i = 0; i < n; ++i) order[i] = i;
+    for (int i = 0; i < n; ++i) {
+        if (!in[i] || !bop[i] || !out[i]) return fail(ctx, MLORA_USAGE, "null tensor pointer");
+        if (K[i] <= 0 || K[i] % 8) return fail(ctx, MLORA_SHAPE, "down-projection width must be a positive multiple of 8");
+    }
+    // Forward: projections reading the same input (q, k, v, gate, up <- x) go
+    // through the shared-input kernel, up to 5 per launch — x enters the SMs once
+    // per rank chunk instead of once per projection.
+    std::vector<int> order;
+    std::vector<bool> taken(n, false);
+    for (int i = 0; i < n; ++i) {
+        if (taken[i]) continue;
+        std::vector<int> same{i};
+        if (!B_MN && down_multi_enabled())
+            for (int j = i + 1; j < n; ++j)
+                if (!taken[j] && in[j] == in[i] && K[j] == K[i]) same.push_back(j);
+        if (same.size() < 2) {
+            order.push_back(i);
+            continue;
+        }
+        for (size_t c0 = 0; c0 < same.size(); c0 += kDownMultiMax) {
+            const int nb = static_cast<int>(std::min<size_t>(kDownMultiMax, same.size() - c0));
+            if (nb == 1) {
+                order.push_back(same[c0]);
+                continue;
+            }
+            const void* bops[kDownMultiMax];
+            void* outs[kDownMultiMax];
+            for (int b = 0; b < nb; ++b) {
+                bops[b] = bop[same[c0 + b]];
+                outs[b] = out[same[c0 + b]];
+            }
+            mlora_status st = launch_down_multi_n(ctx, plan, nb, K[i], in[i], bops, outs, s);
+            if (st != MLORA_OK) return st;
+        }
+        for (int j : same) taken[j] = true;
+    }
+    // Everything else: one grouped launch, one problem per projection.  Tile
+    // order: equal widths interleave the problems tile by tile (projections fed
+    // by one hidden state stream it concurrently and share L2); mixed widths
+    // run back to back, widest first — interleaving would hand each cluster
+    // tiles of a single problem whenever the cluster count is a multiple of the
+    // problem count (74 clusters, 2 problems: one half of the grid gets every
+    // 11008-wide tile), a 2.7x load imbalance.
+    const int nrest = static_cast<int>(order.size());
     bool same_k = true;
-    for (int i = 1; i < n; ++i) same_k = same_k && K[i] == K[0];
+    for (int oi = 1; oi < nrest; ++oi) same_k = same_k && K[order[oi]] == K[order[0]];
     if (!same_k) std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return K[x] > K[y]; });
-    for (int i0 = 0; i0 < n; i0 += kGroupMax) {
+    for (int i0 = 0; i0 < nrest; i0 += kGroupMax) {
         ProblemSet<kGroupMax> set;
-        for (int oi = i0; oi < std::min(n, i0 + kGroupMax); ++oi) {
+        for (int oi = i0; oi < std::min(nrest, i0 + kGroupMax); ++oi) {
             const int i = order[oi];
-            if (!in[i] || !bop[i] || !out[i]) return fail(ctx, MLORA_USAGE, "null tensor pointer");
-            if (K[i] <= 0 || K[i] % 8) return fail(ctx, MLORA_SHAPE, "down-projection width must be a positive multiple of 8");
             CUtensorMap tA, tB;
             mlora_status st;
             if ((st = get_tmap(ctx, in[i], K[i], M, K[i], 64, 128, &tA)) != MLORA_OK) return st;

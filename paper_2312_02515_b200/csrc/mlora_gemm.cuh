@@ -35,6 +35,7 @@ constexpr int kBK = 64;         // 64 bf16 = one 128 B swizzle row
 constexpr int kUmmaK = 16;      // K per tcgen05.mma kind::f16
 constexpr int kNumThreads = 192;
 
+
 struct GemmParams {
     int M;             // valid output rows (tokens for BASE/DOWN, features for GRAD*)
     int N;             // valid output cols (d for BASE, R_pad for DOWN/GRAD*)
@@ -99,6 +100,56 @@ __device__ __forceinline__ TileInfo decode_tile(const GemmParams& p, int t) {
     return ti;
 }
 
+__device__ __forceinline__ int job_of_row(const int* seg, int num_jobs, int row) {
+    // largest j with seg[j] <= row (segments partition [0, M))
+    int lo = 0, hi = num_jobs - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (__ldg(seg + mid) <= row) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+// MODE_DOWN epilogue for one row of a 64-column chunk tile: H/G = s_j * acc on
+// the columns of the row's own job, exactly 0 on every other column (a select,
+// not a multiply, so a non-finite acc of another job's columns never leaks).
+// The first chunk tile of an m-block (aux & 1) also zero-fills the row's
+// columns outside the m-block's LoRA k-block range, so H/G are fully
+// block-diagonal in HBM.
+template <int BN>
+__device__ __forceinline__ void down_store_row(const GemmParams& p, __nv_bfloat16* out, int row, int m0, int n0,
+                                               int aux, const float* accv) {
+    const int jr = job_of_row(p.seg, p.num_jobs, row);
+    const int c_lo = __ldg(p.roff + jr), c_hi = __ldg(p.roff + jr + 1);
+    const float s = __ldg(p.scale + jr);
+    uint4* dst = reinterpret_cast<uint4*>(out + (long long)row * p.ldo + n0);
+#pragma unroll
+    for (int g = 0; g < BN / 8; ++g) {
+        if (n0 + 8 * g + 8 > p.N) break;
+        float f[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const int cc = n0 + 8 * g + e;
+            f[e] = (cc >= c_lo && cc < c_hi) ? s * accv[8 * g + e] : 0.f;
+        }
+        uint4 w;
+        w.x = sm100::pack_bf16x2(f[0], f[1]);
+        w.y = sm100::pack_bf16x2(f[2], f[3]);
+        w.z = sm100::pack_bf16x2(f[4], f[5]);
+        w.w = sm100::pack_bf16x2(f[6], f[7]);
+        dst[g] = w;
+    }
+    if (aux & 1) {
+        const int mb = m0 / kBM;
+        const int z0 = __ldg(p.ext_tab + 2 * mb) * kBK;
+        const int z1 = __ldg(p.ext_tab + 2 * mb + 1) * kBK;
+        uint4* rowp = reinterpret_cast<uint4*>(out + (long long)row * p.ldo);
+        const uint4 zero = make_uint4(0, 0, 0, 0);
+        for (int cc = 0; cc < p.N; cc += 8)
+            if (cc < z0 || cc >= z1) rowp[cc / 8] = zero;
+    }
+}
+
 template <int BN, int STAGES, int KSPLIT = 1>
 struct GemmSmem {
     static constexpr int kABytes = kBM * kBK * 2;
@@ -113,15 +164,6 @@ struct GemmSmem {
     static constexpr int kDynBytes = kBytes + 1024;  // manual 1 KB alignment slack
 };
 
-__device__ __forceinline__ int job_of_row(const int* seg, int num_jobs, int row) {
-    // largest j with seg[j] <= row (segments partition [0, M))
-    int lo = 0, hi = num_jobs - 1;
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (__ldg(seg + mid) <= row) lo = mid; else hi = mid - 1;
-    }
-    return lo;
-}
 
 // One GEMM problem of a (possibly grouped) launch: its operand tensor maps, its
 // parameters and the global index of its first tile.  A launch carries up to NP
@@ -386,39 +428,7 @@ mlora_gemm_kernel(const __grid_constant__ GemmProblemSet<NP> ps) {
                         if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(pempty_bar), 1));
                     }
                 }
-                if (store && row_ok) {
-                    const int jr = job_of_row(p.seg, p.num_jobs, row);
-                    const int c_lo = __ldg(p.roff + jr), c_hi = __ldg(p.roff + jr + 1);
-                    const float s = __ldg(p.scale + jr);
-                    uint4* dst = reinterpret_cast<uint4*>(out + (long long)row * p.ldo + ti.n0);
-#pragma unroll
-                    for (int g = 0; g < BN / 8; ++g) {
-                        if (ti.n0 + 8 * g + 8 > p.N) break;
-                        float f[8];
-#pragma unroll
-                        for (int e = 0; e < 8; ++e) {
-                            const int cc = ti.n0 + 8 * g + e;
-                            f[e] = (cc >= c_lo && cc < c_hi) ? s * accv[8 * g + e] : 0.f;
-                        }
-                        uint4 w;
-                        w.x = pack_bf16x2(f[0], f[1]);
-                        w.y = pack_bf16x2(f[2], f[3]);
-                        w.z = pack_bf16x2(f[4], f[5]);
-                        w.w = pack_bf16x2(f[6], f[7]);
-                        dst[g] = w;
-                    }
-                    if (ti.aux & 1) {
-                        // first chunk tile of this m-block: define every other column
-                        // of the row (zero) so H/G are fully block-diagonal in HBM.
-                        const int mb = ti.m0 / kBM;
-                        const int z0 = __ldg(p.ext_tab + 2 * mb) * kBK;
-                        const int z1 = __ldg(p.ext_tab + 2 * mb + 1) * kBK;
-                        uint4* rowp = reinterpret_cast<uint4*>(out + (long long)row * p.ldo);
-                        const uint4 zero = make_uint4(0, 0, 0, 0);
-                        for (int cc = 0; cc < p.N; cc += 8)
-                            if (cc < z0 || cc >= z1) rowp[cc / 8] = zero;
-                    }
-                }
+                if (store && row_ok) down_store_row<BN>(p, out, row, ti.m0, ti.n0, ti.aux, accv);
             } else if constexpr (MODE == MODE_GRADT) {
                 float* out = static_cast<float*>(p.out) + (long long)ti.aux * p.split_stride;
 #pragma unroll 1
