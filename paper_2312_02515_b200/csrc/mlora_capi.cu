@@ -1054,8 +1054,8 @@ mlora_status mlora_loss_from_rowsq(mlora_ctx* ctx, const mlora_plan* plan, const
     if (st != MLORA_OK) return st;
     float* row_acc = static_cast<float*>(ctx->workspace);
     ProfScope ps(ctx, 4, s);
-    MLORA_CUDA_TRY(ctx, launch_k(rowsq_rows_kernel, dim3(std::min(cdiv(plan->rows, 256), 4 * ctx->num_sms)),
-                                 dim3(256), 0, s, 1, a, row_acc));
+    MLORA_CUDA_TRY(ctx, launch_k(rowsq_rows_kernel, dim3(cdiv(plan->rows, 32)), dim3(32, kRowSqSlices), 0, s, 1, a,
+                                 row_acc));
     MLORA_CUDA_TRY(ctx, launch_k(segment_loss_kernel, dim3(plan->J), dim3(1024), 0, s, 1,
                                  static_cast<const float*>(row_acc), static_cast<const int*>(plan->d_seg), loss));
     ctx->launches += 2;
