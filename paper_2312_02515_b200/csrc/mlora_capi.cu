@@ -22,6 +22,8 @@
 #include <vector>
 
 #include "../../include/mlora.h"
+#include <nvtx3/nvToolsExt.h>
+
 #include "mlora_aux.cuh"
 #include "mlora_gemm.cuh"
 #include "mlora_quad.cuh"
@@ -214,12 +216,18 @@ cudaEvent_t pool_event(mlora_ctx* ctx) {
 
 // Kernel kinds for the live profile: 0 base fwd, 1 base dX, 2 down (H/G), 3 grad (dA/dB),
 // 4 aux (reduce/pack/adam/loss).
+// Every launch site opens one: an NVTX range named after the kernel kind (free
+// unless a profiler is attached — nsys/ncu timelines then group the launches
+// per op), plus, while live profiling is on, a CUDA-event pair on the stream.
 struct ProfScope {
     mlora_ctx* ctx;
     int kind;
     cudaStream_t stream;
     cudaEvent_t a = nullptr, b = nullptr;
     ProfScope(mlora_ctx* c, int k, cudaStream_t s) : ctx(c), kind(k), stream(s) {
+        static const char* const kNames[] = {"mlora.base_fwd", "mlora.base_dx", "mlora.down",
+                                             "mlora.grad",     "mlora.aux",     "mlora.adam"};
+        nvtxRangePushA(kind >= 0 && kind < 6 ? kNames[kind] : "mlora");
         if (ctx->profiling) {
             a = pool_event(ctx);
             b = pool_event(ctx);
@@ -231,6 +239,7 @@ struct ProfScope {
             cudaEventRecord(b, stream);
             ctx->prof_pending.emplace_back(kind, a, b);
         }
+        nvtxRangePop();
     }
 };
 
