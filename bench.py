@@ -251,7 +251,12 @@ def main():
             W0[name] = torch.empty(d, k, dtype=torch.bfloat16, device=dev)
     ctx = F.Context(dev)
     # one GPU per rank: the native communicator (libmlora.so -> NCCL), all W0 in one group
-    comm = PL.NativeComm(ctx) if world > 1 and not share else None
+    comm, replication = None, "none (1 rank)" if world == 1 else "torch.distributed"
+    if world > 1 and not share:
+        try:
+            comm, replication = PL.NativeComm(ctx), "mlora_broadcast_base (one NCCL group)"
+        except Exception as e:  # setup only, never timed: keep the run alive, say so
+            print(f"[bench] native communicator unavailable ({e}); W0 via torch.distributed", file=sys.stderr)
     PL.broadcast_base_weights(W0, src=0, comm=comm)
     torch.cuda.synchronize()
 
@@ -363,7 +368,7 @@ def main():
         "config": {"workload": cfg["workload"], "jobs_per_gpu": J, "ranks": cfg["ranks"], "lrs": cfg["lrs"],
                    "tokens_per_step_per_gpu": rows, "effective_tokens_per_step_per_gpu": rows,
                    "padding_ratio": 0.0, "parallelism": f"adapter-parallel (jobs partitioned) x{world}, "
-                   "W0 replicated once at init (mlora_broadcast_base: one NCCL group)",
+                   f"W0 replicated once at init: {replication}",
                    "l2": "no flush; per-step working set (7 projections' W0 = 0.39 GB + activations) > 126 MB L2",
                    "flops_per_token": fpt},
         "step_tflops": step_tflops, "step_frac_of_peak": step_tflops / peak,

@@ -27,10 +27,14 @@ iteration is <= the iterations it has done.  The job then leaves the candidate
 set, and a `job_stopped` record is appended to `Trace.stops` (the reference's
 scheduler.on_stop_event).  A job stopped for a non-finite loss is also
 quarantined (FusedLoraLayer.quarantine): its bf16 operand copies are zeroed, so
-its NaN adapter cannot reach the shared rank k-blocks of other jobs' tiles.  Pipelined, a step's losses are read while the next
-step is already queued, so a stop seen in step t's losses takes effect from
-step t+2.  With `pipelined=False` it takes effect from step t+1, as in the
-reference.
+its NaN adapter cannot reach the shared rank k-blocks of other jobs' tiles.
+Pipelined, a step's losses are read while the next step is already queued, so a
+stop seen in step t's losses takes effect from step t+2.  With
+`pipelined=False` it takes effect from step t+1, as in the reference.
+
+With `checkpoint_dir`, each job's adapter and AdamW state is saved
+(FusedLoraLayer.save_job: reference layout, atomic write) when the job
+completes or is stopped.
 
 Row order: the kernels need each job's rows contiguous and in adapter order, so
 the fused rows are placed in job-index order; the selection (urgency) order is
@@ -96,6 +100,7 @@ class _JobState:
     losses: list = field(default_factory=list)      # one per completed iteration
     accuracies: list = field(default_factory=list)
     stopped: str | None = None                      # stop cause once early-stopped
+    saved: bool = False                             # adapter checkpoint written
 
     @property
     def finished(self) -> bool:
@@ -117,6 +122,7 @@ class _JobState:
 class Trace:
     events: list = field(default_factory=list)
     stops: list = field(default_factory=list)       # job_stopped records (early stopping)
+    checkpoints: list = field(default_factory=list)  # {job, path, iterations, cause} per saved adapter
     busy_time: float = 0.0
 
     def metrics(self) -> dict:
@@ -136,8 +142,9 @@ class FusedExecutor:
     def __init__(self, ctx: F.Context, shapes, jobs: list[JobConfig], max_concurrent: int,
                  strategy: str = "minpad", padded: bool = False, seed: int = 0, W0: dict | None = None,
                  pipelined: bool = True, early_stopping: bool = False, patience: int = 3,
-                 accuracy_fn=None):
+                 accuracy_fn=None, checkpoint_dir: str | None = None):
         self.ctx = ctx
+        self.checkpoint_dir = checkpoint_dir  # a job's adapter is saved when it completes or stops
         self.early_stopping = early_stopping
         self.patience = patience
         self.accuracy_fn = accuracy_fn  # (job_id, iteration, loss) -> accuracy or None
@@ -193,7 +200,19 @@ class FusedExecutor:
                     self.trace.stops.append({"type": "job_stopped", "time": self.clock, "job": js.cfg.id,
                                              "iteration": stop[0], "cause": stop[1],
                                              "iterations_done": js.done})
+            if self.checkpoint_dir is not None and js.finished and not js.saved:
+                self._checkpoint(i, js.stopped or "completed")
         return ev
+
+    def _checkpoint(self, i: int, cause: str) -> None:
+        """Save job i's adapter + AdamW state (reference layout, atomic write).
+        The host copy waits for the work already queued on the stream."""
+        import os
+        js = self.jobs[i]
+        path = os.path.join(self.checkpoint_dir, f"{js.cfg.id}.pt")
+        self.layer.save_job(path, i)
+        js.saved = True
+        self.trace.checkpoints.append({"job": js.cfg.id, "path": path, "iterations": js.done, "cause": cause})
 
     def step(self) -> dict | None:
         """Select, pack and enqueue the next fused iteration.  Pipelined (default):

@@ -101,7 +101,7 @@ def test_pipelined_executor_matches_synchronous():
 
 
 @pytest.mark.parametrize("pipelined", [False, True])
-def test_executor_early_stopping_on_real_losses(pipelined):
+def test_executor_early_stopping_on_real_losses(pipelined, tmp_path):
     """detect_stop (progress.cpp:90-124) on the device's real per-job losses: a
     job driven to overflow by a huge learning rate stops on its first
     non-finite loss, a job whose accuracy stream declines stops after
@@ -116,8 +116,14 @@ def test_executor_early_stopping_on_real_losses(pipelined):
                         lr=(1e30 if j == 1 else 1e-3), submit_time=float(j), iterations=7) for j in range(4)]
     acc = lambda job, it, loss: 1.0 / it if job == "job2" else float(it)  # noqa: E731
     ex = X.FusedExecutor(ctx, TINY, jobs, max_concurrent=4, seed=11, pipelined=pipelined,
-                         early_stopping=True, patience=2, accuracy_fn=acc)
+                         early_stopping=True, patience=2, accuracy_fn=acc, checkpoint_dir=str(tmp_path))
     trace = ex.run()
+    # every job's adapter was checkpointed once, when it completed or stopped
+    saved = {c["job"]: c for c in trace.checkpoints}
+    assert set(saved) == {j.id for j in jobs}
+    assert saved["job0"]["cause"] == "completed" and saved["job0"]["iterations"] == 7
+    assert saved["job2"]["cause"] == "accuracy_decline"
+    assert all((tmp_path / f"{j.id}.pt").exists() for j in jobs)
     stops = {s["job"]: s for s in trace.stops}
     assert set(stops) == {"job1", "job2"}, trace.stops
     assert stops["job1"]["cause"] == "nan_loss" and stops["job2"]["cause"] == "accuracy_decline"
@@ -196,3 +202,41 @@ def test_diverged_job_leaves_other_jobs_bitwise_unchanged():
     assert torch.isfinite(calm).all()
     assert not torch.isfinite(wild[1:, 1]).any()            # diverged from step 2 on
     assert torch.equal(calm[:, [0, 2, 3]], wild[:, [0, 2, 3]])  # the others never noticed
+
+
+def test_adapter_checkpoint_resume_is_exact(tmp_path):
+    """Save every job after 3 steps, resume into a freshly initialised layer and
+    continue: the next steps' per-job losses are bitwise those of the
+    uninterrupted run (masters, AdamW moments and step counts all restored).
+    Checkpoints are per job in the reference layout (A_j r x k, B_j d x r)."""
+    from paper_2312_02515_b200 import errors as E
+    from paper_2312_02515_b200 import fused as F
+    from paper_2312_02515_b200.layer import TINY, FusedLoraLayer
+
+    ctx = F.Context(0)
+    seg = [0, 100, 100, 256]  # job 1 absent: its slot must round-trip untouched too
+    mk = lambda seed, W0=None: FusedLoraLayer(ctx, TINY, [8, 16, 8], [2.0, 1.0, 0.5],  # noqa: E731
+                                              [1e-2, 5e-3, 2e-2], rows=256, seed=seed, W0=W0)
+    g = torch.Generator().manual_seed(8)
+    xs = [((torch.rand(256, 256, generator=g) * 2 - 1).to(torch.bfloat16)).cuda() for _ in range(5)]
+    a = mk(1)
+    a.set_layout(seg)
+    for x in xs[:3]:
+        a.step(x)
+    paths = [str(tmp_path / f"job{j}.pt") for j in range(3)]
+    for j in range(3):
+        a.save_job(paths[j], j)
+    want = [a.step(x).clone() for x in xs[3:]]
+    b = mk(99, W0={p.name: p.W0 for p in a.proj})  # same frozen base, different initial adapters
+    b.set_layout(seg)
+    for j in range(3):
+        b.load_job(paths[j], j)
+    got = [b.step(x).clone() for x in xs[3:]]
+    torch.cuda.synchronize()
+    assert all(torch.equal(w, g_) for w, g_ in zip(want, got))
+    st = torch.load(paths[1])
+    assert tuple(st["proj"]["q"]["A"].shape) == (16, 256) and tuple(st["proj"]["q"]["B"].shape) == (256, 16)
+    with pytest.raises(E.UsageError):
+        b.load_job(paths[0], 1)  # rank 8 checkpoint into a rank-16 slot
+    with pytest.raises(E.UsageError):
+        b.load_job(paths[2], 0)  # same rank, different scale
