@@ -167,11 +167,12 @@ mlora_status mlora_linear_bwd(mlora_ctx* ctx, const mlora_plan* plan, int32_t d,
 mlora_status mlora_down_group(mlora_ctx* ctx, const mlora_plan* plan, int32_t n, int32_t backward,
                               const int32_t* width, const void* const* in, const void* const* adapter,
                               void* const* out, void* stream);
-/* Y = X W0^T + H B_cat^T (CTA-pair tcgen05 GEMM; optional fused row sums, see _ex). */
+/* Y = X W0^T + H B_cat^T (CTA-pair tcgen05 GEMM; optional fused row sums, see _ex).
+ * H == B_cat == NULL: the plain frozen GEMM Y = X W0^T (e.g. a model's LM head). */
 mlora_status mlora_base_fwd(mlora_ctx* ctx, const mlora_plan* plan, int32_t d, int32_t k, const void* X,
                             const void* W0, const void* H, const void* B_cat, void* Y, float* row_sq,
                             void* stream);
-/* dX = dY W0 + G A_cat. */
+/* dX = dY W0 + G A_cat  (G == A_cat == NULL: dX = dY W0). */
 mlora_status mlora_base_dx(mlora_ctx* ctx, const mlora_plan* plan, int32_t d, int32_t k, const void* dY,
                            const void* W0, const void* G, const void* A_cat, void* dX, void* stream);
 /* dA_cat_i = G_i^T X_i and dB_cat_i = dY_i^T H_i for n projections (two grouped launches + at most one
@@ -276,6 +277,65 @@ mlora_status mlora_rope(int64_t rows, int32_t heads, int32_t head_dim, const voi
  * detect_stop (progress.cpp:90-124). */
 mlora_status mlora_segment_sumsq_loss(mlora_ctx* ctx, const mlora_plan* plan, const void* const* Y,
                                       const int32_t* cols, int32_t num_tensors, float* loss, void* stream);
+
+/* ---------------------------------------------------------------- decoder-layer kernels (configs C1, C4)
+ * The kernels around the LoRA linears that a whole LLaMA / ChatGLM2-shaped
+ * decoder needs to be fine-tuned on the fused batch end to end
+ * (paper_2312_02515_b200/model.py).  No reference counterpart (the reference
+ * has no model: SURVEY.md App. A), parity unpinned: checked against a PyTorch
+ * fp32 restatement of the same model.  Deterministic; bf16 tensors, fp32 math.
+ *
+ * Frozen token embedding: x[t] = E[tokens[t]] (E bf16 [V, h], h % 8 == 0;
+ * tokens device int32, caller-validated to [0, V)). */
+mlora_status mlora_embed(int64_t rows, int32_t h, int32_t V, const int32_t* tokens, const void* E, void* x,
+                         void* stream);
+/* Residual add fused into RMSNorm: x_out = bf16(x + delta) (skipped when delta == NULL),
+ * y = x_out * rstd * w, rstd = 1 / sqrt(mean(x_out^2) + eps).  x_out must not alias x. */
+mlora_status mlora_add_rmsnorm(int64_t rows, int32_t h, const void* x, const void* delta, const void* w, float eps,
+                               void* x_out, void* y, float* rstd, void* stream);
+/* RMSNorm backward for a frozen weight, summing the n_dy <= 4 gradients that
+ * reach y (e.g. the dX of q, k, v) and adding the residual gradient dres
+ * (may be NULL): dx = dres + rstd (g - xhat mean(g xhat)), g = w sum_i dy_i. */
+mlora_status mlora_rmsnorm_bwd_sum(int64_t rows, int32_t h, int32_t n_dy, const void* const* dy, const void* dres,
+                                   const void* x, const void* w, const float* rstd, void* dx, void* stream);
+/* SwiGLU: out[t, c] = silu(gate[t, c]) * up[t, c] (out is rows x f, contiguous; gate / up
+ * are column slices with row strides ld_*, e.g. the two halves of ChatGLM2's h_to_4h). */
+mlora_status mlora_swiglu_fwd(int64_t rows, int32_t f, const void* gate, int64_t ld_gate, const void* up,
+                              int64_t ld_up, void* out, void* stream);
+mlora_status mlora_swiglu_bwd(int64_t rows, int32_t f, const void* gate, int64_t ld_gate, const void* up,
+                              int64_t ld_up, const void* dout, void* dgate, int64_t ld_dgate, void* dup,
+                              int64_t ld_dup, void* stream);
+
+/* Causal attention over the fused row layout.  Sequence s owns rows
+ * seq_offsets[s] .. seq_offsets[s+1] (device int32, S + 1 entries); its real
+ * tokens are the first seq_lens[s] rows (device int32 [S]; NULL: all), the
+ * rest are padding (output 0, no gradient).  Grouped-query: query head h reads
+ * K/V head h / (heads / kv_heads) (ChatGLM2 multi-query: kv_heads = 2).
+ * head_dim 64 or 128.  RoPE (rotate-half, the angle of mlora_rope with
+ * pos = row - seq start) is applied to Q and K inside the kernel when
+ * rope_base > 0.  lse: fp32 [heads, rows] (natural log), saved for backward. */
+typedef struct mlora_attn_desc {
+    const int32_t* seq_offsets;
+    const int32_t* seq_lens;
+    int64_t rows;
+    int32_t num_seqs;
+    int32_t max_len;  /* >= the longest slot (host-side bound for the grid) */
+    int32_t heads;
+    int32_t kv_heads;
+    int32_t head_dim;
+    float rope_base;
+    float softmax_scale;
+    int32_t _pad;
+} mlora_attn_desc;
+
+/* q: rows x ldq (head h at column h * head_dim), k / v: rows x ld (K/V head g at g * head_dim). */
+mlora_status mlora_attn_fwd(const mlora_attn_desc* desc, const void* q, int64_t ldq, const void* k, int64_t ldk,
+                            const void* v, int64_t ldv, void* o, int64_t ldo, float* lse, void* stream);
+/* dq, dk, dv (bf16, written, same column layout as q, k, v); dsum: fp32 [heads, rows] scratch. */
+mlora_status mlora_attn_bwd(const mlora_attn_desc* desc, const void* q, int64_t ldq, const void* k, int64_t ldk,
+                            const void* v, int64_t ldv, const void* o, int64_t ldo, const void* dout, int64_t lddo,
+                            const float* lse, float* dsum, void* dq, int64_t lddq, void* dk, int64_t lddk, void* dv,
+                            int64_t lddv, void* stream);
 
 /* ---------------------------------------------------------------- multi-GPU
  * Adapter-parallel: jobs are partitioned across GPUs (one process and one

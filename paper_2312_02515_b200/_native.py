@@ -28,6 +28,12 @@ class FusedShapeC(C.Structure):
     _fields_ = [("max_len", i32), ("sequences", i64), ("total_tokens", i64), ("padding_tokens", i64)]
 
 
+class AttnDescC(C.Structure):
+    _fields_ = [("seq_offsets", vp), ("seq_lens", vp), ("rows", i64), ("num_seqs", i32), ("max_len", i32),
+                ("heads", i32), ("kv_heads", i32), ("head_dim", i32), ("rope_base", f32), ("softmax_scale", f32),
+                ("_pad", i32)]
+
+
 class AdamGroupC(C.Structure):
     _fields_ = [("p", vp), ("g", vp), ("m", vp), ("v", vp), ("p_bf16", vp), ("rows", i64),
                 ("cols", i64), ("layout", i32), ("_pad", i32)]
@@ -76,6 +82,15 @@ _OPTIONAL = {
     "mlora_rmsnorm_fwd": (i32, [i64, i32, vp, vp, f32, vp, vp, vp]),
     "mlora_rmsnorm_bwd": (i32, [i64, i32, vp, vp, vp, vp, vp, vp, vp, i32, vp]),
     "mlora_rope": (i32, [i64, i32, i32, vp, vp, vp, f32, i32, vp]),
+    # decoder-layer kernels (model.py)
+    "mlora_embed": (i32, [i64, i32, i32, vp, vp, vp, vp]),
+    "mlora_add_rmsnorm": (i32, [i64, i32, vp, vp, vp, f32, vp, vp, vp, vp]),
+    "mlora_rmsnorm_bwd_sum": (i32, [i64, i32, i32, C.POINTER(vp), vp, vp, vp, vp, vp, vp]),
+    "mlora_swiglu_fwd": (i32, [i64, i32, vp, i64, vp, i64, vp, vp]),
+    "mlora_swiglu_bwd": (i32, [i64, i32, vp, i64, vp, i64, vp, vp, i64, vp, i64, vp]),
+    "mlora_attn_fwd": (i32, [C.POINTER(AttnDescC), vp, i64, vp, i64, vp, i64, vp, i64, vp, vp]),
+    "mlora_attn_bwd": (i32, [C.POINTER(AttnDescC), vp, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp, vp, vp, i64,
+                             vp, i64, vp, i64, vp]),
     # multi-GPU boundary (NCCL resolved at first use)
     "mlora_comm_id_bytes": (i32, []),
     "mlora_comm_nccl_version": (i32, [C.POINTER(i32)]),

@@ -371,18 +371,27 @@ mlora_status run_base(mlora_ctx* ctx, const mlora_plan* plan, const void* A0, in
     const bool quad = base_kernel_variant() == 2;
     const int M = plan->rows;
     const uint32_t bbox = quad ? 64 : pair ? 128 : 256;  // K-major B rows staged per TMA box
+    // A1 == B1 == NULL: no LoRA term (frozen GEMM, e.g. an LM head): the CTA-pair
+    // kernel then runs no extra k-blocks (ext_tab == NULL) and never reads tA1/tB1.
+    const bool lora = A1 != nullptr;
+    if (!lora && (!pair || quad))
+        return fail(ctx, MLORA_USAGE, "a GEMM without a LoRA term needs the CTA-pair base kernel");
     CUtensorMap tA0, tB0, tA1, tB1;
     mlora_status st;
     if ((st = get_tmap(ctx, A0, K0, M, lda0, 64, 128, &tA0)) != MLORA_OK) return st;
-    if ((st = get_tmap(ctx, A1, R, M, R, 64, 128, &tA1)) != MLORA_OK) return st;
+    if (lora && (st = get_tmap(ctx, A1, R, M, R, 64, 128, &tA1)) != MLORA_OK) return st;
     if (!B_MN) {
         // B0 = W0 [N=d, K0=k], B1 = B_cat [N=d, R]
         if ((st = get_tmap(ctx, B0, K0, N, K0, 64, bbox, &tB0)) != MLORA_OK) return st;
-        if ((st = get_tmap(ctx, B1, R, N, R, 64, bbox, &tB1)) != MLORA_OK) return st;
+        if (lora && (st = get_tmap(ctx, B1, R, N, R, 64, bbox, &tB1)) != MLORA_OK) return st;
     } else {
         // B0 = W0 [K0=d, N=k] (n contiguous), B1 = A_cat [R, N=k]
         if ((st = get_tmap(ctx, B0, N, K0, N, 64, 64, &tB0)) != MLORA_OK) return st;
-        if ((st = get_tmap(ctx, B1, N, R, N, 64, 64, &tB1)) != MLORA_OK) return st;
+        if (lora && (st = get_tmap(ctx, B1, N, R, N, 64, 64, &tB1)) != MLORA_OK) return st;
+    }
+    if (!lora) {
+        tA1 = tA0;
+        tB1 = tB0;
     }
     GemmParams pb{};
     pb.M = M;
@@ -415,7 +424,7 @@ mlora_status run_base(mlora_ctx* ctx, const mlora_plan* plan, const void* A0, in
         pb.n_mblk = plan->n_mblk256;
         pb.n_nblk = cdiv(N, kPairBN);
         pb.num_tiles = pb.n_mblk * pb.n_nblk;
-        pb.ext_tab = plan->d_ext256;
+        pb.ext_tab = lora ? plan->d_ext256 : nullptr;
         return launch_base_pair<B_MN>(ctx, tA0, tB0, tA1, tB1, pb, s);
     }
     pb.n_mblk = plan->n_mblk;
@@ -1123,7 +1132,7 @@ mlora_status mlora_base_fwd(mlora_ctx* ctx, const mlora_plan* plan, int32_t d, i
                             void* stream) {
     mlora_status st = check_dims(ctx, plan, d, k);
     if (st != MLORA_OK) return st;
-    if (!X || !W0 || !H || !B_cat || !Y) return fail(ctx, MLORA_USAGE, "null tensor pointer");
+    if (!X || !W0 || !Y || (!H != !B_cat)) return fail(ctx, MLORA_USAGE, "null tensor pointer");
     DeviceGuard g(ctx->device);
     return run_base<false>(ctx, plan, X, k, k, W0, H, B_cat, plan->R_pad, d, Y, static_cast<cudaStream_t>(stream),
                            row_sq);
@@ -1133,7 +1142,7 @@ mlora_status mlora_base_dx(mlora_ctx* ctx, const mlora_plan* plan, int32_t d, in
                            const void* W0, const void* G, const void* A_cat, void* dX, void* stream) {
     mlora_status st = check_dims(ctx, plan, d, k);
     if (st != MLORA_OK) return st;
-    if (!dY || !W0 || !G || !A_cat || !dX) return fail(ctx, MLORA_USAGE, "null tensor pointer");
+    if (!dY || !W0 || !dX || (!G != !A_cat)) return fail(ctx, MLORA_USAGE, "null tensor pointer");
     DeviceGuard g(ctx->device);
     return run_base<true>(ctx, plan, dY, d, d, W0, G, A_cat, plan->R_pad, k, dX, static_cast<cudaStream_t>(stream));
 }

@@ -576,7 +576,8 @@ mlora_base_pair_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_co
                 pair_tile_coords(p, t, mb, nb);
                 const int m0 = mb * kPairBM + static_cast<int>(cta) * 128;
                 const int n0 = nb * kPairBN + static_cast<int>(cta) * 128;
-                const int xb0 = __ldg(p.ext_tab + 2 * mb), xb1 = __ldg(p.ext_tab + 2 * mb + 1);
+                const int xb0 = p.ext_tab ? __ldg(p.ext_tab + 2 * mb) : 0;
+                const int xb1 = p.ext_tab ? __ldg(p.ext_tab + 2 * mb + 1) : 0;
                 const int nmain = p.num_kb;
                 const int nk = nmain + (xb1 - xb0);
                 for (int it = 0; it < nk; ++it) {
@@ -609,7 +610,7 @@ mlora_base_pair_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_co
             for (int t = cluster_id; t < p.num_tiles; t += nclusters, ++local) {
                 int mb, nb;
                 pair_tile_coords(p, t, mb, nb);
-                const int nk = p.num_kb + (__ldg(p.ext_tab + 2 * mb + 1) - __ldg(p.ext_tab + 2 * mb));
+                const int nk = p.num_kb + (p.ext_tab ? __ldg(p.ext_tab + 2 * mb + 1) - __ldg(p.ext_tab + 2 * mb) : 0);
                 const int acc = local & 1;
                 const uint32_t use = static_cast<uint32_t>(local >> 1);
                 mbar_wait(tempty_bar + acc, (use & 1u) ^ 1u);
