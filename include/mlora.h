@@ -313,7 +313,11 @@ mlora_status mlora_swiglu_bwd(int64_t rows, int32_t f, const void* gate, int64_t
  * K/V head h / (heads / kv_heads) (ChatGLM2 multi-query: kv_heads = 2).
  * head_dim 64 or 128.  RoPE (rotate-half, the angle of mlora_rope with
  * pos = row - seq start) is applied to Q and K inside the kernel when
- * rope_base > 0.  lse: fp32 [heads, rows] (natural log), saved for backward. */
+ * rope_base > 0.  lse: fp32 [heads, rows] (natural log), saved for backward.
+ * flags & MLORA_ATTN_PREROTATED: q and k were already rotated by
+ * mlora_attn_rope (saved once per step, so no tile re-rotates them); the
+ * backward still returns dq / dk with respect to the UNROTATED q and k. */
+#define MLORA_ATTN_PREROTATED 1
 typedef struct mlora_attn_desc {
     const int32_t* seq_offsets;
     const int32_t* seq_lens;
@@ -325,12 +329,15 @@ typedef struct mlora_attn_desc {
     int32_t head_dim;
     float rope_base;
     float softmax_scale;
-    int32_t _pad;
+    int32_t flags;
 } mlora_attn_desc;
 
 /* q: rows x ldq (head h at column h * head_dim), k / v: rows x ld (K/V head g at g * head_dim). */
 mlora_status mlora_attn_fwd(const mlora_attn_desc* desc, const void* q, int64_t ldq, const void* k, int64_t ldk,
                             const void* v, int64_t ldv, void* o, int64_t ldo, float* lse, void* stream);
+/* dst = RoPE(src) for n_heads heads per row (pos = row - sequence start; padding rows -> 0). */
+mlora_status mlora_attn_rope(const mlora_attn_desc* desc, const void* src, int64_t ld_src, int32_t n_heads, void* dst,
+                             int64_t ld_dst, void* stream);
 /* dq, dk, dv (bf16, written, same column layout as q, k, v); dsum: fp32 [heads, rows] scratch. */
 mlora_status mlora_attn_bwd(const mlora_attn_desc* desc, const void* q, int64_t ldq, const void* k, int64_t ldk,
                             const void* v, int64_t ldv, const void* o, int64_t ldo, const void* dout, int64_t lddo,

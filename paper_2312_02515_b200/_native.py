@@ -31,7 +31,7 @@ class FusedShapeC(C.Structure):
 class AttnDescC(C.Structure):
     _fields_ = [("seq_offsets", vp), ("seq_lens", vp), ("rows", i64), ("num_seqs", i32), ("max_len", i32),
                 ("heads", i32), ("kv_heads", i32), ("head_dim", i32), ("rope_base", f32), ("softmax_scale", f32),
-                ("_pad", i32)]
+                ("flags", i32)]
 
 
 class AdamGroupC(C.Structure):
@@ -89,6 +89,7 @@ _OPTIONAL = {
     "mlora_swiglu_fwd": (i32, [i64, i32, vp, i64, vp, i64, vp, vp]),
     "mlora_swiglu_bwd": (i32, [i64, i32, vp, i64, vp, i64, vp, vp, i64, vp, i64, vp]),
     "mlora_attn_fwd": (i32, [C.POINTER(AttnDescC), vp, i64, vp, i64, vp, i64, vp, i64, vp, vp]),
+    "mlora_attn_rope": (i32, [C.POINTER(AttnDescC), vp, i64, i32, vp, i64, vp]),
     "mlora_attn_bwd": (i32, [C.POINTER(AttnDescC), vp, i64, vp, i64, vp, i64, vp, i64, vp, i64, vp, vp, vp, i64,
                              vp, i64, vp, i64, vp]),
     # multi-GPU boundary (NCCL resolved at first use)

@@ -15,9 +15,10 @@
 // transpose to a [batch, heads, len, head_dim] tensor is ever materialised.
 // Q/K/V are column slices of the projection outputs (row stride ld), which
 // covers ChatGLM2's fused qkv output (multi-query: 2 K/V groups) as well as
-// LLaMA's separate q, k, v.  Attention is not on the BatchFusion hot path; the
-// tiles run on the CUDA cores in fp32 (64 x 64 tiles, 4 x 4 register blocking)
-// — correct and deterministic, not a tensor-core kernel.
+// LLaMA's separate q, k, v.  Attention is not on the BatchFusion hot path: its
+// 64 x 64 tiles run on the warp-level tensor-core MMA (mma.sync bf16, fp32
+// accumulation), flash-style (no score matrix in HBM), with a deterministic
+// two-kernel backward (dK/dV per key tile, dQ per query tile; no atomics).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -30,7 +31,6 @@
 namespace {
 
 constexpr int kBM = 64;  // rows (queries or keys) per attention tile
-constexpr int kThreads = 256;
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kLn2 = 0.6931471805599453f;
 
@@ -166,6 +166,8 @@ struct AttnArgs {
     int heads, kv_heads;
     float rope_base;     // 0: no rotary
     float scale;         // softmax scale (1/sqrt(head_dim) normally)
+    int rope_in;         // rotate Q/K while staging (they arrive unrotated)
+    int vec;             // every staged row is 16-byte aligned: cp.async staging
     long long rows;
     const __nv_bfloat16 *q, *k, *v, *o, *dO;
     long long ldq, ldk, ldv, ldo, lddo;
@@ -175,11 +177,20 @@ struct AttnArgs {
     float* dsum;         // [heads][rows], sum_d dO * O
 };
 
+// Tensor-core tiles (legacy warp-level mma.sync m16n8k16 bf16 -> fp32; the
+// attention is outside the BatchFusion hot path, so it uses the simple warp
+// MMA rather than tcgen05).  4 warps per CTA, each owning 16 rows of a 64-row
+// tile; 64-column key / query tiles staged in shared memory as bf16 with a
+// padded row stride (conflict-free ldmatrix); RoPE applied while staging.
+constexpr int kWarps = 4;
+constexpr int kTcThreads = 32 * kWarps;
+
 template <int HD>
 struct Tile {
-    static constexpr int LD = HD + 4;     // fp32 row stride of Q/K/V/dO tiles
-    static constexpr int PLD = kBM + 4;   // fp32 row stride of P / dS tiles
-    static constexpr int DV = HD / 64;    // float4 column groups per thread: d = tx*4 + 64c + e
+    static constexpr int LDH = HD + 8;      // bf16 row stride of staged tiles (16 B pad)
+    static constexpr int LDF = HD + 4;      // fp32 row stride of the epilogue staging tile
+    static constexpr int TILE = kBM * LDH;  // bf16 elements per staged tile
+    static constexpr int KS = HD / 16;      // k-steps over the head dim
 };
 
 __device__ __forceinline__ void seq_range(const AttnArgs& a, int s, int& start, int& len) {
@@ -188,13 +199,72 @@ __device__ __forceinline__ void seq_range(const AttnArgs& a, int s, int& start, 
     len = a.seq_len ? min(a.seq_len[s], slot) : slot;
 }
 
-// Load rows [r0, r0 + 64) of one head (column offset col) into a fp32 tile,
-// rotating pairs (i, i + HD/2) by pos * base^(-2i/HD) (the same angle as
-// mlora_rope) when rope != 0; rows at or beyond `len` are zero.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void ldsm4(uint32_t (&r)[4], uint32_t addr) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr));
+}
+__device__ __forceinline__ void ldsm4t(uint32_t (&r)[4], uint32_t addr) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]) : "r"(addr));
+}
+__device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+                 "{%0,%1,%2,%3};"
+                 : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+                 : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ uint32_t pack2(float lo, float hi) {
+    const __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+// Stage rows [r0, r0 + 64) of one head (column offset col) as bf16 [64][LDH],
+// rotating pairs (i, i + HD/2) by pos * base^(-2i/HD) — the angle of
+// mlora_rope — when rope; rows at or beyond len are zero.  async: issue
+// cp.async copies (the caller commits / waits), for tiles that need no rotation.
 template <int HD>
-__device__ void load_tile(float* dst, const __nv_bfloat16* src, long long ld, int start, int r0, int len, int col,
-                          float rope_base, bool rope) {
-    constexpr int half = HD / 2, LD = Tile<HD>::LD;
+__device__ void stage(__nv_bfloat16* dst, const __nv_bfloat16* src, long long ld, int start, int r0, int len, int col,
+                      float rope_base, bool rope, bool async = false) {
+    constexpr int half = HD / 2, LDH = Tile<HD>::LDH;
+    if (!rope && async) {  // cp.async 16-byte chunks (rows must be 16-byte aligned); zero-fill past len
+        for (int e = threadIdx.x; e < kBM * (HD / 8); e += blockDim.x) {
+            const int r = e / (HD / 8), c = (e % (HD / 8)) * 8;
+            __nv_bfloat16* d = dst + r * LDH + c;
+            if (r0 + r < len)
+                cp_async16(smem_u32(d), src + (long long)(start + r0 + r) * ld + col + c);
+            else
+                *reinterpret_cast<uint4*>(d) = make_uint4(0, 0, 0, 0);
+        }
+        return;
+    }
+    if (!rope) {
+        for (int e = threadIdx.x; e < kBM * (HD / 8); e += blockDim.x) {
+            const int r = e / (HD / 8), c = (e % (HD / 8)) * 8;
+            uint4 v = make_uint4(0, 0, 0, 0);
+            if (r0 + r < len) {
+                const __nv_bfloat16* p = src + (long long)(start + r0 + r) * ld + col + c;
+                if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+                    v = *reinterpret_cast<const uint4*>(p);
+                } else {
+                    const uint32_t* q = reinterpret_cast<const uint32_t*>(p);
+                    v = make_uint4(q[0], q[1], q[2], q[3]);
+                }
+            }
+            *reinterpret_cast<uint4*>(dst + r * LDH + c) = v;
+        }
+        return;
+    }
+    const float lb = log2f(rope_base);
     for (int e = threadIdx.x; e < kBM * (half / 2); e += blockDim.x) {
         const int r = e / (half / 2), i = (e % (half / 2)) * 2;
         const int pos = r0 + r;
@@ -203,39 +273,33 @@ __device__ void load_tile(float* dst, const __nv_bfloat16* src, long long ld, in
             const __nv_bfloat16* p = src + (long long)(start + pos) * ld + col;
             const float2 A = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(p + i));
             const float2 B = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(p + i + half));
-            a0 = A.x, a1 = A.y, b0 = B.x, b1 = B.y;
-            if (rope) {
-                const float lb = log2f(rope_base);
-                float s0, c0, s1, c1;
-                sincosf(pos * exp2f(-(2.f * i / HD) * lb), &s0, &c0);
-                sincosf(pos * exp2f(-(2.f * (i + 1) / HD) * lb), &s1, &c1);
-                const float ra0 = a0 * c0 - b0 * s0, rb0 = b0 * c0 + a0 * s0;
-                const float ra1 = a1 * c1 - b1 * s1, rb1 = b1 * c1 + a1 * s1;
-                a0 = ra0, b0 = rb0, a1 = ra1, b1 = rb1;
-            }
+            float s0, c0, s1, c1;
+            sincosf(pos * exp2f(-(2.f * i / HD) * lb), &s0, &c0);
+            sincosf(pos * exp2f(-(2.f * (i + 1) / HD) * lb), &s1, &c1);
+            a0 = A.x * c0 - B.x * s0, b0 = B.x * c0 + A.x * s0;
+            a1 = A.y * c1 - B.y * s1, b1 = B.y * c1 + A.y * s1;
         }
-        float* d = dst + r * LD;
-        *reinterpret_cast<float2*>(d + i) = make_float2(a0, a1);
-        *reinterpret_cast<float2*>(d + i + half) = make_float2(b0, b1);
+        *reinterpret_cast<__nv_bfloat162*>(dst + r * LDH + i) = __floats2bfloat162_rn(a0, a1);
+        *reinterpret_cast<__nv_bfloat162*>(dst + r * LDH + i + half) = __floats2bfloat162_rn(b0, b1);
     }
 }
 
-// Store a fp32 tile [64][LD] (already scaled) as bf16 rows of one head, applying
-// the inverse rotation when rope != 0; rows at or beyond len are written as 0.
+// Store a fp32 staging tile [64][LDF] (already scaled) as bf16 rows of one
+// head, applying the inverse rotation when rope; rows in [len, slot) get 0.
 template <int HD>
 __device__ void store_tile(const float* srcs, __nv_bfloat16* dst, long long ld, int start, int r0, int len, int col,
                            int slot, float rope_base, bool rope) {
-    constexpr int half = HD / 2, LD = Tile<HD>::LD;
+    constexpr int half = HD / 2, LDF = Tile<HD>::LDF;
+    const float lb = rope ? log2f(rope_base) : 0.f;
     for (int e = threadIdx.x; e < kBM * (half / 2); e += blockDim.x) {
         const int r = e / (half / 2), i = (e % (half / 2)) * 2;
         const int pos = r0 + r;
         if (pos >= slot) continue;
-        const float* s = srcs + r * LD;
+        const float* s = srcs + r * LDF;
         float a0 = s[i], a1 = s[i + 1], b0 = s[i + half], b1 = s[i + half + 1];
         if (pos >= len) {
             a0 = a1 = b0 = b1 = 0.f;
         } else if (rope) {
-            const float lb = log2f(rope_base);
             float s0, c0, s1, c1;
             sincosf(pos * exp2f(-(2.f * i / HD) * lb), &s0, &c0);
             sincosf(pos * exp2f(-(2.f * (i + 1) / HD) * lb), &s1, &c1);
@@ -249,82 +313,82 @@ __device__ void store_tile(const float* srcs, __nv_bfloat16* dst, long long ld, 
     }
 }
 
-// acc[a][b] = sum_d X[ty*4 + a][d] * Y[tx + 16 b][d] over one 64 x 64 tile pair.
+// acc[nt][4] (+)= X[warp rows 16][HD] . Y[64 rows][HD]^T  — X, Y staged bf16 tiles;
+// the A operand (this warp's 16 rows of X) and B operand (rows of Y, "col") both
+// come through non-transposed ldmatrix.
 template <int HD>
-__device__ __forceinline__ void tile_dot(const float* X, const float* Y, int ty, int tx, float acc[4][4]) {
-    constexpr int LD = Tile<HD>::LD;
+__device__ __forceinline__ void mma_xyT(float (&acc)[8][4], const __nv_bfloat16* X, const __nv_bfloat16* Y,
+                                        int warp, int lane) {
+    constexpr int LDH = Tile<HD>::LDH;
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int n = 0; n < 8; ++n) acc[n][0] = acc[n][1] = acc[n][2] = acc[n][3] = 0.f;
+    const int mi = lane >> 3, r = lane & 7;
 #pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = 0.f;
-#pragma unroll 4
-    for (int d = 0; d < HD; d += 4) {
-        float4 x[4], y[4];
+    for (int ks = 0; ks < HD / 16; ++ks) {
+        uint32_t a[4];
+        ldsm4(a, smem_u32(X + (warp * 16 + (mi & 1) * 8 + r) * LDH + ks * 16 + (mi >> 1) * 8));
 #pragma unroll
-        for (int a = 0; a < 4; ++a) x[a] = *reinterpret_cast<const float4*>(X + (ty * 4 + a) * LD + d);
-#pragma unroll
-        for (int b = 0; b < 4; ++b) y[b] = *reinterpret_cast<const float4*>(Y + (tx + 16 * b) * LD + d);
-#pragma unroll
-        for (int a = 0; a < 4; ++a)
-#pragma unroll
-            for (int b = 0; b < 4; ++b)
-                acc[a][b] += x[a].x * y[b].x + x[a].y * y[b].y + x[a].z * y[b].z + x[a].w * y[b].w;
-    }
-}
-
-// acc[a][c*4+e] += sum_i P[i][ty*4 + a] * Z[i][tx*4 + 64c + e]   (transposed-P product; P row stride PLD)
-template <int HD, bool TRANS>
-__device__ __forceinline__ void tile_pz(const float* P, const float* Z, int ty, int tx, float acc[4][HD / 16]) {
-    constexpr int LD = Tile<HD>::LD, PLD = Tile<HD>::PLD, DV = Tile<HD>::DV;
-#pragma unroll 2
-    for (int i = 0; i < kBM; ++i) {
-        float p[4];
-        if constexpr (TRANS) {
-            const float4 q = *reinterpret_cast<const float4*>(P + i * PLD + ty * 4);
-            p[0] = q.x, p[1] = q.y, p[2] = q.z, p[3] = q.w;
-        } else {
-#pragma unroll
-            for (int a = 0; a < 4; ++a) p[a] = P[(ty * 4 + a) * PLD + i];
-        }
-#pragma unroll
-        for (int c = 0; c < DV; ++c) {
-            const float4 z = *reinterpret_cast<const float4*>(Z + i * LD + tx * 4 + 64 * c);
-#pragma unroll
-            for (int a = 0; a < 4; ++a) {
-                acc[a][c * 4 + 0] = fmaf(p[a], z.x, acc[a][c * 4 + 0]);
-                acc[a][c * 4 + 1] = fmaf(p[a], z.y, acc[a][c * 4 + 1]);
-                acc[a][c * 4 + 2] = fmaf(p[a], z.z, acc[a][c * 4 + 2]);
-                acc[a][c * 4 + 3] = fmaf(p[a], z.w, acc[a][c * 4 + 3]);
-            }
+        for (int p = 0; p < 4; ++p) {
+            uint32_t b[4];
+            ldsm4(b, smem_u32(Y + (p * 16 + (mi >> 1) * 8 + r) * LDH + ks * 16 + (mi & 1) * 8));
+            mma16816(acc[2 * p], a, b[0], b[1]);
+            mma16816(acc[2 * p + 1], a, b[2], b[3]);
         }
     }
 }
 
+// out[nt][4] += P[warp rows 16][64] (registers, as fp32 accumulators of mma_xyT)
+//             . Z[64 rows][HD]   — Z staged bf16, consumed through ldmatrix.trans.
 template <int HD>
-__device__ __forceinline__ void acc_to_smem(float* dst, const float acc[4][HD / 16], int ty, int tx, float s) {
-    constexpr int LD = Tile<HD>::LD, DV = Tile<HD>::DV;
+__device__ __forceinline__ void mma_pz(float (&out)[HD / 8][4], const float (&P)[8][4], const __nv_bfloat16* Z,
+                                       int lane) {
+    constexpr int LDH = Tile<HD>::LDH;
+    const int mi = lane >> 3, r = lane & 7;
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int j = 0; j < 4; ++j) {  // 16-row chunks of Z (k of this product)
+        uint32_t a[4];
+        a[0] = pack2(P[2 * j][0], P[2 * j][1]);
+        a[1] = pack2(P[2 * j][2], P[2 * j][3]);
+        a[2] = pack2(P[2 * j + 1][0], P[2 * j + 1][1]);
+        a[3] = pack2(P[2 * j + 1][2], P[2 * j + 1][3]);
 #pragma unroll
-        for (int c = 0; c < DV; ++c)
-            *reinterpret_cast<float4*>(dst + (ty * 4 + a) * LD + tx * 4 + 64 * c) =
-                make_float4(s * acc[a][c * 4 + 0], s * acc[a][c * 4 + 1], s * acc[a][c * 4 + 2],
-                            s * acc[a][c * 4 + 3]);
+        for (int e = 0; e < HD / 16; ++e) {
+            uint32_t b[4];
+            ldsm4t(b, smem_u32(Z + (j * 16 + (mi & 1) * 8 + r) * LDH + e * 16 + (mi >> 1) * 8));
+            mma16816(out[2 * e], a, b[0], b[1]);
+            mma16816(out[2 * e + 1], a, b[2], b[3]);
+        }
+    }
+}
+
+// Write this warp's 16 x HD accumulator rows (scaled) into the fp32 staging tile.
+template <int HD>
+__device__ __forceinline__ void acc_to_stage(float* st, const float (&acc)[HD / 8][4], int warp, int lane, float s) {
+    constexpr int LDF = Tile<HD>::LDF;
+    const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+    for (int n = 0; n < HD / 8; ++n) {
+        const int c = n * 8 + 2 * t;
+        *reinterpret_cast<float2*>(st + (warp * 16 + g) * LDF + c) = make_float2(s * acc[n][0], s * acc[n][1]);
+        *reinterpret_cast<float2*>(st + (warp * 16 + g + 8) * LDF + c) = make_float2(s * acc[n][2], s * acc[n][3]);
+    }
 }
 
 template <int HD>
-constexpr size_t attn_smem_fwd() {
-    return sizeof(float) * (3 * kBM * Tile<HD>::LD + kBM * Tile<HD>::PLD);
+constexpr size_t attn_smem_fwd() {  // Q + double-buffered (K, V)
+    return sizeof(__nv_bfloat16) * 5 * Tile<HD>::TILE;
 }
 template <int HD>
-constexpr size_t attn_smem_bwd() {
-    return sizeof(float) * (4 * kBM * Tile<HD>::LD + 2 * kBM * Tile<HD>::PLD + 2 * kBM);
+constexpr size_t attn_smem_bwd() {  // two fixed tiles + double-buffered pair (+ lse, dsum per buffer)
+    return sizeof(__nv_bfloat16) * 6 * Tile<HD>::TILE + sizeof(float) * 4 * kBM;
 }
+static_assert(2 * Tile<64>::TILE * 2 >= kBM * Tile<64>::LDF * 4, "stage fits two bf16 tiles");
+static_assert(2 * Tile<128>::TILE * 2 >= kBM * Tile<128>::LDF * 4, "stage fits two bf16 tiles");
 
 // Forward: one CTA per (query tile, sequence, head).  Online softmax in the
 // log2 domain; O = softmax(scale Q K^T, causal) V; lse in natural log.
 template <int HD>
-__global__ void __launch_bounds__(kThreads) attn_fwd_kernel(AttnArgs a) {
+__global__ void __launch_bounds__(kTcThreads) attn_fwd_kernel(AttnArgs a) {
     pdl_prologue();
     int start, len;
     seq_range(a, blockIdx.y, start, len);
@@ -332,83 +396,118 @@ __global__ void __launch_bounds__(kThreads) attn_fwd_kernel(AttnArgs a) {
     const int q0 = blockIdx.x * kBM;
     if (q0 >= slot) return;
     const int h = blockIdx.z, kvh = h / (a.heads / a.kv_heads);
-    constexpr int LD = Tile<HD>::LD, PLD = Tile<HD>::PLD, DV = Tile<HD>::DV;
-    extern __shared__ __align__(16) float sm[];
-    float* Qs = sm;
-    float* Ks = Qs + kBM * LD;
-    float* Vs = Ks + kBM * LD;
-    float* Ps = Vs + kBM * LD;
-    const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
-    const bool rope = a.rope_base > 0.f;
+    constexpr int TILE = Tile<HD>::TILE;
+    extern __shared__ __align__(16) __nv_bfloat16 smh[];
+    __nv_bfloat16* Qs = smh;  // then (K, V) x 2 buffers
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const bool rope = a.rope_in != 0, async = a.vec != 0;
     const float c2 = a.scale * kLog2e;
+    auto fetch = [&](int kt) {  // K/V tile kt into buffer kt & 1
+        __nv_bfloat16* Kb = Qs + TILE * (1 + 2 * (kt & 1));
+        stage<HD>(Kb, a.k, a.ldk, start, kt * kBM, len, kvh * HD, a.rope_base, rope, async);
+        stage<HD>(Kb + TILE, a.v, a.ldv, start, kt * kBM, len, kvh * HD, a.rope_base, false, async);
+        cp_async_commit();
+    };
 
-    load_tile<HD>(Qs, a.q, a.ldq, start, q0, len, h * HD, a.rope_base, rope);
-    float m[4], l[4], o[4][HD / 16];
+    stage<HD>(Qs, a.q, a.ldq, start, q0, len, h * HD, a.rope_base, rope, async);
+    float m[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
+    float o[HD / 8][4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        m[i] = -INFINITY;
-        l[i] = 0.f;
-#pragma unroll
-        for (int c = 0; c < HD / 16; ++c) o[i][c] = 0.f;
-    }
+    for (int n = 0; n < HD / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+    const int qr0 = q0 + warp * 16 + g;  // this thread's rows: qr0 and qr0 + 8
     const int nkt = q0 < len ? (min(q0 + kBM, len) + kBM - 1) / kBM : 0;
+    if (nkt > 0) fetch(0);
     for (int kt = 0; kt < nkt; ++kt) {
+        if (kt + 1 < nkt) {
+            fetch(kt + 1);  // overlaps this tile's MMAs
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
         __syncthreads();
-        load_tile<HD>(Ks, a.k, a.ldk, start, kt * kBM, len, kvh * HD, a.rope_base, rope);
-        load_tile<HD>(Vs, a.v, a.ldv, start, kt * kBM, len, kvh * HD, a.rope_base, false);
-        __syncthreads();
-        float s[4][4];
-        tile_dot<HD>(Qs, Ks, ty, tx, s);
+        const __nv_bfloat16* Ks = Qs + TILE * (1 + 2 * (kt & 1));
+        const __nv_bfloat16* Vs = Ks + TILE;
+        float s[8][4];
+        mma_xyT<HD>(s, Qs, Ks, warp, lane);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int qi = q0 + ty * 4 + i;
+        for (int hr = 0; hr < 2; ++hr) {  // rows g (hr 0) and g + 8 (hr 1)
+            const int qi = qr0 + 8 * hr;
             float mx = -INFINITY;
 #pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                const int kj = kt * kBM + tx + 16 * b;
-                s[i][b] = (kj <= qi && qi < len) ? s[i][b] * c2 : -INFINITY;
-                mx = fmaxf(mx, s[i][b]);
-            }
+            for (int n = 0; n < 8; ++n)
 #pragma unroll
-            for (int off = 8; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
-            const float mn = fmaxf(m[i], mx);
-            const float alpha = mn == -INFINITY ? 1.f : exp2f(m[i] - mn);
+                for (int c = 0; c < 2; ++c) {
+                    const int kj = kt * kBM + n * 8 + 2 * t + c;
+                    float& v = s[n][2 * hr + c];
+                    v = (kj <= qi && qi < len) ? v * c2 : -INFINITY;
+                    mx = fmaxf(mx, v);
+                }
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+            const float mn = fmaxf(m[hr], mx);
+            const float alpha = mn == -INFINITY ? 1.f : exp2f(m[hr] - mn);
             float ps = 0.f;
 #pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                const float p = mn == -INFINITY ? 0.f : exp2f(s[i][b] - mn);
-                Ps[(ty * 4 + i) * PLD + tx + 16 * b] = p;
-                ps += p;
+            for (int n = 0; n < 8; ++n)
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    float& v = s[n][2 * hr + c];
+                    v = mn == -INFINITY ? 0.f : exp2f(v - mn);
+                    ps += v;
+                }
+            l[hr] = l[hr] * alpha + ps;
+            m[hr] = mn;
+#pragma unroll
+            for (int n = 0; n < HD / 8; ++n) {
+                o[n][2 * hr] *= alpha;
+                o[n][2 * hr + 1] *= alpha;
             }
-            l[i] = l[i] * alpha + ps;
-            m[i] = mn;
-#pragma unroll
-            for (int c = 0; c < HD / 16; ++c) o[i][c] *= alpha;
         }
-        __syncwarp();  // P rows of this thread group are written by the same half-warp
-        tile_pz<HD, false>(Ps, Vs, ty, tx, o);
+        mma_pz<HD>(o, s, Vs, lane);
+        __syncthreads();  // buffer kt & 1 is refilled by the next iteration's fetch
     }
-    // epilogue
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        float lt = l[i];
-#pragma unroll
-        for (int off = 8; off > 0; off >>= 1) lt += __shfl_xor_sync(0xffffffffu, lt, off);
-        const int qi = q0 + ty * 4 + i;
+    for (int hr = 0; hr < 2; ++hr) {
+        float lt = l[hr];
+        lt += __shfl_xor_sync(0xffffffffu, lt, 1);
+        lt += __shfl_xor_sync(0xffffffffu, lt, 2);
+        const int qi = qr0 + 8 * hr;
         if (qi >= slot) continue;
         const bool ok = qi < len && lt > 0.f;
         const float inv = ok ? 1.f / lt : 0.f;
         __nv_bfloat16* dst = a.out + (long long)(start + qi) * a.ldout + h * HD;
 #pragma unroll
-        for (int c = 0; c < DV; ++c) {
-            const __nv_bfloat162 v0 = __floats2bfloat162_rn(o[i][c * 4 + 0] * inv, o[i][c * 4 + 1] * inv);
-            const __nv_bfloat162 v1 = __floats2bfloat162_rn(o[i][c * 4 + 2] * inv, o[i][c * 4 + 3] * inv);
-            uint2 pk;
-            pk.x = *reinterpret_cast<const uint32_t*>(&v0);
-            pk.y = *reinterpret_cast<const uint32_t*>(&v1);
-            *reinterpret_cast<uint2*>(dst + tx * 4 + 64 * c) = pk;
+        for (int n = 0; n < HD / 8; ++n)
+            *reinterpret_cast<uint32_t*>(dst + n * 8 + 2 * t) = pack2(o[n][2 * hr] * inv, o[n][2 * hr + 1] * inv);
+        if (t == 0) a.lse[(long long)h * a.rows + start + qi] = ok ? (m[hr] + log2f(lt)) * kLn2 : 0.f;
+    }
+}
+
+// dst = RoPE(src) for n_heads heads of every row (pos = row - its sequence start;
+// rows past len are zeroed): one CTA per (64-row tile, sequence); each angle is
+// computed once and applied to every head.
+__global__ void attn_rope_kernel(AttnArgs a, const __nv_bfloat16* __restrict__ src, long long lds, int n_heads, int hd,
+                                 __nv_bfloat16* __restrict__ dst, long long ldd) {
+    pdl_prologue();
+    int start, len;
+    seq_range(a, blockIdx.y, start, len);
+    const int slot = a.seq_off[blockIdx.y + 1] - start;
+    const int r0 = blockIdx.x * kBM;
+    if (r0 >= slot) return;
+    const int half = hd / 2;
+    const float lb = log2f(a.rope_base);
+    for (int e = threadIdx.x; e < kBM * half; e += blockDim.x) {
+        const int r = e / half, i = e % half, pos = r0 + r;
+        if (pos >= slot) continue;
+        float sn = 0.f, cs = 0.f;
+        if (pos < len) sincosf(pos * exp2f(-(2.f * i / hd) * lb), &sn, &cs);
+        const __nv_bfloat16* s = src + (long long)(start + pos) * lds;
+        __nv_bfloat16* d = dst + (long long)(start + pos) * ldd;
+        for (int h = 0; h < n_heads; ++h) {
+            const float x0 = __bfloat162float(s[h * hd + i]), x1 = __bfloat162float(s[h * hd + i + half]);
+            d[h * hd + i] = __float2bfloat16_rn(x0 * cs - x1 * sn);
+            d[h * hd + i + half] = __float2bfloat16_rn(x1 * cs + x0 * sn);
         }
-        if (tx == 0) a.lse[(long long)h * a.rows + start + qi] = ok ? (m[i] + log2f(lt)) * kLn2 : 0.f;
     }
 }
 
@@ -428,34 +527,22 @@ __global__ void attn_dsum_kernel(AttnArgs a, int hd) {
     if (lane == 0) a.dsum[(long long)h * a.rows + t] = s;
 }
 
-// P and dS of one (query tile, key tile): P = exp(scale Q K^T - lse) (causal,
-// masked to 0), dS = P (dO V^T - dsum).  Written to Ps / dSs [64][PLD] (rows = queries).
-template <int HD>
-__device__ __forceinline__ void p_ds_tile(const float* Qs, const float* Ks, const float* dOs, const float* Vs,
-                                          const float* lse2, const float* dsm, int q0, int k0, int len, float c2,
-                                          float* Ps, float* dSs, int ty, int tx) {
-    constexpr int PLD = Tile<HD>::PLD;
-    float s[4][4], dp[4][4];
-    tile_dot<HD>(Qs, Ks, ty, tx, s);
-    tile_dot<HD>(dOs, Vs, ty, tx, dp);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const int r = ty * 4 + i, qi = q0 + r;
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            const int c = tx + 16 * b, kj = k0 + c;
-            const float p = (kj <= qi && qi < len) ? exp2f(s[i][b] * c2 - lse2[r]) : 0.f;
-            Ps[r * PLD + c] = p;
-            dSs[r * PLD + c] = p * (dp[i][b] - dsm[r]);
-        }
+__device__ __forceinline__ void load_stats(const AttnArgs& a, int h, int start, int q0, int len, float* lse2,
+                                           float* dsm) {
+    for (int r = threadIdx.x; r < kBM; r += blockDim.x) {
+        const bool ok = q0 + r < len;
+        lse2[r] = ok ? a.lse[(long long)h * a.rows + start + q0 + r] * kLog2e : 0.f;
+        dsm[r] = ok ? a.dsum[(long long)h * a.rows + start + q0 + r] : 0.f;
     }
 }
 
-// dK, dV: one CTA per (key tile, sequence, K/V head); loops over the query
-// heads of its group and the query tiles at or after the key tile (causal), so
-// the GQA / MQA head sum is a fixed-order register accumulation.
+// dK, dV: one CTA per (key tile, sequence, K/V head); loops over the query heads
+// of its group and the query tiles at or after the key tile (causal), so the
+// GQA / MQA head sum is a fixed-order register accumulation.  Each warp owns
+// 16 keys and computes the transposed products directly (S^T = K Q^T,
+// dP^T = V dO^T), so P^T and dS^T are A operands straight from registers.
 template <int HD>
-__global__ void __launch_bounds__(kThreads) attn_bwd_dkv_kernel(AttnArgs a) {
+__global__ void __launch_bounds__(kTcThreads) attn_bwd_dkv_kernel(AttnArgs a) {
     pdl_prologue();
     int start, len;
     seq_range(a, blockIdx.y, start, len);
@@ -463,58 +550,82 @@ __global__ void __launch_bounds__(kThreads) attn_bwd_dkv_kernel(AttnArgs a) {
     const int k0 = blockIdx.x * kBM;
     if (k0 >= slot) return;
     const int kvh = blockIdx.z, group = a.heads / a.kv_heads;
-    constexpr int LD = Tile<HD>::LD, PLD = Tile<HD>::PLD;
-    extern __shared__ __align__(16) float sm[];
-    float* Ks = sm;
-    float* Vs = Ks + kBM * LD;
-    float* Qs = Vs + kBM * LD;
-    float* dOs = Qs + kBM * LD;
-    float* Ps = dOs + kBM * LD;
-    float* dSs = Ps + kBM * PLD;
-    float* lse2 = dSs + kBM * PLD;
-    float* dsm = lse2 + kBM;
-    const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
-    const bool rope = a.rope_base > 0.f;
+    constexpr int TILE = Tile<HD>::TILE;
+    extern __shared__ __align__(16) __nv_bfloat16 smh[];
+    __nv_bfloat16* Ks = smh;
+    __nv_bfloat16* Vs = Ks + TILE;  // then (Q, dO) x 2 buffers, then (lse, dsum) x 2
+    float* stats = reinterpret_cast<float*>(Vs + 5 * TILE);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const bool rope = a.rope_in != 0, async = a.vec != 0;
     const float c2 = a.scale * kLog2e;
+    const int qt0 = k0 / kBM, nq = (len + kBM - 1) / kBM - qt0;  // query tiles at or after the key tile
+    const int nit = nq > 0 ? group * nq : 0;                       // (query head, query tile) pairs
+    auto fetch = [&](int it) {
+        const int h = kvh * group + it / nq, q0 = (qt0 + it % nq) * kBM, b = it & 1;
+        __nv_bfloat16* Qb = Vs + TILE * (1 + 2 * b);
+        stage<HD>(Qb, a.q, a.ldq, start, q0, len, h * HD, a.rope_base, rope, async);
+        stage<HD>(Qb + TILE, a.dO, a.lddo, start, q0, len, h * HD, a.rope_base, false, async);
+        load_stats(a, h, start, q0, len, stats + b * 2 * kBM, stats + b * 2 * kBM + kBM);
+        cp_async_commit();
+    };
 
-    load_tile<HD>(Ks, a.k, a.ldk, start, k0, len, kvh * HD, a.rope_base, rope);
-    load_tile<HD>(Vs, a.v, a.ldv, start, k0, len, kvh * HD, a.rope_base, false);
-    float dk[4][HD / 16], dv[4][HD / 16];
+    stage<HD>(Ks, a.k, a.ldk, start, k0, len, kvh * HD, a.rope_base, rope, async);
+    stage<HD>(Vs, a.v, a.ldv, start, k0, len, kvh * HD, a.rope_base, false, async);
+    float dk[HD / 8][4], dv[HD / 8][4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int n = 0; n < HD / 8; ++n)
 #pragma unroll
-        for (int c = 0; c < HD / 16; ++c) dk[i][c] = dv[i][c] = 0.f;
-    const int nqt = (len + kBM - 1) / kBM;
-    for (int hh = 0; hh < group; ++hh) {
-        const int h = kvh * group + hh;
-        for (int qt = k0 / kBM; qt < nqt; ++qt) {
-            const int q0 = qt * kBM;
-            __syncthreads();
-            load_tile<HD>(Qs, a.q, a.ldq, start, q0, len, h * HD, a.rope_base, rope);
-            load_tile<HD>(dOs, a.dO, a.lddo, start, q0, len, h * HD, a.rope_base, false);
-            for (int r = tid; r < kBM; r += blockDim.x) {
-                const bool ok = q0 + r < len;
-                lse2[r] = ok ? a.lse[(long long)h * a.rows + start + q0 + r] * kLog2e : 0.f;
-                dsm[r] = ok ? a.dsum[(long long)h * a.rows + start + q0 + r] : 0.f;
-            }
-            __syncthreads();
-            p_ds_tile<HD>(Qs, Ks, dOs, Vs, lse2, dsm, q0, k0, len, c2, Ps, dSs, ty, tx);
-            __syncthreads();
-            tile_pz<HD, true>(Ps, dOs, ty, tx, dv);   // dV[j] += sum_i P[i][j] dO[i]
-            tile_pz<HD, true>(dSs, Qs, ty, tx, dk);   // dK[j] += sum_i dS[i][j] Q[i]
+        for (int c = 0; c < 4; ++c) dk[n][c] = dv[n][c] = 0.f;
+    const int kr0 = k0 + warp * 16 + g;  // this thread's keys: kr0 and kr0 + 8
+    if (nit > 0) fetch(0);
+    for (int it = 0; it < nit; ++it) {
+        if (it + 1 < nit) {
+            fetch(it + 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
         }
+        __syncthreads();
+        const int q0 = (qt0 + it % nq) * kBM, b = it & 1;
+        const __nv_bfloat16* Qs = Vs + TILE * (1 + 2 * b);
+        const __nv_bfloat16* dOs = Qs + TILE;
+        const float* lse2 = stats + b * 2 * kBM;
+        const float* dsm = lse2 + kBM;
+        float p[8][4];
+        mma_xyT<HD>(p, Ks, Qs, warp, lane);  // S^T: rows = keys, cols = queries
+#pragma unroll
+        for (int n = 0; n < 8; ++n)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int kj = kr0 + 8 * (e >> 1), cq = n * 8 + 2 * t + (e & 1), qi = q0 + cq;
+                p[n][e] = (kj <= qi && qi < len) ? exp2f(p[n][e] * c2 - lse2[cq]) : 0.f;
+            }
+        mma_pz<HD>(dv, p, dOs, lane);          // dV += P^T dO
+        float ds[8][4];
+        mma_xyT<HD>(ds, Vs, dOs, warp, lane);  // dP^T = V dO^T
+#pragma unroll
+        for (int n = 0; n < 8; ++n)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) ds[n][e] = p[n][e] * (ds[n][e] - dsm[n * 8 + 2 * t + (e & 1)]);
+        mma_pz<HD>(dk, ds, Qs, lane);          // dK += dS^T Q
+        __syncthreads();                       // buffer b is refilled by the next fetch
     }
+    cp_async_wait<0>();
     __syncthreads();
-    acc_to_smem<HD>(Ks, dk, ty, tx, a.scale);
-    acc_to_smem<HD>(Vs, dv, ty, tx, 1.f);
+    float* st = reinterpret_cast<float*>(Vs + TILE);  // the (Q, dO) buffers are free: fp32 staging
+    const bool rope_out = a.rope_base > 0.f;
+    acc_to_stage<HD>(st, dk, warp, lane, a.scale);
     __syncthreads();
-    store_tile<HD>(Ks, a.dk, a.lddk, start, k0, len, kvh * HD, slot, a.rope_base, rope);
-    store_tile<HD>(Vs, a.dv, a.lddv, start, k0, len, kvh * HD, slot, a.rope_base, false);
+    store_tile<HD>(st, a.dk, a.lddk, start, k0, len, kvh * HD, slot, a.rope_base, rope_out);
+    __syncthreads();
+    acc_to_stage<HD>(st, dv, warp, lane, 1.f);
+    __syncthreads();
+    store_tile<HD>(st, a.dv, a.lddv, start, k0, len, kvh * HD, slot, a.rope_base, false);
 }
 
 // dQ: one CTA per (query tile, sequence, head); loops over key tiles 0..qt.
 template <int HD>
-__global__ void __launch_bounds__(kThreads) attn_bwd_dq_kernel(AttnArgs a) {
+__global__ void __launch_bounds__(kTcThreads) attn_bwd_dq_kernel(AttnArgs a) {
     pdl_prologue();
     int start, len;
     seq_range(a, blockIdx.y, start, len);
@@ -522,46 +633,61 @@ __global__ void __launch_bounds__(kThreads) attn_bwd_dq_kernel(AttnArgs a) {
     const int q0 = blockIdx.x * kBM;
     if (q0 >= slot) return;
     const int h = blockIdx.z, kvh = h / (a.heads / a.kv_heads);
-    constexpr int LD = Tile<HD>::LD, PLD = Tile<HD>::PLD;
-    extern __shared__ __align__(16) float sm[];
-    float* Qs = sm;
-    float* dOs = Qs + kBM * LD;
-    float* Ks = dOs + kBM * LD;
-    float* Vs = Ks + kBM * LD;
-    float* Ps = Vs + kBM * LD;
-    float* dSs = Ps + kBM * PLD;
-    float* lse2 = dSs + kBM * PLD;
+    constexpr int TILE = Tile<HD>::TILE;
+    extern __shared__ __align__(16) __nv_bfloat16 smh[];
+    __nv_bfloat16* Qs = smh;
+    __nv_bfloat16* dOs = Qs + TILE;  // then (K, V) x 2 buffers, then lse, dsum
+    float* lse2 = reinterpret_cast<float*>(dOs + 5 * TILE);
     float* dsm = lse2 + kBM;
-    const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
-    const bool rope = a.rope_base > 0.f;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const bool rope = a.rope_in != 0, async = a.vec != 0;
     const float c2 = a.scale * kLog2e;
+    auto fetch = [&](int kt) {
+        __nv_bfloat16* Kb = dOs + TILE * (1 + 2 * (kt & 1));
+        stage<HD>(Kb, a.k, a.ldk, start, kt * kBM, len, kvh * HD, a.rope_base, rope, async);
+        stage<HD>(Kb + TILE, a.v, a.ldv, start, kt * kBM, len, kvh * HD, a.rope_base, false, async);
+        cp_async_commit();
+    };
 
-    load_tile<HD>(Qs, a.q, a.ldq, start, q0, len, h * HD, a.rope_base, rope);
-    load_tile<HD>(dOs, a.dO, a.lddo, start, q0, len, h * HD, a.rope_base, false);
-    for (int r = tid; r < kBM; r += blockDim.x) {
-        const bool ok = q0 + r < len;
-        lse2[r] = ok ? a.lse[(long long)h * a.rows + start + q0 + r] * kLog2e : 0.f;
-        dsm[r] = ok ? a.dsum[(long long)h * a.rows + start + q0 + r] : 0.f;
-    }
-    float dq[4][HD / 16];
+    stage<HD>(Qs, a.q, a.ldq, start, q0, len, h * HD, a.rope_base, rope, async);
+    stage<HD>(dOs, a.dO, a.lddo, start, q0, len, h * HD, a.rope_base, false, async);
+    load_stats(a, h, start, q0, len, lse2, dsm);
+    float dq[HD / 8][4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int c = 0; c < HD / 16; ++c) dq[i][c] = 0.f;
+    for (int n = 0; n < HD / 8; ++n) dq[n][0] = dq[n][1] = dq[n][2] = dq[n][3] = 0.f;
+    const int qrl0 = warp * 16 + g;  // this thread's tile rows: qrl0 and qrl0 + 8
     const int nkt = q0 < len ? (min(q0 + kBM, len) + kBM - 1) / kBM : 0;
+    if (nkt > 0) fetch(0);
     for (int kt = 0; kt < nkt; ++kt) {
+        if (kt + 1 < nkt) {
+            fetch(kt + 1);
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
         __syncthreads();
-        load_tile<HD>(Ks, a.k, a.ldk, start, kt * kBM, len, kvh * HD, a.rope_base, rope);
-        load_tile<HD>(Vs, a.v, a.ldv, start, kt * kBM, len, kvh * HD, a.rope_base, false);
+        const __nv_bfloat16* Ks = dOs + TILE * (1 + 2 * (kt & 1));
+        const __nv_bfloat16* Vs = Ks + TILE;
+        float p[8][4], ds[8][4];
+        mma_xyT<HD>(p, Qs, Ks, warp, lane);   // S
+        mma_xyT<HD>(ds, dOs, Vs, warp, lane); // dP
+#pragma unroll
+        for (int n = 0; n < 8; ++n)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int rl = qrl0 + 8 * (e >> 1), qi = q0 + rl, kj = kt * kBM + n * 8 + 2 * t + (e & 1);
+                const float pv = (kj <= qi && qi < len) ? exp2f(p[n][e] * c2 - lse2[rl]) : 0.f;
+                ds[n][e] = pv * (ds[n][e] - dsm[rl]);
+            }
+        mma_pz<HD>(dq, ds, Ks, lane);          // dQ += dS K
         __syncthreads();
-        p_ds_tile<HD>(Qs, Ks, dOs, Vs, lse2, dsm, q0, kt * kBM, len, c2, Ps, dSs, ty, tx);
-        __syncwarp();  // dS rows of this thread group are written by the same half-warp
-        tile_pz<HD, false>(dSs, Ks, ty, tx, dq);  // dQ[i] += sum_j dS[i][j] K[j]
     }
+    cp_async_wait<0>();
     __syncthreads();
-    acc_to_smem<HD>(Qs, dq, ty, tx, a.scale);
+    float* st = reinterpret_cast<float*>(dOs + TILE);  // the (K, V) buffers are free: fp32 staging
+    acc_to_stage<HD>(st, dq, warp, lane, a.scale);
     __syncthreads();
-    store_tile<HD>(Qs, a.dq, a.lddq, start, q0, len, h * HD, slot, a.rope_base, rope);
+    store_tile<HD>(st, a.dq, a.lddq, start, q0, len, h * HD, slot, a.rope_base, a.rope_base > 0.f);
 }
 
 template <typename... KArgs, typename... Args>
@@ -585,10 +711,14 @@ mlora_status check_attn(const mlora_attn_desc* d) {
     if (d->head_dim != 64 && d->head_dim != 128) return MLORA_SHAPE;
     if (d->rope_base != 0.f && !(d->rope_base > 1.f)) return MLORA_USAGE;
     if (!(d->softmax_scale > 0.f)) return MLORA_USAGE;
+    if (d->flags & ~MLORA_ATTN_PREROTATED) return MLORA_USAGE;
     return MLORA_OK;
 }
 
 bool ld_ok(long long ld, int cols) { return ld >= cols && (ld % 2) == 0; }
+
+// cp.async staging needs every staged row 16-byte aligned.
+bool rows16(const void* p, long long ld) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0 && (ld % 8) == 0; }
 
 AttnArgs attn_args(const mlora_attn_desc* d) {
     AttnArgs a{};
@@ -599,6 +729,7 @@ AttnArgs attn_args(const mlora_attn_desc* d) {
     a.rope_base = d->rope_base;
     a.scale = d->softmax_scale;
     a.rows = d->rows;
+    a.rope_in = d->rope_base > 0.f && !(d->flags & MLORA_ATTN_PREROTATED);
     return a;
 }
 
@@ -609,7 +740,7 @@ cudaError_t launch_attn(K kernel, const mlora_attn_desc* d, int heads_z, size_t 
         cudaSuccess)
         return cudaErrorInvalidValue;
     const dim3 grid((d->max_len + kBM - 1) / kBM, d->num_seqs, heads_z);
-    return launch(kernel, grid, dim3(kThreads), smem, stream, a);
+    return launch(kernel, grid, dim3(kTcThreads), smem, stream, a);
 }
 
 }  // namespace
@@ -688,9 +819,25 @@ mlora_status mlora_attn_fwd(const mlora_attn_desc* d, const void* q, int64_t ldq
     a.q = bf(q), a.k = bf(k), a.v = bf(v), a.out = bfw(o);
     a.ldq = ldq, a.ldk = ldk, a.ldv = ldv, a.ldout = ldo;
     a.lse = lse;
+    a.vec = rows16(q, ldq) && rows16(k, ldk) && rows16(v, ldv);
     const cudaError_t e = hd == 64 ? launch_attn(attn_fwd_kernel<64>, d, d->heads, attn_smem_fwd<64>(), stream, a)
                                    : launch_attn(attn_fwd_kernel<128>, d, d->heads, attn_smem_fwd<128>(), stream, a);
     return e == cudaSuccess ? MLORA_OK : MLORA_CUDA;
+}
+
+mlora_status mlora_attn_rope(const mlora_attn_desc* d, const void* src, int64_t ld_src, int32_t n_heads, void* dst,
+                             int64_t ld_dst, void* stream) {
+    mlora_status st = check_attn(d);
+    if (st != MLORA_OK) return st;
+    if (!src || !dst || n_heads < 1 || !(d->rope_base > 1.f)) return MLORA_USAGE;
+    if (!ld_ok(ld_src, n_heads * d->head_dim) || !ld_ok(ld_dst, n_heads * d->head_dim)) return MLORA_SHAPE;
+    AttnArgs a = attn_args(d);
+    const dim3 grid((d->max_len + kBM - 1) / kBM, d->num_seqs);
+    return launch(attn_rope_kernel, grid, dim3(256), 0, stream, a, bf(src), static_cast<long long>(ld_src),
+                  static_cast<int>(n_heads), static_cast<int>(d->head_dim), bfw(dst),
+                  static_cast<long long>(ld_dst)) == cudaSuccess
+               ? MLORA_OK
+               : MLORA_CUDA;
 }
 
 mlora_status mlora_attn_bwd(const mlora_attn_desc* d, const void* q, int64_t ldq, const void* k, int64_t ldk,
@@ -710,6 +857,7 @@ mlora_status mlora_attn_bwd(const mlora_attn_desc* d, const void* q, int64_t ldq
     a.dq = bfw(dq), a.dk = bfw(dk), a.dv = bfw(dv);
     a.lddq = lddq, a.lddk = lddk, a.lddv = lddv;
     a.lse = const_cast<float*>(lse);
+    a.vec = rows16(q, ldq) && rows16(k, ldk) && rows16(v, ldv) && rows16(dout, lddo);
     a.dsum = dsum;
     const long long warps = d->rows * d->heads;
     if (launch(attn_dsum_kernel, dim3(static_cast<unsigned>((warps * 32 + 255) / 256)), dim3(256), 0, stream, a,

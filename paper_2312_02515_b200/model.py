@@ -153,6 +153,8 @@ class _Layer:
     rstd1: torch.Tensor | None = None
     rstd2: torch.Tensor | None = None
     attn: torch.Tensor | None = None    # attention output
+    qr: torch.Tensor | None = None      # RoPE(q), RoPE(k): rotated once, read by every attention tile
+    kr: torch.Tensor | None = None
     lse: torch.Tensor | None = None
     act: torch.Tensor | None = None     # SwiGLU output
 
@@ -204,6 +206,8 @@ class MultiLoraDecoder:
             L.rstd1 = torch.empty(rows, dtype=torch.float32, device=dev)
             L.rstd2 = torch.empty(rows, dtype=torch.float32, device=dev)
             L.attn = torch.empty(rows, h, dtype=bf, device=dev)
+            L.qr = torch.empty(rows, h, dtype=bf, device=dev)
+            L.kr = torch.empty(rows, cfg.kv_heads * cfg.head_dim, dtype=bf, device=dev)
             L.lse = torch.empty(cfg.heads, rows, dtype=torch.float32, device=dev)
             L.act = torch.empty(rows, cfg.ffn, dtype=bf, device=dev)
             self.layers.append(L)
@@ -357,8 +361,11 @@ class MultiLoraDecoder:
     def _attn_fwd(self, L: _Layer, q, k, v, stream) -> None:
         cfg, r = self.cfg, self.rows
         lse = L.lse.view(-1)[: cfg.heads * r].view(cfg.heads, r)
-        M.attn_fwd(self.layout, q, k, v, cfg.heads, cfg.kv_heads, cfg.head_dim, cfg.rope_base, out=L.attn[:r],
-                   lse=lse, stream=stream)
+        qr, kr = L.qr[:r], L.kr[:r]
+        M.attn_rope(self.layout, q, cfg.heads, cfg.head_dim, cfg.rope_base, out=qr, stream=stream)
+        M.attn_rope(self.layout, k, cfg.kv_heads, cfg.head_dim, cfg.rope_base, out=kr, stream=stream)
+        M.attn_fwd(self.layout, qr, kr, v, cfg.heads, cfg.kv_heads, cfg.head_dim, cfg.rope_base, out=L.attn[:r],
+                   lse=lse, prerotated=True, stream=stream)
 
     # ------------------------------------------------------------ backward
     def backward(self, stream=None) -> None:
@@ -393,12 +400,12 @@ class MultiLoraDecoder:
             # ---- attention: x1 = x_in + o(attn(q, k, v))
             self._down([(P[out_p], d_x1)], True, s)
             d_attn = self._dx_gemm(P[out_p], d_x1, s)
-            q, k, v = self._qkv_views(L)
+            _, _, v = self._qkv_views(L)
             dq, dk, dv = self._qkv_views(L, grad=True)
             lse = L.lse.view(-1)[: cfg.heads * r].view(cfg.heads, r)
             dsum = self._dsum.view(-1)[: cfg.heads * r].view(cfg.heads, r)
-            M.attn_bwd(self.layout, q, k, v, L.attn[:r], d_attn, lse, dq, dk, dv, cfg.heads, cfg.kv_heads,
-                       cfg.head_dim, cfg.rope_base, dsum=dsum, stream=sm)
+            M.attn_bwd(self.layout, L.qr[:r], L.kr[:r], v, L.attn[:r], d_attn, lse, dq, dk, dv, cfg.heads,
+                       cfg.kv_heads, cfg.head_dim, cfg.rope_base, dsum=dsum, prerotated=True, stream=sm)
             dys_attn = [self._dy[n][:r] for n in attn_p]
             self._down([(P[n], dy) for n, dy in zip(attn_p, dys_attn)], True, s)
             d_in = None

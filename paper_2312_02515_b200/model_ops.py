@@ -142,29 +142,43 @@ class AttnLayout:
         self.d_len = torch.tensor(lens, dtype=torch.int32, device=device)
 
     def desc(self, heads: int, kv_heads: int, head_dim: int, rope_base: float = 10000.0,
-             scale: float | None = None) -> "N.AttnDescC":
+             scale: float | None = None, prerotated: bool = False) -> "N.AttnDescC":
         return N.AttnDescC(self.d_off.data_ptr(), self.d_len.data_ptr(), self.rows, len(self.lens), self.max_len,
                            heads, kv_heads, head_dim, float(rope_base),
-                           float(head_dim ** -0.5 if scale is None else scale), 0)
+                           float(head_dim ** -0.5 if scale is None else scale), 1 if prerotated else 0)
+
+
+def attn_rope(layout: AttnLayout, x: torch.Tensor, n_heads: int, head_dim: int, rope_base: float = 10000.0,
+              out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """RoPE of n_heads heads of every row (position within its sequence); x may be a column slice."""
+    out = torch.empty(x.shape[0], n_heads * head_dim, dtype=torch.bfloat16, device=x.device) if out is None else out
+    d = layout.desc(n_heads, n_heads, head_dim, rope_base)
+    N.check(N.lib().mlora_attn_rope(C.byref(d), x.data_ptr(), x.stride(0), n_heads, out.data_ptr(), out.stride(0),
+                                    _s(stream)))
+    return out
 
 
 def attn_fwd(layout: AttnLayout, q, k, v, heads: int, kv_heads: int, head_dim: int, rope_base: float = 10000.0,
-             out: torch.Tensor | None = None, lse: torch.Tensor | None = None, stream=None):
-    """Causal attention (RoPE fused) over the fused rows; q/k/v may be column slices."""
+             out: torch.Tensor | None = None, lse: torch.Tensor | None = None, prerotated: bool = False,
+             stream=None):
+    """Causal attention (RoPE fused unless q/k come prerotated by attn_rope) over
+    the fused rows; q/k/v may be column slices."""
     rows = layout.rows
     out = torch.empty(rows, heads * head_dim, dtype=torch.bfloat16, device=q.device) if out is None else out
     lse = torch.empty(heads, rows, dtype=torch.float32, device=q.device) if lse is None else lse
-    d = layout.desc(heads, kv_heads, head_dim, rope_base)
+    d = layout.desc(heads, kv_heads, head_dim, rope_base, prerotated=prerotated)
     N.check(N.lib().mlora_attn_fwd(C.byref(d), q.data_ptr(), q.stride(0), k.data_ptr(), k.stride(0), v.data_ptr(),
                                    v.stride(0), out.data_ptr(), out.stride(0), lse.data_ptr(), _s(stream)))
     return out, lse
 
 
 def attn_bwd(layout: AttnLayout, q, k, v, o, dout, lse, dq, dk, dv, heads: int, kv_heads: int, head_dim: int,
-             rope_base: float = 10000.0, dsum: torch.Tensor | None = None, stream=None) -> None:
+             rope_base: float = 10000.0, dsum: torch.Tensor | None = None, prerotated: bool = False,
+             stream=None) -> None:
+    """dq / dk are with respect to the unrotated q / k in both modes."""
     rows = layout.rows
     dsum = torch.empty(heads, rows, dtype=torch.float32, device=q.device) if dsum is None else dsum
-    d = layout.desc(heads, kv_heads, head_dim, rope_base)
+    d = layout.desc(heads, kv_heads, head_dim, rope_base, prerotated=prerotated)
     N.check(N.lib().mlora_attn_bwd(C.byref(d), q.data_ptr(), q.stride(0), k.data_ptr(), k.stride(0), v.data_ptr(),
                                    v.stride(0), o.data_ptr(), o.stride(0), dout.data_ptr(), dout.stride(0),
                                    lse.data_ptr(), dsum.data_ptr(), dq.data_ptr(), dq.stride(0), dk.data_ptr(),

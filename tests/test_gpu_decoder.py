@@ -57,8 +57,9 @@ def attn_ref(q, k, v, offsets, lens, heads, kv_heads, hd, base):
     return out
 
 
-@pytest.mark.parametrize("hd,heads,kv,padded", [(64, 4, 4, False), (128, 4, 2, True), (128, 8, 1, False)])
-def test_attention_fwd_bwd_vs_torch(hd, heads, kv, padded):
+@pytest.mark.parametrize("hd,heads,kv,padded,prerot", [(64, 4, 4, False, False), (128, 4, 2, True, False),
+                                                       (128, 8, 1, False, True), (64, 4, 2, True, True)])
+def test_attention_fwd_bwd_vs_torch(hd, heads, kv, padded, prerot):
     from paper_2312_02515_b200 import model_ops as M
     dev = torch.device("cuda", 0)
     g = torch.Generator().manual_seed(hd + heads + kv)
@@ -74,11 +75,14 @@ def test_attention_fwd_bwd_vs_torch(hd, heads, kv, padded):
     qkv = mk((heads + 2 * kv) * hd)
     q, k, v = qkv[:, :heads * hd], qkv[:, heads * hd:(heads + kv) * hd], qkv[:, (heads + kv) * hd:]
     lay = M.AttnLayout(offsets, lens, device=dev)
-    o, lse = M.attn_fwd(lay, q, k, v, heads, kv, hd, base)
+    qa, ka = q, k
+    if prerot:  # RoPE applied once up front (mlora_attn_rope), the kernels skip it
+        qa, ka = M.attn_rope(lay, q, heads, hd, base), M.attn_rope(lay, k, kv, hd, base)
+    o, lse = M.attn_fwd(lay, qa, ka, v, heads, kv, hd, base, prerotated=prerot)
     do = mk(heads * hd)
     dqkv = torch.full_like(qkv, float("nan"))
     dq, dk, dv = dqkv[:, :heads * hd], dqkv[:, heads * hd:(heads + kv) * hd], dqkv[:, (heads + kv) * hd:]
-    M.attn_bwd(lay, q, k, v, o, do, lse, dq, dk, dv, heads, kv, hd, base)
+    M.attn_bwd(lay, qa, ka, v, o, do, lse, dq, dk, dv, heads, kv, hd, base, prerotated=prerot)
     torch.cuda.synchronize()
     qf, kf, vf = (t.float().clone().requires_grad_(True) for t in (q, k, v))
     ref = attn_ref(qf, kf, vf, offsets, lens, heads, kv, hd, base)

@@ -78,9 +78,9 @@ def main():
     dq, dk, dv = m._qkv_views(L, grad=True)
     e0.record()
     for _ in range(a.steps):
-        M.attn_fwd(m.layout, q, k, v, cfg.heads, cfg.kv_heads, cfg.head_dim, cfg.rope_base, out=L.attn[:r], lse=lse)
-        M.attn_bwd(m.layout, q, k, v, L.attn[:r], L.x1[:r], lse, dq, dk, dv, cfg.heads, cfg.kv_heads, cfg.head_dim,
-                   cfg.rope_base)
+        m._attn_fwd(L, q, k, v, None)
+        M.attn_bwd(m.layout, L.qr[:r], L.kr[:r], v, L.attn[:r], L.x1[:r], lse, dq, dk, dv, cfg.heads, cfg.kv_heads,
+                   cfg.head_dim, cfg.rope_base, prerotated=True)
     e1.record()
     torch.cuda.synchronize()
     attn_ms = e0.elapsed_time(e1) / a.steps * cfg.layers
