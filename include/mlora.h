@@ -214,6 +214,14 @@ typedef struct mlora_adam_group {
 mlora_status mlora_adam_step(mlora_ctx* ctx, const mlora_plan* plan, const mlora_adam_group* groups,
                              int32_t num_groups, const float* lr, const int32_t* step, float beta1,
                              float beta2, float eps, float weight_decay, void* stream);
+/* As mlora_adam_step; loss_gate (device fp32 [J], may be NULL) skips every job
+ * whose loss is not finite this step, without a host sync: its p, m, v stay
+ * untouched (skip-on-overflow), so a diverged job's NaN gradient never reaches
+ * its adapter — which the next step's fused tiles share with the other jobs. */
+mlora_status mlora_adam_step_ex(mlora_ctx* ctx, const mlora_plan* plan, const mlora_adam_group* groups,
+                                int32_t num_groups, const float* lr, const int32_t* step, float beta1,
+                                float beta2, float eps, float weight_decay, const float* loss_gate,
+                                void* stream);
 
 /* ---------------------------------------------------------------- fp64 path
  * Device fp64 GEMM with the reference's exact per-element operation order

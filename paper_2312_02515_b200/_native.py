@@ -72,6 +72,8 @@ _SIGS = {
     "mlora_zero_nonfinite_rows": (i32, [vp, vp, vp, C.POINTER(vp), C.POINTER(i32), i32, vp]),
     "mlora_adam_step": (i32, [vp, vp, C.POINTER(AdamGroupC), i32, C.POINTER(f32), C.POINTER(i32), f32, f32,
                               f32, f32, vp]),
+    "mlora_adam_step_ex": (i32, [vp, vp, C.POINTER(AdamGroupC), i32, C.POINTER(f32), C.POINTER(i32), f32, f32,
+                                 f32, f32, vp, vp]),
 }
 
 # Optional groups (present once the corresponding kernels are built).

@@ -135,6 +135,7 @@ struct AdamArgs {
     float bc1[kMaxJobs];   // 1 - beta1^t_j
     float bc2[kMaxJobs];   // 1 - beta2^t_j
     float beta1, beta2, eps, wd;
+    const float* loss_gate;  // device [J] or NULL: a job whose loss is not finite is skipped
 };
 
 // AdamW over all groups.  bytes/param: read p,g,m,v (16) + write p,m,v (12)
@@ -153,6 +154,7 @@ __global__ void adam_kernel(const __grid_constant__ AdamArgs a) {
         const int j = job_of_col(a.roff, a.J, static_cast<int>(G.layout == 0 ? row : col));
         const float lr = a.lr[j], bc1 = a.bc1[j], bc2 = a.bc2[j];
         if (bc1 == 0.f) continue;  // step 0: job not in this fused batch -> p, m, v untouched
+        if (a.loss_gate && !isfinite(__ldg(a.loss_gate + j))) continue;  // skip-on-overflow (diverged job)
         float4 p = reinterpret_cast<float4*>(G.p)[e / 4];
         const float4 g = reinterpret_cast<const float4*>(G.g)[e / 4];
         float4 m = reinterpret_cast<float4*>(G.m)[e / 4];

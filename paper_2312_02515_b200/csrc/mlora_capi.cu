@@ -1200,6 +1200,14 @@ mlora_status mlora_pack_adapters(mlora_ctx* ctx, const mlora_plan* plan, int32_t
 mlora_status mlora_adam_step(mlora_ctx* ctx, const mlora_plan* plan, const mlora_adam_group* groups,
                              int32_t num_groups, const float* lr, const int32_t* step, float beta1,
                              float beta2, float eps, float weight_decay, void* stream) {
+    return mlora_adam_step_ex(ctx, plan, groups, num_groups, lr, step, beta1, beta2, eps, weight_decay, nullptr,
+                              stream);
+}
+
+mlora_status mlora_adam_step_ex(mlora_ctx* ctx, const mlora_plan* plan, const mlora_adam_group* groups,
+                                int32_t num_groups, const float* lr, const int32_t* step, float beta1,
+                                float beta2, float eps, float weight_decay, const float* loss_gate,
+                                void* stream) {
     if (!ctx || !plan || (num_groups > 0 && !groups) || !lr || !step)
         return fail(ctx, MLORA_USAGE, "null argument");
     if (!(beta1 >= 0.f && beta1 < 1.f && beta2 >= 0.f && beta2 < 1.f && eps > 0.f))
@@ -1219,6 +1227,7 @@ mlora_status mlora_adam_step(mlora_ctx* ctx, const mlora_plan* plan, const mlora
     a.beta2 = beta2;
     a.eps = eps;
     a.wd = weight_decay;
+    a.loss_gate = loss_gate;
     for (int g0 = 0; g0 < num_groups; g0 += kMaxAdamGroups) {
         const int ng = std::min(kMaxAdamGroups, num_groups - g0);
         long long start4 = 0;

@@ -36,6 +36,15 @@ With `checkpoint_dir`, each job's adapter and AdamW state is saved
 (FusedLoraLayer.save_job: reference layout, atomic write) when the job
 completes or is stopped.
 
+Two step backends.  Default: one transformer layer's LoRA'd projections
+(FusedLoraLayer) on synthetic hidden states, loss L_j = 1/2 sum ||Y||^2.  With
+`model=DecoderConfig`: the whole decoder (model.MultiLoraDecoder) on each job's
+token sequences, so the per-job losses detect_stop consumes are the real
+padding-masked cross-entropy (K4).  A job's dataset items are then token
+sequences (JobConfig.tokens, or deterministic synthetic tokens per item when
+absent), so an epoch revisits the same items and the CE falls as the adapters
+learn.
+
 Row order: the kernels need each job's rows contiguous and in adapter order, so
 the fused rows are placed in job-index order; the selection (urgency) order is
 kept as the routing order reported in the event.  The linear layer is
@@ -90,6 +99,7 @@ class JobConfig:
     priority: int = 1
     submit_time: float = 0.0
     iterations: int = 10           # true_iterations
+    tokens: list | None = None     # decoder backend: token ids of each dataset item (len == lengths[i])
 
 
 @dataclass
@@ -106,11 +116,13 @@ class _JobState:
     def finished(self) -> bool:
         return self.stopped is not None or self.done >= self.cfg.iterations
 
-    def peek(self) -> list:
+    def peek_items(self) -> range:
         n = len(self.cfg.lengths)
         pos = self.cursor % n
-        take = min(self.cfg.batch_size, n - pos)
-        return list(self.cfg.lengths[pos:pos + take])
+        return range(pos, pos + min(self.cfg.batch_size, n - pos))
+
+    def peek(self) -> list:
+        return [self.cfg.lengths[i] for i in self.peek_items()]
 
     def commit(self, n_items: int) -> None:
         self.cursor += n_items
@@ -142,7 +154,7 @@ class FusedExecutor:
     def __init__(self, ctx: F.Context, shapes, jobs: list[JobConfig], max_concurrent: int,
                  strategy: str = "minpad", padded: bool = False, seed: int = 0, W0: dict | None = None,
                  pipelined: bool = True, early_stopping: bool = False, patience: int = 3,
-                 accuracy_fn=None, checkpoint_dir: str | None = None):
+                 accuracy_fn=None, checkpoint_dir: str | None = None, model=None):
         self.ctx = ctx
         self.checkpoint_dir = checkpoint_dir  # a job's adapter is saved when it completes or stops
         self.early_stopping = early_stopping
@@ -157,15 +169,32 @@ class FusedExecutor:
         max_len = max(max(j.lengths) for j in jobs)
         max_bs = max(j.batch_size for j in jobs)
         capacity = max_concurrent * max_bs * max_len
-        self.layer = FusedLoraLayer(ctx, shapes, [j.rank for j in jobs], [j.scale for j in jobs],
-                                    [j.lr for j in jobs], rows=capacity, seed=seed, W0=W0)
-        self.k_in = shapes[0][2]
+        self.model = model
+        if model is None:
+            self.layer = FusedLoraLayer(ctx, shapes, [j.rank for j in jobs], [j.scale for j in jobs],
+                                        [j.lr for j in jobs], rows=capacity, seed=seed, W0=W0)
+            self.k_in = shapes[0][2]
+        else:
+            from .model import MultiLoraDecoder
+            for j in jobs:
+                if j.tokens is not None and [len(t) for t in j.tokens] != list(j.lengths):
+                    raise ValueError(f"job {j.id}: token sequences do not match its lengths")
+            self.layer = MultiLoraDecoder(ctx, model, [j.rank for j in jobs], [j.scale for j in jobs],
+                                          [j.lr for j in jobs], capacity=capacity, seed=seed)
         self.gen = torch.Generator(device=ctx.device).manual_seed(seed + 1)
         self.trace = Trace()
         self.clock = 0.0
         self._pending = None  # the enqueued step whose time/losses have not been collected yet
         self._loss_host = [torch.empty(len(jobs), dtype=torch.float32).pin_memory() for _ in range(2)]
         self._slot = 0
+
+    def _item_tokens(self, i: int, item: int) -> list:
+        """Token ids of job i's dataset item (given, or synthetic and fixed per item)."""
+        cfg = self.jobs[i].cfg
+        if cfg.tokens is not None:
+            return list(cfg.tokens[item])
+        g = torch.Generator().manual_seed(1_000_003 * (i + 1) + item)
+        return torch.randint(0, self.model.vocab, (cfg.lengths[item],), generator=g).tolist()
 
     def active(self) -> list[int]:
         return [i for i, js in enumerate(self.jobs) if not js.finished]
@@ -233,22 +262,36 @@ class FusedExecutor:
             if j in batches:
                 r = lay.seg[in_batch.index(j) + 1]
             seg.append(r)
-        self.layer.set_layout(seg)                           # stream-ordered plan update, no host sync
-        x = torch.empty(lay.rows, self.k_in, device=self.ctx.device)
-        x.uniform_(-1.0, 1.0, generator=self.gen)
-        x = x.to(torch.bfloat16)
-        if self.padded:  # pad rows are zero, exactly as fuse() builds them
-            mask = torch.zeros(lay.rows, dtype=torch.bool)
-            for rows in lay.seq_rows:
-                for r0, L in rows:
-                    mask[r0:r0 + L] = True
-            x[~mask.to(self.ctx.device, non_blocking=True)] = 0
         active = [j in batches for j in range(len(self.jobs))]
+        if self.model is None:
+            self.layer.set_layout(seg)                       # stream-ordered plan update, no host sync
+            x = torch.empty(lay.rows, self.k_in, device=self.ctx.device)
+            x.uniform_(-1.0, 1.0, generator=self.gen)
+            x = x.to(torch.bfloat16)
+            if self.padded:  # pad rows are zero, exactly as fuse() builds them
+                mask = torch.zeros(lay.rows, dtype=torch.bool)
+                for rows in lay.seq_rows:
+                    for r0, L in rows:
+                        mask[r0:r0 + L] = True
+                x[~mask.to(self.ctx.device, non_blocking=True)] = 0
+        else:
+            from .model import pack_tokens
+            seqs = [[self._item_tokens(j, it) for it in self.jobs[j].peek_items()] if j in batches else []
+                    for j in range(len(self.jobs))]
+            tb = pack_tokens(seqs, padded=self.padded)
+            if tb.seg != seg:
+                raise RuntimeError("token layout disagrees with the packer's layout")
+            self.layer.set_batch(tb)                         # stream-ordered uploads, no host sync
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         slot = self._loss_host[self._slot]
         self._slot ^= 1
         e0.record()
-        loss = self.layer.step(x, active=active)
+        if self.model is None:
+            loss = self.layer.step(x, active=active)
+        else:
+            loss = self.layer.forward()
+            self.layer.backward()
+            self.layer.optimizer_step(active=active)
         slot.copy_(loss, non_blocking=True)                  # D2H of this step's per-job losses
         e1.record()
         prev = self._collect()                               # step t-1 (normally finished already)

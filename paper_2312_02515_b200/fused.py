@@ -239,8 +239,9 @@ class AdamState:
 
 
 def adam_step(ctx: Context, plan: Plan, states, grads, lr, step, beta1=0.9, beta2=0.999, eps=1e-8,
-              weight_decay=0.0, stream=None) -> None:
-    """One fused AdamW launch over every adapter tensor (per-job lr and step)."""
+              weight_decay=0.0, stream=None, loss_gate: torch.Tensor | None = None) -> None:
+    """One fused AdamW launch over every adapter tensor (per-job lr and step).
+    loss_gate (device fp32 [J]): jobs whose loss is not finite are skipped."""
     J = plan.num_jobs
     groups = (N.AdamGroupC * len(states))()
     for i, (st, g) in enumerate(zip(states, grads)):
@@ -249,5 +250,5 @@ def adam_step(ctx: Context, plan: Plan, states, grads, lr, step, beta1=0.9, beta
                                  st.p.shape[0], st.p.shape[1], st.layout, 0)
     lr_c = (N.f32 * J)(*[float(x) for x in lr])
     step_c = (N.i32 * J)(*[int(x) for x in step])
-    N.check(N.lib().mlora_adam_step(ctx.handle, plan.handle, groups, len(states), lr_c, step_c, beta1, beta2,
-                                    eps, weight_decay, _stream_handle(stream)), ctx.handle)
+    N.check(N.lib().mlora_adam_step_ex(ctx.handle, plan.handle, groups, len(states), lr_c, step_c, beta1, beta2,
+                                       eps, weight_decay, N.ptr(loss_gate), _stream_handle(stream)), ctx.handle)

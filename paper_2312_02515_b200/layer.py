@@ -43,6 +43,94 @@ def flops_per_token(shapes, rank: int) -> int:
     return sum(4 * d * k + 6 * rank * (d + k) for _, d, k, _ in shapes)
 
 
+class AdapterJobsMixin:
+    """Per-job adapter management shared by FusedLoraLayer and the decoder
+    (model.MultiLoraDecoder): quarantine and checkpoint / resume.  Needs
+    `ctx, plan, ranks, scales, lrs, step_count` and `named_projections()` ->
+    [(key, projection with d, k, A, B: fused.AdamState)]."""
+
+    def quarantine(self, job: int) -> None:
+        """Zero job `job`'s bf16 operand copies (its rows of every A_cat, its
+        columns of every B_cat, on every projection), stream-ordered.  The
+        fused kernels rely on structural zeros: the other jobs' rows of H_cat / G_cat are exactly 0
+        and multiply this job's adapter inside a shared 64-column rank k-block.
+        0 * NaN is NaN, so a diverged adapter could poison its neighbours.  The
+        executor calls this when early stopping retires a job with a
+        non-finite loss.  Its fp32 masters and moments are kept for inspection."""
+        r0, r1 = self.plan.rank_offsets[job], self.plan.rank_offsets[job + 1]
+        for _, p in self.named_projections():
+            p.A.p_bf16[r0:r1].zero_()
+            p.B.p_bf16[:, r0:r1].zero_()
+
+    # ------------------------------------------------------------ checkpoint / resume
+    CKPT_FORMAT = "mlora-adapter-v1"
+
+    def job_state(self, job: int) -> dict:
+        """Job `job`'s adapter and AdamW state in the reference's layout
+        (AdapterWeights, lora.hpp:34-41: A_j r x k, B_j d x r, fp32), copied to
+        host after everything already queued on the current stream."""
+        r0, r = self.plan.rank_offsets[job], self.ranks[job]
+        proj = {}
+        for key, p in self.named_projections():
+            proj[key] = {"d": p.d, "k": p.k,
+                         "A": p.A.p[r0:r0 + r].cpu(), "mA": p.A.m[r0:r0 + r].cpu(), "vA": p.A.v[r0:r0 + r].cpu(),
+                         "B": p.B.p[:, r0:r0 + r].cpu(), "mB": p.B.m[:, r0:r0 + r].cpu(),
+                         "vB": p.B.v[:, r0:r0 + r].cpu()}
+        return {"format": self.CKPT_FORMAT, "rank": r, "scale": self.scales[job], "lr": self.lrs[job],
+                "step": self.step_count[job], "proj": proj}
+
+    def save_job(self, path: str, job: int) -> None:
+        """Atomically write job `job`'s state (temp file + fsync + rename, as the
+        reference writes its outputs: io.cpp:404-414 atomic_write)."""
+        import os
+        state = self.job_state(job)
+        d = os.path.dirname(os.path.abspath(path))
+        os.makedirs(d, exist_ok=True)
+        tmp = path + ".tmp"
+        with open(tmp, "wb") as f:
+            torch.save(state, f)
+            f.flush()
+            os.fsync(f.fileno())
+        os.replace(tmp, path)
+
+    def load_job(self, path_or_state, job: int) -> None:
+        """Resume job `job` from a saved state: fp32 masters, AdamW moments and
+        step count go into the job's cat-layout slices, the bf16 operand copies
+        are refreshed.  UsageError on a foreign file or a rank / scale mismatch
+        (as AdapterWeights::validate, lora.cpp:62-70); ShapeError on projection
+        dims."""
+        from . import errors as E
+        st = torch.load(path_or_state, map_location="cpu") if isinstance(path_or_state, str) else path_or_state
+        if not isinstance(st, dict) or st.get("format") != self.CKPT_FORMAT:
+            raise E.UsageError("not an mlora adapter checkpoint")
+        if st["rank"] != self.ranks[job]:
+            raise E.UsageError(f"checkpoint rank {st['rank']} != slot rank {self.ranks[job]}")
+        if float(st["scale"]) != float(self.scales[job]):  # s_j lives in the plan's device tables
+            raise E.UsageError(f"checkpoint scale {st['scale']} != slot scale {self.scales[job]}")
+        named = self.named_projections()
+        names = {key for key, _ in named}
+        if set(st["proj"]) != names:
+            raise E.ShapeError(f"checkpoint projections {sorted(st['proj'])} != layer {sorted(names)}")
+        r0, r = self.plan.rank_offsets[job], self.ranks[job]
+        for key, p in named:
+            q = st["proj"][key]
+            if (q["d"], q["k"]) != (p.d, p.k) or tuple(q["A"].shape) != (r, p.k) or tuple(q["B"].shape) != (p.d, r):
+                raise E.ShapeError(f"projection {key}: checkpoint shape does not match the layer")
+        dev = self.ctx.device
+        for key, p in named:
+            q = st["proj"][key]
+            p.A.p[r0:r0 + r] = q["A"].to(dev)
+            p.A.m[r0:r0 + r] = q["mA"].to(dev)
+            p.A.v[r0:r0 + r] = q["vA"].to(dev)
+            p.A.p_bf16[r0:r0 + r] = p.A.p[r0:r0 + r].to(torch.bfloat16)
+            p.B.p[:, r0:r0 + r] = q["B"].to(dev)
+            p.B.m[:, r0:r0 + r] = q["mB"].to(dev)
+            p.B.v[:, r0:r0 + r] = q["vB"].to(dev)
+            p.B.p_bf16[:, r0:r0 + r] = p.B.p[:, r0:r0 + r].to(torch.bfloat16)
+        self.lrs[job] = float(st["lr"])
+        self.step_count[job] = int(st["step"])
+
+
 @dataclass
 class Projection:
     name: str
@@ -61,7 +149,7 @@ class Projection:
     row_sq: torch.Tensor               # fp32 [ceil(d/256), rows] fused-loss row partials
 
 
-class FusedLoraLayer:
+class FusedLoraLayer(AdapterJobsMixin):
     """All adapters of J jobs on one layer's projections, cat layout, on one GPU."""
 
     def __init__(self, ctx: F.Context, shapes, ranks, scales, lrs, rows: int, seed: int = 0,
@@ -113,18 +201,8 @@ class FusedLoraLayer:
         self.plan.update(seg_offsets)  # stream-ordered, no host sync
         self.cur_rows = rows
 
-    def quarantine(self, job: int) -> None:
-        """Zero job `job`'s bf16 operand copies (its rows of every A_cat, its
-        columns of every B_cat), stream-ordered.  The fused kernels rely on
-        structural zeros: the other jobs' rows of H_cat / G_cat are exactly 0
-        and multiply this job's adapter inside a shared 64-column rank k-block.
-        0 * NaN is NaN, so a diverged adapter could poison its neighbours.  The
-        executor calls this when early stopping retires a job with a
-        non-finite loss.  Its fp32 masters and moments are kept for inspection."""
-        r0, r1 = self.plan.rank_offsets[job], self.plan.rank_offsets[job + 1]
-        for p in self.proj:
-            p.A.p_bf16[r0:r1].zero_()
-            p.B.p_bf16[:, r0:r1].zero_()
+    def named_projections(self):
+        return [(p.name, p) for p in self.proj]
 
     def _views(self, p: Projection, rows: int):
         nblk = p.row_sq.shape[0]
@@ -214,73 +292,6 @@ class FusedLoraLayer:
                                    (N.vp * n)(*[p.dA.data_ptr() for p in self.proj]),
                                    (N.vp * n)(*[p.dB.data_ptr() for p in self.proj]), s), ctx.handle)
         return self.loss
-
-    # ------------------------------------------------------------ checkpoint / resume
-    CKPT_FORMAT = "mlora-adapter-v1"
-
-    def job_state(self, job: int) -> dict:
-        """Job `job`'s adapter and AdamW state in the reference's layout
-        (AdapterWeights, lora.hpp:34-41: A_j r x k, B_j d x r, fp32), copied to
-        host after everything already queued on the current stream."""
-        r0, r = self.plan.rank_offsets[job], self.ranks[job]
-        proj = {}
-        for p in self.proj:
-            proj[p.name] = {"d": p.d, "k": p.k,
-                            "A": p.A.p[r0:r0 + r].cpu(), "mA": p.A.m[r0:r0 + r].cpu(), "vA": p.A.v[r0:r0 + r].cpu(),
-                            "B": p.B.p[:, r0:r0 + r].cpu(), "mB": p.B.m[:, r0:r0 + r].cpu(),
-                            "vB": p.B.v[:, r0:r0 + r].cpu()}
-        return {"format": self.CKPT_FORMAT, "rank": r, "scale": self.scales[job], "lr": self.lrs[job],
-                "step": self.step_count[job], "proj": proj}
-
-    def save_job(self, path: str, job: int) -> None:
-        """Atomically write job `job`'s state (temp file + fsync + rename, as the
-        reference writes its outputs: io.cpp:404-414 atomic_write)."""
-        import os
-        state = self.job_state(job)
-        d = os.path.dirname(os.path.abspath(path))
-        os.makedirs(d, exist_ok=True)
-        tmp = path + ".tmp"
-        with open(tmp, "wb") as f:
-            torch.save(state, f)
-            f.flush()
-            os.fsync(f.fileno())
-        os.replace(tmp, path)
-
-    def load_job(self, path_or_state, job: int) -> None:
-        """Resume job `job` from a saved state: fp32 masters, AdamW moments and
-        step count go into the job's cat-layout slices, the bf16 operand copies
-        are refreshed.  UsageError on a foreign file or a rank / scale mismatch
-        (as AdapterWeights::validate, lora.cpp:62-70); ShapeError on projection
-        dims."""
-        from . import errors as E
-        st = torch.load(path_or_state, map_location="cpu") if isinstance(path_or_state, str) else path_or_state
-        if not isinstance(st, dict) or st.get("format") != self.CKPT_FORMAT:
-            raise E.UsageError("not an mlora adapter checkpoint")
-        if st["rank"] != self.ranks[job]:
-            raise E.UsageError(f"checkpoint rank {st['rank']} != slot rank {self.ranks[job]}")
-        if float(st["scale"]) != float(self.scales[job]):  # s_j lives in the plan's device tables
-            raise E.UsageError(f"checkpoint scale {st['scale']} != slot scale {self.scales[job]}")
-        names = {p.name for p in self.proj}
-        if set(st["proj"]) != names:
-            raise E.ShapeError(f"checkpoint projections {sorted(st['proj'])} != layer {sorted(names)}")
-        r0, r = self.plan.rank_offsets[job], self.ranks[job]
-        for p in self.proj:
-            q = st["proj"][p.name]
-            if (q["d"], q["k"]) != (p.d, p.k) or tuple(q["A"].shape) != (r, p.k) or tuple(q["B"].shape) != (p.d, r):
-                raise E.ShapeError(f"projection {p.name}: checkpoint shape does not match the layer")
-        dev = self.ctx.device
-        for p in self.proj:
-            q = st["proj"][p.name]
-            p.A.p[r0:r0 + r] = q["A"].to(dev)
-            p.A.m[r0:r0 + r] = q["mA"].to(dev)
-            p.A.v[r0:r0 + r] = q["vA"].to(dev)
-            p.A.p_bf16[r0:r0 + r] = p.A.p[r0:r0 + r].to(torch.bfloat16)
-            p.B.p[:, r0:r0 + r] = q["B"].to(dev)
-            p.B.m[:, r0:r0 + r] = q["mB"].to(dev)
-            p.B.v[:, r0:r0 + r] = q["vB"].to(dev)
-            p.B.p_bf16[:, r0:r0 + r] = p.B.p[:, r0:r0 + r].to(torch.bfloat16)
-        self.lrs[job] = float(st["lr"])
-        self.step_count[job] = int(st["step"])
 
     def optimizer_step(self, active=None, stream=None) -> None:
         """AdamW on every adapter; jobs not in `active` (bool per job) keep p, m, v

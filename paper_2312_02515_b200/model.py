@@ -36,6 +36,7 @@ from . import _native as N
 from . import errors
 from . import fused as F
 from . import model_ops as M
+from .layer import AdapterJobsMixin
 
 
 @dataclass(frozen=True)
@@ -159,7 +160,7 @@ class _Layer:
     act: torch.Tensor | None = None     # SwiGLU output
 
 
-class MultiLoraDecoder:
+class MultiLoraDecoder(AdapterJobsMixin):
     """J LoRA jobs fine-tuning one frozen decoder on fused batches, on one GPU."""
 
     def __init__(self, ctx: F.Context, cfg: DecoderConfig, ranks, scales, lrs, capacity: int, seed: int = 0,
@@ -228,6 +229,10 @@ class MultiLoraDecoder:
         self._inv = torch.empty(self.J, dtype=torch.float32, device=dev)
         self.batch: TokenBatch | None = None
 
+    def named_projections(self):
+        """(key, projection) of every LoRA'd linear: keys 'layer.name' (checkpoints, quarantine)."""
+        return [(f"{li}.{name}", p) for li, L in enumerate(self.layers) for name, p in L.proj.items()]
+
     # ------------------------------------------------------------ batch
     def set_batch(self, batch: TokenBatch) -> None:
         """Install one fused batch: job segments (plan), attention layout, tokens."""
@@ -290,6 +295,21 @@ class MultiLoraDecoder:
             (N.vp * n)(*[self._g[p.name].data_ptr() for p, _, _ in items]),
             (N.vp * n)(*[p.dA.data_ptr() for p, _, _ in items]), (N.vp * n)(*[p.dB.data_ptr() for p, _, _ in items]),
             s), self.ctx.handle)
+
+    def _guard(self, tensors, s) -> None:
+        """Job isolation under divergence (as the layer step's guard):
+        for every job whose CE is not finite, zero its rows of the tensors the
+        grouped dA / dB reductions read.  Those reductions run over several jobs'
+        rows inside one 64-column rank block and rely on structural zeros
+        (H, G block-diagonal); 0 * inf = NaN would otherwise leak a diverged job
+        into its neighbours' gradients.  All-finite: one launch reading J floats."""
+        uniq = {}
+        for t in tensors:
+            uniq.setdefault(t.data_ptr(), t.shape[1])
+        n = len(uniq)
+        N.check(N.lib().mlora_zero_nonfinite_rows(self.ctx.handle, self.plan.handle, self.loss.data_ptr(),
+                                                  (N.vp * n)(*uniq.keys()), (N.i32 * n)(*uniq.values()), n, s),
+                self.ctx.handle)
 
     def _qkv_views(self, L: _Layer, grad: bool = False):
         cfg, r = self.cfg, self.rows
@@ -418,6 +438,7 @@ class MultiLoraDecoder:
             items.append((P[out_p], L.attn[:r], d_x1))
             items += [(P[n], L.h2[:r], dy) for n, dy in zip(up_p, dys_up)]
             items.append((P[down_p], L.act[:r], d_out))
+            self._guard([x for _, x, _ in items] + [dy for _, _, dy in items], s)
             self._grads(items, s)
             if d_in is not None:
                 # the next (lower) layer's output gradient; the buffer d_out held is
@@ -436,15 +457,18 @@ class MultiLoraDecoder:
 
     def optimizer_step(self, active=None, stream=None) -> None:
         """One AdamW over every adapter (per-job lr; jobs with no rows in the
-        batch, or marked inactive, are left untouched)."""
+        batch, marked inactive, or whose loss this step is not finite are left
+        untouched)."""
         if active is None:
             seg = self.batch.seg
             active = [seg[j + 1] > seg[j] for j in range(self.J)]
         self.step_count = [c + (1 if a else 0) for c, a in zip(self.step_count, active)]
         steps = [c if a else 0 for c, a in zip(self.step_count, active)]
         st = self.adapter_tensors()
+        # skip-on-overflow: a job whose CE is not finite this step keeps its adapter
+        # (no host sync), so its NaN gradient cannot reach the fused tiles it shares
         F.adam_step(self.ctx, self.plan, [a for a, _ in st], [g for _, g in st], self.lrs, steps,
-                    weight_decay=self.weight_decay, stream=stream)
+                    weight_decay=self.weight_decay, stream=stream, loss_gate=self.loss)
 
     def step(self, batch: TokenBatch | None = None, stream=None) -> torch.Tensor:
         """One fine-tuning step of every job in the batch: forward, per-job CE,

@@ -138,8 +138,9 @@ class AttnLayout:
         self.offsets, self.lens = off, lens
         self.rows = off[-1]
         self.max_len = max(1, max(b - a for a, b in zip(off, off[1:])))
-        self.d_off = torch.tensor(off, dtype=torch.int32, device=device)
-        self.d_len = torch.tensor(lens, dtype=torch.int32, device=device)
+        # pinned staging + async copies: stream-ordered, the host never waits for the device
+        self.d_off = torch.tensor(off, dtype=torch.int32).pin_memory().to(device, non_blocking=True)
+        self.d_len = torch.tensor(lens, dtype=torch.int32).pin_memory().to(device, non_blocking=True)
 
     def desc(self, heads: int, kv_heads: int, head_dim: int, rope_base: float = 10000.0,
              scale: float | None = None, prerotated: bool = False) -> "N.AttnDescC":

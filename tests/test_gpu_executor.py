@@ -240,3 +240,82 @@ def test_adapter_checkpoint_resume_is_exact(tmp_path):
         b.load_job(paths[0], 1)  # rank 8 checkpoint into a rank-16 slot
     with pytest.raises(E.UsageError):
         b.load_job(paths[2], 0)  # same rank, different scale
+
+
+# ---------------------------------------------------------------- decoder backend (real CE losses)
+@pytest.mark.parametrize("padded", [False, True])
+def test_decoder_executor_selection_accounting_and_ce(padded):
+    """model=TINY_LLAMA: the same MinPad selection / ξ accounting as the layer
+    backend, and the per-job losses the executor reports are the decoder's
+    padding-masked CE (≈ ln V on the first visit, falling on revisits)."""
+    from paper_2312_02515_b200 import executor as X
+    from paper_2312_02515_b200 import fused as F
+    from paper_2312_02515_b200 import model as MD
+    from paper_2312_02515_b200 import packer
+
+    ctx = F.Context(0)
+    jobs = make_jobs(X, packer)
+    for j in jobs:
+        j.iterations = 12
+        j.lr = 5e-3
+    ex = X.FusedExecutor(ctx, None, jobs, max_concurrent=3, strategy="minpad", padded=padded, seed=5,
+                         pipelined=True, model=MD.TINY_LLAMA)
+    cursors = [0] * len(jobs)
+    done = [0] * len(jobs)
+    evs = []
+    while True:
+        live = [i for i in range(len(jobs)) if done[i] < jobs[i].iterations]
+        if not live:
+            break
+        cands = [O.BatchCandidate(f"c{n}", O.next_candidate_batch(jobs[i].lengths, cursors[i], jobs[i].batch_size),
+                                  jobs[i].priority, jobs[i].submit_time) for n, i in enumerate(live)]
+        want = O.select_minpad(cands, 3)
+        chosen = [live[int(c[1:])] for c in want.chosen]
+        shape = O.fused_shape([c.item_lengths for c in (cands[int(c[1:])] for c in want.chosen)])
+        evs.append(([jobs[i].id for i in chosen], shape.total_tokens, shape.padding_tokens))
+        ex.step()
+        for i in chosen:
+            b = O.next_candidate_batch(jobs[i].lengths, cursors[i], jobs[i].batch_size)
+            cursors[i] = O.commit_batch(cursors[i], len(b), len(jobs[i].lengths))
+            done[i] += 1
+    ex.flush()
+    got = [(e["routing"], e["total_tokens"], e["padding_tokens"]) for e in ex.trace.events]
+    assert got == evs
+    ln_v = math.log(MD.TINY_LLAMA.vocab)
+    for e in ex.trace.events:
+        assert all(math.isfinite(v) and 0 < v < 3 * ln_v for v in e["losses"].values())
+    # each job's dataset repeats every epoch: its CE on a revisited item has fallen
+    js = ex.jobs[0]
+    assert js.losses[-1] < js.losses[0] - 0.1, js.losses
+
+
+def test_decoder_diverged_job_is_isolated_and_stopped():
+    """A job at lr 1e30 diverges (non-finite CE); AdamW's loss gate keeps its
+    adapter finite, so every other job's CE stays bitwise identical to a run in
+    which it trains normally; the executor stops it with nan_loss."""
+    from paper_2312_02515_b200 import executor as X
+    from paper_2312_02515_b200 import fused as F
+    from paper_2312_02515_b200 import model as MD
+
+    ctx = F.Context(0)
+    g = torch.Generator().manual_seed(3)
+    seqs = [[torch.randint(0, 1024, (n,), generator=g).tolist() for n in (40, 17)] for _ in range(3)]
+    batch = MD.pack_tokens(seqs)
+    runs = []
+    for lr1 in (1e-3, 1e30):
+        m = MD.MultiLoraDecoder(ctx, MD.TINY_LLAMA, [8, 16, 8], [2.0] * 3, [1e-3, lr1, 2e-3],
+                                capacity=batch.rows, seed=12)
+        runs.append([m.step(batch).clone() for _ in range(4)])
+    torch.cuda.synchronize()
+    assert not math.isfinite(runs[1][-1][1].item())
+    for a, b in zip(*runs):
+        assert torch.equal(a[0], b[0]) and torch.equal(a[2], b[2])
+    # through the executor: the diverged job is stopped on its CE, the others finish
+    jobs = [X.JobConfig(id=f"j{i}", lengths=[24, 31, 9, 40], batch_size=2, rank=8, lr=lr, iterations=6)
+            for i, lr in enumerate([2e-3, 1e30, 1e-3])]
+    ex = X.FusedExecutor(ctx, None, jobs, max_concurrent=3, early_stopping=True, model=MD.TINY_LLAMA,
+                         pipelined=False, seed=2)
+    tr = ex.run()
+    assert [s["job"] for s in tr.stops] == ["j1"] and tr.stops[0]["cause"] == "nan_loss"
+    assert ex.jobs[0].done == 6 and ex.jobs[2].done == 6
+    assert all(math.isfinite(v) for v in ex.jobs[0].losses + ex.jobs[2].losses)
