@@ -73,32 +73,67 @@ __global__ void embed_kernel(const int* __restrict__ tokens, const uint4* __rest
     for (int i = threadIdx.x; i < h8; i += blockDim.x) x[t * h8 + i] = E[tok * h8 + i];
 }
 
+// 8 x bf16 <-> 8 x fp32 through one 16-byte access
+__device__ __forceinline__ void ld8(const __nv_bfloat16* p, float (&f)[8]) {
+    const uint4 u = *reinterpret_cast<const uint4*>(p);
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const float2 x = __bfloat1622float2(h[e]);
+        f[2 * e] = x.x, f[2 * e + 1] = x.y;
+    }
+}
+__device__ __forceinline__ void st8(__nv_bfloat16* p, const float (&f)[8]) {
+    uint4 u;
+    uint32_t* w = &u.x;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const __nv_bfloat162 r = __floats2bfloat162_rn(f[2 * e], f[2 * e + 1]);
+        w[e] = *reinterpret_cast<const uint32_t*>(&r);
+    }
+    *reinterpret_cast<uint4*>(p) = u;
+}
+
 // ---------------------------------------------------------------- residual add + RMSNorm
 // xo = bf16(x + delta) (the residual stream, when delta != NULL), y = xo * rstd * w.
-// bytes/row: 2h (x) + 2h (delta) + 2h (xo) + 2h (y).
-__global__ void add_rmsnorm_kernel(const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ delta,
-                                   const __nv_bfloat16* __restrict__ w, int h, float eps,
-                                   __nv_bfloat16* __restrict__ xo, __nv_bfloat16* __restrict__ y,
-                                   float* __restrict__ rstd) {
+// One CTA per row, 16-byte accesses (h % 8 == 0); the row is kept in shared
+// memory between the two passes.  bytes/row: 2h (x) + 2h (delta) + 2h (xo) + 2h (y).
+__global__ void __launch_bounds__(256) add_rmsnorm_kernel(const __nv_bfloat16* __restrict__ x,
+                                                          const __nv_bfloat16* __restrict__ delta,
+                                                          const __nv_bfloat16* __restrict__ w, int h, float eps,
+                                                          __nv_bfloat16* __restrict__ xo,
+                                                          __nv_bfloat16* __restrict__ y, float* __restrict__ rstd) {
     pdl_prologue();
+    extern __shared__ __align__(16) float row[];
     __shared__ float red[32];
     const long long o = (long long)blockIdx.x * h;
-    const __nv_bfloat16* src = delta ? xo : x;
     float ss = 0.f;
-    for (int i = threadIdx.x; i < h; i += blockDim.x) {
-        float v = __bfloat162float(x[o + i]);
+    for (int i = threadIdx.x * 8; i < h; i += blockDim.x * 8) {
+        float v[8];
+        ld8(x + o + i, v);
         if (delta) {
-            const __nv_bfloat16 s = __float2bfloat16_rn(v + __bfloat162float(delta[o + i]));
-            xo[o + i] = s;
-            v = __bfloat162float(s);
+            float d[8];
+            ld8(delta + o + i, d);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) v[e] = __bfloat162float(__float2bfloat16_rn(v[e] + d[e]));
+            st8(xo + o + i, v);  // exact: v already holds bf16 values
         }
-        ss = fmaf(v, v, ss);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            row[i + e] = v[e];
+            ss = fmaf(v[e], v[e], ss);
+        }
     }
-    ss = block_sum(ss, red);  // (its __syncthreads also orders the xo writes before the re-read)
+    ss = block_sum(ss, red);
     const float r = rsqrtf(ss / h + eps);
     if (threadIdx.x == 0) rstd[blockIdx.x] = r;
-    for (int i = threadIdx.x; i < h; i += blockDim.x)
-        y[o + i] = __float2bfloat16_rn(__bfloat162float(src[o + i]) * r * __bfloat162float(w[i]));
+    for (int i = threadIdx.x * 8; i < h; i += blockDim.x * 8) {
+        float wv[8], v[8];
+        ld8(w + i, wv);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[e] = row[i + e] * r * wv[e];
+        st8(y + o + i, v);
+    }
 }
 
 // dx = dres + rstd (g - xhat mean(g xhat)), g = w * sum_k dy_k  (frozen w: no dw).
@@ -107,56 +142,83 @@ struct SumArgs {
     int n;
 };
 
-__global__ void rmsnorm_bwd_sum_kernel(SumArgs a, const __nv_bfloat16* __restrict__ dres,
-                                       const __nv_bfloat16* __restrict__ x, const __nv_bfloat16* __restrict__ w,
-                                       const float* __restrict__ rstd, int h, __nv_bfloat16* __restrict__ dx) {
+__global__ void __launch_bounds__(256) rmsnorm_bwd_sum_kernel(SumArgs a, const __nv_bfloat16* __restrict__ dres,
+                                                              const __nv_bfloat16* __restrict__ x,
+                                                              const __nv_bfloat16* __restrict__ w,
+                                                              const float* __restrict__ rstd, int h,
+                                                              __nv_bfloat16* __restrict__ dx) {
     pdl_prologue();
+    extern __shared__ __align__(16) float gs[];  // g for the row, then reused in pass 2
     __shared__ float red[32];
     const long long o = (long long)blockIdx.x * h;
     const float r = rstd[blockIdx.x];
-    auto g_at = [&](int i) {
-        float s = 0.f;
-        for (int k = 0; k < a.n; ++k) s += __bfloat162float(a.dy[k][o + i]);
-        return s * __bfloat162float(w[i]);
-    };
     float dot = 0.f;
-    for (int i = threadIdx.x; i < h; i += blockDim.x) dot = fmaf(g_at(i), __bfloat162float(x[o + i]) * r, dot);
+    for (int i = threadIdx.x * 8; i < h; i += blockDim.x * 8) {
+        float g[8], t[8], wv[8], xv[8];
+        ld8(a.dy[0] + o + i, g);
+        for (int k = 1; k < a.n; ++k) {
+            ld8(a.dy[k] + o + i, t);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) g[e] += t[e];
+        }
+        ld8(w + i, wv);
+        ld8(x + o + i, xv);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            g[e] *= wv[e];
+            gs[i + e] = g[e];
+            dot = fmaf(g[e], xv[e] * r, dot);
+        }
+    }
     dot = block_sum(dot, red) / h;
-    for (int i = threadIdx.x; i < h; i += blockDim.x) {
-        const float xh = __bfloat162float(x[o + i]) * r;
-        float v = r * (g_at(i) - xh * dot);
-        if (dres) v += __bfloat162float(dres[o + i]);
-        dx[o + i] = __float2bfloat16_rn(v);
+    for (int i = threadIdx.x * 8; i < h; i += blockDim.x * 8) {
+        float xv[8], d[8], out[8];
+        ld8(x + o + i, xv);
+        if (dres) ld8(dres + o + i, d);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) out[e] = r * (gs[i + e] - xv[e] * r * dot) + (dres ? d[e] : 0.f);
+        st8(dx + o + i, out);
     }
 }
 
 // ---------------------------------------------------------------- SwiGLU
+// Grid (column chunks of 8 x 256, rows): 16-byte accesses, no integer division.
 __device__ __forceinline__ float sigmoidf_(float g) { return 1.f / (1.f + __expf(-g)); }
 
-__global__ void swiglu_fwd_kernel(long long n, int f, const __nv_bfloat16* __restrict__ g, long long ldg,
+__global__ void swiglu_fwd_kernel(int f, const __nv_bfloat16* __restrict__ g, long long ldg,
                                   const __nv_bfloat16* __restrict__ u, long long ldu, __nv_bfloat16* __restrict__ out) {
     pdl_prologue();
-    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
-        const long long t = e / f, c = e % f;
-        const float gv = __bfloat162float(g[t * ldg + c]);
-        out[e] = __float2bfloat16_rn(gv * sigmoidf_(gv) * __bfloat162float(u[t * ldu + c]));
-    }
+    const long long t = blockIdx.y;
+    const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+    if (c >= f) return;
+    float gv[8], uv[8], o[8];
+    ld8(g + t * ldg + c, gv);
+    ld8(u + t * ldu + c, uv);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) o[e] = gv[e] * sigmoidf_(gv[e]) * uv[e];
+    st8(out + t * f + c, o);
 }
 
-__global__ void swiglu_bwd_kernel(long long n, int f, const __nv_bfloat16* __restrict__ g, long long ldg,
+__global__ void swiglu_bwd_kernel(int f, const __nv_bfloat16* __restrict__ g, long long ldg,
                                   const __nv_bfloat16* __restrict__ u, long long ldu,
                                   const __nv_bfloat16* __restrict__ dout, __nv_bfloat16* __restrict__ dg,
                                   long long lddg, __nv_bfloat16* __restrict__ du, long long lddu) {
     pdl_prologue();
-    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
-        const long long t = e / f, c = e % f;
-        const float gv = __bfloat162float(g[t * ldg + c]);
-        const float uv = __bfloat162float(u[t * ldu + c]);
-        const float d = __bfloat162float(dout[e]);
-        const float sg = sigmoidf_(gv);
-        dg[t * lddg + c] = __float2bfloat16_rn(d * uv * sg * (1.f + gv * (1.f - sg)));
-        du[t * lddu + c] = __float2bfloat16_rn(d * gv * sg);
+    const long long t = blockIdx.y;
+    const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+    if (c >= f) return;
+    float gv[8], uv[8], d[8], og[8], ou[8];
+    ld8(g + t * ldg + c, gv);
+    ld8(u + t * ldu + c, uv);
+    ld8(dout + t * f + c, d);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const float sg = sigmoidf_(gv[e]);
+        og[e] = d[e] * uv[e] * sg * (1.f + gv[e] * (1.f - sg));
+        ou[e] = d[e] * gv[e] * sg;
     }
+    st8(dg + t * lddg + c, og);
+    st8(du + t * lddu + c, ou);
 }
 
 // ---------------------------------------------------------------- attention
@@ -190,7 +252,6 @@ struct Tile {
     static constexpr int LDH = HD + 8;      // bf16 row stride of staged tiles (16 B pad)
     static constexpr int LDF = HD + 4;      // fp32 row stride of the epilogue staging tile
     static constexpr int TILE = kBM * LDH;  // bf16 elements per staged tile
-    static constexpr int KS = HD / 16;      // k-steps over the head dim
 };
 
 __device__ __forceinline__ void seq_range(const AttnArgs& a, int s, int& start, int& len) {
@@ -484,8 +545,9 @@ __global__ void __launch_bounds__(kTcThreads) attn_fwd_kernel(AttnArgs a) {
 }
 
 // dst = RoPE(src) for n_heads heads of every row (pos = row - its sequence start;
-// rows past len are zeroed): one CTA per (64-row tile, sequence); each angle is
-// computed once and applied to every head.
+// rows past len are zeroed): one CTA per (64-row tile, sequence); each thread
+// owns 8 consecutive rotation pairs (16-byte accesses) and applies their
+// angles to every head.
 __global__ void attn_rope_kernel(AttnArgs a, const __nv_bfloat16* __restrict__ src, long long lds, int n_heads, int hd,
                                  __nv_bfloat16* __restrict__ dst, long long ldd) {
     pdl_prologue();
@@ -494,19 +556,30 @@ __global__ void attn_rope_kernel(AttnArgs a, const __nv_bfloat16* __restrict__ s
     const int slot = a.seq_off[blockIdx.y + 1] - start;
     const int r0 = blockIdx.x * kBM;
     if (r0 >= slot) return;
-    const int half = hd / 2;
+    const int half = hd / 2, chunks = half / 8;
     const float lb = log2f(a.rope_base);
-    for (int e = threadIdx.x; e < kBM * half; e += blockDim.x) {
-        const int r = e / half, i = e % half, pos = r0 + r;
+    for (int e = threadIdx.x; e < kBM * chunks; e += blockDim.x) {
+        const int r = e / chunks, i = (e % chunks) * 8, pos = r0 + r;
         if (pos >= slot) continue;
-        float sn = 0.f, cs = 0.f;
-        if (pos < len) sincosf(pos * exp2f(-(2.f * i / hd) * lb), &sn, &cs);
-        const __nv_bfloat16* s = src + (long long)(start + pos) * lds;
-        __nv_bfloat16* d = dst + (long long)(start + pos) * ldd;
+        float sn[8], cs[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            sn[k] = cs[k] = 0.f;  // padding rows -> 0
+            if (pos < len) sincosf(pos * exp2f(-(2.f * (i + k) / hd) * lb), &sn[k], &cs[k]);
+        }
+        const __nv_bfloat16* s = src + (long long)(start + pos) * lds + i;
+        __nv_bfloat16* d = dst + (long long)(start + pos) * ldd + i;
         for (int h = 0; h < n_heads; ++h) {
-            const float x0 = __bfloat162float(s[h * hd + i]), x1 = __bfloat162float(s[h * hd + i + half]);
-            d[h * hd + i] = __float2bfloat16_rn(x0 * cs - x1 * sn);
-            d[h * hd + i + half] = __float2bfloat16_rn(x1 * cs + x0 * sn);
+            float x0[8], x1[8], y0[8], y1[8];
+            ld8(s + h * hd, x0);
+            ld8(s + h * hd + half, x1);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                y0[k] = x0[k] * cs[k] - x1[k] * sn[k];
+                y1[k] = x1[k] * cs[k] + x0[k] * sn[k];
+            }
+            st8(d + h * hd, y0);
+            st8(d + h * hd + half, y1);
         }
     }
 }
@@ -719,6 +792,8 @@ bool ld_ok(long long ld, int cols) { return ld >= cols && (ld % 2) == 0; }
 
 // cp.async staging needs every staged row 16-byte aligned.
 bool rows16(const void* p, long long ld) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0 && (ld % 8) == 0; }
+bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+bool slice_ok(const void* p, long long ld, int f) { return al16(p) && ld % 8 == 0 && ld >= f; }
 
 AttnArgs attn_args(const mlora_attn_desc* d) {
     AttnArgs a{};
@@ -758,34 +833,38 @@ mlora_status mlora_embed(int64_t rows, int32_t h, int32_t V, const int32_t* toke
 
 mlora_status mlora_add_rmsnorm(int64_t rows, int32_t h, const void* x, const void* delta, const void* w, float eps,
                                void* x_out, void* y, float* rstd, void* stream) {
-    if (rows < 1 || h < 1 || !x || !w || !y || !rstd || (delta && !x_out) || !(eps > 0.f)) return MLORA_USAGE;
-    return launch(add_rmsnorm_kernel, dim3(static_cast<unsigned>(rows)), dim3(256), 0, stream, bf(x), bf(delta), bf(w),
-                  static_cast<int>(h), eps, bfw(x_out), bfw(y), rstd) == cudaSuccess
+    if (rows < 1 || h < 8 || !x || !w || !y || !rstd || (delta && !x_out) || !(eps > 0.f)) return MLORA_USAGE;
+    if (h % 8 || h > 16384 || !al16(x) || !al16(w) || !al16(y) || (delta && (!al16(delta) || !al16(x_out))))
+        return MLORA_SHAPE;  // 16-byte rows, row staged in shared memory
+    return launch(add_rmsnorm_kernel, dim3(static_cast<unsigned>(rows)), dim3(256), sizeof(float) * h, stream, bf(x),
+                  bf(delta), bf(w), static_cast<int>(h), eps, bfw(x_out), bfw(y), rstd) == cudaSuccess
                ? MLORA_OK
                : MLORA_CUDA;
 }
 
 mlora_status mlora_rmsnorm_bwd_sum(int64_t rows, int32_t h, int32_t n_dy, const void* const* dy, const void* dres,
                                    const void* x, const void* w, const float* rstd, void* dx, void* stream) {
-    if (rows < 1 || h < 1 || n_dy < 1 || n_dy > 4 || !dy || !x || !w || !rstd || !dx) return MLORA_USAGE;
+    if (rows < 1 || h < 8 || n_dy < 1 || n_dy > 4 || !dy || !x || !w || !rstd || !dx) return MLORA_USAGE;
+    if (h % 8 || h > 16384 || !al16(x) || !al16(w) || !al16(dx) || (dres && !al16(dres))) return MLORA_SHAPE;
     SumArgs a{};
     for (int i = 0; i < n_dy; ++i) {
         if (!dy[i]) return MLORA_USAGE;
+        if (!al16(dy[i])) return MLORA_SHAPE;
         a.dy[i] = bf(dy[i]);
     }
     a.n = n_dy;
-    return launch(rmsnorm_bwd_sum_kernel, dim3(static_cast<unsigned>(rows)), dim3(256), 0, stream, a, bf(dres), bf(x),
-                  bf(w), rstd, static_cast<int>(h), bfw(dx)) == cudaSuccess
+    return launch(rmsnorm_bwd_sum_kernel, dim3(static_cast<unsigned>(rows)), dim3(256), sizeof(float) * h, stream, a,
+                  bf(dres), bf(x), bf(w), rstd, static_cast<int>(h), bfw(dx)) == cudaSuccess
                ? MLORA_OK
                : MLORA_CUDA;
 }
 
 mlora_status mlora_swiglu_fwd(int64_t rows, int32_t f, const void* gate, int64_t ld_gate, const void* up,
                               int64_t ld_up, void* out, void* stream) {
-    if (rows < 1 || f < 1 || !gate || !up || !out || ld_gate < f || ld_up < f) return MLORA_USAGE;
-    const long long n = rows * (long long)f;
-    const unsigned blocks = static_cast<unsigned>(std::min<long long>((n + 255) / 256, 148LL * 16));
-    return launch(swiglu_fwd_kernel, dim3(blocks), dim3(256), 0, stream, n, static_cast<int>(f), bf(gate),
+    if (rows < 1 || f < 1 || !gate || !up || !out || rows > 65535LL * 1024) return MLORA_USAGE;
+    if (f % 8 || !slice_ok(gate, ld_gate, f) || !slice_ok(up, ld_up, f) || !al16(out)) return MLORA_SHAPE;
+    const dim3 grid((f / 8 + 255) / 256, static_cast<unsigned>(rows));
+    return launch(swiglu_fwd_kernel, grid, dim3(256), 0, stream, static_cast<int>(f), bf(gate),
                   static_cast<long long>(ld_gate), bf(up), static_cast<long long>(ld_up), bfw(out)) == cudaSuccess
                ? MLORA_OK
                : MLORA_CUDA;
@@ -794,12 +873,12 @@ mlora_status mlora_swiglu_fwd(int64_t rows, int32_t f, const void* gate, int64_t
 mlora_status mlora_swiglu_bwd(int64_t rows, int32_t f, const void* gate, int64_t ld_gate, const void* up,
                               int64_t ld_up, const void* dout, void* dgate, int64_t ld_dgate, void* dup,
                               int64_t ld_dup, void* stream) {
-    if (rows < 1 || f < 1 || !gate || !up || !dout || !dgate || !dup || ld_gate < f || ld_up < f || ld_dgate < f ||
-        ld_dup < f)
-        return MLORA_USAGE;
-    const long long n = rows * (long long)f;
-    const unsigned blocks = static_cast<unsigned>(std::min<long long>((n + 255) / 256, 148LL * 16));
-    return launch(swiglu_bwd_kernel, dim3(blocks), dim3(256), 0, stream, n, static_cast<int>(f), bf(gate),
+    if (rows < 1 || f < 1 || !gate || !up || !dout || !dgate || !dup) return MLORA_USAGE;
+    if (f % 8 || !slice_ok(gate, ld_gate, f) || !slice_ok(up, ld_up, f) || !al16(dout) ||
+        !slice_ok(dgate, ld_dgate, f) || !slice_ok(dup, ld_dup, f))
+        return MLORA_SHAPE;
+    const dim3 grid((f / 8 + 255) / 256, static_cast<unsigned>(rows));
+    return launch(swiglu_bwd_kernel, grid, dim3(256), 0, stream, static_cast<int>(f), bf(gate),
                   static_cast<long long>(ld_gate), bf(up), static_cast<long long>(ld_up), bf(dout), bfw(dgate),
                   static_cast<long long>(ld_dgate), bfw(dup), static_cast<long long>(ld_dup)) == cudaSuccess
                ? MLORA_OK
@@ -830,7 +909,9 @@ mlora_status mlora_attn_rope(const mlora_attn_desc* d, const void* src, int64_t 
     mlora_status st = check_attn(d);
     if (st != MLORA_OK) return st;
     if (!src || !dst || n_heads < 1 || !(d->rope_base > 1.f)) return MLORA_USAGE;
-    if (!ld_ok(ld_src, n_heads * d->head_dim) || !ld_ok(ld_dst, n_heads * d->head_dim)) return MLORA_SHAPE;
+    if (!ld_ok(ld_src, n_heads * d->head_dim) || !ld_ok(ld_dst, n_heads * d->head_dim) || !rows16(src, ld_src) ||
+        !rows16(dst, ld_dst))
+        return MLORA_SHAPE;
     AttnArgs a = attn_args(d);
     const dim3 grid((d->max_len + kBM - 1) / kBM, d->num_seqs);
     return launch(attn_rope_kernel, grid, dim3(256), 0, stream, a, bf(src), static_cast<long long>(ld_src),

@@ -47,92 +47,122 @@ __device__ __forceinline__ T block_reduce(T v, T* red, bool is_max) {
 }
 
 // ---------------------------------------------------------------- masked CE
-// One CTA per row.  The row (V bf16) is read from HBM once into shared memory,
-// max / sum-exp are reduced from smem, then dlogits = (softmax - onehot) / n_j
-// is written (0 for pad rows).  bytes/row: 2V read + 2V write.
-__global__ void masked_ce_kernel(const __nv_bfloat16* __restrict__ logits, int V, const int* __restrict__ labels,
-                                 const uint8_t* __restrict__ mask, const int* __restrict__ seg, int J,
-                                 float* __restrict__ row_loss, __nv_bfloat16* __restrict__ dlogits) {
-    pdl_prologue();
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    __nv_bfloat16* srow = reinterpret_cast<__nv_bfloat16*>(smem_raw);
-    __shared__ float red[32];
-    const int row = blockIdx.x;
-    const bool real = mask == nullptr || mask[row] != 0;
-    const __nv_bfloat16* src = logits + (long long)row * V;
-    // stage the row (16-byte vectors when aligned)
-    float mx = -INFINITY;
-    if ((V & 7) == 0) {
-        const uint4* s4 = reinterpret_cast<const uint4*>(src);
-        uint4* d4 = reinterpret_cast<uint4*>(srow);
-        for (int i = threadIdx.x; i < V / 8; i += blockDim.x) {
-            const uint4 w = s4[i];
-            d4[i] = w;
-            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const float2 f = __bfloat1622float2(h[e]);
-                mx = fmaxf(mx, fmaxf(f.x, f.y));
-            }
-        }
-    } else {
-        for (int i = threadIdx.x; i < V; i += blockDim.x) {
-            srow[i] = src[i];
-            mx = fmaxf(mx, __bfloat162float(src[i]));
-        }
-    }
-    mx = block_reduce(mx, red, true);
-    float se = 0.f;
-    for (int i = threadIdx.x; i < V; i += blockDim.x) se += __expf(__bfloat162float(srow[i]) - mx);
-    se = block_reduce(se, red, false);
-    const float lse = mx + __logf(se);
-    const int label = labels[row];
-    if (threadIdx.x == 0) row_loss[row] = real ? lse - __bfloat162float(srow[label]) : 0.f;
-    if (dlogits) {
-        // per-row gradient of the row loss; the per-job mean's 1/n_j is applied by
-        // scale_rows_kernel once segment_mean_kernel has counted the real rows
-        __nv_bfloat16* dst = dlogits + (long long)row * V;
-        const float keep = real ? 1.f : 0.f;
-        for (int i = threadIdx.x; i < V; i += blockDim.x) {
-            const float p = __expf(__bfloat162float(srow[i]) - lse);
-            dst[i] = __float2bfloat16_rn(keep * (p - (i == label ? 1.f : 0.f)));
-        }
-    }
-    (void)seg;
-    (void)J;
-}
-
-// loss[j] = sum of row_loss over job j's real rows / max(1, #real rows): fixed order.
-__global__ void segment_mean_kernel(const float* __restrict__ row_loss, const uint8_t* __restrict__ mask,
-                                    const int* __restrict__ seg, float* __restrict__ loss,
-                                    float* __restrict__ inv_count) {
+// Three launches: per-job real-row counts (inv_count, needed by the row pass),
+// the row pass, and the per-job mean.  Row pass: a persistent grid, one row per
+// CTA at a time; pass 1 streams the row from HBM once with 16-byte loads and an
+// online (max, sum-exp); pass 2 re-reads it (L2-resident: at most
+// gridDim.x rows are open) and writes dlogits = (softmax - onehot) / n_j
+// (0 on pad rows), rounded once.  bytes/row: 2V read (+ 2V write for dlogits).
+__global__ void ce_count_kernel(const uint8_t* __restrict__ mask, const int* __restrict__ seg,
+                                float* __restrict__ inv_count) {
     pdl_prologue();
     __shared__ float red[32];
     const int j = blockIdx.x;
-    float acc = 0.f, cnt = 0.f;
-    for (int r = seg[j] + threadIdx.x; r < seg[j + 1]; r += blockDim.x) {
-        acc += row_loss[r];
-        cnt += (mask == nullptr || mask[r]) ? 1.f : 0.f;
-    }
-    acc = block_reduce(acc, red, false);
+    float cnt = 0.f;
+    for (int r = seg[j] + threadIdx.x; r < seg[j + 1]; r += blockDim.x) cnt += (mask == nullptr || mask[r]) ? 1.f : 0.f;
     cnt = block_reduce(cnt, red, false);
-    if (threadIdx.x == 0) {
-        loss[j] = cnt > 0.f ? acc / cnt : 0.f;
-        if (inv_count) inv_count[j] = cnt > 0.f ? 1.f / cnt : 0.f;
+    if (threadIdx.x == 0) inv_count[j] = cnt > 0.f ? 1.f / cnt : 0.f;
+}
+
+__device__ __forceinline__ void ms_merge(float& m, float& s, float m2, float s2) {
+    const float mn = fmaxf(m, m2);
+    if (mn == -INFINITY) return;
+    s = (m == -INFINITY ? 0.f : s * __expf(m - mn)) + (m2 == -INFINITY ? 0.f : s2 * __expf(m2 - mn));
+    m = mn;
+}
+
+__global__ void __launch_bounds__(256) ce_rows_kernel(const __nv_bfloat16* __restrict__ logits, int V,
+                                                      const int* __restrict__ labels, const uint8_t* __restrict__ mask,
+                                                      const int* __restrict__ seg, int J,
+                                                      const float* __restrict__ inv_count, long long rows,
+                                                      float* __restrict__ row_loss, __nv_bfloat16* __restrict__ dlogits) {
+    pdl_prologue();
+    __shared__ float rm[8], rs[8];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const bool vec = (V & 7) == 0;
+    for (long long row = blockIdx.x; row < rows; row += gridDim.x) {
+        const __nv_bfloat16* src = logits + row * V;
+        float m = -INFINITY, sum = 0.f;
+        if (vec) {
+            const uint4* s4 = reinterpret_cast<const uint4*>(src);
+#pragma unroll 4
+            for (int i = threadIdx.x; i < V / 8; i += blockDim.x) {
+                const uint4 u = s4[i];
+                const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+                float f[8];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float2 x = __bfloat1622float2(h[e]);
+                    f[2 * e] = x.x, f[2 * e + 1] = x.y;
+                }
+                float cm = f[0];
+#pragma unroll
+                for (int e = 1; e < 8; ++e) cm = fmaxf(cm, f[e]);
+                float cs = 0.f;
+#pragma unroll
+                for (int e = 0; e < 8; ++e) cs += __expf(f[e] - cm);
+                ms_merge(m, sum, cm, cs);
+            }
+        } else {
+            for (int i = threadIdx.x; i < V; i += blockDim.x) ms_merge(m, sum, __bfloat162float(src[i]), 1.f);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, sum, o);
+            ms_merge(m, sum, m2, s2);
+        }
+        if (lane == 0) rm[w] = m, rs[w] = sum;
+        __syncthreads();
+        m = rm[0], sum = rs[0];
+        for (int k = 1; k < static_cast<int>(blockDim.x >> 5); ++k) ms_merge(m, sum, rm[k], rs[k]);
+        __syncthreads();  // rm / rs are reused by the next row
+        const float lse = m + __logf(sum);
+        const bool real = mask == nullptr || mask[row] != 0;
+        const int label = labels[row];
+        if (threadIdx.x == 0) row_loss[row] = real ? lse - __bfloat162float(src[label]) : 0.f;
+        if (!dlogits) continue;
+        int j = 0;
+        for (int t = 1; t < J; ++t)
+            if (seg[t] <= row) j = t;
+        const float sc = real ? inv_count[j] : 0.f;
+        __nv_bfloat16* dst = dlogits + row * V;
+        if (vec) {
+            const uint4* s4 = reinterpret_cast<const uint4*>(src);
+            uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll 4
+            for (int i = threadIdx.x; i < V / 8; i += blockDim.x) {
+                const uint4 u = s4[i];
+                const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+                uint4 o;
+                uint32_t* ow = &o.x;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float2 x = __bfloat1622float2(h[e]);
+                    const int c = i * 8 + 2 * e;
+                    const float g0 = sc * (__expf(x.x - lse) - (c == label ? 1.f : 0.f));
+                    const float g1 = sc * (__expf(x.y - lse) - (c + 1 == label ? 1.f : 0.f));
+                    const __nv_bfloat162 r = __floats2bfloat162_rn(g0, g1);
+                    ow[e] = *reinterpret_cast<const uint32_t*>(&r);
+                }
+                d4[i] = o;
+            }
+        } else {
+            for (int i = threadIdx.x; i < V; i += blockDim.x)
+                dst[i] = __float2bfloat16_rn(sc * (__expf(__bfloat162float(src[i]) - lse) - (i == label ? 1.f : 0.f)));
+        }
     }
 }
 
-// dlogits of job j's rows *= 1/n_j  (so dlogits = d mean_j / d logits)
-__global__ void scale_rows_kernel(__nv_bfloat16* __restrict__ d, long long V, const int* __restrict__ seg, int J,
-                                  const float* __restrict__ inv_count) {
+// loss[j] = (sum of row_loss over job j's rows) * inv_count[j]: fixed order.
+__global__ void ce_loss_kernel(const float* __restrict__ row_loss, const int* __restrict__ seg,
+                               const float* __restrict__ inv_count, float* __restrict__ loss) {
     pdl_prologue();
-    const int row = blockIdx.x;
-    int j = 0;
-    for (int t = 1; t < J; ++t)
-        if (seg[t] <= row) j = t;
-    const float s = inv_count[j];
-    __nv_bfloat16* p = d + row * V;
-    for (long long i = threadIdx.x; i < V; i += blockDim.x) p[i] = __float2bfloat16_rn(s * __bfloat162float(p[i]));
+    __shared__ float red[32];
+    const int j = blockIdx.x;
+    float acc = 0.f;
+    for (int r = seg[j] + threadIdx.x; r < seg[j + 1]; r += blockDim.x) acc += row_loss[r];
+    acc = block_reduce(acc, red, false);
+    if (threadIdx.x == 0) loss[j] = acc * inv_count[j];
 }
 
 // ---------------------------------------------------------------- RMSNorm
@@ -239,22 +269,22 @@ mlora_status mlora_masked_ce(int32_t num_jobs, const int32_t* seg_dev, int64_t r
                              float* inv_count, void* dlogits, void* stream) {
     if (rows < 1 || V < 1 || num_jobs < 1 || !seg_dev || !logits || !labels || !row_loss || !loss || !inv_count)
         return MLORA_USAGE;
-    const size_t smem = static_cast<size_t>(V) * 2;
-    if (smem > 200 * 1024) return MLORA_SHAPE;
-    if (cudaFuncSetAttribute(masked_ce_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem)) != cudaSuccess)
+    if ((reinterpret_cast<uintptr_t>(logits) & 15) || (reinterpret_cast<uintptr_t>(dlogits) & 15))
+        return MLORA_USAGE;  // 16-byte aligned rows (V % 8 == 0 takes the vector path)
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int* seg = static_cast<const int*>(seg_dev);
+    if (launch(ce_count_kernel, dim3(num_jobs), dim3(1024), 0, stream, mask, seg, inv_count) != cudaSuccess)
         return MLORA_CUDA;
-    auto* d = static_cast<__nv_bfloat16*>(dlogits);
-    if (launch(masked_ce_kernel, dim3(static_cast<unsigned>(rows)), dim3(512), smem, stream,
-               static_cast<const __nv_bfloat16*>(logits), static_cast<int>(V), labels, mask,
-               static_cast<const int*>(seg_dev), static_cast<int>(num_jobs), row_loss, d) != cudaSuccess)
+    const unsigned grid = static_cast<unsigned>(std::min<long long>(rows, 4LL * sms));
+    if (launch(ce_rows_kernel, dim3(grid), dim3(256), 0, stream, static_cast<const __nv_bfloat16*>(logits),
+               static_cast<int>(V), labels, mask, seg, static_cast<int>(num_jobs),
+               static_cast<const float*>(inv_count), static_cast<long long>(rows), row_loss,
+               static_cast<__nv_bfloat16*>(dlogits)) != cudaSuccess)
         return MLORA_CUDA;
-    if (launch(segment_mean_kernel, dim3(num_jobs), dim3(1024), 0, stream, static_cast<const float*>(row_loss), mask,
-               static_cast<const int*>(seg_dev), loss, inv_count) != cudaSuccess)
-        return MLORA_CUDA;
-    if (d && launch(scale_rows_kernel, dim3(static_cast<unsigned>(rows)), dim3(256), 0, stream, d,
-                    static_cast<long long>(V), static_cast<const int*>(seg_dev), static_cast<int>(num_jobs),
-                    static_cast<const float*>(inv_count)) != cudaSuccess)
+    if (launch(ce_loss_kernel, dim3(num_jobs), dim3(1024), 0, stream, static_cast<const float*>(row_loss), seg,
+               static_cast<const float*>(inv_count), loss) != cudaSuccess)
         return MLORA_CUDA;
     return MLORA_OK;
 }
