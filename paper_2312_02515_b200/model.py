@@ -164,7 +164,9 @@ class MultiLoraDecoder(AdapterJobsMixin):
     """J LoRA jobs fine-tuning one frozen decoder on fused batches, on one GPU."""
 
     def __init__(self, ctx: F.Context, cfg: DecoderConfig, ranks, scales, lrs, capacity: int, seed: int = 0,
-                 lora_init: str = "random", weight_decay: float = 0.0):
+                 lora_init: str = "random", weight_decay: float = 0.0, frozen: "MultiLoraDecoder | None" = None):
+        """frozen: share another decoder's frozen base (embedding, norms, W0, LM
+        head) instead of initialising one — e.g. to resume jobs on the same base."""
         if capacity < 1:
             raise errors.UsageError("capacity must be >= 1 row")
         self.ctx, self.cfg = ctx, cfg
@@ -183,14 +185,22 @@ class MultiLoraDecoder(AdapterJobsMixin):
 
         h, V, rows = cfg.hidden, cfg.vocab, capacity
         bf = torch.bfloat16
-        self.embed_w = U(V, h).to(bf).to(dev)
-        self.head_w = U(V, h, scale=h ** -0.5).to(bf).to(dev)
-        self.final_norm = (1 + U(h, scale=0.1)).to(bf).to(dev)
+        if frozen is not None and frozen.cfg != cfg:
+            raise errors.ShapeError("frozen base has a different config")
+        if frozen is None:
+            self.embed_w = U(V, h).to(bf).to(dev)
+            self.head_w = U(V, h, scale=h ** -0.5).to(bf).to(dev)
+            self.final_norm = (1 + U(h, scale=0.1)).to(bf).to(dev)
+        else:
+            self.embed_w, self.head_w, self.final_norm = frozen.embed_w, frozen.head_w, frozen.final_norm
         self.layers: list[_Layer] = []
-        for _ in range(cfg.layers):
-            L = _Layer((1 + U(h, scale=0.1)).to(bf).to(dev), (1 + U(h, scale=0.1)).to(bf).to(dev))
+        for li in range(cfg.layers):
+            if frozen is None:
+                L = _Layer((1 + U(h, scale=0.1)).to(bf).to(dev), (1 + U(h, scale=0.1)).to(bf).to(dev))
+            else:
+                L = _Layer(frozen.layers[li].norm1, frozen.layers[li].norm2)
             for name, d, k in cfg.projections():
-                W0 = U(d, k, scale=k ** -0.5).to(bf).to(dev)
+                W0 = U(d, k, scale=k ** -0.5).to(bf).to(dev) if frozen is None else frozen.layers[li].proj[name].W0
                 As = [U(r, k, scale=k ** -0.5).to(dev) for r in self.ranks]
                 if lora_init == "zero_b":
                     Bs = [torch.zeros(d, r, device=dev) for r in self.ranks]

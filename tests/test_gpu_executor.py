@@ -319,3 +319,32 @@ def test_decoder_diverged_job_is_isolated_and_stopped():
     assert [s["job"] for s in tr.stops] == ["j1"] and tr.stops[0]["cause"] == "nan_loss"
     assert ex.jobs[0].done == 6 and ex.jobs[2].done == 6
     assert all(math.isfinite(v) for v in ex.jobs[0].losses + ex.jobs[2].losses)
+
+
+def test_decoder_checkpoint_resume_is_exact(tmp_path):
+    """Decoder jobs saved after 3 steps and resumed into a fresh decoder on the
+    same frozen base continue with bitwise-identical per-job CE (every layer's
+    adapters, AdamW moments and step counts restored; keys 'layer.proj')."""
+    from paper_2312_02515_b200 import fused as F
+    from paper_2312_02515_b200 import model as MD
+
+    ctx = F.Context(0)
+    g = torch.Generator().manual_seed(21)
+    seqs = [[torch.randint(0, 1024, (n,), generator=g).tolist() for n in ns] for ns in ([30, 12], [], [50])]
+    batch = MD.pack_tokens(seqs)
+    a = MD.MultiLoraDecoder(ctx, MD.TINY_CHATGLM2, [8, 16, 8], [2.0, 1.0, 0.5], [1e-2, 5e-3, 2e-2],
+                            capacity=batch.rows, seed=5)
+    for _ in range(3):
+        a.step(batch)
+    paths = [str(tmp_path / f"job{j}.pt") for j in range(3)]
+    for j in range(3):
+        a.save_job(paths[j], j)
+    want = [a.step(batch).clone() for _ in range(2)]
+    b = MD.MultiLoraDecoder(ctx, MD.TINY_CHATGLM2, [8, 16, 8], [2.0, 1.0, 0.5], [1e-2, 5e-3, 2e-2],
+                            capacity=batch.rows, seed=77, frozen=a)
+    for j in range(3):
+        b.load_job(paths[j], j)
+    got = [b.step(batch).clone() for _ in range(2)]
+    torch.cuda.synchronize()
+    assert all(torch.equal(w, g_) for w, g_ in zip(want, got))
+    assert "1.h_to_4h" in torch.load(paths[0])["proj"]
