@@ -244,8 +244,6 @@ struct AttnArgs {
 // MMA rather than tcgen05).  4 warps per CTA, each owning 16 rows of a 64-row
 // tile; 64-column key / query tiles staged in shared memory as bf16 with a
 // padded row stride (conflict-free ldmatrix); RoPE applied while staging.
-constexpr int kWarps = 4;
-constexpr int kTcThreads = 32 * kWarps;
 
 template <int HD>
 struct Tile {
@@ -435,48 +433,75 @@ __device__ __forceinline__ void acc_to_stage(float* st, const float (&acc)[HD / 
     }
 }
 
-template <int HD>
-constexpr size_t attn_smem_fwd() {  // Q + double-buffered (K, V)
-    return sizeof(__nv_bfloat16) * 5 * Tile<HD>::TILE;
-}
-template <int HD>
-constexpr size_t attn_smem_bwd() {  // two fixed tiles + double-buffered pair (+ lse, dsum per buffer)
-    return sizeof(__nv_bfloat16) * 6 * Tile<HD>::TILE + sizeof(float) * 4 * kBM;
-}
-static_assert(2 * Tile<64>::TILE * 2 >= kBM * Tile<64>::LDF * 4, "stage fits two bf16 tiles");
-static_assert(2 * Tile<128>::TILE * 2 >= kBM * Tile<128>::LDF * 4, "stage fits two bf16 tiles");
+// Each CTA owns R rows (R / 16 warps x 16) of the tile it accumulates (queries
+// in the forward and dQ kernels, keys in the dK/dV kernel) and streams the other
+// operand in 64-row tiles, double-buffered.  The forward uses R = 128 (every
+// staged K/V tile feeds 128 query rows); the backward kernels use R = 64, whose
+// larger grids balance better (the MQA dK/dV grid has only kv_heads = 2 heads).
+constexpr int kFwdRows = 128;
+constexpr int kBwdRows = 64;
 
-// Forward: one CTA per (query tile, sequence, head).  Online softmax in the
+template <int HD, int R>
+constexpr size_t attn_smem_fwd() {  // Q (R rows) + double-buffered (K, V) 64-row tiles
+    return sizeof(__nv_bfloat16) * Tile<HD>::LDH * (R + 4 * kBM);
+}
+template <int HD, int R>
+constexpr size_t attn_smem_bwd() {  // two R-row tiles + double-buffered 64-row pair + lse, dsum
+    // (dQ: lse, dsum for R rows; dK/dV: lse, dsum for each of the two 64-row buffers)
+    return sizeof(__nv_bfloat16) * Tile<HD>::LDH * (2 * R + 4 * kBM) + sizeof(float) * 4 * (R > kBM ? R : kBM);
+}
+// the fp32 epilogue stage (R x LDF) reuses the double-buffered region
+static_assert(4 * kBM * Tile<64>::LDH * 2 >= kBwdRows * Tile<64>::LDF * 4, "stage fits the streamed buffers");
+static_assert(4 * kBM * Tile<128>::LDH * 2 >= kBwdRows * Tile<128>::LDF * 4, "stage fits the streamed buffers");
+
+template <int HD, int R>
+__device__ __forceinline__ void stage_rows(__nv_bfloat16* dst, const __nv_bfloat16* src, long long ld, int start,
+                                           int r0, int len, int col, float rope_base, bool rope, bool async) {
+#pragma unroll
+    for (int h = 0; h < R / kBM; ++h)
+        stage<HD>(dst + h * kBM * Tile<HD>::LDH, src, ld, start, r0 + h * kBM, len, col, rope_base, rope, async);
+}
+
+template <int HD, int R>
+__device__ __forceinline__ void store_rows(const float* st, __nv_bfloat16* dst, long long ld, int start, int r0,
+                                           int len, int col, int slot, float rope_base, bool rope) {
+#pragma unroll
+    for (int h = 0; h < R / kBM; ++h)
+        store_tile<HD>(st + h * kBM * Tile<HD>::LDF, dst, ld, start, r0 + h * kBM, len, col, slot, rope_base, rope);
+}
+
+// Forward: one CTA per (128-query block, sequence, head).  Online softmax in the
 // log2 domain; O = softmax(scale Q K^T, causal) V; lse in natural log.
-template <int HD>
-__global__ void __launch_bounds__(kTcThreads) attn_fwd_kernel(AttnArgs a) {
+template <int HD, int R>
+__global__ void __launch_bounds__(2 * R, 2) attn_fwd_kernel(AttnArgs a) {
     pdl_prologue();
     int start, len;
     seq_range(a, blockIdx.y, start, len);
     const int slot = a.seq_off[blockIdx.y + 1] - start;
-    const int q0 = blockIdx.x * kBM;
+    const int q0 = blockIdx.x * R;
     if (q0 >= slot) return;
     const int h = blockIdx.z, kvh = h / (a.heads / a.kv_heads);
     constexpr int TILE = Tile<HD>::TILE;
     extern __shared__ __align__(16) __nv_bfloat16 smh[];
-    __nv_bfloat16* Qs = smh;  // then (K, V) x 2 buffers
+    __nv_bfloat16* Qs = smh;
+    __nv_bfloat16* KV = Qs + R * Tile<HD>::LDH;  // (K, V) x 2 buffers
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
     const bool rope = a.rope_in != 0, async = a.vec != 0;
     const float c2 = a.scale * kLog2e;
     auto fetch = [&](int kt) {  // K/V tile kt into buffer kt & 1
-        __nv_bfloat16* Kb = Qs + TILE * (1 + 2 * (kt & 1));
+        __nv_bfloat16* Kb = KV + 2 * TILE * (kt & 1);
         stage<HD>(Kb, a.k, a.ldk, start, kt * kBM, len, kvh * HD, a.rope_base, rope, async);
         stage<HD>(Kb + TILE, a.v, a.ldv, start, kt * kBM, len, kvh * HD, a.rope_base, false, async);
         cp_async_commit();
     };
 
-    stage<HD>(Qs, a.q, a.ldq, start, q0, len, h * HD, a.rope_base, rope, async);
+    stage_rows<HD, R>(Qs, a.q, a.ldq, start, q0, len, h * HD, a.rope_base, rope, async);
     float m[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
     float o[HD / 8][4];
 #pragma unroll
     for (int n = 0; n < HD / 8; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
     const int qr0 = q0 + warp * 16 + g;  // this thread's rows: qr0 and qr0 + 8
-    const int nkt = q0 < len ? (min(q0 + kBM, len) + kBM - 1) / kBM : 0;
+    const int nkt = q0 < len ? (min(q0 + R, len) + kBM - 1) / kBM : 0;
     if (nkt > 0) fetch(0);
     for (int kt = 0; kt < nkt; ++kt) {
         if (kt + 1 < nkt) {
@@ -486,45 +511,48 @@ __global__ void __launch_bounds__(kTcThreads) attn_fwd_kernel(AttnArgs a) {
             cp_async_wait<0>();
         }
         __syncthreads();
-        const __nv_bfloat16* Ks = Qs + TILE * (1 + 2 * (kt & 1));
-        const __nv_bfloat16* Vs = Ks + TILE;
-        float s[8][4];
-        mma_xyT<HD>(s, Qs, Ks, warp, lane);
+        // a warp whose 16 queries all precede this key tile has nothing to add
+        if (kt * kBM <= q0 + warp * 16 + 15) {
+            const __nv_bfloat16* Ks = KV + 2 * TILE * (kt & 1);
+            const __nv_bfloat16* Vs = Ks + TILE;
+            float s[8][4];
+            mma_xyT<HD>(s, Qs, Ks, warp, lane);
 #pragma unroll
-        for (int hr = 0; hr < 2; ++hr) {  // rows g (hr 0) and g + 8 (hr 1)
-            const int qi = qr0 + 8 * hr;
-            float mx = -INFINITY;
+            for (int hr = 0; hr < 2; ++hr) {  // rows g (hr 0) and g + 8 (hr 1)
+                const int qi = qr0 + 8 * hr;
+                float mx = -INFINITY;
 #pragma unroll
-            for (int n = 0; n < 8; ++n)
+                for (int n = 0; n < 8; ++n)
 #pragma unroll
-                for (int c = 0; c < 2; ++c) {
-                    const int kj = kt * kBM + n * 8 + 2 * t + c;
-                    float& v = s[n][2 * hr + c];
-                    v = (kj <= qi && qi < len) ? v * c2 : -INFINITY;
-                    mx = fmaxf(mx, v);
+                    for (int c = 0; c < 2; ++c) {
+                        const int kj = kt * kBM + n * 8 + 2 * t + c;
+                        float& v = s[n][2 * hr + c];
+                        v = (kj <= qi && qi < len) ? v * c2 : -INFINITY;
+                        mx = fmaxf(mx, v);
+                    }
+                mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+                mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+                const float mn = fmaxf(m[hr], mx);
+                const float alpha = mn == -INFINITY ? 1.f : exp2f(m[hr] - mn);
+                float ps = 0.f;
+#pragma unroll
+                for (int n = 0; n < 8; ++n)
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        float& v = s[n][2 * hr + c];
+                        v = mn == -INFINITY ? 0.f : exp2f(v - mn);
+                        ps += v;
+                    }
+                l[hr] = l[hr] * alpha + ps;
+                m[hr] = mn;
+#pragma unroll
+                for (int n = 0; n < HD / 8; ++n) {
+                    o[n][2 * hr] *= alpha;
+                    o[n][2 * hr + 1] *= alpha;
                 }
-            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-            const float mn = fmaxf(m[hr], mx);
-            const float alpha = mn == -INFINITY ? 1.f : exp2f(m[hr] - mn);
-            float ps = 0.f;
-#pragma unroll
-            for (int n = 0; n < 8; ++n)
-#pragma unroll
-                for (int c = 0; c < 2; ++c) {
-                    float& v = s[n][2 * hr + c];
-                    v = mn == -INFINITY ? 0.f : exp2f(v - mn);
-                    ps += v;
-                }
-            l[hr] = l[hr] * alpha + ps;
-            m[hr] = mn;
-#pragma unroll
-            for (int n = 0; n < HD / 8; ++n) {
-                o[n][2 * hr] *= alpha;
-                o[n][2 * hr + 1] *= alpha;
             }
+            mma_pz<HD>(o, s, Vs, lane);
         }
-        mma_pz<HD>(o, s, Vs, lane);
         __syncthreads();  // buffer kt & 1 is refilled by the next iteration's fetch
     }
 #pragma unroll
@@ -600,50 +628,51 @@ __global__ void attn_dsum_kernel(AttnArgs a, int hd) {
     if (lane == 0) a.dsum[(long long)h * a.rows + t] = s;
 }
 
-__device__ __forceinline__ void load_stats(const AttnArgs& a, int h, int start, int q0, int len, float* lse2,
+__device__ __forceinline__ void load_stats(const AttnArgs& a, int h, int start, int q0, int n, int len, float* lse2,
                                            float* dsm) {
-    for (int r = threadIdx.x; r < kBM; r += blockDim.x) {
+    for (int r = threadIdx.x; r < n; r += blockDim.x) {
         const bool ok = q0 + r < len;
         lse2[r] = ok ? a.lse[(long long)h * a.rows + start + q0 + r] * kLog2e : 0.f;
         dsm[r] = ok ? a.dsum[(long long)h * a.rows + start + q0 + r] : 0.f;
     }
 }
 
-// dK, dV: one CTA per (key tile, sequence, K/V head); loops over the query heads
-// of its group and the query tiles at or after the key tile (causal), so the
-// GQA / MQA head sum is a fixed-order register accumulation.  Each warp owns
+// dK, dV: one CTA per (128-key block, sequence, K/V head); loops over the query
+// heads of its group and the 64-query tiles that can see the block (causal), so
+// the GQA / MQA head sum is a fixed-order register accumulation.  Each warp owns
 // 16 keys and computes the transposed products directly (S^T = K Q^T,
 // dP^T = V dO^T), so P^T and dS^T are A operands straight from registers.
-template <int HD>
-__global__ void __launch_bounds__(kTcThreads) attn_bwd_dkv_kernel(AttnArgs a) {
+template <int HD, int R>
+__global__ void __launch_bounds__(2 * R) attn_bwd_dkv_kernel(AttnArgs a) {
     pdl_prologue();
     int start, len;
     seq_range(a, blockIdx.y, start, len);
     const int slot = a.seq_off[blockIdx.y + 1] - start;
-    const int k0 = blockIdx.x * kBM;
+    const int k0 = blockIdx.x * R;
     if (k0 >= slot) return;
     const int kvh = blockIdx.z, group = a.heads / a.kv_heads;
     constexpr int TILE = Tile<HD>::TILE;
     extern __shared__ __align__(16) __nv_bfloat16 smh[];
     __nv_bfloat16* Ks = smh;
-    __nv_bfloat16* Vs = Ks + TILE;  // then (Q, dO) x 2 buffers, then (lse, dsum) x 2
-    float* stats = reinterpret_cast<float*>(Vs + 5 * TILE);
+    __nv_bfloat16* Vs = Ks + R * Tile<HD>::LDH;
+    __nv_bfloat16* QD = Vs + R * Tile<HD>::LDH;  // (Q, dO) x 2 buffers, then (lse, dsum) x 2
+    float* stats = reinterpret_cast<float*>(QD + 4 * TILE);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
     const bool rope = a.rope_in != 0, async = a.vec != 0;
     const float c2 = a.scale * kLog2e;
-    const int qt0 = k0 / kBM, nq = (len + kBM - 1) / kBM - qt0;  // query tiles at or after the key tile
+    const int qt0 = k0 / kBM, nq = (len + kBM - 1) / kBM - qt0;  // query tiles at or after the key block
     const int nit = nq > 0 ? group * nq : 0;                       // (query head, query tile) pairs
     auto fetch = [&](int it) {
         const int h = kvh * group + it / nq, q0 = (qt0 + it % nq) * kBM, b = it & 1;
-        __nv_bfloat16* Qb = Vs + TILE * (1 + 2 * b);
+        __nv_bfloat16* Qb = QD + 2 * TILE * b;
         stage<HD>(Qb, a.q, a.ldq, start, q0, len, h * HD, a.rope_base, rope, async);
         stage<HD>(Qb + TILE, a.dO, a.lddo, start, q0, len, h * HD, a.rope_base, false, async);
-        load_stats(a, h, start, q0, len, stats + b * 2 * kBM, stats + b * 2 * kBM + kBM);
+        load_stats(a, h, start, q0, kBM, len, stats + b * 2 * kBM, stats + b * 2 * kBM + kBM);
         cp_async_commit();
     };
 
-    stage<HD>(Ks, a.k, a.ldk, start, k0, len, kvh * HD, a.rope_base, rope, async);
-    stage<HD>(Vs, a.v, a.ldv, start, k0, len, kvh * HD, a.rope_base, false, async);
+    stage_rows<HD, R>(Ks, a.k, a.ldk, start, k0, len, kvh * HD, a.rope_base, rope, async);
+    stage_rows<HD, R>(Vs, a.v, a.ldv, start, k0, len, kvh * HD, a.rope_base, false, async);
     float dk[HD / 8][4], dv[HD / 8][4];
 #pragma unroll
     for (int n = 0; n < HD / 8; ++n)
@@ -660,76 +689,80 @@ __global__ void __launch_bounds__(kTcThreads) attn_bwd_dkv_kernel(AttnArgs a) {
         }
         __syncthreads();
         const int q0 = (qt0 + it % nq) * kBM, b = it & 1;
-        const __nv_bfloat16* Qs = Vs + TILE * (1 + 2 * b);
-        const __nv_bfloat16* dOs = Qs + TILE;
-        const float* lse2 = stats + b * 2 * kBM;
-        const float* dsm = lse2 + kBM;
-        float p[8][4];
-        mma_xyT<HD>(p, Ks, Qs, warp, lane);  // S^T: rows = keys, cols = queries
+        // a warp whose 16 keys all follow this query tile sees only masked pairs
+        if (k0 + warp * 16 <= q0 + kBM - 1) {
+            const __nv_bfloat16* Qs = QD + 2 * TILE * b;
+            const __nv_bfloat16* dOs = Qs + TILE;
+            const float* lse2 = stats + b * 2 * kBM;
+            const float* dsm = lse2 + kBM;
+            float p[8][4];
+            mma_xyT<HD>(p, Ks, Qs, warp, lane);  // S^T: rows = keys, cols = queries
 #pragma unroll
-        for (int n = 0; n < 8; ++n)
+            for (int n = 0; n < 8; ++n)
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int kj = kr0 + 8 * (e >> 1), cq = n * 8 + 2 * t + (e & 1), qi = q0 + cq;
-                p[n][e] = (kj <= qi && qi < len) ? exp2f(p[n][e] * c2 - lse2[cq]) : 0.f;
-            }
-        mma_pz<HD>(dv, p, dOs, lane);          // dV += P^T dO
-        float ds[8][4];
-        mma_xyT<HD>(ds, Vs, dOs, warp, lane);  // dP^T = V dO^T
+                for (int e = 0; e < 4; ++e) {
+                    const int kj = kr0 + 8 * (e >> 1), cq = n * 8 + 2 * t + (e & 1), qi = q0 + cq;
+                    p[n][e] = (kj <= qi && qi < len) ? exp2f(p[n][e] * c2 - lse2[cq]) : 0.f;
+                }
+            mma_pz<HD>(dv, p, dOs, lane);          // dV += P^T dO
+            float ds[8][4];
+            mma_xyT<HD>(ds, Vs, dOs, warp, lane);  // dP^T = V dO^T
 #pragma unroll
-        for (int n = 0; n < 8; ++n)
+            for (int n = 0; n < 8; ++n)
 #pragma unroll
-            for (int e = 0; e < 4; ++e) ds[n][e] = p[n][e] * (ds[n][e] - dsm[n * 8 + 2 * t + (e & 1)]);
-        mma_pz<HD>(dk, ds, Qs, lane);          // dK += dS^T Q
-        __syncthreads();                       // buffer b is refilled by the next fetch
+                for (int e = 0; e < 4; ++e) ds[n][e] = p[n][e] * (ds[n][e] - dsm[n * 8 + 2 * t + (e & 1)]);
+            mma_pz<HD>(dk, ds, Qs, lane);          // dK += dS^T Q
+        }
+        __syncthreads();                           // buffer b is refilled by the next fetch
     }
     cp_async_wait<0>();
     __syncthreads();
-    float* st = reinterpret_cast<float*>(Vs + TILE);  // the (Q, dO) buffers are free: fp32 staging
+    float* st = reinterpret_cast<float*>(QD);  // the (Q, dO) buffers are free: fp32 staging
     const bool rope_out = a.rope_base > 0.f;
     acc_to_stage<HD>(st, dk, warp, lane, a.scale);
     __syncthreads();
-    store_tile<HD>(st, a.dk, a.lddk, start, k0, len, kvh * HD, slot, a.rope_base, rope_out);
+    store_rows<HD, R>(st, a.dk, a.lddk, start, k0, len, kvh * HD, slot, a.rope_base, rope_out);
     __syncthreads();
     acc_to_stage<HD>(st, dv, warp, lane, 1.f);
     __syncthreads();
-    store_tile<HD>(st, a.dv, a.lddv, start, k0, len, kvh * HD, slot, a.rope_base, false);
+    store_rows<HD, R>(st, a.dv, a.lddv, start, k0, len, kvh * HD, slot, a.rope_base, false);
 }
 
-// dQ: one CTA per (query tile, sequence, head); loops over key tiles 0..qt.
-template <int HD>
-__global__ void __launch_bounds__(kTcThreads) attn_bwd_dq_kernel(AttnArgs a) {
+// dQ: one CTA per (128-query block, sequence, head); loops over the key tiles it sees.
+template <int HD, int R>
+__global__ void __launch_bounds__(2 * R) attn_bwd_dq_kernel(AttnArgs a) {
     pdl_prologue();
     int start, len;
     seq_range(a, blockIdx.y, start, len);
     const int slot = a.seq_off[blockIdx.y + 1] - start;
-    const int q0 = blockIdx.x * kBM;
+    const int q0 = blockIdx.x * R;
     if (q0 >= slot) return;
     const int h = blockIdx.z, kvh = h / (a.heads / a.kv_heads);
     constexpr int TILE = Tile<HD>::TILE;
     extern __shared__ __align__(16) __nv_bfloat16 smh[];
     __nv_bfloat16* Qs = smh;
-    __nv_bfloat16* dOs = Qs + TILE;  // then (K, V) x 2 buffers, then lse, dsum
-    float* lse2 = reinterpret_cast<float*>(dOs + 5 * TILE);
-    float* dsm = lse2 + kBM;
+    __nv_bfloat16* dOs = Qs + R * Tile<HD>::LDH;
+    __nv_bfloat16* KV = dOs + R * Tile<HD>::LDH;  // (K, V) x 2 buffers, then lse, dsum
+    float* lse2 = reinterpret_cast<float*>(KV + 4 * TILE);
+    float* dsm = lse2 + R;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
     const bool rope = a.rope_in != 0, async = a.vec != 0;
     const float c2 = a.scale * kLog2e;
     auto fetch = [&](int kt) {
-        __nv_bfloat16* Kb = dOs + TILE * (1 + 2 * (kt & 1));
+        __nv_bfloat16* Kb = KV + 2 * TILE * (kt & 1);
         stage<HD>(Kb, a.k, a.ldk, start, kt * kBM, len, kvh * HD, a.rope_base, rope, async);
         stage<HD>(Kb + TILE, a.v, a.ldv, start, kt * kBM, len, kvh * HD, a.rope_base, false, async);
         cp_async_commit();
     };
 
-    stage<HD>(Qs, a.q, a.ldq, start, q0, len, h * HD, a.rope_base, rope, async);
-    stage<HD>(dOs, a.dO, a.lddo, start, q0, len, h * HD, a.rope_base, false, async);
-    load_stats(a, h, start, q0, len, lse2, dsm);
+    stage_rows<HD, R>(Qs, a.q, a.ldq, start, q0, len, h * HD, a.rope_base, rope, async);
+    stage_rows<HD, R>(dOs, a.dO, a.lddo, start, q0, len, h * HD, a.rope_base, false, async);
+    load_stats(a, h, start, q0, R, len, lse2, dsm);
     float dq[HD / 8][4];
 #pragma unroll
     for (int n = 0; n < HD / 8; ++n) dq[n][0] = dq[n][1] = dq[n][2] = dq[n][3] = 0.f;
-    const int qrl0 = warp * 16 + g;  // this thread's tile rows: qrl0 and qrl0 + 8
-    const int nkt = q0 < len ? (min(q0 + kBM, len) + kBM - 1) / kBM : 0;
+    const int qrl0 = warp * 16 + g;  // this thread's block rows: qrl0 and qrl0 + 8
+    const int nkt = q0 < len ? (min(q0 + R, len) + kBM - 1) / kBM : 0;
     if (nkt > 0) fetch(0);
     for (int kt = 0; kt < nkt; ++kt) {
         if (kt + 1 < nkt) {
@@ -739,28 +772,30 @@ __global__ void __launch_bounds__(kTcThreads) attn_bwd_dq_kernel(AttnArgs a) {
             cp_async_wait<0>();
         }
         __syncthreads();
-        const __nv_bfloat16* Ks = dOs + TILE * (1 + 2 * (kt & 1));
-        const __nv_bfloat16* Vs = Ks + TILE;
-        float p[8][4], ds[8][4];
-        mma_xyT<HD>(p, Qs, Ks, warp, lane);   // S
-        mma_xyT<HD>(ds, dOs, Vs, warp, lane); // dP
+        if (kt * kBM <= q0 + warp * 16 + 15) {
+            const __nv_bfloat16* Ks = KV + 2 * TILE * (kt & 1);
+            const __nv_bfloat16* Vs = Ks + TILE;
+            float p[8][4], ds[8][4];
+            mma_xyT<HD>(p, Qs, Ks, warp, lane);   // S
+            mma_xyT<HD>(ds, dOs, Vs, warp, lane); // dP
 #pragma unroll
-        for (int n = 0; n < 8; ++n)
+            for (int n = 0; n < 8; ++n)
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const int rl = qrl0 + 8 * (e >> 1), qi = q0 + rl, kj = kt * kBM + n * 8 + 2 * t + (e & 1);
-                const float pv = (kj <= qi && qi < len) ? exp2f(p[n][e] * c2 - lse2[rl]) : 0.f;
-                ds[n][e] = pv * (ds[n][e] - dsm[rl]);
-            }
-        mma_pz<HD>(dq, ds, Ks, lane);          // dQ += dS K
+                for (int e = 0; e < 4; ++e) {
+                    const int rl = qrl0 + 8 * (e >> 1), qi = q0 + rl, kj = kt * kBM + n * 8 + 2 * t + (e & 1);
+                    const float pv = (kj <= qi && qi < len) ? exp2f(p[n][e] * c2 - lse2[rl]) : 0.f;
+                    ds[n][e] = pv * (ds[n][e] - dsm[rl]);
+                }
+            mma_pz<HD>(dq, ds, Ks, lane);          // dQ += dS K
+        }
         __syncthreads();
     }
     cp_async_wait<0>();
     __syncthreads();
-    float* st = reinterpret_cast<float*>(dOs + TILE);  // the (K, V) buffers are free: fp32 staging
+    float* st = reinterpret_cast<float*>(KV);  // the (K, V) buffers are free: fp32 staging
     acc_to_stage<HD>(st, dq, warp, lane, a.scale);
     __syncthreads();
-    store_tile<HD>(st, a.dq, a.lddq, start, q0, len, h * HD, slot, a.rope_base, a.rope_base > 0.f);
+    store_rows<HD, R>(st, a.dq, a.lddq, start, q0, len, h * HD, slot, a.rope_base, a.rope_base > 0.f);
 }
 
 template <typename... KArgs, typename... Args>
@@ -809,13 +844,13 @@ AttnArgs attn_args(const mlora_attn_desc* d) {
 }
 
 template <typename K>
-cudaError_t launch_attn(K kernel, const mlora_attn_desc* d, int heads_z, size_t smem, void* stream,
+cudaError_t launch_attn(K kernel, int rows_per_cta, const mlora_attn_desc* d, int heads_z, size_t smem, void* stream,
                         const AttnArgs& a) {
     if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
         cudaSuccess)
         return cudaErrorInvalidValue;
-    const dim3 grid((d->max_len + kBM - 1) / kBM, d->num_seqs, heads_z);
-    return launch(kernel, grid, dim3(kTcThreads), smem, stream, a);
+    const dim3 grid((d->max_len + rows_per_cta - 1) / rows_per_cta, d->num_seqs, heads_z);
+    return launch(kernel, grid, dim3(2 * rows_per_cta), smem, stream, a);
 }
 
 }  // namespace
@@ -899,8 +934,10 @@ mlora_status mlora_attn_fwd(const mlora_attn_desc* d, const void* q, int64_t ldq
     a.ldq = ldq, a.ldk = ldk, a.ldv = ldv, a.ldout = ldo;
     a.lse = lse;
     a.vec = rows16(q, ldq) && rows16(k, ldk) && rows16(v, ldv);
-    const cudaError_t e = hd == 64 ? launch_attn(attn_fwd_kernel<64>, d, d->heads, attn_smem_fwd<64>(), stream, a)
-                                   : launch_attn(attn_fwd_kernel<128>, d, d->heads, attn_smem_fwd<128>(), stream, a);
+    constexpr int R = kFwdRows;
+    const cudaError_t e =
+        hd == 64 ? launch_attn(attn_fwd_kernel<64, R>, R, d, d->heads, attn_smem_fwd<64, R>(), stream, a)
+                 : launch_attn(attn_fwd_kernel<128, R>, R, d, d->heads, attn_smem_fwd<128, R>(), stream, a);
     return e == cudaSuccess ? MLORA_OK : MLORA_CUDA;
 }
 
@@ -945,12 +982,15 @@ mlora_status mlora_attn_bwd(const mlora_attn_desc* d, const void* q, int64_t ldq
                hd) != cudaSuccess)
         return MLORA_CUDA;
     cudaError_t e;
+    constexpr int R = kBwdRows;
     if (hd == 64) {
-        e = launch_attn(attn_bwd_dkv_kernel<64>, d, d->kv_heads, attn_smem_bwd<64>(), stream, a);
-        if (e == cudaSuccess) e = launch_attn(attn_bwd_dq_kernel<64>, d, d->heads, attn_smem_bwd<64>(), stream, a);
+        e = launch_attn(attn_bwd_dkv_kernel<64, R>, R, d, d->kv_heads, attn_smem_bwd<64, R>(), stream, a);
+        if (e == cudaSuccess)
+            e = launch_attn(attn_bwd_dq_kernel<64, R>, R, d, d->heads, attn_smem_bwd<64, R>(), stream, a);
     } else {
-        e = launch_attn(attn_bwd_dkv_kernel<128>, d, d->kv_heads, attn_smem_bwd<128>(), stream, a);
-        if (e == cudaSuccess) e = launch_attn(attn_bwd_dq_kernel<128>, d, d->heads, attn_smem_bwd<128>(), stream, a);
+        e = launch_attn(attn_bwd_dkv_kernel<128, R>, R, d, d->kv_heads, attn_smem_bwd<128, R>(), stream, a);
+        if (e == cudaSuccess)
+            e = launch_attn(attn_bwd_dq_kernel<128, R>, R, d, d->heads, attn_smem_bwd<128, R>(), stream, a);
     }
     return e == cudaSuccess ? MLORA_OK : MLORA_CUDA;
 }
