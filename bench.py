@@ -372,8 +372,10 @@ def main():
                    "l2": "no flush; per-step working set (7 projections' W0 = 0.39 GB + activations) > 126 MB L2",
                    "flops_per_token": fpt},
         "step_tflops": step_tflops, "step_frac_of_peak": step_tflops / peak,
+        "step_frac_of_sustained_peak": step_tflops / peaks["bf16_sustained"],
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                     "frac_of_sustained": (achieved / peaks["bf16_sustained"]) if achieved else None,
                      "kernel": "mlora_base_pair_kernel (cta_group::2, 256x256 tile) forward: X W0^T + H B^T",
                      "peak_kind": ("sustained" if use_sustained else "burst") + " bf16, " + peaks["source"],
                      "launches": cnt, "avg_launch_us": 1e3 * ms / cnt if cnt else None},
