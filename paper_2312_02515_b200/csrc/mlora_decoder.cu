@@ -185,40 +185,42 @@ __global__ void __launch_bounds__(256) rmsnorm_bwd_sum_kernel(SumArgs a, const _
 // Grid (column chunks of 8 x 256, rows): 16-byte accesses, no integer division.
 __device__ __forceinline__ float sigmoidf_(float g) { return 1.f / (1.f + __expf(-g)); }
 
-__global__ void swiglu_fwd_kernel(int f, const __nv_bfloat16* __restrict__ g, long long ldg,
+__global__ void swiglu_fwd_kernel(long long rows, int f, const __nv_bfloat16* __restrict__ g, long long ldg,
                                   const __nv_bfloat16* __restrict__ u, long long ldu, __nv_bfloat16* __restrict__ out) {
     pdl_prologue();
-    const long long t = blockIdx.y;
     const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
     if (c >= f) return;
-    float gv[8], uv[8], o[8];
-    ld8(g + t * ldg + c, gv);
-    ld8(u + t * ldu + c, uv);
+    for (long long t = blockIdx.y; t < rows; t += gridDim.y) {
+        float gv[8], uv[8], o[8];
+        ld8(g + t * ldg + c, gv);
+        ld8(u + t * ldu + c, uv);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) o[e] = gv[e] * sigmoidf_(gv[e]) * uv[e];
-    st8(out + t * f + c, o);
+        for (int e = 0; e < 8; ++e) o[e] = gv[e] * sigmoidf_(gv[e]) * uv[e];
+        st8(out + t * f + c, o);
+    }
 }
 
-__global__ void swiglu_bwd_kernel(int f, const __nv_bfloat16* __restrict__ g, long long ldg,
+__global__ void swiglu_bwd_kernel(long long rows, int f, const __nv_bfloat16* __restrict__ g, long long ldg,
                                   const __nv_bfloat16* __restrict__ u, long long ldu,
                                   const __nv_bfloat16* __restrict__ dout, __nv_bfloat16* __restrict__ dg,
                                   long long lddg, __nv_bfloat16* __restrict__ du, long long lddu) {
     pdl_prologue();
-    const long long t = blockIdx.y;
     const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
     if (c >= f) return;
-    float gv[8], uv[8], d[8], og[8], ou[8];
-    ld8(g + t * ldg + c, gv);
-    ld8(u + t * ldu + c, uv);
-    ld8(dout + t * f + c, d);
+    for (long long t = blockIdx.y; t < rows; t += gridDim.y) {
+        float gv[8], uv[8], d[8], og[8], ou[8];
+        ld8(g + t * ldg + c, gv);
+        ld8(u + t * ldu + c, uv);
+        ld8(dout + t * f + c, d);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-        const float sg = sigmoidf_(gv[e]);
-        og[e] = d[e] * uv[e] * sg * (1.f + gv[e] * (1.f - sg));
-        ou[e] = d[e] * gv[e] * sg;
+        for (int e = 0; e < 8; ++e) {
+            const float sg = sigmoidf_(gv[e]);
+            og[e] = d[e] * uv[e] * sg * (1.f + gv[e] * (1.f - sg));
+            ou[e] = d[e] * gv[e] * sg;
+        }
+        st8(dg + t * lddg + c, og);
+        st8(du + t * lddu + c, ou);
     }
-    st8(dg + t * lddg + c, og);
-    st8(du + t * lddu + c, ou);
 }
 
 // ---------------------------------------------------------------- attention
@@ -815,6 +817,7 @@ cudaError_t launch(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, void* strea
 
 mlora_status check_attn(const mlora_attn_desc* d) {
     if (!d || !d->seq_offsets || d->num_seqs < 1 || d->max_len < 1 || d->rows < 1) return MLORA_USAGE;
+    if (d->num_seqs > 65535 || d->heads > 65535) return MLORA_SHAPE;  // grid y / z
     if (d->heads < 1 || d->kv_heads < 1 || d->heads % d->kv_heads != 0) return MLORA_SHAPE;
     if (d->head_dim != 64 && d->head_dim != 128) return MLORA_SHAPE;
     if (d->rope_base != 0.f && !(d->rope_base > 1.f)) return MLORA_USAGE;
@@ -896,10 +899,11 @@ mlora_status mlora_rmsnorm_bwd_sum(int64_t rows, int32_t h, int32_t n_dy, const 
 
 mlora_status mlora_swiglu_fwd(int64_t rows, int32_t f, const void* gate, int64_t ld_gate, const void* up,
                               int64_t ld_up, void* out, void* stream) {
-    if (rows < 1 || f < 1 || !gate || !up || !out || rows > 65535LL * 1024) return MLORA_USAGE;
+    if (rows < 1 || f < 1 || !gate || !up || !out) return MLORA_USAGE;
     if (f % 8 || !slice_ok(gate, ld_gate, f) || !slice_ok(up, ld_up, f) || !al16(out)) return MLORA_SHAPE;
-    const dim3 grid((f / 8 + 255) / 256, static_cast<unsigned>(rows));
-    return launch(swiglu_fwd_kernel, grid, dim3(256), 0, stream, static_cast<int>(f), bf(gate),
+    const dim3 grid((f / 8 + 255) / 256, static_cast<unsigned>(std::min<int64_t>(rows, 65535)));
+    return launch(swiglu_fwd_kernel, grid, dim3(256), 0, stream, static_cast<long long>(rows), static_cast<int>(f),
+                  bf(gate),
                   static_cast<long long>(ld_gate), bf(up), static_cast<long long>(ld_up), bfw(out)) == cudaSuccess
                ? MLORA_OK
                : MLORA_CUDA;
@@ -912,8 +916,9 @@ mlora_status mlora_swiglu_bwd(int64_t rows, int32_t f, const void* gate, int64_t
     if (f % 8 || !slice_ok(gate, ld_gate, f) || !slice_ok(up, ld_up, f) || !al16(dout) ||
         !slice_ok(dgate, ld_dgate, f) || !slice_ok(dup, ld_dup, f))
         return MLORA_SHAPE;
-    const dim3 grid((f / 8 + 255) / 256, static_cast<unsigned>(rows));
-    return launch(swiglu_bwd_kernel, grid, dim3(256), 0, stream, static_cast<int>(f), bf(gate),
+    const dim3 grid((f / 8 + 255) / 256, static_cast<unsigned>(std::min<int64_t>(rows, 65535)));
+    return launch(swiglu_bwd_kernel, grid, dim3(256), 0, stream, static_cast<long long>(rows), static_cast<int>(f),
+                  bf(gate),
                   static_cast<long long>(ld_gate), bf(up), static_cast<long long>(ld_up), bf(dout), bfw(dgate),
                   static_cast<long long>(ld_dgate), bfw(dup), static_cast<long long>(ld_dup)) == cudaSuccess
                ? MLORA_OK

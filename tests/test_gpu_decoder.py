@@ -320,3 +320,17 @@ def test_training_reduces_each_jobs_loss():
     torch.cuda.synchronize()
     assert last[0] < first[0] - 0.05 and last[1] < first[1] - 0.05, (first, last)
     assert torch.equal(last[2], first[2])
+
+
+def test_swiglu_more_rows_than_grid_y():
+    """Row loops cover batches beyond the 65535 grid-y limit."""
+    from paper_2312_02515_b200 import model_ops as M
+    dev = torch.device("cuda", 0)
+    g = torch.Generator().manual_seed(6)
+    rows, f = 70001, 16
+    gate = torch.randn(rows, f, generator=g).to(torch.bfloat16).to(dev)
+    up = torch.randn(rows, f, generator=g).to(torch.bfloat16).to(dev)
+    a = M.swiglu_fwd(gate, up)
+    ref = torch.nn.functional.silu(gate.float()) * up.float()
+    assert rel(a.float(), ref) < 5e-3
+    assert rel(a[-5:].float(), ref[-5:]) < 5e-3
