@@ -102,3 +102,46 @@ def test_comm_host_entry_points(lib):
         N.check(lib.mlora_broadcast_base(None, 0, None, None, 0, None))
     assert lib.mlora_comm_rank(None) == -1 and lib.mlora_comm_size(None) == -1
     assert lib.mlora_comm_destroy(None) == 0
+
+
+def test_decoder_entry_points_validate_before_device_work(lib):
+    """The decoder-layer entry points reject bad arguments on the host with the
+    reference's error taxonomy before touching the device (fake, never
+    dereferenced device pointers; no GPU needed)."""
+    fake = 1 << 20  # 16-byte aligned, never dereferenced: every call below fails validation first
+    odd = fake + 2  # 2-byte aligned only
+    off = (C.c_int32 * 3)()
+
+    def desc(**kw):
+        d = dict(seq_offsets=C.addressof(off), seq_lens=None, rows=128, num_seqs=2, max_len=64, heads=4,
+                 kv_heads=2, head_dim=64, rope_base=10000.0, softmax_scale=0.125, flags=0)
+        d.update(kw)
+        return N.AttnDescC(**d)
+
+    def st(fn, *a):
+        return fn(*a)
+
+    # attention: shape / usage taxonomy
+    assert st(lib.mlora_attn_fwd, C.byref(desc(kv_heads=3)), fake, 256, fake, 128, fake, 128, fake, 256, fake,
+              None) == 2
+    assert st(lib.mlora_attn_fwd, C.byref(desc(head_dim=96)), fake, 384, fake, 192, fake, 192, fake, 384, fake,
+              None) == 2
+    assert st(lib.mlora_attn_fwd, C.byref(desc(softmax_scale=0.0)), fake, 256, fake, 128, fake, 128, fake, 256,
+              fake, None) == 1
+    assert st(lib.mlora_attn_fwd, C.byref(desc(flags=4)), fake, 256, fake, 128, fake, 128, fake, 256, fake,
+              None) == 1
+    assert st(lib.mlora_attn_fwd, None, fake, 256, fake, 128, fake, 128, fake, 256, fake, None) == 1
+    assert st(lib.mlora_attn_fwd, C.byref(desc()), fake, 100, fake, 128, fake, 128, fake, 256, fake, None) == 2
+    assert st(lib.mlora_attn_rope, C.byref(desc()), odd, 256, 4, fake, 256, None) == 2
+    assert st(lib.mlora_attn_rope, C.byref(desc(rope_base=0.0)), fake, 256, 4, fake, 256, None) == 1
+    # SwiGLU / norms / embedding
+    assert st(lib.mlora_swiglu_fwd, 4, 12, fake, 12, fake, 12, fake, None) == 2          # f % 8
+    assert st(lib.mlora_swiglu_fwd, 4, 16, odd, 16, fake, 16, fake, None) == 2           # misaligned slice
+    assert st(lib.mlora_swiglu_bwd, 4, 16, fake, 16, fake, 16, fake, fake, 8, fake, 16, None) == 2  # ld < f
+    assert st(lib.mlora_add_rmsnorm, 4, 12, fake, None, fake, 1e-6, None, fake, fake, None) == 2
+    assert st(lib.mlora_add_rmsnorm, 4, 16, fake, fake, fake, 1e-6, None, fake, fake, None) == 1  # delta w/o x_out
+    assert st(lib.mlora_add_rmsnorm, 4, 16, fake, None, fake, 0.0, None, fake, fake, None) == 1    # eps
+    dys = (N.vp * 5)(*([fake] * 5))
+    assert st(lib.mlora_rmsnorm_bwd_sum, 4, 16, 5, dys, None, fake, fake, fake, fake, None) == 1   # > 4 inputs
+    assert st(lib.mlora_embed, 4, 12, 10, fake, fake, fake, None) == 1                               # h % 8
+    assert st(lib.mlora_masked_ce, 2, fake, 4, 64, odd, fake, None, fake, fake, fake, None, None) == 1
