@@ -40,7 +40,12 @@ CONFIGS = {
     # name: (shape set, ranks, lrs, sequences per job, tokens per sequence)
     "c2": dict(shapes="llama7b", ranks=[16, 16, 16, 16], lrs=[1e-4, 2e-4, 5e-5, 3e-4], seqs=4, seq_len=512,
                workload="llama7b-layer(q,k,v,o,gate,up,down) x 4 jobs r16, batch 4x512/job, fwd+bwd+AdamW"),
+    # model level (not the headline): BASELINE C4, the whole ChatGLM2-6B-shaped decoder
+    "c4": dict(decoder="chatglm2-6b", ranks=[16] * 6, lrs=[1e-4, 2e-4, 5e-5, 3e-4, 1e-4, 2e-4], seqs=4,
+               seq_len=512, workload="chatglm2-6b decoder (28 layers, MQA, V 65024) x 6 jobs r16, batch 4x512/job, "
+                                     "fwd + per-job masked CE + bwd + AdamW"),
 }
+DECODER_METRIC = "effective (non-pad) tokens/sec, ChatGLM2-6B decoder, 6 fused LoRA jobs (model level, BASELINE C4)"
 
 
 def load_peaks():
@@ -204,6 +209,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
+    if "decoder" in cfg:
+        return run_decoder(args, cfg)
     if args.impl == "reference":
         return run_reference_arm(args, cfg)
 
@@ -388,6 +395,135 @@ def main():
         "clocks": clocks,
         "losses": losses,
         "cpu_baseline": cpu,
+    }
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_decoder(args, cfg):
+    """Model-level bench (--config c4): the whole decoder fine-tuning step per
+    rank (jobs partitioned, frozen base broadcast once from rank 0, no
+    steady-state collective), timed like the headline: CUDA events, max over ranks."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps({"impl": "reference", "unavailable": "the reference has no decoder / model arithmetic "
+                              "(SURVEY.md App. A); its BatchFusion arm is --config c2"}))
+        return 0
+    import torch
+    import torch.distributed as dist
+    from paper_2312_02515_b200 import fused as F
+    from paper_2312_02515_b200 import model as MD
+    from paper_2312_02515_b200 import parallel as PL
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    mc = MD.CONFIGS[cfg["decoder"]]
+    per_job = cfg["seqs"] * cfg["seq_len"]
+    all_ranks, all_lrs = cfg["ranks"] * world, cfg["lrs"] * world
+    mine = PL.partition_jobs([per_job] * len(all_ranks), world)[rank]
+    J = len(mine)
+    g = torch.Generator().manual_seed(100 + rank)
+    seqs = [[torch.randint(0, mc.vocab, (cfg["seq_len"],), generator=g).tolist() for _ in range(cfg["seqs"])]
+            for _ in range(J)]
+    batch = MD.pack_tokens(seqs)
+    ctx = F.Context(dev)
+    m = MD.MultiLoraDecoder(ctx, mc, [all_ranks[j] for j in mine], [2.0] * J, [all_lrs[j] for j in mine],
+                            capacity=batch.rows, seed=1000 + rank)
+    comm, replication = None, "none (1 rank)"
+    if world > 1:
+        try:
+            comm, replication = PL.NativeComm(ctx), "mlora_broadcast_base (one NCCL group)"
+        except Exception as e:
+            replication = f"torch.distributed ({e})"
+        PL.broadcast_base_weights(m.frozen_tensors(), src=0, comm=comm)
+    m.set_batch(batch)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(max(args.warmup, 3)):
+        m.step()
+    barrier()
+    from paper_2312_02515_b200 import model_ops as MO
+    sampler = ClockSampler(dev)
+    launches0 = ctx.launches + MO.LAUNCHES[0]
+    sampler.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        m.step()
+    e1.record(stream)
+    barrier()
+    clocks = sampler.stop()
+    launches = ctx.launches + MO.LAUNCHES[0] - launches0
+    ms_total = PL.max_over_ranks(e0.elapsed_time(e1), device=dev)
+    eff = int(PL.sum_over_ranks(batch.real_tokens, device=dev))
+    value = eff * args.steps / (ms_total / 1e3)
+    # e2e through the public call with host token lists: set_batch (pinned H2D of
+    # tokens / labels / mask / layout) + step + D2H of the per-job losses, every step
+    host_loss = torch.empty(J, dtype=torch.float32).pin_memory()
+    barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(args.steps):
+        host_loss.copy_(m.step(batch), non_blocking=True)
+    f1.record(stream)
+    barrier()
+    e2e_ms = PL.max_over_ranks(f0.elapsed_time(f1), device=dev)
+    # live per-kernel timing of the base GEMM (dominant kernel), a separate pass
+    ctx.profile(reset=True)
+    ctx.set_profiling(True)
+    for _ in range(args.steps):
+        m.step()
+    barrier()
+    ctx.set_profiling(False)
+    prof = ctx.profile(reset=True)
+    flops = m.flops_per_step()
+    peaks = load_peaks()
+    cnt, kms = prof["base_fwd"]
+    lin_fwd = 0
+    for li in range(mc.layers):
+        for _, d, k in mc.projections():
+            lin_fwd += 2 * batch.rows * d * k + 2 * batch.rows * d * cfg["ranks"][0]
+    lin_fwd += 2 * batch.rows * mc.hidden * mc.vocab
+    achieved = lin_fwd * args.steps / (kms / 1e3) / 1e12 if kms > 0 else None
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+    line = {
+        "metric": DECODER_METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms_total / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random tokens/weights, seeded)",
+        "config": {"workload": cfg["workload"], "jobs_per_gpu": J, "tokens_per_step_per_gpu": batch.rows,
+                   "effective_tokens_per_step_per_gpu": batch.real_tokens,
+                   "parallelism": f"adapter-parallel (jobs partitioned) x{world}, frozen base replicated once: "
+                                  f"{replication}", "l2": "no flush; 12.5 GB of frozen weights per step >> L2",
+                   "model_flops_per_step_per_gpu": flops},
+        "step_tflops": flops * world / (ms_total / args.steps / 1e3) / 1e12,
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peaks["bf16_sustained"], "unit": "TFLOP/s",
+                     "frac": achieved / peaks["bf16_sustained"] if achieved else None, "traffic": None,
+                     "frac_of_burst": achieved / peaks["bf16"] if achieved else None,
+                     "kernel": "mlora_base_pair_kernel forward (every LoRA'd linear + the frozen LM head)",
+                     "peak_kind": "sustained bf16, " + peaks["source"], "launches": cnt},
+        "kernel_ms_per_step": {k: round(v[1] / args.steps, 3) for k, v in prof.items()},
+        "e2e": {"value": eff * args.steps / (e2e_ms / 1e3), "unit": UNIT,
+                "h2d_bytes_per_step": 9 * batch.rows + 4 * (2 * len(batch.seq_lens) + 1 + J + 1),
+                "d2h_bytes_per_step": 4 * J, "ms_per_step": e2e_ms / args.steps},
+        "gpu_launches": launches, "clocks": clocks, "losses": host_loss.tolist(),
+        "cpu_baseline": None,
+        "cpu_baseline_note": "the reference has no model arithmetic; its CPU path is per linear (--config c2)",
     }
     print(json.dumps(line))
     if world > 1:

@@ -178,34 +178,34 @@ class MultiLoraDecoder(AdapterJobsMixin):
         dev = ctx.device
         self.plan = F.Plan(ctx, [0] * self.J + [capacity], self.ranks, self.scales)
         R = self.plan.rank_padded
-        g = torch.Generator(device="cpu").manual_seed(seed)
+        g = torch.Generator(device=dev).manual_seed(seed)  # seeded init, generated in HBM
 
         def U(*shape, scale=1.0):
-            return ((torch.rand(*shape, generator=g) * 2 - 1) * scale)
+            return (torch.rand(*shape, generator=g, device=dev) * 2 - 1) * scale
 
         h, V, rows = cfg.hidden, cfg.vocab, capacity
         bf = torch.bfloat16
         if frozen is not None and frozen.cfg != cfg:
             raise errors.ShapeError("frozen base has a different config")
         if frozen is None:
-            self.embed_w = U(V, h).to(bf).to(dev)
-            self.head_w = U(V, h, scale=h ** -0.5).to(bf).to(dev)
-            self.final_norm = (1 + U(h, scale=0.1)).to(bf).to(dev)
+            self.embed_w = U(V, h).to(bf)
+            self.head_w = U(V, h, scale=h ** -0.5).to(bf)
+            self.final_norm = (1 + U(h, scale=0.1)).to(bf)
         else:
             self.embed_w, self.head_w, self.final_norm = frozen.embed_w, frozen.head_w, frozen.final_norm
         self.layers: list[_Layer] = []
         for li in range(cfg.layers):
             if frozen is None:
-                L = _Layer((1 + U(h, scale=0.1)).to(bf).to(dev), (1 + U(h, scale=0.1)).to(bf).to(dev))
+                L = _Layer((1 + U(h, scale=0.1)).to(bf), (1 + U(h, scale=0.1)).to(bf))
             else:
                 L = _Layer(frozen.layers[li].norm1, frozen.layers[li].norm2)
             for name, d, k in cfg.projections():
-                W0 = U(d, k, scale=k ** -0.5).to(bf).to(dev) if frozen is None else frozen.layers[li].proj[name].W0
-                As = [U(r, k, scale=k ** -0.5).to(dev) for r in self.ranks]
+                W0 = U(d, k, scale=k ** -0.5).to(bf) if frozen is None else frozen.layers[li].proj[name].W0
+                As = [U(r, k, scale=k ** -0.5) for r in self.ranks]
                 if lora_init == "zero_b":
                     Bs = [torch.zeros(d, r, device=dev) for r in self.ranks]
                 else:
-                    Bs = [U(d, r, scale=r ** -0.5).to(dev) for r in self.ranks]
+                    Bs = [U(d, r, scale=r ** -0.5) for r in self.ranks]
                 A32, B32, A16, B16 = F.pack_adapters(ctx, self.plan, d, k, As, Bs)
                 L.proj[name] = _Proj(name, d, k, W0, F.AdamState.of(A32, A16, 0), F.AdamState.of(B32, B16, 1),
                                      torch.zeros(R, k, device=dev), torch.zeros(d, R, device=dev),
@@ -238,6 +238,16 @@ class MultiLoraDecoder(AdapterJobsMixin):
         self._row_loss = torch.empty(rows, dtype=torch.float32, device=dev)
         self._inv = torch.empty(self.J, dtype=torch.float32, device=dev)
         self.batch: TokenBatch | None = None
+
+    def frozen_tensors(self) -> dict:
+        """Every frozen base tensor by name (what a multi-GPU run replicates once
+        from rank 0: parallel.broadcast_base_weights)."""
+        out = {"embed": self.embed_w, "head": self.head_w, "final_norm": self.final_norm}
+        for li, L in enumerate(self.layers):
+            out[f"{li}.norm1"], out[f"{li}.norm2"] = L.norm1, L.norm2
+            for name, p in L.proj.items():
+                out[f"{li}.{name}.W0"] = p.W0
+        return out
 
     def named_projections(self):
         """(key, projection) of every LoRA'd linear: keys 'layer.name' (checkpoints, quarantine)."""
@@ -386,6 +396,7 @@ class MultiLoraDecoder(AdapterJobsMixin):
                                         self.labels[:r].data_ptr(), self.mask[:r].data_ptr(),
                                         self._row_loss[:r].data_ptr(), self.loss.data_ptr(), self._inv.data_ptr(),
                                         self.dlogits[:r].data_ptr(), s))
+        M._count(3)
         return self.loss
 
     def _attn_fwd(self, L: _Layer, q, k, v, stream) -> None:
