@@ -334,3 +334,35 @@ def test_swiglu_more_rows_than_grid_y():
     ref = torch.nn.functional.silu(gate.float()) * up.float()
     assert rel(a.float(), ref) < 5e-3
     assert rel(a[-5:].float(), ref[-5:]) < 5e-3
+
+
+def test_attention_long_sequence():
+    """One 2100-token sequence beside a 1-token one: 33 key tiles, multi-block causal, fused RoPE."""
+    from paper_2312_02515_b200 import model_ops as M
+    dev = torch.device("cuda", 0)
+    g = torch.Generator().manual_seed(8)
+    heads, kv, hd = 8, 2, 128
+    offsets, lens = [0, 2100, 2101], [2100, 1]
+    rows = offsets[-1]
+    q = torch.randn(rows, heads * hd, generator=g).to(torch.bfloat16).to(dev)
+    k = torch.randn(rows, kv * hd, generator=g).to(torch.bfloat16).to(dev)
+    v = torch.randn(rows, kv * hd, generator=g).to(torch.bfloat16).to(dev)
+    do = torch.randn(rows, heads * hd, generator=g).to(torch.bfloat16).to(dev)
+    lay = M.AttnLayout(offsets, lens, device=dev)
+    o, lse = M.attn_fwd(lay, q, k, v, heads, kv, hd)
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    M.attn_bwd(lay, q, k, v, o, do, lse, dq, dk, dv, heads, kv, hd)
+    torch.cuda.synchronize()
+    qf, kf, vf = (t.float().clone().requires_grad_(True) for t in (q, k, v))
+    ref = attn_ref(qf, kf, vf, offsets, lens, heads, kv, hd, 10000.0)
+    ref.backward(do.float())
+    assert rel(o.float(), ref) < 1e-2
+    for got, want in ((dq, qf.grad), (dk, kf.grad), (dv, vf.grad)):
+        assert rel(got.float(), want) < 1e-2
+
+
+def test_llama13b_width_layer_matches_torch():
+    """LLaMA-13B widths (h 5120, 40 heads, ffn 13824), one layer, V 32000, ranks 8/16/32/64."""
+    from paper_2312_02515_b200 import model as MD
+    cfg = MD.LLAMA_13B.with_layers(1)
+    run_parity(cfg, [8, 16, 32, 64], [2.0] * 4, [1e-4] * 4, [[90, 33], [128], [7, 64], [200]], padded=False, seed=13)
