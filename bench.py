@@ -419,12 +419,20 @@ def run_decoder(args, cfg):
     from paper_2312_02515_b200 import model as MD
     from paper_2312_02515_b200 import parallel as PL
 
+    share = os.environ.get("MLORA_BENCH_SHARE_GPU") == "1"  # multi-rank logic on a 1-GPU box (gloo)
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if share:
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     mc = MD.CONFIGS[cfg["decoder"]]
+    if os.environ.get("MLORA_BENCH_LAYERS"):  # smaller smoke of the same path (never a reported number)
+        mc = mc.with_layers(int(os.environ["MLORA_BENCH_LAYERS"]))
     per_job = cfg["seqs"] * cfg["seq_len"]
     all_ranks, all_lrs = cfg["ranks"] * world, cfg["lrs"] * world
     mine = PL.partition_jobs([per_job] * len(all_ranks), world)[rank]
@@ -438,10 +446,13 @@ def run_decoder(args, cfg):
                             capacity=batch.rows, seed=1000 + rank)
     comm, replication = None, "none (1 rank)"
     if world > 1:
-        try:
-            comm, replication = PL.NativeComm(ctx), "mlora_broadcast_base (one NCCL group)"
-        except Exception as e:
-            replication = f"torch.distributed ({e})"
+        if not share:
+            try:
+                comm, replication = PL.NativeComm(ctx), "mlora_broadcast_base (one NCCL group)"
+            except Exception as e:
+                replication = f"torch.distributed ({e})"
+        else:
+            replication = "torch.distributed (gloo, shared GPU)"
         PL.broadcast_base_weights(m.frozen_tensors(), src=0, comm=comm)
     m.set_batch(batch)
     stream = torch.cuda.current_stream()
@@ -506,7 +517,8 @@ def run_decoder(args, cfg):
         "metric": DECODER_METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms_total / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random tokens/weights, seeded)",
-        "config": {"workload": cfg["workload"], "jobs_per_gpu": J, "tokens_per_step_per_gpu": batch.rows,
+        "config": {"workload": cfg["workload"].replace("28 layers", f"{mc.layers} layers"), "jobs_per_gpu": J,
+                   "tokens_per_step_per_gpu": batch.rows,
                    "effective_tokens_per_step_per_gpu": batch.real_tokens,
                    "parallelism": f"adapter-parallel (jobs partitioned) x{world}, frozen base replicated once: "
                                   f"{replication}", "l2": "no flush; 12.5 GB of frozen weights per step >> L2",
