@@ -355,3 +355,41 @@ def test_launch_count_independent_of_jobs(F, ctx, J):
     test_launch_count_independent_of_jobs.counts = getattr(test_launch_count_independent_of_jobs, "counts", set())
     test_launch_count_independent_of_jobs.counts.add(per_step)
     assert len(test_launch_count_independent_of_jobs.counts) == 1  # identical for every J
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_randomised_layouts_fuzz(F, ctx, seed):
+    """Random fused layouts vs the oracle: 1-12 jobs with random (possibly empty
+    or 1-row) segments, ranks 1-64, scales, and d, k any multiples of 8 up to
+    600 (K / N tails, R_pad over several 64-column chunks)."""
+    rng = np.random.default_rng(1000 + seed)
+    J = int(rng.integers(1, 13))
+    lens = [int(x) if rng.random() > 0.15 else 0 for x in rng.integers(1, 260, J)]
+    if sum(lens) == 0:
+        lens[0] = 1
+    if seed % 4 == 0:
+        lens[int(rng.integers(J))] = 1
+    seg = [0] + [int(x) for x in np.cumsum(lens)]
+    ranks = [int(x) for x in rng.integers(1, 65, J)]
+    scales = [float(x) for x in rng.choice([0.25, 0.5, 1.0, 2.0, 4.0], J)]
+    lo = -(-max(ranks) // 8)  # rank <= min(d, k) (AdapterWeights::validate, lora.cpp:62-70)
+    d, k = 8 * int(rng.integers(lo, 76)), 8 * int(rng.integers(lo, 76))
+    X, W0, As, Bs, dY = make_case(seg, ranks, d, k, seed=seed)
+    plan, Y, H, dX, dAs, dBs, _ = run_device(F, ctx, seg, ranks, scales, X, W0, As, Bs, dY)
+    A64, B64 = [f64(a) for a in As], [f64(b) for b in Bs]
+    Yr = O.segmented_forward(f64(X), f64(W0), A64, B64, scales, seg)
+    dXr, dAr, dBr = O.segmented_backward(f64(dY), f64(X), f64(W0), A64, B64, scales, seg)
+    ro = plan.rank_offsets
+    Hh = H.float().cpu().numpy()
+    for j in range(J):
+        a, b = seg[j], seg[j + 1]
+        if b == a:
+            assert np.abs(dAs[j]).max() == 0 and np.abs(dBs[j]).max() == 0, (seed, j)
+            continue
+        assert rel(Y[a:b], Yr[a:b]) < TOL, (seed, j)
+        assert rel(dX[a:b], dXr[a:b]) < TOL, (seed, j)
+        assert rel(dAs[j], dAr[j]) < TOL, (seed, j)
+        assert rel(dBs[j], dBr[j]) < TOL, (seed, j)
+        blk = Hh[a:b].copy()
+        blk[:, ro[j]:ro[j] + ranks[j]] = 0
+        assert np.all(blk == 0), (seed, j)
