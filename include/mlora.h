@@ -235,6 +235,23 @@ mlora_status mlora_f64_gemm(int64_t M, int64_t N, int64_t K, const double* A, in
 /* c = a + b elementwise (lora.cpp:36-42), device fp64. */
 mlora_status mlora_f64_add(int64_t n, const double* a, const double* b, double* c, void* stream);
 
+/* Device fuse — replaces the data / mask half of fusim::fuse (lora.hpp:88,
+ * lora.cpp:114-158) for bf16 hidden states that already live in HBM.
+ * Sequence i (FusedBatch order: job order, then sequence order) is copied
+ * from src[i] (device, lens[i] rows, row stride ld_src[i] elements, or dim
+ * when ld_src == NULL) into the fused matrix dst (bf16, dim columns):
+ *   padded = 1: the reference layout — every sequence in a max_len slot,
+ *               max_len = max lens, the slot's tail rows zero-filled;
+ *   padded = 0: packed — real rows back to back.
+ * mask (device uint8, may be NULL) gets 1 on copied rows and 0 on pad rows;
+ * row_offsets (host, num_seqs + 1, may be NULL) receives each sequence's first
+ * row.  USAGE on no sequences / an empty sequence (lora.cpp:115, 131), as the
+ * reference.  A pure copy: bit-exact.  Routing and ξ accounting stay on the
+ * host (mlora_fused_shape_of). */
+mlora_status mlora_fuse_rows(mlora_ctx* ctx, int32_t num_seqs, const void* const* src, const int64_t* ld_src,
+                             const int32_t* lens, int64_t dim, int32_t padded, void* dst, uint8_t* mask,
+                             int64_t* row_offsets, void* stream);
+
 /* Non-finite guard, between the loss and the backward.  For every job j with a
  * non-finite loss[j] (device fp32 [J]), zero its rows seg[j]..seg[j+1] of each
  * bf16 row-major tensor (rows x cols[t]), normally the backward's dY.  The fused

@@ -70,6 +70,8 @@ _SIGS = {
     "mlora_pack_adapters": (i32, [vp, vp, i32, i32, C.POINTER(vp), C.POINTER(vp), vp, vp, vp, vp, vp]),
     "mlora_segment_sumsq_loss": (i32, [vp, vp, C.POINTER(vp), C.POINTER(i32), i32, vp, vp]),
     "mlora_zero_nonfinite_rows": (i32, [vp, vp, vp, C.POINTER(vp), C.POINTER(i32), i32, vp]),
+    "mlora_fuse_rows": (i32, [vp, i32, C.POINTER(vp), C.POINTER(i64), C.POINTER(i32), i64, i32, vp, vp,
+                              C.POINTER(i64), vp]),
     "mlora_adam_step": (i32, [vp, vp, C.POINTER(AdamGroupC), i32, C.POINTER(f32), C.POINTER(i32), f32, f32,
                               f32, f32, vp]),
     "mlora_adam_step_ex": (i32, [vp, vp, C.POINTER(AdamGroupC), i32, C.POINTER(f32), C.POINTER(i32), f32, f32,

@@ -254,6 +254,44 @@ __global__ void zero_nonfinite_rows_kernel(const __grid_constant__ GuardArgs a) 
     }
 }
 
+// ---------------------------------------------------------------- device fuse
+// fusim::fuse (lora.cpp:114-158) for bf16 hidden states on the device:
+// sequence s of the fused batch (job order, then sequence order) is copied from
+// its own buffer to rows off[s] .. off[s] + len[s] of the fused matrix; in the
+// padded layout the slot's remaining rows (to off[s+1]) are zero-filled, and
+// mask[row] = 1 exactly on copied rows.  One CTA per (32-row chunk of a slot,
+// sequence), 16-byte copies.  A pure copy: bit-exact.
+constexpr int kFuseMaxSeqs = 256;  // per launch (kernel parameter table)
+struct FuseArgs {
+    const __nv_bfloat16* src[kFuseMaxSeqs];
+    long long ld[kFuseMaxSeqs];   // source row stride (elements)
+    long long off[kFuseMaxSeqs + 1];
+    int len[kFuseMaxSeqs];
+    int nseq;
+    long long dim;                // elements per row (multiple of 8)
+    __nv_bfloat16* dst;
+    uint8_t* mask;
+};
+
+__global__ void fuse_rows_kernel(const __grid_constant__ FuseArgs a) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int s = blockIdx.y;
+    const long long slot = a.off[s + 1] - a.off[s];
+    const int r0 = blockIdx.x * 32;
+    if (r0 >= slot) return;
+    const int r1 = static_cast<int>(slot < r0 + 32 ? slot : r0 + 32);
+    const int n8 = static_cast<int>(a.dim / 8);
+    const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+    for (int e = threadIdx.x; e < (r1 - r0) * n8; e += blockDim.x) {
+        const int r = r0 + e / n8, c = e % n8;
+        uint4* d = reinterpret_cast<uint4*>(a.dst + (a.off[s] + r) * a.dim) + c;
+        *d = r < a.len[s] ? reinterpret_cast<const uint4*>(a.src[s] + r * a.ld[s])[c] : z;
+    }
+    if (a.mask)
+        for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) a.mask[a.off[s] + r] = r < a.len[s] ? 1 : 0;
+}
+
 __global__ void segment_loss_kernel(const float* __restrict__ row_acc, const int* __restrict__ seg,
                                     float* __restrict__ loss) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");

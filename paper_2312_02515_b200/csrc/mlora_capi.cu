@@ -1281,6 +1281,49 @@ mlora_status mlora_segment_sumsq_loss(mlora_ctx* ctx, const mlora_plan* plan, co
     return MLORA_OK;
 }
 
+mlora_status mlora_fuse_rows(mlora_ctx* ctx, int32_t num_seqs, const void* const* src, const int64_t* ld_src,
+                             const int32_t* lens, int64_t dim, int32_t padded, void* dst, uint8_t* mask,
+                             int64_t* row_offsets, void* stream) {
+    if (!ctx || !src || !lens || !dst) return fail(ctx, MLORA_USAGE, "null argument");
+    if (num_seqs < 1) return fail(ctx, MLORA_USAGE, "fuse: no sequences");  // lora.cpp:115
+    if (dim < 8 || dim % 8) return fail(ctx, MLORA_SHAPE, "fuse: row width must be a positive multiple of 8");
+    if (reinterpret_cast<uintptr_t>(dst) % 16) return fail(ctx, MLORA_USAGE, "tensor base pointer must be 16-byte aligned");
+    int max_len = 0;
+    for (int i = 0; i < num_seqs; ++i) {
+        if (lens[i] < 1) return fail(ctx, MLORA_USAGE, "fuse: empty sequence");  // lora.cpp:131
+        if (!src[i] || reinterpret_cast<uintptr_t>(src[i]) % 16)
+            return fail(ctx, MLORA_USAGE, "fuse: null or misaligned sequence buffer");
+        const long long ld = ld_src ? ld_src[i] : dim;
+        if (ld < dim || ld % 8) return fail(ctx, MLORA_SHAPE, "fuse: source row stride must be >= dim, multiple of 8");
+        max_len = std::max(max_len, lens[i]);
+    }
+    DeviceGuard g(ctx->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    long long base = 0;
+    for (int s0 = 0; s0 < num_seqs; s0 += kFuseMaxSeqs) {
+        FuseArgs a{};
+        a.nseq = std::min(kFuseMaxSeqs, num_seqs - s0);
+        a.dim = dim;
+        a.dst = static_cast<__nv_bfloat16*>(dst);
+        a.mask = mask;
+        a.off[0] = base;
+        int chunk_max = 0;
+        for (int i = 0; i < a.nseq; ++i) {
+            a.src[i] = static_cast<const __nv_bfloat16*>(src[s0 + i]);
+            a.ld[i] = ld_src ? ld_src[s0 + i] : dim;
+            a.len[i] = lens[s0 + i];
+            a.off[i + 1] = a.off[i] + (padded ? max_len : lens[s0 + i]);
+            if (row_offsets) row_offsets[s0 + i] = a.off[i];
+            chunk_max = std::max<int>(chunk_max, static_cast<int>(a.off[i + 1] - a.off[i]));
+        }
+        base = a.off[a.nseq];
+        MLORA_CUDA_TRY(ctx, launch_k(fuse_rows_kernel, dim3(cdiv(chunk_max, 32), a.nseq), dim3(256), 0, s, 1, a));
+        ++ctx->launches;
+    }
+    if (row_offsets) row_offsets[num_seqs] = base;
+    return MLORA_OK;
+}
+
 mlora_status mlora_zero_nonfinite_rows(mlora_ctx* ctx, const mlora_plan* plan, const float* loss,
                                        void* const* tensors, const int32_t* cols, int32_t num_tensors,
                                        void* stream) {

@@ -37,7 +37,11 @@ With `checkpoint_dir`, each job's adapter and AdamW state is saved
 completes or is stopped.
 
 Two step backends.  Default: one transformer layer's LoRA'd projections
-(FusedLoraLayer) on synthetic hidden states, loss L_j = 1/2 sum ||Y||^2.  With
+(FusedLoraLayer) on synthetic hidden states, loss L_j = 1/2 sum ||Y||^2.  Every
+job's dataset items live in HBM (bf16 [len, k], seeded per item, so an epoch
+revisits the same data) and each step's fused batch is built on the device by
+mlora_fuse_rows — the reference's fuse (lora.cpp:114-158), bit-exact — in the
+packed or the padded layout.  With
 `model=DecoderConfig`: the whole decoder (model.MultiLoraDecoder) on each job's
 token sequences, so the per-job losses detect_stop consumes are the real
 padding-masked cross-entropy (K4).  A job's dataset items are then token
@@ -174,6 +178,11 @@ class FusedExecutor:
             self.layer = FusedLoraLayer(ctx, shapes, [j.rank for j in jobs], [j.scale for j in jobs],
                                         [j.lr for j in jobs], rows=capacity, seed=seed, W0=W0)
             self.k_in = shapes[0][2]
+            gen = torch.Generator(device=ctx.device).manual_seed(seed + 1)
+            self.data = [[(torch.rand(n, self.k_in, generator=gen, device=ctx.device) * 2 - 1).to(torch.bfloat16)
+                          for n in j.lengths] for j in jobs]  # each job's dataset, resident in HBM
+            self._x = torch.empty(capacity, self.k_in, dtype=torch.bfloat16, device=ctx.device)
+            self._mask = torch.empty(capacity, dtype=torch.uint8, device=ctx.device)
         else:
             from .model import MultiLoraDecoder
             for j in jobs:
@@ -181,7 +190,6 @@ class FusedExecutor:
                     raise ValueError(f"job {j.id}: token sequences do not match its lengths")
             self.layer = MultiLoraDecoder(ctx, model, [j.rank for j in jobs], [j.scale for j in jobs],
                                           [j.lr for j in jobs], capacity=capacity, seed=seed)
-        self.gen = torch.Generator(device=ctx.device).manual_seed(seed + 1)
         self.trace = Trace()
         self.clock = 0.0
         self._pending = None  # the enqueued step whose time/losses have not been collected yet
@@ -263,17 +271,15 @@ class FusedExecutor:
                 r = lay.seg[in_batch.index(j) + 1]
             seg.append(r)
         active = [j in batches for j in range(len(self.jobs))]
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()  # the measured iteration includes building the fused batch on the device
         if self.model is None:
             self.layer.set_layout(seg)                       # stream-ordered plan update, no host sync
-            x = torch.empty(lay.rows, self.k_in, device=self.ctx.device)
-            x.uniform_(-1.0, 1.0, generator=self.gen)
-            x = x.to(torch.bfloat16)
-            if self.padded:  # pad rows are zero, exactly as fuse() builds them
-                mask = torch.zeros(lay.rows, dtype=torch.bool)
-                for rows in lay.seq_rows:
-                    for r0, L in rows:
-                        mask[r0:r0 + L] = True
-                x[~mask.to(self.ctx.device, non_blocking=True)] = 0
+            seqs = [self.data[j][it] for j in in_batch for it in self.jobs[j].peek_items()]
+            x, _, offs = F.fuse_rows(self.ctx, seqs, padded=self.padded, out=self._x[:lay.rows],
+                                     mask=self._mask[:lay.rows])  # device fuse: pad rows zero as in fuse()
+            if offs[:-1] != [r0 for rows in lay.seq_rows for r0, _ in rows]:
+                raise RuntimeError("device fuse layout disagrees with the packer's layout")
         else:
             from .model import pack_tokens
             seqs = [[self._item_tokens(j, it) for it in self.jobs[j].peek_items()] if j in batches else []
@@ -282,10 +288,8 @@ class FusedExecutor:
             if tb.seg != seg:
                 raise RuntimeError("token layout disagrees with the packer's layout")
             self.layer.set_batch(tb)                         # stream-ordered uploads, no host sync
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         slot = self._loss_host[self._slot]
         self._slot ^= 1
-        e0.record()
         if self.model is None:
             loss = self.layer.step(x, active=active)
         else:

@@ -252,3 +252,31 @@ def adam_step(ctx: Context, plan: Plan, states, grads, lr, step, beta1=0.9, beta
     step_c = (N.i32 * J)(*[int(x) for x in step])
     N.check(N.lib().mlora_adam_step_ex(ctx.handle, plan.handle, groups, len(states), lr_c, step_c, beta1, beta2,
                                        eps, weight_decay, N.ptr(loss_gate), _stream_handle(stream)), ctx.handle)
+
+
+def fuse_rows(ctx: Context, seqs, padded: bool = False, out: torch.Tensor | None = None,
+              mask: torch.Tensor | None = None, stream=None):
+    """Device fuse (mlora_fuse_rows; fusim::fuse, lora.cpp:114-158): copy each
+    sequence's bf16 rows (device tensors [len_i, dim], FusedBatch order) into one
+    fused matrix, packed or in the reference's padded layout (slot = max len,
+    zero tail).  Returns (X [rows, dim], mask uint8 [rows], row offsets [S+1])."""
+    S = len(seqs)
+    if S == 0:
+        raise errors.UsageError("fuse: no sequences")
+    dim = seqs[0].shape[1]
+    lens = [int(t.shape[0]) for t in seqs]
+    rows = S * max(lens) if padded else sum(lens)
+    dev = ctx.device
+    for i, t in enumerate(seqs):
+        if t.dtype != torch.bfloat16 or not t.is_cuda or t.dim() != 2 or t.shape[1] != dim or t.stride(1) != 1:
+            raise errors.ShapeError(f"sequence {i}: needs a bf16 CUDA [len, {dim}] tensor with unit column stride")
+    if out is None:
+        out = torch.empty(rows, dim, dtype=torch.bfloat16, device=dev)
+    if mask is None:
+        mask = torch.empty(rows, dtype=torch.uint8, device=dev)
+    offs = (N.i64 * (S + 1))()
+    N.check(N.lib().mlora_fuse_rows(ctx.handle, S, (N.vp * S)(*[t.data_ptr() for t in seqs]),
+                                    (N.i64 * S)(*[t.stride(0) for t in seqs]), (N.i32 * S)(*lens), dim,
+                                    1 if padded else 0, out.data_ptr(), mask.data_ptr(), offs,
+                                    _stream_handle(stream)), ctx.handle)
+    return out, mask, list(offs)

@@ -393,3 +393,43 @@ def test_randomised_layouts_fuzz(F, ctx, seed):
         blk = Hh[a:b].copy()
         blk[:, ro[j]:ro[j] + ranks[j]] = 0
         assert np.all(blk == 0), (seed, j)
+
+
+@pytest.mark.parametrize("padded", [False, True])
+def test_device_fuse_bitwise_equals_reference_fuse(F, ctx, padded):
+    """mlora_fuse_rows vs the oracle's fuse (lora.cpp:114-158, pinned to the
+    reference): the fused data (bf16 values), mask and per-sequence row offsets
+    are bit-exact, for ragged lengths incl. 1-row sequences, strided sources and
+    more sequences than one launch's table (300 > 256)."""
+    g = torch.Generator().manual_seed(17 if padded else 18)
+    dim = 200
+    lens = [int(x) for x in torch.randint(1, 40, (300,), generator=g)]
+    lens[3] = 1
+    jobs = [0] * 100 + [1] * 150 + [2] * 50
+    big = bf(torch.randn(sum(lens), dim + 16, generator=g))  # strided: row stride dim + 16
+    seqs, r = [], 0
+    for n in lens:
+        seqs.append(big[r:r + n, :dim])
+        r += n
+    dev = ctx.device
+    bigd = big.to(dev)
+    starts = [0] + [int(x) for x in np.cumsum(lens)[:-1]]
+    X, mask, offs = F.fuse_rows(ctx, [bigd[a:a + n, :dim] for a, n in zip(starts, lens)], padded=padded)
+    torch.cuda.synchronize()
+    batches = {}
+    for j, s in zip(jobs, seqs):
+        batches.setdefault(j, []).append(f64(s))
+    fb = O.fuse([(j, batches[j]) for j in sorted(batches)])
+    if padded:
+        assert X.shape[0] == fb.num_sequences * fb.max_len
+        assert np.array_equal(f64(X.float().cpu()), fb.data)
+        assert np.array_equal(mask.cpu().numpy(), fb.mask)
+        assert offs == [i * fb.max_len for i in range(len(lens) + 1)]
+    else:
+        want = np.concatenate([fb.data[i * fb.max_len:i * fb.max_len + n] for i, n in enumerate(lens)])
+        assert np.array_equal(f64(X.float().cpu()), want)
+        assert mask.cpu().numpy().all()
+        assert offs == [0] + [int(x) for x in np.cumsum(lens)]
+    from paper_2312_02515_b200 import errors as E
+    with pytest.raises(E.UsageError):
+        F.fuse_rows(ctx, [])
