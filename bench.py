@@ -266,6 +266,8 @@ def main():
             print(f"[bench] native communicator unavailable ({e}); W0 via torch.distributed", file=sys.stderr)
     PL.broadcast_base_weights(W0, src=0, comm=comm)
     torch.cuda.synchronize()
+    if comm is not None:
+        comm.close()  # the one-off replication is done: the steady state has no collective
 
     layer = FusedLoraLayer(ctx, shapes, ranks_l, [2.0] * J, lrs_l, rows, seed=1000 + rank, W0=W0)
     layer.set_layout(seg)
@@ -454,6 +456,9 @@ def run_decoder(args, cfg):
         else:
             replication = "torch.distributed (gloo, shared GPU)"
         PL.broadcast_base_weights(m.frozen_tensors(), src=0, comm=comm)
+        torch.cuda.synchronize()
+        if comm is not None:
+            comm.close()  # the one-off replication is done: the steady state has no collective
     m.set_batch(batch)
     stream = torch.cuda.current_stream()
 
