@@ -105,7 +105,9 @@ mlora_status mlora_count_launches(int32_t num_jobs, int32_t mode, int64_t* small
  * kernels.  seg_offsets (host, J+1, non-decreasing, seg[0]=0) partitions the
  * `rows = seg[J]` fused rows; ranks/scales (host, J) give r_j >= 1 and s_j.
  * Builds the device tables (segment offsets, padded rank offsets, per-m-tile
- * LoRA k-block ranges, per-chunk token ranges) with one H2D copy on `stream`. */
+ * LoRA k-block ranges, per-chunk token ranges) with one H2D copy on `stream`.
+ * 1 <= num_jobs <= 128 per plan (USAGE otherwise); more jobs than that go to
+ * further plans / GPUs (adapter-parallel, see the multi-GPU section). */
 mlora_status mlora_plan_create(mlora_ctx* ctx, int32_t num_jobs, const int64_t* seg_offsets,
                                const int32_t* ranks, const float* scales, void* stream,
                                mlora_plan** out);
