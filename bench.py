@@ -40,6 +40,12 @@ CONFIGS = {
     # name: (shape set, ranks, lrs, sequences per job, tokens per sequence)
     "c2": dict(shapes="llama7b", ranks=[16, 16, 16, 16], lrs=[1e-4, 2e-4, 5e-5, 3e-4], seqs=4, seq_len=512,
                workload="llama7b-layer(q,k,v,o,gate,up,down) x 4 jobs r16, batch 4x512/job, fwd+bwd+AdamW"),
+    # BASELINE C5: 32 jobs in total on LLaMA-7B shapes, partitioned across the N GPUs
+    # (strong scaling in jobs: 32 / N jobs, 32 / N x 2048 tokens per GPU per step)
+    "c5": dict(shapes="llama7b", ranks=[16] * 32, lrs=[1e-4, 2e-4, 5e-5, 3e-4] * 8, seqs=4, seq_len=512,
+               jobs_total=True,
+               workload="llama7b-layer(q,k,v,o,gate,up,down) x 32 jobs r16 in total (partitioned over the GPUs), "
+                        "batch 4x512/job, fwd+bwd+AdamW"),
     # model level (not the headline): BASELINE C4, the whole ChatGLM2-6B-shaped decoder
     "c4": dict(decoder="chatglm2-6b", ranks=[16] * 6, lrs=[1e-4, 2e-4, 5e-5, 3e-4, 1e-4, 2e-4], seqs=4,
                seq_len=512, workload="chatglm2-6b decoder (28 layers, MQA, V 65024) x 6 jobs r16, batch 4x512/job, "
@@ -128,16 +134,17 @@ def reference_sample(cfg, seq_len=64, seed=1, replicas=1):
     from paper_2312_02515_b200.layer import SHAPES
     rng = np.random.default_rng(seed)
     calls = []
-    J = len(cfg["ranks"])
+    ranks = cfg["ranks"][:4]  # the reference loops per sequence: its cost per token does not depend on J
+    J = len(ranks)
     for _, d, k, _ in SHAPES[cfg["shapes"]]:
         W0 = rng.uniform(-1, 1, (d, k)) / np.sqrt(k)
         w = ref.Weights(W0)
         del W0
-        As = [rng.uniform(-1, 1, (r, k)) for r in cfg["ranks"]]
-        Bs = [rng.uniform(-1, 1, (d, r)) for r in cfg["ranks"]]
+        As = [rng.uniform(-1, 1, (r, k)) for r in ranks]
+        Bs = [rng.uniform(-1, 1, (d, r)) for r in ranks]
         for _ in range(replicas):
             seqs = [(j, rng.uniform(-1, 1, (seq_len, k))) for j in range(J)]
-            calls.append(ref.FusedCall(w, cfg["ranks"], As, Bs, seqs))
+            calls.append(ref.FusedCall(w, ranks, As, Bs, seqs))
     return calls, J * seq_len * replicas
 
 
@@ -170,7 +177,7 @@ def time_reference(cfg, steps, warmup, seq_len=64, budget_s=None):
     total = sum(times)
     return dict(value=tokens * len(times) / total, unit=UNIT, cores=threads, kind="reference",
                 sample=f"reference fusim::fused_forward (fp64, forward only): {replicas} fused sample(s) of "
-                       f"{len(cfg['ranks'])} jobs x 1 seq x {seq_len} tokens per LLaMA-7B projection x {nproj} "
+                       f"{min(4, len(cfg['ranks']))} jobs x 1 seq x {seq_len} tokens per LLaMA-7B projection x {nproj} "
                        f"projections = {tokens} effective tokens per step, {len(calls)} concurrent reference calls "
                        f"on {threads} host threads ({host_threads()} available); {len(times)} timed steps, {total:.1f} s",
                 ms_per_step=1e3 * total / len(times), steps_run=len(times))
@@ -240,8 +247,9 @@ def main():
     shapes = SHAPES[cfg["shapes"]]
     per_job = cfg["seqs"] * cfg["seq_len"]
     # adapter-parallel weak scaling: 4 jobs per GPU (32 jobs at N=8, C5), partitioned by LPT
-    all_ranks = cfg["ranks"] * world
-    all_lrs = cfg["lrs"] * world
+    # weak scaling (default): the config's jobs on every GPU; C5: a fixed job total split over the GPUs
+    all_ranks = cfg["ranks"] * (1 if cfg.get("jobs_total") else world)
+    all_lrs = cfg["lrs"] * (1 if cfg.get("jobs_total") else world)
     mine = PL.partition_jobs([per_job] * len(all_ranks), world)[rank]
     ranks_l, lrs_l = [all_ranks[j] for j in mine], [all_lrs[j] for j in mine]
     J = len(mine)
@@ -372,7 +380,8 @@ def main():
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong" if cfg.get("jobs_total") else "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random tokens/weights, seeded)",
         "config": {"workload": cfg["workload"], "jobs_per_gpu": J, "ranks": cfg["ranks"], "lrs": cfg["lrs"],
                    "tokens_per_step_per_gpu": rows, "effective_tokens_per_step_per_gpu": rows,
