@@ -1,0 +1,34 @@
+"""bench.py's contract on the host side (no GPU): the reference arm of the
+model-level config reports `unavailable` (the reference has no model), the
+config table covers the BASELINE configs the bench measures, and the CLI parses."""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def run(*args):
+    return subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args], capture_output=True, text=True,
+                          timeout=120, cwd=ROOT)
+
+
+def test_reference_arm_of_decoder_config_is_unavailable():
+    r = run("--impl", "reference", "--config", "c4")
+    assert r.returncode == 0, r.stderr
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and "unavailable" in line
+
+
+def test_config_table():
+    sys.path.insert(0, ROOT)
+    import bench
+    assert bench.CONFIGS["c2"]["ranks"] == [16] * 4 and bench.CONFIGS["c2"]["seqs"] * bench.CONFIGS["c2"]["seq_len"] == 2048
+    assert len(bench.CONFIGS["c5"]["ranks"]) == 32 and bench.CONFIGS["c5"]["jobs_total"]
+    assert bench.CONFIGS["c4"]["decoder"] == "chatglm2-6b" and len(bench.CONFIGS["c4"]["ranks"]) == 6
+
+
+def test_help():
+    r = run("--help")
+    assert r.returncode == 0 and "--config" in r.stdout
