@@ -19,12 +19,14 @@
 // 64 x 64 tiles run on the warp-level tensor-core MMA (mma.sync bf16, fp32
 // accumulation), flash-style (no score matrix in HBM), with a deterministic
 // two-kernel backward (dK/dV per key tile, dQ per query tile; no atomics).
+#include <cooperative_groups.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "../../include/mlora.h"
 
@@ -232,6 +234,7 @@ struct AttnArgs {
     float scale;         // softmax scale (1/sqrt(head_dim) normally)
     int rope_in;         // rotate Q/K while staging (they arrive unrotated)
     int vec;             // every staged row is 16-byte aligned: cp.async staging
+    int hsplit;          // dK/dV: query heads of a K/V group split over a cluster of hsplit CTAs
     long long rows;
     const __nv_bfloat16 *q, *k, *v, *o, *dO;
     long long ldq, ldk, ldv, ldo, lddo;
@@ -374,6 +377,39 @@ __device__ void store_tile(const float* srcs, __nv_bfloat16* dst, long long ld, 
     }
 }
 
+// As store_tile for rows [lo, hi) of the tile, each value the sum (in rank
+// order, so deterministic) of the same element of the n fp32 staging tiles
+// `parts` — the partials of a cluster's CTAs, read over distributed shared memory.
+template <int HD>
+__device__ void store_tile_sum(const float* const* parts, int n, __nv_bfloat16* dst, long long ld, int start, int r0,
+                               int lo, int hi, int len, int col, int slot, float rope_base, bool rope) {
+    constexpr int half = HD / 2, LDF = Tile<HD>::LDF;
+    const float lb = rope ? log2f(rope_base) : 0.f;
+    for (int e = threadIdx.x; e < (hi - lo) * (half / 2); e += blockDim.x) {
+        const int r = lo + e / (half / 2), i = (e % (half / 2)) * 2;
+        const int pos = r0 + r;
+        if (pos >= slot) continue;
+        float a0 = 0.f, a1 = 0.f, b0 = 0.f, b1 = 0.f;
+        for (int k = 0; k < n; ++k) {
+            const float* s = parts[k] + r * LDF;
+            a0 += s[i], a1 += s[i + 1], b0 += s[i + half], b1 += s[i + half + 1];
+        }
+        if (pos >= len) {
+            a0 = a1 = b0 = b1 = 0.f;
+        } else if (rope) {
+            float s0, c0, s1, c1;
+            sincosf(pos * exp2f(-(2.f * i / HD) * lb), &s0, &c0);
+            sincosf(pos * exp2f(-(2.f * (i + 1) / HD) * lb), &s1, &c1);
+            const float ra0 = a0 * c0 + b0 * s0, rb0 = b0 * c0 - a0 * s0;  // R(-theta)
+            const float ra1 = a1 * c1 + b1 * s1, rb1 = b1 * c1 - a1 * s1;
+            a0 = ra0, b0 = rb0, a1 = ra1, b1 = rb1;
+        }
+        __nv_bfloat16* p = dst + (long long)(start + pos) * ld + col;
+        *reinterpret_cast<__nv_bfloat162*>(p + i) = __floats2bfloat162_rn(a0, a1);
+        *reinterpret_cast<__nv_bfloat162*>(p + i + half) = __floats2bfloat162_rn(b0, b1);
+    }
+}
+
 // acc[nt][4] (+)= X[warp rows 16][HD] . Y[64 rows][HD]^T  — X, Y staged bf16 tiles;
 // the A operand (this warp's 16 rows of X) and B operand (rows of Y, "col") both
 // come through non-transposed ldmatrix.
@@ -452,9 +488,10 @@ constexpr size_t attn_smem_bwd() {  // two R-row tiles + double-buffered 64-row 
     // (dQ: lse, dsum for R rows; dK/dV: lse, dsum for each of the two 64-row buffers)
     return sizeof(__nv_bfloat16) * Tile<HD>::LDH * (2 * R + 4 * kBM) + sizeof(float) * 4 * (R > kBM ? R : kBM);
 }
-// the fp32 epilogue stage (R x LDF) reuses the double-buffered region
-static_assert(4 * kBM * Tile<64>::LDH * 2 >= kBwdRows * Tile<64>::LDF * 4, "stage fits the streamed buffers");
-static_assert(4 * kBM * Tile<128>::LDH * 2 >= kBwdRows * Tile<128>::LDF * 4, "stage fits the streamed buffers");
+// the fp32 epilogue stage (R x LDF; dK and dV side by side with a head split)
+// reuses the double-buffered region
+static_assert(4 * kBM * Tile<64>::LDH * 2 >= 2 * kBwdRows * Tile<64>::LDF * 4, "stage fits the streamed buffers");
+static_assert(4 * kBM * Tile<128>::LDH * 2 >= 2 * kBwdRows * Tile<128>::LDF * 4, "stage fits the streamed buffers");
 
 template <int HD, int R>
 __device__ __forceinline__ void stage_rows(__nv_bfloat16* dst, const __nv_bfloat16* src, long long ld, int start,
@@ -639,9 +676,13 @@ __device__ __forceinline__ void load_stats(const AttnArgs& a, int h, int start, 
     }
 }
 
-// dK, dV: one CTA per (128-key block, sequence, K/V head); loops over the query
-// heads of its group and the 64-query tiles that can see the block (causal), so
-// the GQA / MQA head sum is a fixed-order register accumulation.  Each warp owns
+// dK, dV: one CTA per (R-key block, sequence, K/V head, head part); loops over
+// its query heads and the 64-query tiles that can see the block (causal).  With
+// grouped / multi-query attention the group's query heads are split over a
+// cluster of hsplit CTAs (ChatGLM2: 16 query heads per K/V head would otherwise
+// leave one long-running CTA per key block and a 2-head grid); the partial
+// dK / dV meet in distributed shared memory and are summed in rank order, so the
+// result is deterministic and nothing round-trips through HBM.  Each warp owns
 // 16 keys and computes the transposed products directly (S^T = K Q^T,
 // dP^T = V dO^T), so P^T and dS^T are A operands straight from registers.
 template <int HD, int R>
@@ -652,7 +693,9 @@ __global__ void __launch_bounds__(2 * R) attn_bwd_dkv_kernel(AttnArgs a) {
     const int slot = a.seq_off[blockIdx.y + 1] - start;
     const int k0 = blockIdx.x * R;
     if (k0 >= slot) return;
-    const int kvh = blockIdx.z, group = a.heads / a.kv_heads;
+    const int kvh = blockIdx.z / a.hsplit, part = blockIdx.z % a.hsplit;  // part = rank in the cluster
+    const int gh = a.heads / a.kv_heads / a.hsplit;                         // query heads of this CTA
+    const int h0 = kvh * (a.heads / a.kv_heads) + part * gh;
     constexpr int TILE = Tile<HD>::TILE;
     extern __shared__ __align__(16) __nv_bfloat16 smh[];
     __nv_bfloat16* Ks = smh;
@@ -663,9 +706,9 @@ __global__ void __launch_bounds__(2 * R) attn_bwd_dkv_kernel(AttnArgs a) {
     const bool rope = a.rope_in != 0, async = a.vec != 0;
     const float c2 = a.scale * kLog2e;
     const int qt0 = k0 / kBM, nq = (len + kBM - 1) / kBM - qt0;  // query tiles at or after the key block
-    const int nit = nq > 0 ? group * nq : 0;                       // (query head, query tile) pairs
+    const int nit = nq > 0 ? gh * nq : 0;                          // (query head, query tile) pairs
     auto fetch = [&](int it) {
-        const int h = kvh * group + it / nq, q0 = (qt0 + it % nq) * kBM, b = it & 1;
+        const int h = h0 + it / nq, q0 = (qt0 + it % nq) * kBM, b = it & 1;
         __nv_bfloat16* Qb = QD + 2 * TILE * b;
         stage<HD>(Qb, a.q, a.ldq, start, q0, len, h * HD, a.rope_base, rope, async);
         stage<HD>(Qb + TILE, a.dO, a.lddo, start, q0, len, h * HD, a.rope_base, false, async);
@@ -721,6 +764,28 @@ __global__ void __launch_bounds__(2 * R) attn_bwd_dkv_kernel(AttnArgs a) {
     __syncthreads();
     float* st = reinterpret_cast<float*>(QD);  // the (Q, dO) buffers are free: fp32 staging
     const bool rope_out = a.rope_base > 0.f;
+    if (a.hsplit > 1) {
+        // dK and dV partials side by side in this CTA's staging; CTA `part` of the
+        // cluster then sums rows [part R / hsplit, (part + 1) R / hsplit) over all
+        // the cluster's partials (DSMEM, rank order) and stores them.
+        namespace cg = cooperative_groups;
+        cg::cluster_group cluster = cg::this_cluster();
+        float* st_v = st + R * Tile<HD>::LDF;
+        acc_to_stage<HD>(st, dk, warp, lane, a.scale);
+        acc_to_stage<HD>(st_v, dv, warp, lane, 1.f);
+        cluster.sync();
+        const float* pk[8];
+        const float* pv[8];
+        for (int k = 0; k < a.hsplit; ++k) {
+            pk[k] = cluster.map_shared_rank(st, k);
+            pv[k] = cluster.map_shared_rank(st_v, k);
+        }
+        const int lo = part * R / a.hsplit, hi = (part + 1) * R / a.hsplit;
+        store_tile_sum<HD>(pk, a.hsplit, a.dk, a.lddk, start, k0, lo, hi, len, kvh * HD, slot, a.rope_base, rope_out);
+        store_tile_sum<HD>(pv, a.hsplit, a.dv, a.lddv, start, k0, lo, hi, len, kvh * HD, slot, a.rope_base, false);
+        cluster.sync();  // the partials stay readable until every CTA of the cluster is done
+        return;
+    }
     acc_to_stage<HD>(st, dk, warp, lane, a.scale);
     __syncthreads();
     store_rows<HD, R>(st, a.dk, a.lddk, start, k0, len, kvh * HD, slot, a.rope_base, rope_out);
@@ -843,17 +908,50 @@ AttnArgs attn_args(const mlora_attn_desc* d) {
     a.scale = d->softmax_scale;
     a.rows = d->rows;
     a.rope_in = d->rope_base > 0.f && !(d->flags & MLORA_ATTN_PREROTATED);
+    a.hsplit = 1;
     return a;
 }
 
 template <typename K>
 cudaError_t launch_attn(K kernel, int rows_per_cta, const mlora_attn_desc* d, int heads_z, size_t smem, void* stream,
-                        const AttnArgs& a) {
+                        const AttnArgs& a, int cluster_z = 1) {
     if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
         cudaSuccess)
         return cudaErrorInvalidValue;
     const dim3 grid((d->max_len + rows_per_cta - 1) / rows_per_cta, d->num_seqs, heads_z);
-    return launch(kernel, grid, dim3(2 * rows_per_cta), smem, stream, a);
+    if (cluster_z <= 1) return launch(kernel, grid, dim3(2 * rows_per_cta), smem, stream, a);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(2 * rows_per_cta);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = static_cast<cudaStream_t>(stream);
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = cluster_z;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    return cudaLaunchKernelEx(&cfg, kernel, a);
+}
+
+// Query-head split of the dK/dV kernel for grouped / multi-query attention: the
+// largest divisor of the group size up to the cap (cluster size; default 2,
+// MLORA_ATTN_HSPLIT overrides), none for multi-head attention.  ncu at C4
+// (ChatGLM2, 16 query heads per K/V head), dK/dV per layer: 687 us unsplit,
+// 580 / 594 / 643 us with 2 / 4 / 8-CTA clusters.
+int attn_hsplit(const mlora_attn_desc* d) {
+    const int group = d->heads / d->kv_heads;
+    static const int cap = [] {
+        const char* e = std::getenv("MLORA_ATTN_HSPLIT");
+        return e ? std::max(1, std::min(8, std::atoi(e))) : 2;
+    }();
+    int best = 1;
+    for (int s = 2; s <= cap; ++s)
+        if (group % s == 0) best = s;
+    return best;
 }
 
 }  // namespace
@@ -982,6 +1080,7 @@ mlora_status mlora_attn_bwd(const mlora_attn_desc* d, const void* q, int64_t ldq
     a.lse = const_cast<float*>(lse);
     a.vec = rows16(q, ldq) && rows16(k, ldk) && rows16(v, ldv) && rows16(dout, lddo);
     a.dsum = dsum;
+    a.hsplit = attn_hsplit(d);
     const long long warps = d->rows * d->heads;
     if (launch(attn_dsum_kernel, dim3(static_cast<unsigned>((warps * 32 + 255) / 256)), dim3(256), 0, stream, a,
                hd) != cudaSuccess)
@@ -989,11 +1088,13 @@ mlora_status mlora_attn_bwd(const mlora_attn_desc* d, const void* q, int64_t ldq
     cudaError_t e;
     constexpr int R = kBwdRows;
     if (hd == 64) {
-        e = launch_attn(attn_bwd_dkv_kernel<64, R>, R, d, d->kv_heads, attn_smem_bwd<64, R>(), stream, a);
+        e = launch_attn(attn_bwd_dkv_kernel<64, R>, R, d, d->kv_heads * a.hsplit, attn_smem_bwd<64, R>(), stream, a,
+                        a.hsplit);
         if (e == cudaSuccess)
             e = launch_attn(attn_bwd_dq_kernel<64, R>, R, d, d->heads, attn_smem_bwd<64, R>(), stream, a);
     } else {
-        e = launch_attn(attn_bwd_dkv_kernel<128, R>, R, d, d->kv_heads, attn_smem_bwd<128, R>(), stream, a);
+        e = launch_attn(attn_bwd_dkv_kernel<128, R>, R, d, d->kv_heads * a.hsplit, attn_smem_bwd<128, R>(), stream,
+                        a, a.hsplit);
         if (e == cudaSuccess)
             e = launch_attn(attn_bwd_dq_kernel<128, R>, R, d, d->heads, attn_smem_bwd<128, R>(), stream, a);
     }

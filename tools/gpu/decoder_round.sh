@@ -1,2 +1,3 @@
-timeout 900 python -m pytest tests/test_gpu_executor.py tests/test_gpu_parity.py -x -q 2>&1 | tail -15 > gpurun_out/all.log
-timeout 600 python tools/c3_executor.py > gpurun_out/c3.jsonl 2>&1
+timeout 900 python -m pytest tests/test_gpu_decoder.py -x -q 2>&1 | tail -3 > gpurun_out/all.log
+MLORA_ATTN_HSPLIT=4 timeout 900 python -m pytest tests/test_gpu_decoder.py -x -q -k "attention" 2>&1 | tail -3 >> gpurun_out/all.log
+timeout 900 compute-sanitizer --tool racecheck python -m pytest tests/test_gpu_decoder.py -x -q -k "attention_fwd_bwd" 2>&1 | tail -3 >> gpurun_out/all.log
