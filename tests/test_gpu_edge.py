@@ -60,3 +60,22 @@ def test_many_jobs_one_plan():
 
 def test_single_job_with_one_row_tail():
     run([0, 257], [16], [2.0], 256, 256, seed=4)
+
+
+def test_plan_at_the_job_limit_with_rank_64():
+    """128 jobs (the per-plan limit) of rank 64: R_pad = 8192 columns, 128 rank
+    chunks; every table sized by the job limit is exercised at its bound."""
+    J = 128
+    rng = np.random.default_rng(5)
+    lens = rng.integers(1, 24, J)
+    seg = [0] + [int(x) for x in np.cumsum(lens)]
+    plan = run(seg, [64] * J, [1.0] * J, 128, 128, seed=6)
+    assert plan.rank_padded == 64 * J
+
+
+def test_plan_over_the_job_limit_is_a_usage_error():
+    from paper_2312_02515_b200 import errors as E
+    from paper_2312_02515_b200 import fused as F
+    ctx = F.Context(0)
+    with pytest.raises(E.UsageError):
+        F.Plan(ctx, list(range(130)), [8] * 129)
