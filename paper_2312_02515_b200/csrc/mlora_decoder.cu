@@ -484,6 +484,12 @@ constexpr size_t attn_smem_fwd() {  // Q (R rows) + double-buffered (K, V) 64-ro
     return sizeof(__nv_bfloat16) * Tile<HD>::LDH * (R + 4 * kBM);
 }
 template <int HD, int R>
+constexpr size_t attn_smem_dq1() {  // dQ, single-buffered: Q, dO (R rows) + one (K, V) pair + lse, dsum
+    return sizeof(__nv_bfloat16) * Tile<HD>::LDH * (2 * R + 2 * kBM) + sizeof(float) * 2 * R;
+}
+static_assert(2 * kBM * Tile<128>::LDH * 2 >= kBwdRows * Tile<128>::LDF * 4, "dQ stage fits one (K, V) pair");
+static_assert(2 * kBM * Tile<64>::LDH * 2 >= kBwdRows * Tile<64>::LDF * 4, "dQ stage fits one (K, V) pair");
+template <int HD, int R>
 constexpr size_t attn_smem_bwd() {  // two R-row tiles + double-buffered 64-row pair + lse, dsum
     // (dQ: lse, dsum for R rows; dK/dV: lse, dsum for each of the two 64-row buffers)
     return sizeof(__nv_bfloat16) * Tile<HD>::LDH * (2 * R + 4 * kBM) + sizeof(float) * 4 * (R > kBM ? R : kBM);
@@ -795,9 +801,12 @@ __global__ void __launch_bounds__(2 * R) attn_bwd_dkv_kernel(AttnArgs a) {
     store_rows<HD, R>(st, a.dv, a.lddv, start, k0, len, kvh * HD, slot, a.rope_base, false);
 }
 
-// dQ: one CTA per (128-query block, sequence, head); loops over the key tiles it sees.
+// dQ: one CTA per (R-query block, sequence, head); loops over the key tiles it
+// sees.  K/V tiles are single-buffered so three CTAs fit per SM (12 warps): at
+// C4 that beats a double-buffered pipeline at two CTAs per SM (ncu per layer:
+// 446 vs 496 us) — the other CTAs hide each tile's load latency.
 template <int HD, int R>
-__global__ void __launch_bounds__(2 * R) attn_bwd_dq_kernel(AttnArgs a) {
+__global__ void __launch_bounds__(2 * R, 3) attn_bwd_dq_kernel(AttnArgs a) {
     pdl_prologue();
     int start, len;
     seq_range(a, blockIdx.y, start, len);
@@ -809,18 +818,12 @@ __global__ void __launch_bounds__(2 * R) attn_bwd_dq_kernel(AttnArgs a) {
     extern __shared__ __align__(16) __nv_bfloat16 smh[];
     __nv_bfloat16* Qs = smh;
     __nv_bfloat16* dOs = Qs + R * Tile<HD>::LDH;
-    __nv_bfloat16* KV = dOs + R * Tile<HD>::LDH;  // (K, V) x 2 buffers, then lse, dsum
-    float* lse2 = reinterpret_cast<float*>(KV + 4 * TILE);
+    __nv_bfloat16* KV = dOs + R * Tile<HD>::LDH;  // one (K, V) pair, then lse, dsum
+    float* lse2 = reinterpret_cast<float*>(KV + 2 * TILE);
     float* dsm = lse2 + R;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
     const bool rope = a.rope_in != 0, async = a.vec != 0;
     const float c2 = a.scale * kLog2e;
-    auto fetch = [&](int kt) {
-        __nv_bfloat16* Kb = KV + 2 * TILE * (kt & 1);
-        stage<HD>(Kb, a.k, a.ldk, start, kt * kBM, len, kvh * HD, a.rope_base, rope, async);
-        stage<HD>(Kb + TILE, a.v, a.ldv, start, kt * kBM, len, kvh * HD, a.rope_base, false, async);
-        cp_async_commit();
-    };
 
     stage_rows<HD, R>(Qs, a.q, a.ldq, start, q0, len, h * HD, a.rope_base, rope, async);
     stage_rows<HD, R>(dOs, a.dO, a.lddo, start, q0, len, h * HD, a.rope_base, false, async);
@@ -830,17 +833,14 @@ __global__ void __launch_bounds__(2 * R) attn_bwd_dq_kernel(AttnArgs a) {
     for (int n = 0; n < HD / 8; ++n) dq[n][0] = dq[n][1] = dq[n][2] = dq[n][3] = 0.f;
     const int qrl0 = warp * 16 + g;  // this thread's block rows: qrl0 and qrl0 + 8
     const int nkt = q0 < len ? (min(q0 + R, len) + kBM - 1) / kBM : 0;
-    if (nkt > 0) fetch(0);
     for (int kt = 0; kt < nkt; ++kt) {
-        if (kt + 1 < nkt) {
-            fetch(kt + 1);
-            cp_async_wait<1>();
-        } else {
-            cp_async_wait<0>();
-        }
+        stage<HD>(KV, a.k, a.ldk, start, kt * kBM, len, kvh * HD, a.rope_base, rope, async);
+        stage<HD>(KV + TILE, a.v, a.ldv, start, kt * kBM, len, kvh * HD, a.rope_base, false, async);
+        cp_async_commit();
+        cp_async_wait<0>();
         __syncthreads();
         if (kt * kBM <= q0 + warp * 16 + 15) {
-            const __nv_bfloat16* Ks = KV + 2 * TILE * (kt & 1);
+            const __nv_bfloat16* Ks = KV;
             const __nv_bfloat16* Vs = Ks + TILE;
             float p[8][4], ds[8][4];
             mma_xyT<HD>(p, Qs, Ks, warp, lane);   // S
@@ -1091,12 +1091,12 @@ mlora_status mlora_attn_bwd(const mlora_attn_desc* d, const void* q, int64_t ldq
         e = launch_attn(attn_bwd_dkv_kernel<64, R>, R, d, d->kv_heads * a.hsplit, attn_smem_bwd<64, R>(), stream, a,
                         a.hsplit);
         if (e == cudaSuccess)
-            e = launch_attn(attn_bwd_dq_kernel<64, R>, R, d, d->heads, attn_smem_bwd<64, R>(), stream, a);
+            e = launch_attn(attn_bwd_dq_kernel<64, R>, R, d, d->heads, attn_smem_dq1<64, R>(), stream, a);
     } else {
         e = launch_attn(attn_bwd_dkv_kernel<128, R>, R, d, d->kv_heads * a.hsplit, attn_smem_bwd<128, R>(), stream,
                         a, a.hsplit);
         if (e == cudaSuccess)
-            e = launch_attn(attn_bwd_dq_kernel<128, R>, R, d, d->heads, attn_smem_bwd<128, R>(), stream, a);
+            e = launch_attn(attn_bwd_dq_kernel<128, R>, R, d, d->heads, attn_smem_dq1<128, R>(), stream, a);
     }
     return e == cudaSuccess ? MLORA_OK : MLORA_CUDA;
 }

@@ -1,1 +1,4 @@
-timeout 900 python -m pytest tests/test_gpu_edge.py -x -q 2>&1 | tail -15 > gpurun_out/all.log
+timeout 900 python -m pytest tests/test_gpu_decoder.py tests/test_gpu_executor.py -x -q 2>&1 | tail -2 > gpurun_out/all.log
+timeout 900 compute-sanitizer --tool racecheck python -m pytest tests/test_gpu_decoder.py -x -q -k "attention_fwd_bwd" 2>&1 | tail -2 >> gpurun_out/all.log
+timeout 600 python tools/decoder_probe.py --cfg chatglm2-6b --jobs 6 --seqs 4 --len 512 > gpurun_out/probe.log 2>&1
+timeout 600 python tools/decoder_probe.py --cfg llama-7b --layers 4 --jobs 4 --seqs 4 --len 512 >> gpurun_out/probe.log 2>&1
