@@ -29,6 +29,7 @@
 #include <cstdlib>
 
 #include "../../include/mlora.h"
+#include "sm100.cuh"
 
 namespace {
 
@@ -657,6 +658,258 @@ __global__ void attn_rope_kernel(AttnArgs a, const __nv_bfloat16* __restrict__ s
     }
 }
 
+// ---------------------------------------------------------------- tcgen05 forward
+// The forward on the 5th-generation tensor cores: one CTA of 4 warps per
+// (128-query block, sequence, head).  Thread t owns query row t, which is also
+// TMEM lane t.  Per 64-key tile:
+//   S[128 x 64]  = Q K^T   tcgen05.mma, M=128 N=64, operands K-major in smem
+//   softmax      each thread reads its S row from TMEM, online max / sum-exp,
+//                writes P (bf16) straight into the swizzled smem A operand
+//   O[128 x HD] += P V     tcgen05.mma, M=128 N=HD, V as an MN-major B operand,
+//                          accumulating in TMEM across the key tiles
+// The softmax runs against a per-row reference max that is only raised (and O
+// rescaled in TMEM by the owning thread) when a tile's max exceeds it by more
+// than 2^8: P then stays <= 256 (exact in bf16's range, fp32 sums), and the O
+// read-modify-write happens a handful of times per row instead of every tile.
+// Operand tiles use the 128-byte-swizzle layout (16-byte chunk c of row r at
+// chunk c ^ (r & 7) of a 1024-byte, 8-row atom), written with cp.async (Q, K,
+// V) or st.shared (P), then fence.proxy.async before the MMA reads them.
+// Q and K must come pre-rotated (mlora_attn_rope); otherwise the mma.sync
+// kernel above runs.
+namespace tc5 = mlora::sm100;
+
+template <int HD>
+struct TcAttn {
+    static constexpr int BQ = 128, BK = 64, NB = HD / 64;  // 64-column (128-byte) blocks per head row
+    static constexpr int Q_BYTES = BQ * 128 * NB;           // NB blocks of [128 rows x 128 B]
+    static constexpr int K_BYTES = BK * 128 * NB;
+    static constexpr int V_BYTES = BK * 128 * NB;
+    static constexpr int P_BYTES = BQ * 128;                 // [128 rows x 64 keys] bf16
+    static constexpr int SMEM = Q_BYTES + K_BYTES + V_BYTES + P_BYTES + 1024 + 64;
+    static constexpr uint32_t S_COL = 0, O_COL = 128, TMEM_COLS = 256;
+    static constexpr uint32_t IDESC_S = tc5::idesc_bf16_f32(128, BK, false, false);
+    static constexpr uint32_t IDESC_O = tc5::idesc_bf16_f32(128, HD, false, true);
+};
+
+// cp.async rows [r0, r0 + n) of one head (64-column blocks) into a swizzled region
+// of `rows` rows per block; rows at or beyond len are zero-filled.
+template <int HD>
+__device__ __forceinline__ void stage_sw128(uint8_t* region, int rows, const __nv_bfloat16* src, long long ld,
+                                            int start, int r0, int len, int col) {
+    constexpr int NB = HD / 64;
+    for (int e = threadIdx.x; e < rows * NB * 8; e += blockDim.x) {
+        const int ch = e & 7, rb = e >> 3, r = rb % rows, b = rb / rows;
+        uint8_t* dst = region + b * rows * 128 + r * 128 + ((ch ^ (r & 7)) << 4);
+        if (r0 + r < len)
+            cp_async16(smem_u32(dst), src + (long long)(start + r0 + r) * ld + col + b * 64 + ch * 8);
+        else
+            *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
+    }
+}
+
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// 32 lanes x 32 consecutive fp32 columns, the store twin of tmem_ld32.
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+        "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]),
+        "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]),
+        "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+template <int HD>
+__global__ void __launch_bounds__(128, 1) attn_fwd_tc_kernel(AttnArgs a) {
+    using T = TcAttn<HD>;
+    pdl_prologue();
+    int start, len;
+    seq_range(a, blockIdx.y, start, len);
+    const int slot = a.seq_off[blockIdx.y + 1] - start;
+    const int q0 = blockIdx.x * T::BQ;
+    if (q0 >= slot) return;
+    const int h = blockIdx.z, kvh = h / (a.heads / a.kv_heads);
+    extern __shared__ uint8_t smraw[];
+    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+    uint8_t* Qs = base;
+    uint8_t* Ks = Qs + T::Q_BYTES;
+    uint8_t* Vs = Ks + T::K_BYTES;
+    uint8_t* Ps = Vs + T::V_BYTES;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(Ps + T::P_BYTES);
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
+    const int warp = threadIdx.x >> 5, row = threadIdx.x;
+    if (threadIdx.x == 0) {
+        tc5::mbar_init(bar, 1);
+        tc5::fence_barrier_init();
+    }
+    if (warp == 0) {
+        tc5::tmem_alloc(tslot, T::TMEM_COLS);
+        tc5::tmem_relinquish();
+    }
+    const int nkt = q0 < len ? (min(q0 + T::BQ, len) + T::BK - 1) / T::BK : 0;
+    // cp.async groups complete in issue order: [Q + K_0], [V_0], then per tile kt
+    // [K_kt+1] (issued once S_kt is computed) and [V_kt+1] (once O_kt is).
+    stage_sw128<HD>(Qs, T::BQ, a.q, a.ldq, start, q0, len, h * HD);
+    if (nkt > 0) stage_sw128<HD>(Ks, T::BK, a.k, a.ldk, start, 0, len, kvh * HD);
+    cp_async_commit();
+    if (nkt > 0) stage_sw128<HD>(Vs, T::BK, a.v, a.ldv, start, 0, len, kvh * HD);
+    cp_async_commit();
+    tc5::tc_fence_before();
+    __syncthreads();
+    tc5::tc_fence_after();
+    const uint32_t tmem = *tslot;
+    const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+    const float c2 = a.scale * kLog2e;
+    const int qi = q0 + row;
+    float m = -INFINITY, l = 0.f;  // m: the row's reference max (log2 domain)
+    uint32_t phase = 0;
+    for (int kt = 0; kt < nkt; ++kt) {
+        cp_async_wait<1>();  // K_kt (and Q) landed; V_kt may still be in flight
+        fence_proxy_async();
+        __syncthreads();
+        if (threadIdx.x == 0) {  // S = Q K^T
+            tc5::tc_fence_after();
+#pragma unroll
+            for (int j = 0; j < HD / 16; ++j) {
+                const uint64_t ad = tc5::sdesc_sw128(smem_u32(Qs + (j / 4) * T::BQ * 128 + (j % 4) * 32), 16, 1024);
+                const uint64_t bd = tc5::sdesc_sw128(smem_u32(Ks + (j / 4) * T::BK * 128 + (j % 4) * 32), 16, 1024);
+                tc5::mma_bf16(tmem + T::S_COL, ad, bd, T::IDESC_S, j > 0 ? 1u : 0u);
+            }
+            tc5::tc_commit(bar);
+        }
+        tc5::mbar_wait(bar, phase);
+        phase ^= 1u;
+        tc5::tc_fence_after();
+        // K_kt is consumed: prefetch K_kt+1 under the softmax and the P V product
+        if (kt + 1 < nkt) stage_sw128<HD>(Ks, T::BK, a.k, a.ldk, start, (kt + 1) * T::BK, len, kvh * HD);
+        cp_async_commit();
+        // ---- softmax of this thread's row (64 keys)
+        float s[64];
+        {
+            uint32_t v[32];
+            tc5::tmem_ld32(tmem + lane_base + T::S_COL, v);
+            tc5::tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < 32; ++c) s[c] = __uint_as_float(v[c]);
+            tc5::tmem_ld32(tmem + lane_base + T::S_COL + 32, v);
+            tc5::tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < 32; ++c) s[32 + c] = __uint_as_float(v[c]);
+        }
+        float mx = -INFINITY;
+#pragma unroll
+        for (int c = 0; c < 64; ++c) {
+            const int kj = kt * T::BK + c;
+            s[c] = (kj <= qi && qi < len) ? s[c] * c2 : -INFINITY;
+            mx = fmaxf(mx, s[c]);
+        }
+        // raise the reference max where a row's tile max exceeds it by > 2^8 and
+        // rescale what O and l hold so far.  tcgen05.ld / st are warp-collective
+        // (.sync.aligned): the O read-modify-write runs for the whole warp when any
+        // of its rows needs it (alpha = 1 for the others).
+        const bool raise = mx > m + 8.f;
+        const float alpha = !raise ? 1.f : (m == -INFINITY ? 0.f : exp2f(m - mx));
+        if (kt > 0 && __any_sync(0xffffffffu, raise)) {
+#pragma unroll
+            for (int c0 = 0; c0 < HD; c0 += 32) {
+                uint32_t v[32];
+                tc5::tmem_ld32(tmem + lane_base + T::O_COL + c0, v);
+                tc5::tmem_wait_ld();
+#pragma unroll
+                for (int c = 0; c < 32; ++c) v[c] = __float_as_uint(__uint_as_float(v[c]) * alpha);
+                tmem_st32(tmem + lane_base + T::O_COL + c0, v);
+            }
+            tmem_wait_st();
+        }
+        if (raise) {
+            l *= alpha;
+            m = mx;
+        }
+        const float mn = m;
+        float ps = 0.f;
+        uint8_t* prow = Ps + row * 128;
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) {
+            float p[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                p[e] = mn == -INFINITY ? 0.f : exp2f(s[ch * 8 + e] - mn);
+                ps += p[e];
+            }
+            uint4 w;
+            w.x = pack2(p[0], p[1]);
+            w.y = pack2(p[2], p[3]);
+            w.z = pack2(p[4], p[5]);
+            w.w = pack2(p[6], p[7]);
+            *reinterpret_cast<uint4*>(prow + ((ch ^ (row & 7)) << 4)) = w;
+        }
+        l += ps;
+        cp_async_wait<1>();  // V_kt landed (K_kt+1 may still be in flight)
+        fence_proxy_async();
+        tc5::tc_fence_before();
+        __syncthreads();
+        if (threadIdx.x == 0) {  // O_t = P V
+            tc5::tc_fence_after();
+#pragma unroll
+            for (int j = 0; j < T::BK / 16; ++j) {
+                const uint64_t ad = tc5::sdesc_sw128(smem_u32(Ps + j * 32), 16, 1024);
+                const uint64_t bd = tc5::sdesc_sw128(smem_u32(Vs + j * 2048), T::BK * 128, 1024);
+                tc5::mma_bf16(tmem + T::O_COL, ad, bd, T::IDESC_O, (kt > 0 || j > 0) ? 1u : 0u);
+            }
+            tc5::tc_commit(bar);
+        }
+        tc5::mbar_wait(bar, phase);
+        phase ^= 1u;
+        tc5::tc_fence_after();
+        // V_kt is consumed: prefetch V_kt+1 under the output update and the next S
+        if (kt + 1 < nkt) stage_sw128<HD>(Vs, T::BK, a.v, a.ldv, start, (kt + 1) * T::BK, len, kvh * HD);
+        cp_async_commit();
+        tc5::tc_fence_before();
+        __syncthreads();  // P and S are reused by the next tile
+    }
+    cp_async_wait<0>();
+    // ---- epilogue
+    if (nkt > 0) {  // every warp reads its rows of O (collective tcgen05.ld)
+        const bool ok = qi < len && l > 0.f;
+        const float inv = ok ? 1.f / l : 0.f;
+        __nv_bfloat16* dst = a.out + (long long)(start + qi) * a.ldout + h * HD;
+#pragma unroll
+        for (int c0 = 0; c0 < HD; c0 += 32) {
+            uint32_t v[32];
+            tc5::tmem_ld32(tmem + lane_base + T::O_COL + c0, v);
+            tc5::tmem_wait_ld();
+            if (qi < slot) {
+#pragma unroll
+                for (int c = 0; c < 32; c += 8) {
+                    uint4 w;
+                    w.x = pack2(__uint_as_float(v[c]) * inv, __uint_as_float(v[c + 1]) * inv);
+                    w.y = pack2(__uint_as_float(v[c + 2]) * inv, __uint_as_float(v[c + 3]) * inv);
+                    w.z = pack2(__uint_as_float(v[c + 4]) * inv, __uint_as_float(v[c + 5]) * inv);
+                    w.w = pack2(__uint_as_float(v[c + 6]) * inv, __uint_as_float(v[c + 7]) * inv);
+                    *reinterpret_cast<uint4*>(dst + c0 + c) = w;
+                }
+            }
+        }
+    } else if (qi < slot) {  // a block entirely past the real tokens: zero output
+        __nv_bfloat16* dst = a.out + (long long)(start + qi) * a.ldout + h * HD;
+        for (int c = 0; c < HD; c += 8) *reinterpret_cast<uint4*>(dst + c) = make_uint4(0, 0, 0, 0);
+    }
+    if (qi < slot) {
+        const bool ok = qi < len && l > 0.f;
+        a.lse[(long long)h * a.rows + start + qi] = ok ? (m + log2f(l)) * kLn2 : 0.f;
+    }
+    tc5::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc5::tc_fence_after();
+        tc5::tmem_dealloc(tmem, T::TMEM_COLS);
+    }
+}
+
 // dsum[h][t] = sum_d dO[t, h*HD + d] * O[t, h*HD + d]   (one warp per (row, head))
 __global__ void attn_dsum_kernel(AttnArgs a, int hd) {
     pdl_prologue();
@@ -937,6 +1190,17 @@ cudaError_t launch_attn(K kernel, int rows_per_cta, const mlora_attn_desc* d, in
     return cudaLaunchKernelEx(&cfg, kernel, a);
 }
 
+// Grid (rows_per_cta-row blocks, sequences, heads_z) with an explicit block size.
+template <typename K>
+cudaError_t launch_attn_rows(K kernel, int rows_per_cta, int threads, const mlora_attn_desc* d, int heads_z,
+                             size_t smem, void* stream, const AttnArgs& a) {
+    if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
+        cudaSuccess)
+        return cudaErrorInvalidValue;
+    const dim3 grid((d->max_len + rows_per_cta - 1) / rows_per_cta, d->num_seqs, heads_z);
+    return launch(kernel, grid, dim3(threads), smem, stream, a);
+}
+
 // Query-head split of the dK/dV kernel for grouped / multi-query attention: the
 // largest divisor of the group size up to the cap (cluster size; default 2,
 // MLORA_ATTN_HSPLIT overrides), none for multi-head attention.  ncu at C4
@@ -1037,10 +1301,21 @@ mlora_status mlora_attn_fwd(const mlora_attn_desc* d, const void* q, int64_t ldq
     a.ldq = ldq, a.ldk = ldk, a.ldv = ldv, a.ldout = ldo;
     a.lse = lse;
     a.vec = rows16(q, ldq) && rows16(k, ldk) && rows16(v, ldv);
-    constexpr int R = kFwdRows;
-    const cudaError_t e =
-        hd == 64 ? launch_attn(attn_fwd_kernel<64, R>, R, d, d->heads, attn_smem_fwd<64, R>(), stream, a)
-                 : launch_attn(attn_fwd_kernel<128, R>, R, d, d->heads, attn_smem_fwd<128, R>(), stream, a);
+    static const bool tc = [] {  // MLORA_ATTN_TC=0 keeps the mma.sync forward (A/B knob)
+        const char* e = std::getenv("MLORA_ATTN_TC");
+        return !(e && e[0] == '0');
+    }();
+    cudaError_t e;
+    if (tc && a.vec && !a.rope_in && (reinterpret_cast<uintptr_t>(o) & 15) == 0 && ldo % 8 == 0) {
+        // the tcgen05 kernel: 128 query rows per CTA, one thread per row
+        const size_t smem = hd == 64 ? TcAttn<64>::SMEM : TcAttn<128>::SMEM;
+        e = hd == 64 ? launch_attn_rows(attn_fwd_tc_kernel<64>, 128, 128, d, d->heads, smem, stream, a)
+                     : launch_attn_rows(attn_fwd_tc_kernel<128>, 128, 128, d, d->heads, smem, stream, a);
+    } else {
+        constexpr int R = kFwdRows;
+        e = hd == 64 ? launch_attn(attn_fwd_kernel<64, R>, R, d, d->heads, attn_smem_fwd<64, R>(), stream, a)
+                     : launch_attn(attn_fwd_kernel<128, R>, R, d, d->heads, attn_smem_fwd<128, R>(), stream, a);
+    }
     return e == cudaSuccess ? MLORA_OK : MLORA_CUDA;
 }
 

@@ -366,3 +366,25 @@ def test_llama13b_width_layer_matches_torch():
     from paper_2312_02515_b200 import model as MD
     cfg = MD.LLAMA_13B.with_layers(1)
     run_parity(cfg, [8, 16, 32, 64], [2.0] * 4, [1e-4] * 4, [[90, 33], [128], [7, 64], [200]], padded=False, seed=13)
+
+
+def test_attention_rows_rescale_at_different_tiles():
+    """Scores that grow along the keys for half of the rows and shrink for the
+    other half: rows of one warp raise their softmax reference max at different
+    key tiles (the tcgen05 forward's O rescale must stay warp-collective)."""
+    from paper_2312_02515_b200 import model_ops as M
+    dev = torch.device("cuda", 0)
+    g = torch.Generator().manual_seed(9)
+    heads, kv, hd, n = 2, 1, 128, 700
+    ramp = torch.linspace(0.05, 3.0, n)[:, None]
+    k = (torch.randn(n, kv * hd, generator=g).abs() * ramp).to(torch.bfloat16).to(dev)
+    sign = torch.where(torch.arange(n) % 2 == 0, 1.0, -1.0)[:, None]
+    q = (torch.randn(n, heads * hd, generator=g).abs() * sign).to(torch.bfloat16).to(dev)
+    v = torch.randn(n, kv * hd, generator=g).to(torch.bfloat16).to(dev)
+    lay = M.AttnLayout([0, n], device=dev)
+    o, lse = M.attn_fwd(lay, q, k, v, heads, kv, hd, rope_base=10000.0, prerotated=True)  # q, k taken as rotated
+    torch.cuda.synchronize()
+    qf, kf, vf = q.float(), k.float(), v.float()
+    ref = attn_ref(qf, kf, vf, [0, n], [n], heads, kv, hd, 0.0)  # no rotation: the inputs are "pre-rotated"
+    assert torch.isfinite(o.float()).all()
+    assert rel(o.float(), ref) < 1e-2
