@@ -709,6 +709,13 @@ __device__ __forceinline__ void stage_sw128(uint8_t* region, int rows, const __n
 
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+// 2^x on the SFU, flushing denormals (P below 2^-126 is 0 in bf16 anyway).
+__device__ __forceinline__ float ex2_ftz(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 // 32 lanes x 32 consecutive fp32 columns, the store twin of tmem_ld32.
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
     asm volatile(
@@ -800,13 +807,22 @@ __global__ void __launch_bounds__(128, 1) attn_fwd_tc_kernel(AttnArgs a) {
 #pragma unroll
             for (int c = 0; c < 32; ++c) s[32 + c] = __uint_as_float(v[c]);
         }
+        // interior tiles (every key precedes every query of the block, all rows
+        // real) skip the mask; the softmax scale is folded into the exp2 FMA
+        // (c2 > 0, so max(c2 s) = c2 max(s))
         float mx = -INFINITY;
+        if (kt * T::BK + T::BK - 1 <= q0 && q0 + T::BQ <= len) {
 #pragma unroll
-        for (int c = 0; c < 64; ++c) {
-            const int kj = kt * T::BK + c;
-            s[c] = (kj <= qi && qi < len) ? s[c] * c2 : -INFINITY;
-            mx = fmaxf(mx, s[c]);
+            for (int c = 0; c < 64; ++c) mx = fmaxf(mx, s[c]);
+        } else {
+#pragma unroll
+            for (int c = 0; c < 64; ++c) {
+                const int kj = kt * T::BK + c;
+                s[c] = (kj <= qi && qi < len) ? s[c] : -INFINITY;
+                mx = fmaxf(mx, s[c]);
+            }
         }
+        mx = mx == -INFINITY ? -INFINITY : mx * c2;
         // raise the reference max where a row's tile max exceeds it by > 2^8 and
         // rescale what O and l hold so far.  tcgen05.ld / st are warp-collective
         // (.sync.aligned): the O read-modify-write runs for the whole warp when any
@@ -829,7 +845,8 @@ __global__ void __launch_bounds__(128, 1) attn_fwd_tc_kernel(AttnArgs a) {
             l *= alpha;
             m = mx;
         }
-        const float mn = m;
+        const float nm = m == -INFINITY ? 0.f : -m;  // rows with nothing real yet: P = 0 below
+        const float live = m == -INFINITY ? 0.f : 1.f;
         float ps = 0.f;
         uint8_t* prow = Ps + row * 128;
 #pragma unroll
@@ -837,7 +854,7 @@ __global__ void __launch_bounds__(128, 1) attn_fwd_tc_kernel(AttnArgs a) {
             float p[8];
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
-                p[e] = mn == -INFINITY ? 0.f : exp2f(s[ch * 8 + e] - mn);
+                p[e] = live * ex2_ftz(fmaf(s[ch * 8 + e], c2, nm));
                 ps += p[e];
             }
             uint4 w;

@@ -1,5 +1,4 @@
-timeout 1200 python -m pytest tests -x -q -m gpu 2>&1 | tail -3 > gpurun_out/all.log
-timeout 600 compute-sanitizer --tool racecheck python -m pytest tests/test_gpu_decoder.py -x -q -k "rescale or attention_fwd_bwd" 2>&1 | tail -2 >> gpurun_out/all.log
-timeout 600 compute-sanitizer --tool memcheck python -m pytest tests/test_gpu_decoder.py -x -q -k "rescale or attention_fwd_bwd" 2>&1 | tail -2 >> gpurun_out/all.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke_rc=$? >> gpurun_out/smoke.log
-timeout 900 python bench.py --config c4 --steps 5 --warmup 3 > gpurun_out/bench_c4.log 2>&1
+timeout 600 python -m pytest tests/test_gpu_decoder.py -x -q 2>&1 | tail -2 > gpurun_out/all.log
+for i in 1 2; do
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"attn_fwd" -c 2 --csv --log-file gpurun_out/fwd_tc_$i.csv python tools/decoder_step.py --layers 1 --steps 2 > /dev/null 2>&1
+done
