@@ -1018,13 +1018,20 @@ __global__ void __launch_bounds__(2 * R) attn_bwd_dkv_kernel(AttnArgs a) {
             const float* dsm = lse2 + kBM;
             float p[8][4];
             mma_xyT<HD>(p, Ks, Qs, warp, lane);  // S^T: rows = keys, cols = queries
+            if (k0 + R - 1 <= q0 && q0 + kBM <= len) {  // interior: every key precedes every query
 #pragma unroll
-            for (int n = 0; n < 8; ++n)
+                for (int n = 0; n < 8; ++n)
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int kj = kr0 + 8 * (e >> 1), cq = n * 8 + 2 * t + (e & 1), qi = q0 + cq;
-                    p[n][e] = (kj <= qi && qi < len) ? exp2f(p[n][e] * c2 - lse2[cq]) : 0.f;
-                }
+                    for (int e = 0; e < 4; ++e) p[n][e] = ex2_ftz(fmaf(p[n][e], c2, -lse2[n * 8 + 2 * t + (e & 1)]));
+            } else {
+#pragma unroll
+                for (int n = 0; n < 8; ++n)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int kj = kr0 + 8 * (e >> 1), cq = n * 8 + 2 * t + (e & 1), qi = q0 + cq;
+                        p[n][e] = (kj <= qi && qi < len) ? ex2_ftz(fmaf(p[n][e], c2, -lse2[cq])) : 0.f;
+                    }
+            }
             mma_pz<HD>(dv, p, dOs, lane);          // dV += P^T dO
             float ds[8][4];
             mma_xyT<HD>(ds, Vs, dOs, warp, lane);  // dP^T = V dO^T
@@ -1115,14 +1122,24 @@ __global__ void __launch_bounds__(2 * R, 3) attn_bwd_dq_kernel(AttnArgs a) {
             float p[8][4], ds[8][4];
             mma_xyT<HD>(p, Qs, Ks, warp, lane);   // S
             mma_xyT<HD>(ds, dOs, Vs, warp, lane); // dP
+            if (kt * kBM + kBM - 1 <= q0 && q0 + R <= len) {  // interior: every key precedes every query
 #pragma unroll
-            for (int n = 0; n < 8; ++n)
+                for (int n = 0; n < 8; ++n)
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const int rl = qrl0 + 8 * (e >> 1), qi = q0 + rl, kj = kt * kBM + n * 8 + 2 * t + (e & 1);
-                    const float pv = (kj <= qi && qi < len) ? exp2f(p[n][e] * c2 - lse2[rl]) : 0.f;
-                    ds[n][e] = pv * (ds[n][e] - dsm[rl]);
-                }
+                    for (int e = 0; e < 4; ++e) {
+                        const int rl = qrl0 + 8 * (e >> 1);
+                        ds[n][e] = ex2_ftz(fmaf(p[n][e], c2, -lse2[rl])) * (ds[n][e] - dsm[rl]);
+                    }
+            } else {
+#pragma unroll
+                for (int n = 0; n < 8; ++n)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int rl = qrl0 + 8 * (e >> 1), qi = q0 + rl, kj = kt * kBM + n * 8 + 2 * t + (e & 1);
+                        const float pv = (kj <= qi && qi < len) ? ex2_ftz(fmaf(p[n][e], c2, -lse2[rl])) : 0.f;
+                        ds[n][e] = pv * (ds[n][e] - dsm[rl]);
+                    }
+            }
             mma_pz<HD>(dq, ds, Ks, lane);          // dQ += dS K
         }
         __syncthreads();
