@@ -952,6 +952,173 @@ __device__ __forceinline__ void load_stats(const AttnArgs& a, int h, int start, 
     }
 }
 
+// dQ on the 5th-generation tensor cores: one CTA of 4 warps per (128-query
+// block, sequence, head); thread t owns query row t = TMEM lane t.  Per 64-key
+// tile:  S = Q K^T and dP = dO V^T (tcgen05.mma, M=128 N=64, K-major operands),
+// dS = P (dP - D) with P = exp2(S c2 - lse2) computed by each row's thread and
+// written (bf16) as the swizzled A operand, dQ += dS K (M=128 N=HD, K as an
+// MN-major operand) accumulating in TMEM.  No online softmax: the forward's lse
+// fixes P, so dQ needs no rescaling.  V_kt+1 streams in once dP_kt is computed,
+// K_kt+1 once dQ_kt's product is.  Deterministic (no atomics).
+template <int HD>
+struct TcDq {
+    static constexpr int BQ = 128, BK = 64, NB = HD / 64;
+    static constexpr int Q_BYTES = BQ * 128 * NB, K_BYTES = BK * 128 * NB, DS_BYTES = BQ * 128;
+    static constexpr int SMEM = 2 * Q_BYTES + 2 * K_BYTES + DS_BYTES + 64;  // two CTAs per SM at HD = 128
+    static constexpr uint32_t S_COL = 0, DP_COL = 64, DQ_COL = 128, TMEM_COLS = 256;
+    static constexpr uint32_t IDESC_S = tc5::idesc_bf16_f32(128, BK, false, false);
+    static constexpr uint32_t IDESC_Q = tc5::idesc_bf16_f32(128, HD, false, true);
+};
+
+template <int HD>
+__global__ void __launch_bounds__(128, 1) attn_bwd_dq_tc_kernel(AttnArgs a) {
+    using T = TcDq<HD>;
+    pdl_prologue();
+    int start, len;
+    seq_range(a, blockIdx.y, start, len);
+    const int slot = a.seq_off[blockIdx.y + 1] - start;
+    const int q0 = blockIdx.x * T::BQ;
+    if (q0 >= slot) return;
+    const int h = blockIdx.z, kvh = h / (a.heads / a.kv_heads);
+    extern __shared__ __align__(1024) uint8_t smq[];
+    if ((smem_u32(smq) & 1023) != 0) __trap();  // the swizzled operand tiles need 1 KB alignment
+    uint8_t* Qs = smq;
+    uint8_t* dOs = Qs + T::Q_BYTES;
+    uint8_t* Ks = dOs + T::Q_BYTES;
+    uint8_t* Vs = Ks + T::K_BYTES;
+    uint8_t* dSs = Vs + T::K_BYTES;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(dSs + T::DS_BYTES);
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
+    const int warp = threadIdx.x >> 5, row = threadIdx.x;
+    if (threadIdx.x == 0) {
+        tc5::mbar_init(bar, 1);
+        tc5::fence_barrier_init();
+    }
+    if (warp == 0) {
+        tc5::tmem_alloc(tslot, T::TMEM_COLS);
+        tc5::tmem_relinquish();
+    }
+    const int nkt = q0 < len ? (min(q0 + T::BQ, len) + T::BK - 1) / T::BK : 0;
+    // cp.async groups in issue order: [Q, dO, K_0], [V_0], then per tile [V_kt+1], [K_kt+1]
+    stage_sw128<HD>(Qs, T::BQ, a.q, a.ldq, start, q0, len, h * HD);
+    stage_sw128<HD>(dOs, T::BQ, a.dO, a.lddo, start, q0, len, h * HD);
+    if (nkt > 0) stage_sw128<HD>(Ks, T::BK, a.k, a.ldk, start, 0, len, kvh * HD);
+    cp_async_commit();
+    if (nkt > 0) stage_sw128<HD>(Vs, T::BK, a.v, a.ldv, start, 0, len, kvh * HD);
+    cp_async_commit();
+    tc5::tc_fence_before();
+    __syncthreads();
+    tc5::tc_fence_after();
+    const uint32_t tmem = *tslot;
+    const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+    const float c2 = a.scale * kLog2e;
+    const int qi = q0 + row;
+    const bool real = qi < len;  // this row's lse (log2 units) and D = rowsum(dO O), in registers
+    const float nl = real ? -a.lse[(long long)h * a.rows + start + qi] * kLog2e : 0.f;
+    const float dr = real ? a.dsum[(long long)h * a.rows + start + qi] : 0.f;
+    uint32_t phase = 0;
+    for (int kt = 0; kt < nkt; ++kt) {
+        cp_async_wait<0>();  // K_kt and V_kt (and Q, dO) landed
+        fence_proxy_async();
+        __syncthreads();
+        if (threadIdx.x == 0) {  // S = Q K^T, dP = dO V^T
+            tc5::tc_fence_after();
+#pragma unroll
+            for (int j = 0; j < HD / 16; ++j) {
+                const uint32_t qo = (j / 4) * T::BQ * 128 + (j % 4) * 32, ko = (j / 4) * T::BK * 128 + (j % 4) * 32;
+                tc5::mma_bf16(tmem + T::S_COL, tc5::sdesc_sw128(smem_u32(Qs + qo), 16, 1024),
+                              tc5::sdesc_sw128(smem_u32(Ks + ko), 16, 1024), T::IDESC_S, j > 0 ? 1u : 0u);
+                tc5::mma_bf16(tmem + T::DP_COL, tc5::sdesc_sw128(smem_u32(dOs + qo), 16, 1024),
+                              tc5::sdesc_sw128(smem_u32(Vs + ko), 16, 1024), T::IDESC_S, j > 0 ? 1u : 0u);
+            }
+            tc5::tc_commit(bar);
+        }
+        tc5::mbar_wait(bar, phase);
+        phase ^= 1u;
+        tc5::tc_fence_after();
+        // V_kt is consumed: prefetch V_kt+1 under dS and the dQ product
+        if (kt + 1 < nkt) stage_sw128<HD>(Vs, T::BK, a.v, a.ldv, start, (kt + 1) * T::BK, len, kvh * HD);
+        cp_async_commit();
+        const bool interior = kt * T::BK + T::BK - 1 <= q0 && q0 + T::BQ <= len;
+        uint8_t* drow = dSs + row * 128;
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+            uint32_t sv[32], pv[32];
+            tc5::tmem_ld32(tmem + lane_base + T::S_COL + half * 32, sv);
+            tc5::tmem_ld32(tmem + lane_base + T::DP_COL + half * 32, pv);
+            tc5::tmem_wait_ld();
+#pragma unroll
+            for (int ch = 0; ch < 4; ++ch) {
+                float d[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const int c = ch * 8 + e, kj = kt * T::BK + half * 32 + c;
+                    float p = ex2_ftz(fmaf(__uint_as_float(sv[c]), c2, nl));
+                    if (!interior) p = (kj <= qi && qi < len) ? p : 0.f;
+                    d[e] = p * (__uint_as_float(pv[c]) - dr);
+                }
+                uint4 w;
+                w.x = pack2(d[0], d[1]);
+                w.y = pack2(d[2], d[3]);
+                w.z = pack2(d[4], d[5]);
+                w.w = pack2(d[6], d[7]);
+                const int chunk = half * 4 + ch;
+                *reinterpret_cast<uint4*>(drow + ((chunk ^ (row & 7)) << 4)) = w;
+            }
+        }
+        fence_proxy_async();
+        tc5::tc_fence_before();
+        __syncthreads();
+        if (threadIdx.x == 0) {  // dQ += dS K
+            tc5::tc_fence_after();
+#pragma unroll
+            for (int j = 0; j < T::BK / 16; ++j) {
+                const uint64_t ad = tc5::sdesc_sw128(smem_u32(dSs + j * 32), 16, 1024);
+                const uint64_t bd = tc5::sdesc_sw128(smem_u32(Ks + j * 2048), T::BK * 128, 1024);
+                tc5::mma_bf16(tmem + T::DQ_COL, ad, bd, T::IDESC_Q, (kt > 0 || j > 0) ? 1u : 0u);
+            }
+            tc5::tc_commit(bar);
+        }
+        tc5::mbar_wait(bar, phase);
+        phase ^= 1u;
+        tc5::tc_fence_after();
+        // K_kt is consumed: prefetch K_kt+1
+        if (kt + 1 < nkt) stage_sw128<HD>(Ks, T::BK, a.k, a.ldk, start, (kt + 1) * T::BK, len, kvh * HD);
+        cp_async_commit();
+        tc5::tc_fence_before();
+        __syncthreads();  // S, dP and dS are reused by the next tile
+    }
+    cp_async_wait<0>();
+    // ---- epilogue: dQ (scaled, un-rotated) through an fp32 stage in the Q / dO tiles
+    float* st = reinterpret_cast<float*>(Qs);  // 128 x (HD + 4) fp32 over the (free) Q, dO, K, V tiles
+    __syncthreads();
+    if (nkt > 0) {
+#pragma unroll
+        for (int c0 = 0; c0 < HD; c0 += 32) {
+            uint32_t v[32];
+            tc5::tmem_ld32(tmem + lane_base + T::DQ_COL + c0, v);
+            tc5::tmem_wait_ld();
+#pragma unroll
+            for (int c = 0; c < 32; ++c) st[row * Tile<HD>::LDF + c0 + c] = a.scale * __uint_as_float(v[c]);
+        }
+    } else {
+        for (int c = 0; c < HD; ++c) st[row * Tile<HD>::LDF + c] = 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int hlf = 0; hlf < 2; ++hlf)
+        store_tile<HD>(st + hlf * kBM * Tile<HD>::LDF, a.dq, a.lddq, start, q0 + hlf * kBM, len, h * HD, slot,
+                       a.rope_base, a.rope_base > 0.f);
+    tc5::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc5::tc_fence_after();
+        tc5::tmem_dealloc(tmem, T::TMEM_COLS);
+    }
+}
+static_assert(2 * TcDq<128>::Q_BYTES + 2 * TcDq<128>::K_BYTES >= 128 * Tile<128>::LDF * 4, "dQ stage fits");
+static_assert(2 * TcDq<64>::Q_BYTES + 2 * TcDq<64>::K_BYTES >= 128 * Tile<64>::LDF * 4, "dQ stage fits");
+
 // dK, dV: one CTA per (R-key block, sequence, K/V head, head part); loops over
 // its query heads and the 64-query tiles that can see the block (causal).  With
 // grouped / multi-query attention the group's query heads are split over a
@@ -1224,6 +1391,16 @@ cudaError_t launch_attn(K kernel, int rows_per_cta, const mlora_attn_desc* d, in
     return cudaLaunchKernelEx(&cfg, kernel, a);
 }
 
+// MLORA_ATTN_TC=0 keeps the mma.sync forward / dQ kernels (A/B knob); the
+// tcgen05 ones need pre-rotated Q / K and 16-byte-aligned rows.
+bool attn_tc_enabled() {
+    static const bool tc = [] {
+        const char* e = std::getenv("MLORA_ATTN_TC");
+        return !(e && e[0] == '0');
+    }();
+    return tc;
+}
+
 // Grid (rows_per_cta-row blocks, sequences, heads_z) with an explicit block size.
 template <typename K>
 cudaError_t launch_attn_rows(K kernel, int rows_per_cta, int threads, const mlora_attn_desc* d, int heads_z,
@@ -1335,12 +1512,8 @@ mlora_status mlora_attn_fwd(const mlora_attn_desc* d, const void* q, int64_t ldq
     a.ldq = ldq, a.ldk = ldk, a.ldv = ldv, a.ldout = ldo;
     a.lse = lse;
     a.vec = rows16(q, ldq) && rows16(k, ldk) && rows16(v, ldv);
-    static const bool tc = [] {  // MLORA_ATTN_TC=0 keeps the mma.sync forward (A/B knob)
-        const char* e = std::getenv("MLORA_ATTN_TC");
-        return !(e && e[0] == '0');
-    }();
     cudaError_t e;
-    if (tc && a.vec && !a.rope_in && (reinterpret_cast<uintptr_t>(o) & 15) == 0 && ldo % 8 == 0) {
+    if (attn_tc_enabled() && a.vec && !a.rope_in && (reinterpret_cast<uintptr_t>(o) & 15) == 0 && ldo % 8 == 0) {
         // the tcgen05 kernel: 128 query rows per CTA, one thread per row
         const size_t smem = hd == 64 ? TcAttn<64>::SMEM : TcAttn<128>::SMEM;
         e = hd == 64 ? launch_attn_rows(attn_fwd_tc_kernel<64>, 128, 128, d, d->heads, smem, stream, a)
@@ -1396,16 +1569,19 @@ mlora_status mlora_attn_bwd(const mlora_attn_desc* d, const void* q, int64_t ldq
         return MLORA_CUDA;
     cudaError_t e;
     constexpr int R = kBwdRows;
+    const bool tc = attn_tc_enabled() && a.vec && !a.rope_in && (reinterpret_cast<uintptr_t>(dq) & 3) == 0;
     if (hd == 64) {
         e = launch_attn(attn_bwd_dkv_kernel<64, R>, R, d, d->kv_heads * a.hsplit, attn_smem_bwd<64, R>(), stream, a,
                         a.hsplit);
         if (e == cudaSuccess)
-            e = launch_attn(attn_bwd_dq_kernel<64, R>, R, d, d->heads, attn_smem_dq1<64, R>(), stream, a);
+            e = tc ? launch_attn_rows(attn_bwd_dq_tc_kernel<64>, 128, 128, d, d->heads, TcDq<64>::SMEM, stream, a)
+                   : launch_attn(attn_bwd_dq_kernel<64, R>, R, d, d->heads, attn_smem_dq1<64, R>(), stream, a);
     } else {
         e = launch_attn(attn_bwd_dkv_kernel<128, R>, R, d, d->kv_heads * a.hsplit, attn_smem_bwd<128, R>(), stream,
                         a, a.hsplit);
         if (e == cudaSuccess)
-            e = launch_attn(attn_bwd_dq_kernel<128, R>, R, d, d->heads, attn_smem_dq1<128, R>(), stream, a);
+            e = tc ? launch_attn_rows(attn_bwd_dq_tc_kernel<128>, 128, 128, d, d->heads, TcDq<128>::SMEM, stream, a)
+                   : launch_attn(attn_bwd_dq_kernel<128, R>, R, d, d->heads, attn_smem_dq1<128, R>(), stream, a);
     }
     return e == cudaSuccess ? MLORA_OK : MLORA_CUDA;
 }
