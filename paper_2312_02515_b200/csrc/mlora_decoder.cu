@@ -1119,6 +1119,211 @@ __global__ void __launch_bounds__(128, 1) attn_bwd_dq_tc_kernel(AttnArgs a) {
 static_assert(2 * TcDq<128>::Q_BYTES + 2 * TcDq<128>::K_BYTES >= 128 * Tile<128>::LDF * 4, "dQ stage fits");
 static_assert(2 * TcDq<64>::Q_BYTES + 2 * TcDq<64>::K_BYTES >= 128 * Tile<64>::LDF * 4, "dQ stage fits");
 
+// dK, dV on the 5th-generation tensor cores: one CTA of 4 warps per (128-key
+// block, sequence, K/V head, head part); thread t owns key row t = TMEM lane t.
+// Per (query head, 64-query tile) the CTA computes the transposed products
+//   S^T = K Q^T and dP^T = V dO^T     (tcgen05.mma, M=128 N=64, K-major),
+// each key's thread forms P^T = exp2(S^T c2 - lse2) (causal-masked) and
+// dS^T = P^T (dP^T - D), writes both (bf16) as swizzled A operands, and
+//   dV += P^T dO,  dK += dS^T Q        (M=128 N=HD, dO / Q as MN-major operands)
+// accumulate in TMEM over the group's query heads and the query tiles.  Q / dO
+// tiles are double-buffered (the next pair streams in under the current MMAs).
+// A GQA / MQA group's heads are split over a cluster as in attn_bwd_dkv_kernel;
+// the partials meet in DSMEM, summed in rank order (deterministic).
+template <int HD>
+struct TcDkv {
+    static constexpr int BK = 128, BQ = 64, NB = HD / 64;
+    static constexpr int K_BYTES = BK * 128 * NB, Q_BYTES = BQ * 128 * NB, P_BYTES = BK * 128;
+    static constexpr int SMEM = 2 * K_BYTES + 4 * Q_BYTES + 2 * P_BYTES + 4 * BQ * 4 + 64;
+    static constexpr uint32_t ST_COL = 0, DPT_COL = 64, DV_COL = 128, DK_COL = 128 + HD, TMEM_COLS = 512;
+    static constexpr uint32_t IDESC_S = tc5::idesc_bf16_f32(128, BQ, false, false);
+    static constexpr uint32_t IDESC_G = tc5::idesc_bf16_f32(128, HD, false, true);
+};
+
+template <int HD>
+__global__ void __launch_bounds__(128, 1) attn_bwd_dkv_tc_kernel(AttnArgs a) {
+    using T = TcDkv<HD>;
+    pdl_prologue();
+    int start, len;
+    seq_range(a, blockIdx.y, start, len);
+    const int slot = a.seq_off[blockIdx.y + 1] - start;
+    const int k0 = blockIdx.x * T::BK;
+    if (k0 >= slot) return;
+    const int kvh = blockIdx.z / a.hsplit, part = blockIdx.z % a.hsplit;
+    const int gh = a.heads / a.kv_heads / a.hsplit;
+    const int h0 = kvh * (a.heads / a.kv_heads) + part * gh;
+    extern __shared__ __align__(1024) uint8_t smk[];
+    if ((smem_u32(smk) & 1023) != 0) __trap();
+    uint8_t* Ks = smk;
+    uint8_t* Vs = Ks + T::K_BYTES;
+    uint8_t* QD = Vs + T::K_BYTES;          // (Q, dO) x 2 buffers
+    uint8_t* Pt = QD + 4 * T::Q_BYTES;
+    uint8_t* dSt = Pt + T::P_BYTES;
+    float* stats = reinterpret_cast<float*>(dSt + T::P_BYTES);  // (lse2, dsum) x 2 buffers
+    uint64_t* bar = reinterpret_cast<uint64_t*>(stats + 4 * T::BQ);
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
+    const int warp = threadIdx.x >> 5, row = threadIdx.x;
+    if (threadIdx.x == 0) {
+        tc5::mbar_init(bar, 1);
+        tc5::fence_barrier_init();
+    }
+    if (warp == 0) {
+        tc5::tmem_alloc(tslot, T::TMEM_COLS);
+        tc5::tmem_relinquish();
+    }
+    const int qt0 = k0 / T::BQ, nq = (len + T::BQ - 1) / T::BQ - qt0;
+    const int nit = nq > 0 ? gh * nq : 0;
+    auto fetch = [&](int it) {
+        const int h = h0 + it / nq, q0 = (qt0 + it % nq) * T::BQ, b = it & 1;
+        uint8_t* Qb = QD + 2 * T::Q_BYTES * b;
+        stage_sw128<HD>(Qb, T::BQ, a.q, a.ldq, start, q0, len, h * HD);
+        stage_sw128<HD>(Qb + T::Q_BYTES, T::BQ, a.dO, a.lddo, start, q0, len, h * HD);
+        load_stats(a, h, start, q0, T::BQ, len, stats + b * 2 * T::BQ, stats + b * 2 * T::BQ + T::BQ);
+        cp_async_commit();
+    };
+    stage_sw128<HD>(Ks, T::BK, a.k, a.ldk, start, k0, len, kvh * HD);
+    stage_sw128<HD>(Vs, T::BK, a.v, a.ldv, start, k0, len, kvh * HD);
+    cp_async_commit();
+    if (nit > 0) fetch(0);
+    tc5::tc_fence_before();
+    __syncthreads();
+    tc5::tc_fence_after();
+    const uint32_t tmem = *tslot;
+    const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+    const float c2 = a.scale * kLog2e;
+    const int kj = k0 + row;
+    uint32_t phase = 0;
+    for (int it = 0; it < nit; ++it) {
+        const int q0 = (qt0 + it % nq) * T::BQ, b = it & 1;
+        cp_async_wait<0>();  // K, V and this iteration's (Q, dO, stats) landed
+        fence_proxy_async();
+        __syncthreads();
+        const uint8_t* Qb = QD + 2 * T::Q_BYTES * b;
+        const uint8_t* dOb = Qb + T::Q_BYTES;
+        const float* lse2 = stats + b * 2 * T::BQ;
+        const float* dsm = lse2 + T::BQ;
+        if (threadIdx.x == 0) {  // S^T = K Q^T, dP^T = V dO^T
+            tc5::tc_fence_after();
+#pragma unroll
+            for (int j = 0; j < HD / 16; ++j) {
+                const uint32_t ko = (j / 4) * T::BK * 128 + (j % 4) * 32, qo = (j / 4) * T::BQ * 128 + (j % 4) * 32;
+                tc5::mma_bf16(tmem + T::ST_COL, tc5::sdesc_sw128(smem_u32(Ks + ko), 16, 1024),
+                              tc5::sdesc_sw128(smem_u32(Qb + qo), 16, 1024), T::IDESC_S, j > 0 ? 1u : 0u);
+                tc5::mma_bf16(tmem + T::DPT_COL, tc5::sdesc_sw128(smem_u32(Vs + ko), 16, 1024),
+                              tc5::sdesc_sw128(smem_u32(dOb + qo), 16, 1024), T::IDESC_S, j > 0 ? 1u : 0u);
+            }
+            tc5::tc_commit(bar);
+        }
+        if (it + 1 < nit) fetch(it + 1);  // the other buffer's previous readers finished last iteration
+        tc5::mbar_wait(bar, phase);
+        phase ^= 1u;
+        tc5::tc_fence_after();
+        const bool interior = k0 + T::BK - 1 <= q0 && q0 + T::BQ <= len;
+        uint8_t* prow = Pt + row * 128;
+        uint8_t* drow = dSt + row * 128;
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+            uint32_t sv[32], pv[32];
+            tc5::tmem_ld32(tmem + lane_base + T::ST_COL + half * 32, sv);
+            tc5::tmem_ld32(tmem + lane_base + T::DPT_COL + half * 32, pv);
+            tc5::tmem_wait_ld();
+#pragma unroll
+            for (int ch = 0; ch < 4; ++ch) {
+                float p[8], d[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                    const int cq = half * 32 + ch * 8 + e, qi = q0 + cq;
+                    float pe = ex2_ftz(fmaf(__uint_as_float(sv[ch * 8 + e]), c2, -lse2[cq]));
+                    if (!interior) pe = (kj <= qi && qi < len) ? pe : 0.f;
+                    p[e] = pe;
+                    d[e] = pe * (__uint_as_float(pv[ch * 8 + e]) - dsm[cq]);
+                }
+                const int chunk = half * 4 + ch, off = (chunk ^ (row & 7)) << 4;
+                uint4 w;
+                w.x = pack2(p[0], p[1]), w.y = pack2(p[2], p[3]), w.z = pack2(p[4], p[5]), w.w = pack2(p[6], p[7]);
+                *reinterpret_cast<uint4*>(prow + off) = w;
+                w.x = pack2(d[0], d[1]), w.y = pack2(d[2], d[3]), w.z = pack2(d[4], d[5]), w.w = pack2(d[6], d[7]);
+                *reinterpret_cast<uint4*>(drow + off) = w;
+            }
+        }
+        fence_proxy_async();
+        tc5::tc_fence_before();
+        __syncthreads();
+        if (threadIdx.x == 0) {  // dV += P^T dO, dK += dS^T Q
+            tc5::tc_fence_after();
+#pragma unroll
+            for (int j = 0; j < T::BQ / 16; ++j) {
+                const uint32_t acc = (it > 0 || j > 0) ? 1u : 0u;
+                tc5::mma_bf16(tmem + T::DV_COL, tc5::sdesc_sw128(smem_u32(Pt + j * 32), 16, 1024),
+                              tc5::sdesc_sw128(smem_u32(dOb + j * 2048), T::BQ * 128, 1024), T::IDESC_G, acc);
+                tc5::mma_bf16(tmem + T::DK_COL, tc5::sdesc_sw128(smem_u32(dSt + j * 32), 16, 1024),
+                              tc5::sdesc_sw128(smem_u32(Qb + j * 2048), T::BQ * 128, 1024), T::IDESC_G, acc);
+            }
+            tc5::tc_commit(bar);
+        }
+        tc5::mbar_wait(bar, phase);
+        phase ^= 1u;
+        tc5::tc_fence_after();
+        tc5::tc_fence_before();
+        __syncthreads();  // P^T, dS^T, S^T / dP^T and this (Q, dO) buffer are reused
+    }
+    cp_async_wait<0>();
+    __syncthreads();
+    // ---- epilogue: dK (scaled, un-rotated) then dV, through an fp32 stage over K / V / Q / dO
+    float* st = reinterpret_cast<float*>(smk);
+    const bool rope_out = a.rope_base > 0.f;
+    namespace cg = cooperative_groups;
+    for (int which = 0; which < 2; ++which) {  // 0: dK, 1: dV
+        const uint32_t col = which == 0 ? T::DK_COL : T::DV_COL;
+        const float sc = which == 0 ? a.scale : 1.f;
+        if (nit > 0) {
+#pragma unroll
+            for (int c0 = 0; c0 < HD; c0 += 32) {
+                uint32_t v[32];
+                tc5::tmem_ld32(tmem + lane_base + col + c0, v);
+                tc5::tmem_wait_ld();
+#pragma unroll
+                for (int c = 0; c < 32; ++c) st[row * Tile<HD>::LDF + c0 + c] = sc * __uint_as_float(v[c]);
+            }
+        } else {
+            for (int c = 0; c < HD; ++c) st[row * Tile<HD>::LDF + c] = 0.f;
+        }
+        __nv_bfloat16* dst = which == 0 ? a.dk : a.dv;
+        const long long ld = which == 0 ? a.lddk : a.lddv;
+        const bool rope = which == 0 && rope_out;
+        if (a.hsplit > 1) {
+            cg::cluster_group cluster = cg::this_cluster();
+            cluster.sync();
+            const float* parts[8];
+            for (int k = 0; k < a.hsplit; ++k) parts[k] = cluster.map_shared_rank(st, k);
+            const int lo = part * T::BK / a.hsplit, hi = (part + 1) * T::BK / a.hsplit;
+            for (int hlf = 0; hlf < 2; ++hlf) {  // store_tile_sum covers 64-row tiles
+                const int l0 = max(lo, hlf * kBM), h1 = min(hi, hlf * kBM + kBM);
+                if (l0 >= h1) continue;
+                const float* ph[8];
+                for (int k = 0; k < a.hsplit; ++k) ph[k] = parts[k] + hlf * kBM * Tile<HD>::LDF;
+                store_tile_sum<HD>(ph, a.hsplit, dst, ld, start, k0 + hlf * kBM, l0 - hlf * kBM, h1 - hlf * kBM, len,
+                                   kvh * HD, slot, a.rope_base, rope);
+            }
+            cluster.sync();
+        } else {
+            __syncthreads();
+            for (int hlf = 0; hlf < 2; ++hlf)
+                store_tile<HD>(st + hlf * kBM * Tile<HD>::LDF, dst, ld, start, k0 + hlf * kBM, len, kvh * HD, slot,
+                               a.rope_base, rope);
+            __syncthreads();
+        }
+    }
+    tc5::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc5::tc_fence_after();
+        tc5::tmem_dealloc(tmem, T::TMEM_COLS);
+    }
+}
+static_assert(2 * TcDkv<128>::K_BYTES + 4 * TcDkv<128>::Q_BYTES >= 128 * Tile<128>::LDF * 4, "dK/dV stage fits");
+static_assert(2 * TcDkv<64>::K_BYTES + 4 * TcDkv<64>::Q_BYTES >= 128 * Tile<64>::LDF * 4, "dK/dV stage fits");
+
 // dK, dV: one CTA per (R-key block, sequence, K/V head, head part); loops over
 // its query heads and the 64-query tiles that can see the block (causal).  With
 // grouped / multi-query attention the group's query heads are split over a
@@ -1368,15 +1573,16 @@ AttnArgs attn_args(const mlora_attn_desc* d) {
 
 template <typename K>
 cudaError_t launch_attn(K kernel, int rows_per_cta, const mlora_attn_desc* d, int heads_z, size_t smem, void* stream,
-                        const AttnArgs& a, int cluster_z = 1) {
+                        const AttnArgs& a, int cluster_z = 1, int threads = 0) {
     if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
         cudaSuccess)
         return cudaErrorInvalidValue;
     const dim3 grid((d->max_len + rows_per_cta - 1) / rows_per_cta, d->num_seqs, heads_z);
-    if (cluster_z <= 1) return launch(kernel, grid, dim3(2 * rows_per_cta), smem, stream, a);
+    const dim3 block(threads > 0 ? threads : 2 * rows_per_cta);
+    if (cluster_z <= 1) return launch(kernel, grid, block, smem, stream, a);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
-    cfg.blockDim = dim3(2 * rows_per_cta);
+    cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = static_cast<cudaStream_t>(stream);
     cudaLaunchAttribute attr[2];
@@ -1570,6 +1776,17 @@ mlora_status mlora_attn_bwd(const mlora_attn_desc* d, const void* q, int64_t ldq
     cudaError_t e;
     constexpr int R = kBwdRows;
     const bool tc = attn_tc_enabled() && a.vec && !a.rope_in && (reinterpret_cast<uintptr_t>(dq) & 3) == 0;
+    if (tc) {  // dK / dV on tcgen05: 128-key blocks, one CTA per SM (TMEM: 384 of 512 columns)
+        e = hd == 64 ? launch_attn(attn_bwd_dkv_tc_kernel<64>, 128, d, d->kv_heads * a.hsplit, TcDkv<64>::SMEM, stream,
+                                   a, a.hsplit, 128)
+                     : launch_attn(attn_bwd_dkv_tc_kernel<128>, 128, d, d->kv_heads * a.hsplit, TcDkv<128>::SMEM,
+                                   stream, a, a.hsplit, 128);
+        if (e == cudaSuccess)
+            e = hd == 64 ? launch_attn_rows(attn_bwd_dq_tc_kernel<64>, 128, 128, d, d->heads, TcDq<64>::SMEM, stream, a)
+                         : launch_attn_rows(attn_bwd_dq_tc_kernel<128>, 128, 128, d, d->heads, TcDq<128>::SMEM, stream,
+                                            a);
+        return e == cudaSuccess ? MLORA_OK : MLORA_CUDA;
+    }
     if (hd == 64) {
         e = launch_attn(attn_bwd_dkv_kernel<64, R>, R, d, d->kv_heads * a.hsplit, attn_smem_bwd<64, R>(), stream, a,
                         a.hsplit);
