@@ -1013,9 +1013,22 @@ __global__ void __launch_bounds__(128, 1) attn_bwd_dq_tc_kernel(AttnArgs a) {
     const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
     const float c2 = a.scale * kLog2e;
     const int qi = q0 + row;
-    const bool real = qi < len;  // this row's lse (log2 units) and D = rowsum(dO O), in registers
+    const bool real = qi < len;  // this row's lse (log2 units), in a register
     const float nl = real ? -a.lse[(long long)h * a.rows + start + qi] * kLog2e : 0.f;
-    const float dr = real ? a.dsum[(long long)h * a.rows + start + qi] : 0.f;
+    // D = rowsum(dO * O) of this row, published for the dK/dV kernel that runs next
+    float dr = 0.f;
+    if (real) {
+        const __nv_bfloat16* orow = a.o + (long long)(start + qi) * a.ldo + h * HD;
+        const __nv_bfloat16* drow = a.dO + (long long)(start + qi) * a.lddo + h * HD;
+        for (int c = 0; c < HD; c += 8) {
+            float ov[8], dv[8];
+            ld8(orow + c, ov);
+            ld8(drow + c, dv);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) dr = fmaf(ov[e], dv[e], dr);
+        }
+    }
+    if (qi < slot) a.dsum[(long long)h * a.rows + start + qi] = dr;
     uint32_t phase = 0;
     for (int kt = 0; kt < nkt; ++kt) {
         cp_async_wait<0>();  // K_kt and V_kt (and Q, dO) landed
@@ -1769,24 +1782,26 @@ mlora_status mlora_attn_bwd(const mlora_attn_desc* d, const void* q, int64_t ldq
     a.vec = rows16(q, ldq) && rows16(k, ldk) && rows16(v, ldv) && rows16(dout, lddo);
     a.dsum = dsum;
     a.hsplit = attn_hsplit(d);
+    cudaError_t e;
+    constexpr int R = kBwdRows;
+    const bool tc = attn_tc_enabled() && a.vec && !a.rope_in && (reinterpret_cast<uintptr_t>(dq) & 3) == 0 &&
+                    (reinterpret_cast<uintptr_t>(o) & 15) == 0 && ldo % 8 == 0;
+    if (tc) {
+        // dQ first: its CTAs also compute D = rowsum(dO O) for their rows (no separate pass);
+        // then dK / dV on tcgen05 (128-key blocks, one CTA per SM: 384 of 512 TMEM columns)
+        e = hd == 64 ? launch_attn_rows(attn_bwd_dq_tc_kernel<64>, 128, 128, d, d->heads, TcDq<64>::SMEM, stream, a)
+                     : launch_attn_rows(attn_bwd_dq_tc_kernel<128>, 128, 128, d, d->heads, TcDq<128>::SMEM, stream, a);
+        if (e == cudaSuccess)
+            e = hd == 64 ? launch_attn(attn_bwd_dkv_tc_kernel<64>, 128, d, d->kv_heads * a.hsplit, TcDkv<64>::SMEM,
+                                       stream, a, a.hsplit, 128)
+                         : launch_attn(attn_bwd_dkv_tc_kernel<128>, 128, d, d->kv_heads * a.hsplit, TcDkv<128>::SMEM,
+                                       stream, a, a.hsplit, 128);
+        return e == cudaSuccess ? MLORA_OK : MLORA_CUDA;
+    }
     const long long warps = d->rows * d->heads;
     if (launch(attn_dsum_kernel, dim3(static_cast<unsigned>((warps * 32 + 255) / 256)), dim3(256), 0, stream, a,
                hd) != cudaSuccess)
         return MLORA_CUDA;
-    cudaError_t e;
-    constexpr int R = kBwdRows;
-    const bool tc = attn_tc_enabled() && a.vec && !a.rope_in && (reinterpret_cast<uintptr_t>(dq) & 3) == 0;
-    if (tc) {  // dK / dV on tcgen05: 128-key blocks, one CTA per SM (TMEM: 384 of 512 columns)
-        e = hd == 64 ? launch_attn(attn_bwd_dkv_tc_kernel<64>, 128, d, d->kv_heads * a.hsplit, TcDkv<64>::SMEM, stream,
-                                   a, a.hsplit, 128)
-                     : launch_attn(attn_bwd_dkv_tc_kernel<128>, 128, d, d->kv_heads * a.hsplit, TcDkv<128>::SMEM,
-                                   stream, a, a.hsplit, 128);
-        if (e == cudaSuccess)
-            e = hd == 64 ? launch_attn_rows(attn_bwd_dq_tc_kernel<64>, 128, 128, d, d->heads, TcDq<64>::SMEM, stream, a)
-                         : launch_attn_rows(attn_bwd_dq_tc_kernel<128>, 128, 128, d, d->heads, TcDq<128>::SMEM, stream,
-                                            a);
-        return e == cudaSuccess ? MLORA_OK : MLORA_CUDA;
-    }
     if (hd == 64) {
         e = launch_attn(attn_bwd_dkv_kernel<64, R>, R, d, d->kv_heads * a.hsplit, attn_smem_bwd<64, R>(), stream, a,
                         a.hsplit);
