@@ -100,10 +100,12 @@ class ClockSampler(threading.Thread):
         if not self.ok:
             return
         nv = self.nv
+        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            getattr(nv, "nvmlDeviceGetCurrentClocksThrottleReasons")
         while not self._halt.is_set():
             try:
                 self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
-                self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.reasons |= get_reasons(self.h)
             except Exception:
                 pass
             time.sleep(self.period)
