@@ -20,8 +20,10 @@
 // accumulation), flash-style (no score matrix in HBM), with a deterministic
 // two-kernel backward (dK/dV per key tile, dQ per query tile; no atomics).
 #include <cooperative_groups.h>
+#include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <cmath>
@@ -236,6 +238,7 @@ struct AttnArgs {
     int rope_in;         // rotate Q/K while staging (they arrive unrotated)
     int vec;             // every staged row is 16-byte aligned: cp.async staging
     int hsplit;          // dK/dV: query heads of a K/V group split over a cluster of hsplit CTAs
+    int tma;             // the tensor maps below are valid (dK/dV loads Q / dO tiles by TMA)
     long long rows;
     const __nv_bfloat16 *q, *k, *v, *o, *dO;
     long long ldq, ldk, ldv, ldo, lddo;
@@ -1337,6 +1340,306 @@ __global__ void __launch_bounds__(128, 1) attn_bwd_dkv_tc_kernel(AttnArgs a) {
 static_assert(2 * TcDkv<128>::K_BYTES + 4 * TcDkv<128>::Q_BYTES >= 128 * Tile<128>::LDF * 4, "dK/dV stage fits");
 static_assert(2 * TcDkv<64>::K_BYTES + 4 * TcDkv<64>::Q_BYTES >= 128 * Tile<64>::LDF * 4, "dK/dV stage fits");
 
+// Warp-specialised dK / dV (tcgen05): the same products as attn_bwd_dkv_tc_kernel,
+// pipelined across three roles of one CTA (288 threads):
+//   warps 0-3  elementwise: key row t = TMEM lane t forms P^T, dS^T of pair `it`
+//   warps 4-7  loaders: cp.async of K / V once, then (Q, dO, lse, D) per pair into
+//              two buffers, each refilled once the dV / dK product reading it is done
+//   warp 8     MMA issuer: S^T / dP^T of pair it+1 go out before waiting for pair
+//              it's P^T / dS^T, so they run under the elementwise work; dV / dK of
+//              pair it then run under the elementwise work of pair it+1
+// Handshakes are mbarriers (tcgen05.commit for MMA completion); S^T / dP^T are
+// double-buffered in TMEM (2 x 128 columns) and P^T / dS^T in shared memory.
+template <int HD>
+struct WsDkv {
+    static constexpr int BK = 128, BQ = 64, NB = HD / 64, STAGES = 3;  // (Q, dO, lse, D) stages
+    static constexpr int K_BYTES = BK * 128 * NB, Q_BYTES = BQ * 128 * NB, P_BYTES = BK * 128;
+    static constexpr int SMEM = 2 * K_BYTES + 2 * STAGES * Q_BYTES + 4 * P_BYTES + 2 * STAGES * BQ * 4 + 192;
+    static constexpr uint32_t SBUF = 128, ST_COL = 0, DPT_COL = 64, DV_COL = 256, DK_COL = 256 + HD, TMEM_COLS = 512;
+    static constexpr uint32_t IDESC_S = tc5::idesc_bf16_f32(128, BQ, false, false);
+    static constexpr uint32_t IDESC_G = tc5::idesc_bf16_f32(128, HD, false, true);
+};
+
+// cp.async rows [r0, r0 + rows) of one head into a swizzled region, strided over
+// `nthr` threads (the loader warps) starting at `tid`.
+template <int HD>
+__device__ __forceinline__ void stage_sw128_warp(uint8_t* region, int rows, const __nv_bfloat16* src, long long ld,
+                                                 int start, int r0, int len, int col, int tid, int nthr = 128) {
+    constexpr int NB = HD / 64;
+    for (int e = tid; e < rows * NB * 8; e += nthr) {
+        const int ch = e & 7, rb = e >> 3, r = rb % rows, b = rb / rows;
+        uint8_t* dst = region + b * rows * 128 + r * 128 + ((ch ^ (r & 7)) << 4);
+        if (r0 + r < len)
+            cp_async16(smem_u32(dst), src + (long long)(start + r0 + r) * ld + col + b * 64 + ch * 8);
+        else
+            *reinterpret_cast<uint4*>(dst) = make_uint4(0, 0, 0, 0);
+    }
+}
+
+template <int HD>
+__global__ void __launch_bounds__(288, 1) attn_bwd_dkv_ws_kernel(const __grid_constant__ CUtensorMap tq,
+                                                                  const __grid_constant__ CUtensorMap tdo,
+                                                                  AttnArgs a) {
+    using T = WsDkv<HD>;
+    pdl_prologue();
+    int start, len;
+    seq_range(a, blockIdx.y, start, len);
+    const int slot = a.seq_off[blockIdx.y + 1] - start;
+    const int k0 = blockIdx.x * T::BK;
+    if (k0 >= slot) return;
+    const int kvh = blockIdx.z / a.hsplit, part = blockIdx.z % a.hsplit;
+    const int gh = a.heads / a.kv_heads / a.hsplit;
+    const int h0 = kvh * (a.heads / a.kv_heads) + part * gh;
+    extern __shared__ __align__(1024) uint8_t smw[];
+    if ((smem_u32(smw) & 1023) != 0) __trap();
+    uint8_t* Ks = smw;
+    uint8_t* Vs = Ks + T::K_BYTES;
+    uint8_t* QD = Vs + T::K_BYTES;               // (Q, dO) x STAGES
+    uint8_t* PD = QD + 2 * T::STAGES * T::Q_BYTES;  // (P^T, dS^T) x 2
+    float* stats = reinterpret_cast<float*>(PD + 4 * T::P_BYTES);  // (lse2, dsum) x STAGES
+    uint64_t* kv_full = reinterpret_cast<uint64_t*>(stats + 2 * T::STAGES * T::BQ);
+    uint64_t* tma_full = kv_full + 1;         // [STAGES] TMA bytes of a stage's Q / dO landed
+    uint64_t* qd_full = tma_full + T::STAGES; // [STAGES] loaders: stats written (and tail rows zeroed)
+    uint64_t* qd_free = qd_full + T::STAGES;  // [STAGES] MMA commit (dV / dK of the stage's pair) -> loaders
+    uint64_t* s_full = qd_free + T::STAGES;   // [2] MMA commit -> elementwise
+    uint64_t* p_full = s_full + 2;            // [2] elementwise (128) -> MMA
+    uint64_t* g_done = p_full + 2;            // [2] MMA commit (dV / dK of a pair) -> elementwise
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(g_done + 2);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        tc5::mbar_init(kv_full, 1);
+        for (int i = 0; i < T::STAGES; ++i) {
+            tc5::mbar_init(tma_full + i, 1);
+            tc5::mbar_init(qd_full + i, 1);
+            tc5::mbar_init(qd_free + i, 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            tc5::mbar_init(s_full + i, 1);
+            tc5::mbar_init(p_full + i, 128);
+            tc5::mbar_init(g_done + i, 1);
+        }
+        tc5::fence_barrier_init();
+    }
+    if (warp == 0) {
+        tc5::tmem_alloc(tslot, T::TMEM_COLS);
+        tc5::tmem_relinquish();
+    }
+    tc5::tc_fence_before();
+    __syncthreads();
+    tc5::tc_fence_after();
+    const uint32_t tmem = *tslot;
+    const int qt0 = k0 / T::BQ, nq = (len + T::BQ - 1) / T::BQ - qt0;
+    const int nit = nq > 0 ? gh * nq : 0;
+
+    if (warp >= 4 && warp < 8) {
+        // ------------------------------------------------ loaders (128 threads, named barrier 1):
+        // K / V once by cp.async; per pair the Q / dO tiles by TMA (one thread, 128-byte
+        // swizzle straight into the operand layout) and lse / D by 64 threads
+        const int lt = threadIdx.x - 128;
+        auto loaders_sync = [] { asm volatile("bar.sync 1, 128;" ::: "memory"); };
+        if (lt == 0) {
+            tc5::tma_prefetch_desc(&tq);
+            tc5::tma_prefetch_desc(&tdo);
+        }
+        stage_sw128_warp<HD>(Ks, T::BK, a.k, a.ldk, start, k0, len, kvh * HD, lt);
+        stage_sw128_warp<HD>(Vs, T::BK, a.v, a.ldv, start, k0, len, kvh * HD, lt);
+        cp_async_commit();
+        cp_async_wait<0>();
+        fence_proxy_async();
+        loaders_sync();
+        if (lt == 0) tc5::mbar_arrive(kv_full);
+        for (int it = 0; it < nit; ++it) {
+            const int st = it % T::STAGES, h = h0 + it / nq, q0 = (qt0 + it % nq) * T::BQ;
+            if (it >= T::STAGES) tc5::mbar_wait(qd_free + st, ((it - T::STAGES) / T::STAGES) & 1);
+            uint8_t* Qb = QD + 2 * T::Q_BYTES * st;
+            if (lt == 0) {
+                tc5::mbar_arrive_expect_tx(tma_full + st, 2 * T::Q_BYTES);
+#pragma unroll
+                for (int blk = 0; blk < T::NB; ++blk) {
+                    tc5::tma_load_2d(smem_u32(Qb + blk * T::BQ * 128), &tq, tma_full + st, h * HD + blk * 64,
+                                     start + q0);
+                    tc5::tma_load_2d(smem_u32(Qb + T::Q_BYTES + blk * T::BQ * 128), &tdo, tma_full + st,
+                                     h * HD + blk * 64, start + q0);
+                }
+            }
+            float* lse2 = stats + st * 2 * T::BQ;
+            if (lt < T::BQ) {
+                const bool ok = q0 + lt < len;
+                lse2[lt] = ok ? a.lse[(long long)h * a.rows + start + q0 + lt] * kLog2e : 0.f;
+                lse2[T::BQ + lt] = ok ? a.dsum[(long long)h * a.rows + start + q0 + lt] : 0.f;
+            }
+            if (q0 + T::BQ > len) {
+                // the tile runs past the sequence's real tokens: the box holds the next
+                // rows of the fused batch (another sequence, maybe another job).  Zero
+                // them: masked P / dS are 0, but 0 * inf would still leak a diverged
+                // neighbour into this job's dK / dV.
+                tc5::mbar_wait(tma_full + st, (it / T::STAGES) & 1);
+                const int r0 = max(len - q0, 0);
+                for (int e = lt; e < (T::BQ - r0) * 2 * T::NB * 8; e += 128) {
+                    const int ch = e & 7, rb = e >> 3, r = r0 + rb % (T::BQ - r0), blk = rb / (T::BQ - r0);
+                    *reinterpret_cast<uint4*>(Qb + blk * T::BQ * 128 + r * 128 + (ch << 4)) = make_uint4(0, 0, 0, 0);
+                }
+                fence_proxy_async();
+            }
+            loaders_sync();
+            if (lt == 32) tc5::mbar_arrive(qd_full + st);  // stats written, tails zeroed (release)
+        }
+    } else if (warp == 8) {
+        // ------------------------------------------------ MMA issuer
+        if (lane == 0 && nit > 0) {
+            auto issue_s = [&](int it) {
+                const int b = it & 1, st = it % T::STAGES;
+                tc5::mbar_wait(tma_full + st, (it / T::STAGES) & 1);
+                tc5::mbar_wait(qd_full + st, (it / T::STAGES) & 1);
+                if (it >= 2) tc5::mbar_wait(p_full + b, ((it - 2) >> 1) & 1);  // S buffer b read out
+                tc5::tc_fence_after();
+                const uint8_t* Qb = QD + 2 * T::Q_BYTES * st;
+                const uint8_t* dOb = Qb + T::Q_BYTES;
+                const uint32_t sb = b * T::SBUF;
+#pragma unroll
+                for (int j = 0; j < HD / 16; ++j) {
+                    const uint32_t ko = (j / 4) * T::BK * 128 + (j % 4) * 32, qo = (j / 4) * T::BQ * 128 + (j % 4) * 32;
+                    tc5::mma_bf16(tmem + sb + T::ST_COL, tc5::sdesc_sw128(smem_u32(Ks + ko), 16, 1024),
+                                  tc5::sdesc_sw128(smem_u32(Qb + qo), 16, 1024), T::IDESC_S, j > 0 ? 1u : 0u);
+                    tc5::mma_bf16(tmem + sb + T::DPT_COL, tc5::sdesc_sw128(smem_u32(Vs + ko), 16, 1024),
+                                  tc5::sdesc_sw128(smem_u32(dOb + qo), 16, 1024), T::IDESC_S, j > 0 ? 1u : 0u);
+                }
+                tc5::tc_commit(s_full + b);
+            };
+            tc5::mbar_wait(kv_full, 0);
+            issue_s(0);
+            for (int it = 0; it < nit; ++it) {
+                const int b = it & 1;
+                if (it + 1 < nit) issue_s(it + 1);  // runs under pair it's elementwise work
+                tc5::mbar_wait(p_full + b, (it >> 1) & 1);
+                tc5::tc_fence_after();
+                const uint8_t* Qb = QD + 2 * T::Q_BYTES * (it % T::STAGES);
+                const uint8_t* dOb = Qb + T::Q_BYTES;
+                const uint8_t* Pt = PD + 2 * T::P_BYTES * b;
+                const uint8_t* dSt = Pt + T::P_BYTES;
+#pragma unroll
+                for (int j = 0; j < T::BQ / 16; ++j) {
+                    const uint32_t acc = (it > 0 || j > 0) ? 1u : 0u;
+                    tc5::mma_bf16(tmem + T::DV_COL, tc5::sdesc_sw128(smem_u32(Pt + j * 32), 16, 1024),
+                                  tc5::sdesc_sw128(smem_u32(dOb + j * 2048), T::BQ * 128, 1024), T::IDESC_G, acc);
+                    tc5::mma_bf16(tmem + T::DK_COL, tc5::sdesc_sw128(smem_u32(dSt + j * 32), 16, 1024),
+                                  tc5::sdesc_sw128(smem_u32(Qb + j * 2048), T::BQ * 128, 1024), T::IDESC_G, acc);
+                }
+                tc5::tc_commit(g_done + b);
+                tc5::tc_commit(qd_free + it % T::STAGES);
+            }
+        }
+        __syncwarp();
+    } else {
+        // ------------------------------------------------ elementwise (warps 0-3)
+        const int row = threadIdx.x;
+        const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+        const float c2 = a.scale * kLog2e;
+        const int kj = k0 + row;
+        for (int it = 0; it < nit; ++it) {
+            const int b = it & 1, q0 = (qt0 + it % nq) * T::BQ;
+            tc5::mbar_wait(qd_full + it % T::STAGES, (it / T::STAGES) & 1);  // lse / D of this pair visible
+            tc5::mbar_wait(s_full + b, (it >> 1) & 1);
+            if (it >= 2) tc5::mbar_wait(g_done + b, ((it - 2) >> 1) & 1);  // P / dS buffer b free
+            tc5::tc_fence_after();
+            const float* lse2 = stats + (it % T::STAGES) * 2 * T::BQ;
+            const float* dsm = lse2 + T::BQ;
+            const uint32_t sb = b * T::SBUF;
+            const bool interior = k0 + T::BK - 1 <= q0 && q0 + T::BQ <= len;
+            uint8_t* prow = PD + 2 * T::P_BYTES * b + row * 128;
+            uint8_t* drow = prow + T::P_BYTES;
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                uint32_t sv[32], pv[32];
+                tc5::tmem_ld32(tmem + lane_base + sb + T::ST_COL + half * 32, sv);
+                tc5::tmem_ld32(tmem + lane_base + sb + T::DPT_COL + half * 32, pv);
+                tc5::tmem_wait_ld();
+#pragma unroll
+                for (int ch = 0; ch < 4; ++ch) {
+                    float p[8], d[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        const int cq = half * 32 + ch * 8 + e, qi = q0 + cq;
+                        float pe = ex2_ftz(fmaf(__uint_as_float(sv[ch * 8 + e]), c2, -lse2[cq]));
+                        if (!interior) pe = (kj <= qi && qi < len) ? pe : 0.f;
+                        p[e] = pe;
+                        d[e] = pe * (__uint_as_float(pv[ch * 8 + e]) - dsm[cq]);
+                    }
+                    const int chunk = half * 4 + ch, off = (chunk ^ (row & 7)) << 4;
+                    uint4 w;
+                    w.x = pack2(p[0], p[1]), w.y = pack2(p[2], p[3]), w.z = pack2(p[4], p[5]), w.w = pack2(p[6], p[7]);
+                    *reinterpret_cast<uint4*>(prow + off) = w;
+                    w.x = pack2(d[0], d[1]), w.y = pack2(d[2], d[3]), w.z = pack2(d[4], d[5]), w.w = pack2(d[6], d[7]);
+                    *reinterpret_cast<uint4*>(drow + off) = w;
+                }
+            }
+            fence_proxy_async();
+            tc5::tc_fence_before();
+            tc5::mbar_arrive(p_full + b);  // P^T / dS^T written, S buffer b read out
+        }
+        if (nit > 0) tc5::mbar_wait(g_done + ((nit - 1) & 1), ((nit - 1) >> 1) & 1);  // every product done
+        tc5::tc_fence_after();
+    }
+    __syncthreads();
+    // ---- epilogue (all 9 warps; TMEM read by warps 0-3): dK (scaled, un-rotated) then dV
+    float* st = reinterpret_cast<float*>(smw);
+    const bool rope_out = a.rope_base > 0.f;
+    namespace cg = cooperative_groups;
+    for (int which = 0; which < 2; ++which) {
+        const uint32_t col = which == 0 ? T::DK_COL : T::DV_COL;
+        const float sc = which == 0 ? a.scale : 1.f;
+        if (warp < 4) {
+            const int row = threadIdx.x;
+            const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+            if (nit > 0) {
+#pragma unroll
+                for (int c0 = 0; c0 < HD; c0 += 32) {
+                    uint32_t v[32];
+                    tc5::tmem_ld32(tmem + lane_base + col + c0, v);
+                    tc5::tmem_wait_ld();
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) st[row * Tile<HD>::LDF + c0 + c] = sc * __uint_as_float(v[c]);
+                }
+            } else {
+                for (int c = 0; c < HD; ++c) st[row * Tile<HD>::LDF + c] = 0.f;
+            }
+        }
+        __nv_bfloat16* dst = which == 0 ? a.dk : a.dv;
+        const long long ld = which == 0 ? a.lddk : a.lddv;
+        const bool rope = which == 0 && rope_out;
+        if (a.hsplit > 1) {
+            cg::cluster_group cluster = cg::this_cluster();
+            cluster.sync();
+            const int lo = part * T::BK / a.hsplit, hi = (part + 1) * T::BK / a.hsplit;
+            for (int hlf = 0; hlf < 2; ++hlf) {
+                const int l0 = max(lo, hlf * kBM), h1 = min(hi, hlf * kBM + kBM);
+                if (l0 >= h1) continue;
+                const float* ph[8];
+                for (int k = 0; k < a.hsplit; ++k)
+                    ph[k] = cluster.map_shared_rank(st, k) + hlf * kBM * Tile<HD>::LDF;
+                store_tile_sum<HD>(ph, a.hsplit, dst, ld, start, k0 + hlf * kBM, l0 - hlf * kBM, h1 - hlf * kBM, len,
+                                   kvh * HD, slot, a.rope_base, rope);
+            }
+            cluster.sync();
+        } else {
+            __syncthreads();
+            for (int hlf = 0; hlf < 2; ++hlf)
+                store_tile<HD>(st + hlf * kBM * Tile<HD>::LDF, dst, ld, start, k0 + hlf * kBM, len, kvh * HD, slot,
+                               a.rope_base, rope);
+            __syncthreads();
+        }
+    }
+    tc5::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc5::tc_fence_after();
+        tc5::tmem_dealloc(tmem, T::TMEM_COLS);
+    }
+}
+static_assert(2 * WsDkv<128>::K_BYTES + 2 * WsDkv<128>::STAGES * WsDkv<128>::Q_BYTES >= 128 * Tile<128>::LDF * 4,
+              "stage fits");
+static_assert(WsDkv<128>::SMEM <= 227 * 1024, "dK/dV shared memory");
+
 // dK, dV: one CTA per (R-key block, sequence, K/V head, head part); loops over
 // its query heads and the 64-query tiles that can see the block (causal).  With
 // grouped / multi-query attention the group's query heads are split over a
@@ -1610,6 +1913,50 @@ cudaError_t launch_attn(K kernel, int rows_per_cta, const mlora_attn_desc* d, in
     return cudaLaunchKernelEx(&cfg, kernel, a);
 }
 
+// 2-D TMA map over a [rows, ld] bf16 matrix with 64 x 64 boxes and the 128-byte
+// swizzle of the tcgen05 operand tiles (column = head * head_dim + 64-block).
+bool encode_rows_map(const void* base, long long ld, long long rows, CUtensorMap* out) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    if (!encode || (reinterpret_cast<uintptr_t>(base) & 15) || ld % 8) return false;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(ld), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 2};
+    const cuuint32_t box[2] = {64, 64}, estr[2] = {1, 1};
+    return encode(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// The warp-specialised dK / dV kernel: 128-key blocks, 288 threads, cluster head split.
+template <typename K>
+cudaError_t launch_attn_ws(K kernel, const mlora_attn_desc* d, size_t smem, void* stream, const CUtensorMap& tq,
+                           const CUtensorMap& tdo, const AttnArgs& a) {
+    if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
+        cudaSuccess)
+        return cudaErrorInvalidValue;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((d->max_len + 127) / 128, d->num_seqs, d->kv_heads * a.hsplit);
+    cfg.blockDim = dim3(288);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = static_cast<cudaStream_t>(stream);
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = 1;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = a.hsplit;
+    cfg.attrs = attr;
+    cfg.numAttrs = a.hsplit > 1 ? 2 : 1;
+    return cudaLaunchKernelEx(&cfg, kernel, tq, tdo, a);
+}
+
 // MLORA_ATTN_TC=0 keeps the mma.sync forward / dQ kernels (A/B knob); the
 // tcgen05 ones need pre-rotated Q / K and 16-byte-aligned rows.
 bool attn_tc_enabled() {
@@ -1791,7 +2138,16 @@ mlora_status mlora_attn_bwd(const mlora_attn_desc* d, const void* q, int64_t ldq
         // then dK / dV on tcgen05 (128-key blocks, one CTA per SM: 384 of 512 TMEM columns)
         e = hd == 64 ? launch_attn_rows(attn_bwd_dq_tc_kernel<64>, 128, 128, d, d->heads, TcDq<64>::SMEM, stream, a)
                      : launch_attn_rows(attn_bwd_dq_tc_kernel<128>, 128, 128, d, d->heads, TcDq<128>::SMEM, stream, a);
-        if (e == cudaSuccess)
+        static const bool ws = [] {  // MLORA_ATTN_WS=0: the phase-serial dK / dV kernel (A/B knob)
+            const char* e = std::getenv("MLORA_ATTN_WS");
+            return !(e && e[0] == '0');
+        }();
+        CUtensorMap tq, tdo;
+        const bool maps = ws && encode_rows_map(q, ldq, d->rows, &tq) && encode_rows_map(dout, lddo, d->rows, &tdo);
+        if (e == cudaSuccess && maps)
+            e = hd == 64 ? launch_attn_ws(attn_bwd_dkv_ws_kernel<64>, d, WsDkv<64>::SMEM, stream, tq, tdo, a)
+                         : launch_attn_ws(attn_bwd_dkv_ws_kernel<128>, d, WsDkv<128>::SMEM, stream, tq, tdo, a);
+        else if (e == cudaSuccess)
             e = hd == 64 ? launch_attn(attn_bwd_dkv_tc_kernel<64>, 128, d, d->kv_heads * a.hsplit, TcDkv<64>::SMEM,
                                        stream, a, a.hsplit, 128)
                          : launch_attn(attn_bwd_dkv_tc_kernel<128>, 128, d, d->kv_heads * a.hsplit, TcDkv<128>::SMEM,
