@@ -1640,6 +1640,245 @@ static_assert(2 * WsDkv<128>::K_BYTES + 2 * WsDkv<128>::STAGES * WsDkv<128>::Q_B
               "stage fits");
 static_assert(WsDkv<128>::SMEM <= 227 * 1024, "dK/dV shared memory");
 
+// Warp-specialised dQ (tcgen05), the dK/dV kernel's twin on the query side:
+//   warps 0-3  elementwise: query row t = TMEM lane t computes D = rowsum(dO O)
+//              once, then dS = P (dP - D) per key tile into a swizzled A operand
+//   warps 4-7  loaders: Q / dO once (cp.async); K / V tiles by TMA, 3 stages,
+//              tail rows past the sequence zeroed (job isolation, as in dK/dV)
+//   warp 8     MMA issuer: S = Q K^T and dP = dO V^T one key tile ahead
+//              (double-buffered in TMEM), dQ += dS K accumulated in TMEM
+template <int HD>
+struct WsDq {
+    static constexpr int BQ = 128, BK = 64, NB = HD / 64, STAGES = 3;
+    static constexpr int Q_BYTES = BQ * 128 * NB, K_BYTES = BK * 128 * NB, DS_BYTES = BQ * 128;
+    static constexpr int SMEM = 2 * Q_BYTES + 2 * STAGES * K_BYTES + 2 * DS_BYTES + 192;
+    static constexpr uint32_t SBUF = 128, S_COL = 0, DP_COL = 64, DQ_COL = 256, TMEM_COLS = 512;
+    static constexpr uint32_t IDESC_S = tc5::idesc_bf16_f32(128, BK, false, false);
+    static constexpr uint32_t IDESC_Q = tc5::idesc_bf16_f32(128, HD, false, true);
+};
+
+template <int HD>
+__global__ void __launch_bounds__(288, 1) attn_bwd_dq_ws_kernel(const __grid_constant__ CUtensorMap tk,
+                                                                 const __grid_constant__ CUtensorMap tv,
+                                                                 AttnArgs a) {
+    using T = WsDq<HD>;
+    pdl_prologue();
+    int start, len;
+    seq_range(a, blockIdx.y, start, len);
+    const int slot = a.seq_off[blockIdx.y + 1] - start;
+    const int q0 = blockIdx.x * T::BQ;
+    if (q0 >= slot) return;
+    const int h = blockIdx.z, kvh = h / (a.heads / a.kv_heads);
+    extern __shared__ __align__(1024) uint8_t smd[];
+    if ((smem_u32(smd) & 1023) != 0) __trap();
+    uint8_t* Qs = smd;
+    uint8_t* dOs = Qs + T::Q_BYTES;
+    uint8_t* KV = dOs + T::Q_BYTES;               // (K, V) x STAGES
+    uint8_t* DS = KV + 2 * T::STAGES * T::K_BYTES;  // dS x 2
+    uint64_t* q_full = reinterpret_cast<uint64_t*>(DS + 2 * T::DS_BYTES);
+    uint64_t* tma_full = q_full + 1;              // [STAGES]
+    uint64_t* kv_full = tma_full + T::STAGES;     // [STAGES] tails zeroed
+    uint64_t* kv_free = kv_full + T::STAGES;      // [STAGES] MMA commit after dQ of the tile
+    uint64_t* s_full = kv_free + T::STAGES;       // [2]
+    uint64_t* p_full = s_full + 2;                // [2] (128)
+    uint64_t* g_done = p_full + 2;                // [2] MMA commit after dQ of the tile
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(g_done + 2);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        tc5::mbar_init(q_full, 1);
+        for (int i = 0; i < T::STAGES; ++i) {
+            tc5::mbar_init(tma_full + i, 1);
+            tc5::mbar_init(kv_full + i, 1);
+            tc5::mbar_init(kv_free + i, 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            tc5::mbar_init(s_full + i, 1);
+            tc5::mbar_init(p_full + i, 128);
+            tc5::mbar_init(g_done + i, 1);
+        }
+        tc5::fence_barrier_init();
+    }
+    if (warp == 0) {
+        tc5::tmem_alloc(tslot, T::TMEM_COLS);
+        tc5::tmem_relinquish();
+    }
+    tc5::tc_fence_before();
+    __syncthreads();
+    tc5::tc_fence_after();
+    const uint32_t tmem = *tslot;
+    const int nkt = q0 < len ? (min(q0 + T::BQ, len) + T::BK - 1) / T::BK : 0;
+
+    if (warp >= 4 && warp < 8) {
+        // ------------------------------------------------ loaders
+        const int lt = threadIdx.x - 128;
+        auto loaders_sync = [] { asm volatile("bar.sync 1, 128;" ::: "memory"); };
+        if (lt == 0) {
+            tc5::tma_prefetch_desc(&tk);
+            tc5::tma_prefetch_desc(&tv);
+        }
+        stage_sw128_warp<HD>(Qs, T::BQ, a.q, a.ldq, start, q0, len, h * HD, lt);
+        stage_sw128_warp<HD>(dOs, T::BQ, a.dO, a.lddo, start, q0, len, h * HD, lt);
+        cp_async_commit();
+        cp_async_wait<0>();
+        fence_proxy_async();
+        loaders_sync();
+        if (lt == 0) tc5::mbar_arrive(q_full);
+        for (int kt = 0; kt < nkt; ++kt) {
+            const int st = kt % T::STAGES, k0 = kt * T::BK;
+            if (kt >= T::STAGES) tc5::mbar_wait(kv_free + st, ((kt - T::STAGES) / T::STAGES) & 1);
+            uint8_t* Kb = KV + 2 * T::K_BYTES * st;
+            if (lt == 0) {
+                tc5::mbar_arrive_expect_tx(tma_full + st, 2 * T::K_BYTES);
+#pragma unroll
+                for (int blk = 0; blk < T::NB; ++blk) {
+                    tc5::tma_load_2d(smem_u32(Kb + blk * T::BK * 128), &tk, tma_full + st, kvh * HD + blk * 64,
+                                     start + k0);
+                    tc5::tma_load_2d(smem_u32(Kb + T::K_BYTES + blk * T::BK * 128), &tv, tma_full + st,
+                                     kvh * HD + blk * 64, start + k0);
+                }
+            }
+            if (k0 + T::BK > len) {  // rows past the sequence: zero them (see the dK/dV kernel)
+                tc5::mbar_wait(tma_full + st, (kt / T::STAGES) & 1);
+                const int r0 = max(len - k0, 0);
+                for (int e = lt; e < (T::BK - r0) * 2 * T::NB * 8; e += 128) {
+                    const int ch = e & 7, rb = e >> 3, r = r0 + rb % (T::BK - r0), blk = rb / (T::BK - r0);
+                    *reinterpret_cast<uint4*>(Kb + blk * T::BK * 128 + r * 128 + (ch << 4)) = make_uint4(0, 0, 0, 0);
+                }
+                fence_proxy_async();
+            }
+            loaders_sync();
+            if (lt == 32) tc5::mbar_arrive(kv_full + st);
+        }
+    } else if (warp == 8) {
+        // ------------------------------------------------ MMA issuer
+        if (lane == 0 && nkt > 0) {
+            auto issue_s = [&](int kt) {
+                const int b = kt & 1, st = kt % T::STAGES;
+                tc5::mbar_wait(tma_full + st, (kt / T::STAGES) & 1);
+                tc5::mbar_wait(kv_full + st, (kt / T::STAGES) & 1);
+                if (kt >= 2) tc5::mbar_wait(p_full + b, ((kt - 2) >> 1) & 1);
+                tc5::tc_fence_after();
+                const uint8_t* Kb = KV + 2 * T::K_BYTES * st;
+                const uint8_t* Vb = Kb + T::K_BYTES;
+                const uint32_t sb = b * T::SBUF;
+#pragma unroll
+                for (int j = 0; j < HD / 16; ++j) {
+                    const uint32_t qo = (j / 4) * T::BQ * 128 + (j % 4) * 32, ko = (j / 4) * T::BK * 128 + (j % 4) * 32;
+                    tc5::mma_bf16(tmem + sb + T::S_COL, tc5::sdesc_sw128(smem_u32(Qs + qo), 16, 1024),
+                                  tc5::sdesc_sw128(smem_u32(Kb + ko), 16, 1024), T::IDESC_S, j > 0 ? 1u : 0u);
+                    tc5::mma_bf16(tmem + sb + T::DP_COL, tc5::sdesc_sw128(smem_u32(dOs + qo), 16, 1024),
+                                  tc5::sdesc_sw128(smem_u32(Vb + ko), 16, 1024), T::IDESC_S, j > 0 ? 1u : 0u);
+                }
+                tc5::tc_commit(s_full + b);
+            };
+            tc5::mbar_wait(q_full, 0);
+            issue_s(0);
+            for (int kt = 0; kt < nkt; ++kt) {
+                const int b = kt & 1, st = kt % T::STAGES;
+                if (kt + 1 < nkt) issue_s(kt + 1);
+                tc5::mbar_wait(p_full + b, (kt >> 1) & 1);
+                tc5::tc_fence_after();
+                const uint8_t* Kb = KV + 2 * T::K_BYTES * st;
+                const uint8_t* dSb = DS + T::DS_BYTES * b;
+#pragma unroll
+                for (int j = 0; j < T::BK / 16; ++j)
+                    tc5::mma_bf16(tmem + T::DQ_COL, tc5::sdesc_sw128(smem_u32(dSb + j * 32), 16, 1024),
+                                  tc5::sdesc_sw128(smem_u32(Kb + j * 2048), T::BK * 128, 1024), T::IDESC_Q,
+                                  (kt > 0 || j > 0) ? 1u : 0u);
+                tc5::tc_commit(g_done + b);
+                tc5::tc_commit(kv_free + st);
+            }
+        }
+        __syncwarp();
+    } else {
+        // ------------------------------------------------ elementwise (warps 0-3)
+        const int row = threadIdx.x, qi = q0 + row;
+        const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+        const float c2 = a.scale * kLog2e;
+        const bool real = qi < len;
+        const float nl = real ? -a.lse[(long long)h * a.rows + start + qi] * kLog2e : 0.f;
+        float dr = 0.f;  // D = rowsum(dO O) of this row, published for the dK / dV kernel that runs next
+        if (real) {
+            const __nv_bfloat16* orow = a.o + (long long)(start + qi) * a.ldo + h * HD;
+            const __nv_bfloat16* drow = a.dO + (long long)(start + qi) * a.lddo + h * HD;
+            for (int c = 0; c < HD; c += 8) {
+                float ov[8], dv[8];
+                ld8(orow + c, ov);
+                ld8(drow + c, dv);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) dr = fmaf(ov[e], dv[e], dr);
+            }
+        }
+        if (qi < slot) a.dsum[(long long)h * a.rows + start + qi] = dr;
+        for (int kt = 0; kt < nkt; ++kt) {
+            const int b = kt & 1;
+            tc5::mbar_wait(s_full + b, (kt >> 1) & 1);
+            if (kt >= 2) tc5::mbar_wait(g_done + b, ((kt - 2) >> 1) & 1);  // dS buffer b free
+            tc5::tc_fence_after();
+            const uint32_t sb = b * T::SBUF;
+            const bool interior = kt * T::BK + T::BK - 1 <= q0 && q0 + T::BQ <= len;
+            uint8_t* drow = DS + T::DS_BYTES * b + row * 128;
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                uint32_t sv[32], pv[32];
+                tc5::tmem_ld32(tmem + lane_base + sb + T::S_COL + half * 32, sv);
+                tc5::tmem_ld32(tmem + lane_base + sb + T::DP_COL + half * 32, pv);
+                tc5::tmem_wait_ld();
+#pragma unroll
+                for (int ch = 0; ch < 4; ++ch) {
+                    float d[8];
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        const int c = ch * 8 + e, kj = kt * T::BK + half * 32 + c;
+                        float p = ex2_ftz(fmaf(__uint_as_float(sv[c]), c2, nl));
+                        if (!interior) p = (kj <= qi && qi < len) ? p : 0.f;
+                        d[e] = p * (__uint_as_float(pv[c]) - dr);
+                    }
+                    uint4 w;
+                    w.x = pack2(d[0], d[1]), w.y = pack2(d[2], d[3]), w.z = pack2(d[4], d[5]), w.w = pack2(d[6], d[7]);
+                    *reinterpret_cast<uint4*>(drow + (((half * 4 + ch) ^ (row & 7)) << 4)) = w;
+                }
+            }
+            fence_proxy_async();
+            tc5::tc_fence_before();
+            tc5::mbar_arrive(p_full + b);
+        }
+        if (nkt > 0) tc5::mbar_wait(g_done + ((nkt - 1) & 1), ((nkt - 1) >> 1) & 1);
+        tc5::tc_fence_after();
+    }
+    __syncthreads();
+    // ---- epilogue: dQ (scaled, un-rotated) through an fp32 stage over the K / V stages
+    float* st = reinterpret_cast<float*>(KV);
+    if (warp < 4) {
+        const int row = threadIdx.x;
+        const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+        if (nkt > 0) {
+#pragma unroll
+            for (int c0 = 0; c0 < HD; c0 += 32) {
+                uint32_t v[32];
+                tc5::tmem_ld32(tmem + lane_base + T::DQ_COL + c0, v);
+                tc5::tmem_wait_ld();
+#pragma unroll
+                for (int c = 0; c < 32; ++c) st[row * Tile<HD>::LDF + c0 + c] = a.scale * __uint_as_float(v[c]);
+            }
+        } else {
+            for (int c = 0; c < HD; ++c) st[row * Tile<HD>::LDF + c] = 0.f;
+        }
+    }
+    __syncthreads();
+    for (int hlf = 0; hlf < 2; ++hlf)
+        store_tile<HD>(st + hlf * kBM * Tile<HD>::LDF, a.dq, a.lddq, start, q0 + hlf * kBM, len, h * HD, slot,
+                       a.rope_base, a.rope_base > 0.f);
+    tc5::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc5::tc_fence_after();
+        tc5::tmem_dealloc(tmem, T::TMEM_COLS);
+    }
+}
+static_assert(2 * WsDq<128>::STAGES * WsDq<128>::K_BYTES >= 128 * Tile<128>::LDF * 4, "dQ stage fits");
+static_assert(WsDq<128>::SMEM <= 227 * 1024, "dQ shared memory");
+
 // dK, dV: one CTA per (R-key block, sequence, K/V head, head part); loops over
 // its query heads and the 64-query tiles that can see the block (causal).  With
 // grouped / multi-query attention the group's query heads are split over a
@@ -1957,6 +2196,16 @@ cudaError_t launch_attn_ws(K kernel, const mlora_attn_desc* d, size_t smem, void
     return cudaLaunchKernelEx(&cfg, kernel, tq, tdo, a);
 }
 
+// The warp-specialised dQ kernel: 128-query blocks, 288 threads, one CTA per (block, sequence, head).
+template <typename K>
+cudaError_t launch_attn_wsq(K kernel, const mlora_attn_desc* d, size_t smem, void* stream, const CUtensorMap& tk,
+                            const CUtensorMap& tv, const AttnArgs& a) {
+    if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
+        cudaSuccess)
+        return cudaErrorInvalidValue;
+    return launch(kernel, dim3((d->max_len + 127) / 128, d->num_seqs, d->heads), dim3(288), smem, stream, tk, tv, a);
+}
+
 // MLORA_ATTN_TC=0 keeps the mma.sync forward / dQ kernels (A/B knob); the
 // tcgen05 ones need pre-rotated Q / K and 16-byte-aligned rows.
 bool attn_tc_enabled() {
@@ -2135,13 +2384,20 @@ mlora_status mlora_attn_bwd(const mlora_attn_desc* d, const void* q, int64_t ldq
                     (reinterpret_cast<uintptr_t>(o) & 15) == 0 && ldo % 8 == 0;
     if (tc) {
         // dQ first: its CTAs also compute D = rowsum(dO O) for their rows (no separate pass);
-        // then dK / dV on tcgen05 (128-key blocks, one CTA per SM: 384 of 512 TMEM columns)
-        e = hd == 64 ? launch_attn_rows(attn_bwd_dq_tc_kernel<64>, 128, 128, d, d->heads, TcDq<64>::SMEM, stream, a)
-                     : launch_attn_rows(attn_bwd_dq_tc_kernel<128>, 128, 128, d, d->heads, TcDq<128>::SMEM, stream, a);
-        static const bool ws = [] {  // MLORA_ATTN_WS=0: the phase-serial dK / dV kernel (A/B knob)
+        // then dK / dV.  Both warp-specialised and TMA-fed unless MLORA_ATTN_WS=0 (A/B knob:
+        // the phase-serial tcgen05 kernels)
+        static const bool ws = [] {
             const char* e = std::getenv("MLORA_ATTN_WS");
             return !(e && e[0] == '0');
         }();
+        CUtensorMap tk, tv;
+        if (ws && encode_rows_map(k, ldk, d->rows, &tk) && encode_rows_map(v, ldv, d->rows, &tv))
+            e = hd == 64 ? launch_attn_wsq(attn_bwd_dq_ws_kernel<64>, d, WsDq<64>::SMEM, stream, tk, tv, a)
+                         : launch_attn_wsq(attn_bwd_dq_ws_kernel<128>, d, WsDq<128>::SMEM, stream, tk, tv, a);
+        else
+            e = hd == 64 ? launch_attn_rows(attn_bwd_dq_tc_kernel<64>, 128, 128, d, d->heads, TcDq<64>::SMEM, stream, a)
+                         : launch_attn_rows(attn_bwd_dq_tc_kernel<128>, 128, 128, d, d->heads, TcDq<128>::SMEM, stream,
+                                            a);
         CUtensorMap tq, tdo;
         const bool maps = ws && encode_rows_map(q, ldq, d->rows, &tq) && encode_rows_map(dout, lddo, d->rows, &tdo);
         if (e == cudaSuccess && maps)
