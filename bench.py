@@ -481,9 +481,9 @@ def run_decoder(args, cfg):
     for _ in range(max(args.warmup, 3)):
         m.step()
     barrier()
-    from paper_2312_02515_b200 import model_ops as MO
+    from paper_2312_02515_b200 import _native as NL
     sampler = ClockSampler(dev)
-    launches0 = ctx.launches + MO.LAUNCHES[0]
+    launches0 = ctx.launches + NL.lib().mlora_free_launch_count()
     sampler.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
@@ -493,7 +493,7 @@ def run_decoder(args, cfg):
     e1.record(stream)
     barrier()
     clocks = sampler.stop()
-    launches = ctx.launches + MO.LAUNCHES[0] - launches0
+    launches = ctx.launches + NL.lib().mlora_free_launch_count() - launches0
     ms_total = PL.max_over_ranks(e0.elapsed_time(e1), device=dev)
     eff = int(PL.sum_over_ranks(batch.real_tokens, device=dev))
     value = eff * args.steps / (ms_total / 1e3)

@@ -79,6 +79,9 @@ mlora_status mlora_ctx_destroy(mlora_ctx* ctx);
 int32_t mlora_ctx_num_sms(const mlora_ctx* ctx);
 /* Kernels launched through this context since creation (telemetry). */
 int64_t mlora_ctx_launch_count(const mlora_ctx* ctx);
+/* Kernels launched by the context-free entry points (model / decoder kernels:
+ * masked CE, norms, RoPE, SwiGLU, attention, ...) in this process (telemetry). */
+int64_t mlora_free_launch_count(void);
 /* Live per-kernel timing: while enabled, every launch is bracketed by CUDA
  * events on its own stream.  profile_read synchronises on the recorded events
  * and returns the accumulated launch count / device milliseconds of one kernel

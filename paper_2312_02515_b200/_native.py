@@ -47,6 +47,7 @@ _SIGS = {
     "mlora_ctx_destroy": (i32, [vp]),
     "mlora_ctx_num_sms": (i32, [vp]),
     "mlora_ctx_launch_count": (i64, [vp]),
+    "mlora_free_launch_count": (i64, []),
     "mlora_ctx_set_profiling": (i32, [vp, i32]),
     "mlora_ctx_profile_read": (i32, [vp, i32, C.POINTER(i64), C.POINTER(C.c_double), i32]),
     "mlora_fused_shape_of": (i32, [C.POINTER(i32), i64, C.POINTER(FusedShapeC)]),

@@ -26,6 +26,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
@@ -2079,6 +2080,15 @@ __global__ void __launch_bounds__(2 * R, 3) attn_bwd_dq_kernel(AttnArgs a) {
     store_rows<HD, R>(st, a.dq, a.lddq, start, q0, len, h * HD, slot, a.rope_base, a.rope_base > 0.f);
 }
 
+// Kernels launched by the context-free entry points (decoder / model kernels);
+// the context-bound ones are counted by mlora_ctx_launch_count.
+std::atomic<long long> g_free_launches{0};
+
+cudaError_t counted(cudaError_t e) {
+    if (e == cudaSuccess) g_free_launches.fetch_add(1, std::memory_order_relaxed);
+    return e;
+}
+
 template <typename... KArgs, typename... Args>
 cudaError_t launch(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, void* stream, Args... args) {
     cudaLaunchConfig_t cfg{};
@@ -2091,7 +2101,7 @@ cudaError_t launch(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, void* strea
     attr.val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = &attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k, args...);
+    return counted(cudaLaunchKernelEx(&cfg, k, args...));
 }
 
 mlora_status check_attn(const mlora_attn_desc* d) {
@@ -2149,7 +2159,7 @@ cudaError_t launch_attn(K kernel, int rows_per_cta, const mlora_attn_desc* d, in
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    return cudaLaunchKernelEx(&cfg, kernel, a);
+    return counted(cudaLaunchKernelEx(&cfg, kernel, a));
 }
 
 // 2-D TMA map over a [rows, ld] bf16 matrix with 64 x 64 boxes and the 128-byte
@@ -2193,7 +2203,7 @@ cudaError_t launch_attn_ws(K kernel, const mlora_attn_desc* d, size_t smem, void
     attr[1].val.clusterDim.z = a.hsplit;
     cfg.attrs = attr;
     cfg.numAttrs = a.hsplit > 1 ? 2 : 1;
-    return cudaLaunchKernelEx(&cfg, kernel, tq, tdo, a);
+    return counted(cudaLaunchKernelEx(&cfg, kernel, tq, tdo, a));
 }
 
 // The warp-specialised dQ kernel: 128-query blocks, 288 threads, one CTA per (block, sequence, head).
@@ -2246,7 +2256,12 @@ int attn_hsplit(const mlora_attn_desc* d) {
 
 }  // namespace
 
+// mlora_model.cu's launches report here too
+void mlora_count_free_launch() { g_free_launches.fetch_add(1, std::memory_order_relaxed); }
+
 extern "C" {
+
+int64_t mlora_free_launch_count(void) { return g_free_launches.load(std::memory_order_relaxed); }
 
 mlora_status mlora_embed(int64_t rows, int32_t h, int32_t V, const int32_t* tokens, const void* E, void* x,
                          void* stream) {

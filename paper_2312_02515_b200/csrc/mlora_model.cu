@@ -273,6 +273,10 @@ __global__ void rope_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* 
     }
 }
 
+}  // namespace
+void mlora_count_free_launch();  // mlora_decoder.cu
+namespace {
+
 template <typename... KArgs, typename... Args>
 cudaError_t launch(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, void* stream, Args... args) {
     cudaLaunchConfig_t cfg{};
@@ -285,7 +289,9 @@ cudaError_t launch(void (*k)(KArgs...), dim3 g, dim3 b, size_t smem, void* strea
     attr.val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = &attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, k, args...);
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, k, args...);
+    if (e == cudaSuccess) mlora_count_free_launch();
+    return e;
 }
 
 }  // namespace

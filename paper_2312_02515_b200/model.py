@@ -396,7 +396,6 @@ class MultiLoraDecoder(AdapterJobsMixin):
                                         self.labels[:r].data_ptr(), self.mask[:r].data_ptr(),
                                         self._row_loss[:r].data_ptr(), self.loss.data_ptr(), self._inv.data_ptr(),
                                         self.dlogits[:r].data_ptr(), s))
-        M._count(3)
         return self.loss
 
     def _attn_fwd(self, L: _Layer, q, k, v, stream) -> None:

@@ -10,15 +10,6 @@ from . import _native as N
 from . import errors
 
 
-# kernels launched by the context-free entry points below (the ctx-bound ones
-# are counted by mlora_ctx_launch_count); telemetry for bench.py's gpu_launches
-LAUNCHES = [0]
-
-
-def _count(n: int) -> None:
-    LAUNCHES[0] += n
-
-
 def _s(stream):
     return (stream or torch.cuda.current_stream()).cuda_stream
 
@@ -41,7 +32,6 @@ def masked_ce(logits: torch.Tensor, labels: torch.Tensor, seg_offsets, mask: tor
     N.check(N.lib().mlora_masked_ce(J, seg.data_ptr(), rows, V, logits.data_ptr(), labels.data_ptr(),
                                     None if mask is None else mask.data_ptr(), row_loss.data_ptr(), loss.data_ptr(),
                                     inv.data_ptr(), None if dl is None else dl.data_ptr(), _s(stream)))
-    _count(3)
     return loss, dl
 
 
@@ -51,7 +41,6 @@ def rmsnorm_fwd(x: torch.Tensor, w: torch.Tensor, eps: float = 1e-6, stream=None
     rstd = torch.empty(rows, dtype=torch.float32, device=x.device)
     N.check(N.lib().mlora_rmsnorm_fwd(rows, h, x.data_ptr(), w.data_ptr(), eps, y.data_ptr(), rstd.data_ptr(),
                                       _s(stream)))
-    _count(1)
     return y, rstd
 
 
@@ -64,7 +53,6 @@ def rmsnorm_bwd(dy: torch.Tensor, x: torch.Tensor, w: torch.Tensor, rstd: torch.
     ws = torch.empty(nblk * h, dtype=torch.float32, device=x.device)
     N.check(N.lib().mlora_rmsnorm_bwd(rows, h, dy.data_ptr(), x.data_ptr(), w.data_ptr(), rstd.data_ptr(),
                                       dx.data_ptr(), dw.data_ptr(), ws.data_ptr(), rows_per_block, _s(stream)))
-    _count(2)
     return dx, dw
 
 
@@ -73,7 +61,6 @@ def rope(x: torch.Tensor, pos: torch.Tensor, base: float = 10000.0, inverse: boo
     y = torch.empty_like(x)
     N.check(N.lib().mlora_rope(rows, heads, hd, x.data_ptr(), y.data_ptr(), pos.data_ptr(), base,
                                1 if inverse else 0, _s(stream)))
-    _count(1)
     return y
 
 
@@ -90,7 +77,6 @@ def embed(tokens: torch.Tensor, E: torch.Tensor, out: torch.Tensor | None = None
     V, h = E.shape
     out = torch.empty(tokens.shape[0], h, dtype=torch.bfloat16, device=E.device) if out is None else out
     N.check(N.lib().mlora_embed(tokens.shape[0], h, V, tokens.data_ptr(), E.data_ptr(), out.data_ptr(), _s(stream)))
-    _count(1)
     return out
 
 
@@ -106,7 +92,6 @@ def add_rmsnorm(x: torch.Tensor, delta: torch.Tensor | None, w: torch.Tensor, ep
     N.check(N.lib().mlora_add_rmsnorm(rows, h, x.data_ptr(), None if delta is None else delta.data_ptr(),
                                       w.data_ptr(), eps, None if x_out is None else x_out.data_ptr(), y.data_ptr(),
                                       rstd.data_ptr(), _s(stream)))
-    _count(1)
     return x_out, y, rstd
 
 
@@ -119,7 +104,6 @@ def rmsnorm_bwd_sum(dys, dres: torch.Tensor | None, x: torch.Tensor, w: torch.Te
     N.check(N.lib().mlora_rmsnorm_bwd_sum(rows, h, n, (N.vp * n)(*[d.data_ptr() for d in dys]),
                                           None if dres is None else dres.data_ptr(), x.data_ptr(), w.data_ptr(),
                                           rstd.data_ptr(), out.data_ptr(), _s(stream)))
-    _count(1)
     return out
 
 
@@ -129,7 +113,6 @@ def swiglu_fwd(gate: torch.Tensor, up: torch.Tensor, out: torch.Tensor | None = 
     out = torch.empty(rows, f, dtype=torch.bfloat16, device=gate.device) if out is None else out
     N.check(N.lib().mlora_swiglu_fwd(rows, f, gate.data_ptr(), gate.stride(0), up.data_ptr(), up.stride(0),
                                      out.data_ptr(), _s(stream)))
-    _count(1)
     return out
 
 
@@ -139,7 +122,6 @@ def swiglu_bwd(gate: torch.Tensor, up: torch.Tensor, dout: torch.Tensor, dgate: 
     N.check(N.lib().mlora_swiglu_bwd(rows, f, gate.data_ptr(), gate.stride(0), up.data_ptr(), up.stride(0),
                                      dout.data_ptr(), dgate.data_ptr(), dgate.stride(0), dup.data_ptr(),
                                      dup.stride(0), _s(stream)))
-    _count(1)
 
 
 class AttnLayout:
@@ -174,7 +156,6 @@ def attn_rope(layout: AttnLayout, x: torch.Tensor, n_heads: int, head_dim: int, 
     d = layout.desc(n_heads, n_heads, head_dim, rope_base)
     N.check(N.lib().mlora_attn_rope(C.byref(d), x.data_ptr(), x.stride(0), n_heads, out.data_ptr(), out.stride(0),
                                     _s(stream)))
-    _count(1)
     return out
 
 
@@ -189,7 +170,6 @@ def attn_fwd(layout: AttnLayout, q, k, v, heads: int, kv_heads: int, head_dim: i
     d = layout.desc(heads, kv_heads, head_dim, rope_base, prerotated=prerotated)
     N.check(N.lib().mlora_attn_fwd(C.byref(d), q.data_ptr(), q.stride(0), k.data_ptr(), k.stride(0), v.data_ptr(),
                                    v.stride(0), out.data_ptr(), out.stride(0), lse.data_ptr(), _s(stream)))
-    _count(1)
     return out, lse
 
 
@@ -204,4 +184,3 @@ def attn_bwd(layout: AttnLayout, q, k, v, o, dout, lse, dq, dk, dv, heads: int, 
                                    v.stride(0), o.data_ptr(), o.stride(0), dout.data_ptr(), dout.stride(0),
                                    lse.data_ptr(), dsum.data_ptr(), dq.data_ptr(), dq.stride(0), dk.data_ptr(),
                                    dk.stride(0), dv.data_ptr(), dv.stride(0), _s(stream)))
-    _count(3)
