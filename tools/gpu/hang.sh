@@ -1,2 +1,1 @@
-timeout 600 python -m pytest tests/test_gpu_decoder.py tests/test_gpu_model.py -x -q 2>&1 | tail -2 > gpurun_out/all.log
-MLORA_BENCH_LAYERS=2 timeout 600 python bench.py --config c4 --steps 3 --warmup 3 > gpurun_out/b.log 2>&1
+timeout 900 ncu --set full --clock-control none -k regex:"attn_(fwd_tc|bwd_dq_ws|bwd_dkv_ws)" -c 3 -o gpurun_out/attn_tc_full -f python tools/decoder_step.py --layers 1 --steps 1 > /dev/null 2>&1
