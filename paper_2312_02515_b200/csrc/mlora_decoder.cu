@@ -623,9 +623,10 @@ __global__ void __launch_bounds__(2 * R, 2) attn_fwd_kernel(AttnArgs a) {
 }
 
 // dst = RoPE(src) for n_heads heads of every row (pos = row - its sequence start;
-// rows past len are zeroed): one CTA per (64-row tile, sequence); each thread
-// owns 8 consecutive rotation pairs (16-byte accesses) and applies their
-// angles to every head.
+// rows past len are zeroed): one CTA per (64-row tile, sequence, group of
+// kRopeHeads heads); each thread owns 8 consecutive rotation pairs (16-byte
+// accesses) and applies their angles to the group's heads.
+constexpr int kRopeHeads = 4;
 __global__ void attn_rope_kernel(AttnArgs a, const __nv_bfloat16* __restrict__ src, long long lds, int n_heads, int hd,
                                  __nv_bfloat16* __restrict__ dst, long long ldd) {
     pdl_prologue();
@@ -647,7 +648,9 @@ __global__ void attn_rope_kernel(AttnArgs a, const __nv_bfloat16* __restrict__ s
         }
         const __nv_bfloat16* s = src + (long long)(start + pos) * lds + i;
         __nv_bfloat16* d = dst + (long long)(start + pos) * ldd + i;
-        for (int h = 0; h < n_heads; ++h) {
+        const int h1 = min(n_heads, (static_cast<int>(blockIdx.z) + 1) * kRopeHeads);
+#pragma unroll 4
+        for (int h = blockIdx.z * kRopeHeads; h < h1; ++h) {
             float x0[8], x1[8], y0[8], y1[8];
             ld8(s + h * hd, x0);
             ld8(s + h * hd + half, x1);
@@ -2365,7 +2368,7 @@ mlora_status mlora_attn_rope(const mlora_attn_desc* d, const void* src, int64_t 
         !rows16(dst, ld_dst))
         return MLORA_SHAPE;
     AttnArgs a = attn_args(d);
-    const dim3 grid((d->max_len + kBM - 1) / kBM, d->num_seqs);
+    const dim3 grid((d->max_len + kBM - 1) / kBM, d->num_seqs, (n_heads + kRopeHeads - 1) / kRopeHeads);
     return launch(attn_rope_kernel, grid, dim3(256), 0, stream, a, bf(src), static_cast<long long>(ld_src),
                   static_cast<int>(n_heads), static_cast<int>(d->head_dim), bfw(dst),
                   static_cast<long long>(ld_dst)) == cudaSuccess

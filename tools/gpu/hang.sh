@@ -1,2 +1,2 @@
-timeout 1200 python tools/c4_executor.py > gpurun_out/c4_executor.jsonl 2> gpurun_out/c4_executor.err
-C4_CFG=c3 timeout 1200 python tools/c4_executor.py > gpurun_out/c3_model.jsonl 2> gpurun_out/c3_model.err
+timeout 300 python -m pytest tests/test_gpu_decoder.py -x -q 2>&1 | tail -2 > gpurun_out/all.log
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"attn_rope" -c 2 --csv --log-file gpurun_out/rope.csv python tools/decoder_step.py --layers 1 --steps 1 > /dev/null 2>&1
