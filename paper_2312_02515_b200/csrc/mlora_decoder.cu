@@ -15,10 +15,23 @@
 // transpose to a [batch, heads, len, head_dim] tensor is ever materialised.
 // Q/K/V are column slices of the projection outputs (row stride ld), which
 // covers ChatGLM2's fused qkv output (multi-query: 2 K/V groups) as well as
-// LLaMA's separate q, k, v.  Attention is not on the BatchFusion hot path: its
-// 64 x 64 tiles run on the warp-level tensor-core MMA (mma.sync bf16, fp32
-// accumulation), flash-style (no score matrix in HBM), with a deterministic
-// two-kernel backward (dK/dV per key tile, dQ per query tile; no atomics).
+// LLaMA's separate q, k, v.  Attention is flash-style (no score matrix in HBM)
+// with a deterministic two-kernel backward (dQ per query tile, then dK/dV per
+// key tile; no atomics).  Kernel families:
+//   * elementwise: embed, add_rmsnorm, rmsnorm_bwd_sum, swiglu_{fwd,bwd},
+//     attn_rope (RoPE applied once into separate Q/K buffers);
+//   * mma.sync attention (attn_fwd_kernel / attn_bwd_dq_kernel /
+//     attn_bwd_dkv_kernel, 64-128 row tiles): the fallback for un-rotated
+//     inputs, unaligned row strides and MLORA_ATTN_TC=0;
+//   * tcgen05 attention, the default on pre-rotated inputs: attn_fwd_tc_kernel
+//     (S and O accumulators in TMEM, one query row per thread, lazy rescale),
+//     attn_bwd_dq_ws_kernel and attn_bwd_dkv_ws_kernel (warp-specialised:
+//     TMA loader warps, one MMA-issuing warp, four elementwise warps; dK/dV of
+//     a GQA/MQA group reduced over a thread-block cluster in DSMEM rank order).
+//     The phase-serial *_tc_kernel backwards stay as the MLORA_ATTN_WS=0
+//     fallback.
+// Every kernel launched here bumps the native launch counter
+// (mlora_free_launch_count) so bench.py's gpu_launches is counted, not claimed.
 #include <cooperative_groups.h>
 #include <cuda.h>
 #include <cuda_bf16.h>
