@@ -705,7 +705,7 @@ struct TcAttn {
     static constexpr int K_BYTES = BK * 128 * NB;
     static constexpr int V_BYTES = BK * 128 * NB;
     static constexpr int P_BYTES = BQ * 128;                 // [128 rows x 64 keys] bf16
-    static constexpr int SMEM = Q_BYTES + K_BYTES + V_BYTES + P_BYTES + 1024 + 64;
+    static constexpr int SMEM = Q_BYTES + K_BYTES + 2 * V_BYTES + P_BYTES + 1024 + 64;  // V double-buffered
     static constexpr uint32_t S_COL = 0, O_COL = 128, TMEM_COLS = 256;
     static constexpr uint32_t IDESC_S = tc5::idesc_bf16_f32(128, BK, false, false);
     static constexpr uint32_t IDESC_O = tc5::idesc_bf16_f32(128, HD, false, true);
@@ -764,13 +764,14 @@ __global__ void __launch_bounds__(128, 1) attn_fwd_tc_kernel(AttnArgs a) {
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
     uint8_t* Qs = base;
     uint8_t* Ks = Qs + T::Q_BYTES;
-    uint8_t* Vs = Ks + T::K_BYTES;
-    uint8_t* Ps = Vs + T::V_BYTES;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(Ps + T::P_BYTES);
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
+    uint8_t* Vs = Ks + T::K_BYTES;  // two buffers: V_kt at Vs + (kt & 1) * V_BYTES
+    uint8_t* Ps = Vs + 2 * T::V_BYTES;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(Ps + T::P_BYTES);  // [0] S done, [1] P V done
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2);
     const int warp = threadIdx.x >> 5, row = threadIdx.x;
     if (threadIdx.x == 0) {
         tc5::mbar_init(bar, 1);
+        tc5::mbar_init(bar + 1, 1);
         tc5::fence_barrier_init();
     }
     if (warp == 0) {
@@ -778,40 +779,42 @@ __global__ void __launch_bounds__(128, 1) attn_fwd_tc_kernel(AttnArgs a) {
         tc5::tmem_relinquish();
     }
     const int nkt = q0 < len ? (min(q0 + T::BQ, len) + T::BK - 1) / T::BK : 0;
-    // cp.async groups complete in issue order: [Q + K_0], [V_0], then per tile kt
-    // [K_kt+1] (issued once S_kt is computed) and [V_kt+1] (once O_kt is).
+    // Software pipeline over the key tiles.  The MMA thread issues S_kt+1 = Q K_kt+1^T
+    // ahead of O += P_kt V_kt, so the softmax of tile kt+1 (TMEM load, max, exp2)
+    // runs while the tensor pipe still works on P_kt V_kt; only the P store and
+    // the rare O rescale wait for it.  cp.async groups, in issue order: [Q + K_0],
+    // [V_0], then per tile kt [K_kt+1] (once S_kt is done) and [V_kt+1] (once
+    // P_kt-1 V_kt-1 is done, into the other V buffer).
     stage_sw128<HD>(Qs, T::BQ, a.q, a.ldq, start, q0, len, h * HD);
     if (nkt > 0) stage_sw128<HD>(Ks, T::BK, a.k, a.ldk, start, 0, len, kvh * HD);
     cp_async_commit();
     if (nkt > 0) stage_sw128<HD>(Vs, T::BK, a.v, a.ldv, start, 0, len, kvh * HD);
     cp_async_commit();
+    cp_async_wait<1>();  // Q and K_0
+    fence_proxy_async();
     tc5::tc_fence_before();
     __syncthreads();
     tc5::tc_fence_after();
     const uint32_t tmem = *tslot;
     const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+    auto issue_s = [&]() {  // S = Q K^T into TMEM, K-major operands
+#pragma unroll
+        for (int j = 0; j < HD / 16; ++j) {
+            const uint64_t ad = tc5::sdesc_sw128(smem_u32(Qs + (j / 4) * T::BQ * 128 + (j % 4) * 32), 16, 1024);
+            const uint64_t bd = tc5::sdesc_sw128(smem_u32(Ks + (j / 4) * T::BK * 128 + (j % 4) * 32), 16, 1024);
+            tc5::mma_bf16(tmem + T::S_COL, ad, bd, T::IDESC_S, j > 0 ? 1u : 0u);
+        }
+        tc5::tc_commit(bar);
+    };
+    if (threadIdx.x == 0 && nkt > 0) issue_s();
     const float c2 = a.scale * kLog2e;
     const int qi = q0 + row;
     float m = -INFINITY, l = 0.f;  // m: the row's reference max (log2 domain)
-    uint32_t phase = 0;
+    uint32_t phase_s = 0, phase_o = 0;
     for (int kt = 0; kt < nkt; ++kt) {
-        cp_async_wait<1>();  // K_kt (and Q) landed; V_kt may still be in flight
-        fence_proxy_async();
-        __syncthreads();
-        if (threadIdx.x == 0) {  // S = Q K^T
-            tc5::tc_fence_after();
-#pragma unroll
-            for (int j = 0; j < HD / 16; ++j) {
-                const uint64_t ad = tc5::sdesc_sw128(smem_u32(Qs + (j / 4) * T::BQ * 128 + (j % 4) * 32), 16, 1024);
-                const uint64_t bd = tc5::sdesc_sw128(smem_u32(Ks + (j / 4) * T::BK * 128 + (j % 4) * 32), 16, 1024);
-                tc5::mma_bf16(tmem + T::S_COL, ad, bd, T::IDESC_S, j > 0 ? 1u : 0u);
-            }
-            tc5::tc_commit(bar);
-        }
-        tc5::mbar_wait(bar, phase);
-        phase ^= 1u;
+        tc5::mbar_wait(bar, phase_s);  // S_kt in TMEM (and K_kt consumed)
+        phase_s ^= 1u;
         tc5::tc_fence_after();
-        // K_kt is consumed: prefetch K_kt+1 under the softmax and the P V product
         if (kt + 1 < nkt) stage_sw128<HD>(Ks, T::BK, a.k, a.ldk, start, (kt + 1) * T::BK, len, kvh * HD);
         cp_async_commit();
         // ---- softmax of this thread's row (64 keys)
@@ -843,12 +846,38 @@ __global__ void __launch_bounds__(128, 1) attn_fwd_tc_kernel(AttnArgs a) {
             }
         }
         mx = mx == -INFINITY ? -INFINITY : mx * c2;
-        // raise the reference max where a row's tile max exceeds it by > 2^8 and
-        // rescale what O and l hold so far.  tcgen05.ld / st are warp-collective
-        // (.sync.aligned): the O read-modify-write runs for the whole warp when any
-        // of its rows needs it (alpha = 1 for the others).
+        // raise the reference max where a row's tile max exceeds it by > 2^8
         const bool raise = mx > m + 8.f;
         const float alpha = !raise ? 1.f : (m == -INFINITY ? 0.f : exp2f(m - mx));
+        if (raise) {
+            l *= alpha;
+            m = mx;
+        }
+        const float nm = m == -INFINITY ? 0.f : -m;  // rows with nothing real yet: P = 0 below
+        const float live = m == -INFINITY ? 0.f : 1.f;
+        float ps = 0.f;
+        uint32_t pk[32];
+#pragma unroll
+        for (int c = 0; c < 64; c += 2) {
+            const float p0 = live * ex2_ftz(fmaf(s[c], c2, nm));
+            const float p1 = live * ex2_ftz(fmaf(s[c + 1], c2, nm));
+            ps += p0;
+            ps += p1;
+            pk[c / 2] = pack2(p0, p1);
+        }
+        l += ps;
+        if (kt > 0) {  // P_kt-1 V_kt-1 done: P, the other V buffer and O are free
+            tc5::mbar_wait(bar + 1, phase_o);
+            phase_o ^= 1u;
+            tc5::tc_fence_after();
+        }
+        if (kt + 1 < nkt)
+            stage_sw128<HD>(Vs + ((kt + 1) & 1) * T::V_BYTES, T::BK, a.v, a.ldv, start, (kt + 1) * T::BK, len,
+                            kvh * HD);
+        cp_async_commit();
+        // rescale what O holds so far.  tcgen05.ld / st are warp-collective
+        // (.sync.aligned): the O read-modify-write runs for the whole warp when any
+        // of its rows needs it (alpha = 1 for the others).
         if (kt > 0 && __any_sync(0xffffffffu, raise)) {
 #pragma unroll
             for (int c0 = 0; c0 < HD; c0 += 32) {
@@ -861,52 +890,31 @@ __global__ void __launch_bounds__(128, 1) attn_fwd_tc_kernel(AttnArgs a) {
             }
             tmem_wait_st();
         }
-        if (raise) {
-            l *= alpha;
-            m = mx;
-        }
-        const float nm = m == -INFINITY ? 0.f : -m;  // rows with nothing real yet: P = 0 below
-        const float live = m == -INFINITY ? 0.f : 1.f;
-        float ps = 0.f;
         uint8_t* prow = Ps + row * 128;
 #pragma unroll
-        for (int ch = 0; ch < 8; ++ch) {
-            float p[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                p[e] = live * ex2_ftz(fmaf(s[ch * 8 + e], c2, nm));
-                ps += p[e];
-            }
-            uint4 w;
-            w.x = pack2(p[0], p[1]);
-            w.y = pack2(p[2], p[3]);
-            w.z = pack2(p[4], p[5]);
-            w.w = pack2(p[6], p[7]);
-            *reinterpret_cast<uint4*>(prow + ((ch ^ (row & 7)) << 4)) = w;
-        }
-        l += ps;
-        cp_async_wait<1>();  // V_kt landed (K_kt+1 may still be in flight)
+        for (int ch = 0; ch < 8; ++ch)
+            *reinterpret_cast<uint4*>(prow + ((ch ^ (row & 7)) << 4)) =
+                make_uint4(pk[ch * 4], pk[ch * 4 + 1], pk[ch * 4 + 2], pk[ch * 4 + 3]);
+        cp_async_wait<1>();  // V_kt and K_kt+1 landed (V_kt+1 may still be in flight)
         fence_proxy_async();
         tc5::tc_fence_before();
         __syncthreads();
-        if (threadIdx.x == 0) {  // O_t = P V
+        if (threadIdx.x == 0) {
             tc5::tc_fence_after();
+            if (kt + 1 < nkt) issue_s();  // S_kt+1 first: the next softmax overlaps P_kt V_kt
+            const uint8_t* Vb = Vs + (kt & 1) * T::V_BYTES;
 #pragma unroll
-            for (int j = 0; j < T::BK / 16; ++j) {
+            for (int j = 0; j < T::BK / 16; ++j) {  // O += P V, V an MN-major B operand
                 const uint64_t ad = tc5::sdesc_sw128(smem_u32(Ps + j * 32), 16, 1024);
-                const uint64_t bd = tc5::sdesc_sw128(smem_u32(Vs + j * 2048), T::BK * 128, 1024);
+                const uint64_t bd = tc5::sdesc_sw128(smem_u32(Vb + j * 2048), T::BK * 128, 1024);
                 tc5::mma_bf16(tmem + T::O_COL, ad, bd, T::IDESC_O, (kt > 0 || j > 0) ? 1u : 0u);
             }
-            tc5::tc_commit(bar);
+            tc5::tc_commit(bar + 1);
         }
-        tc5::mbar_wait(bar, phase);
-        phase ^= 1u;
+    }
+    if (nkt > 0) {  // the last P V
+        tc5::mbar_wait(bar + 1, phase_o);
         tc5::tc_fence_after();
-        // V_kt is consumed: prefetch V_kt+1 under the output update and the next S
-        if (kt + 1 < nkt) stage_sw128<HD>(Vs, T::BK, a.v, a.ldv, start, (kt + 1) * T::BK, len, kvh * HD);
-        cp_async_commit();
-        tc5::tc_fence_before();
-        __syncthreads();  // P and S are reused by the next tile
     }
     cp_async_wait<0>();
     // ---- epilogue
