@@ -316,6 +316,26 @@ def main():
     eff_tokens = int(PL.sum_over_ranks(rows, device=dev))  # δ = 0: every fused row is a real token
     value = eff_tokens * args.steps / (ms_total / 1e3)
 
+    # ---------------- end-to-end (right after the headline pass) through the public API with host buffers: every step's
+    # 64 MiB hidden-state batch is copied H2D from pinned memory (copy stream, double
+    # buffered so step i+1's upload overlaps step i) and its per-job losses D2H.
+    from paper_2312_02515_b200.trainer import PipelinedTrainer
+    trainer = PipelinedTrainer(layer, rows, shapes[0][2])
+    losses_host = torch.empty(max(args.steps, 2), J, dtype=torch.float32).pin_memory()
+    trainer.run([x_host] * 2, losses_host[:2])  # warm the pipeline
+    barrier()
+    e2e_sampler = ClockSampler(dev)
+    e2e_sampler.start()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    trainer.run([x_host] * args.steps, losses_host[:args.steps])
+    f1.record(stream)
+    barrier()
+    e2e_clocks = e2e_sampler.stop()
+    e2e_ms = max_over_ranks(f0.elapsed_time(f1))
+    e2e_value = eff_tokens * args.steps / (e2e_ms / 1e3)
+    losses = losses_host[args.steps - 1].tolist()
+
     # ---------------- per-kernel live timing: the same K steps again with every launch
     # bracketed by CUDA events on its own stream (mlora_ctx_set_profiling).  Kept out of
     # the headline pass because events between launches defeat the PDL prologue overlap.
@@ -331,23 +351,6 @@ def main():
     ctx.set_profiling(False)
     prof = ctx.profile(reset=True)
     prof_ms_total = p0.elapsed_time(p1)
-
-    # ---------------- end-to-end through the public API with host buffers: every step's
-    # 64 MiB hidden-state batch is copied H2D from pinned memory (copy stream, double
-    # buffered so step i+1's upload overlaps step i) and its per-job losses D2H.
-    from paper_2312_02515_b200.trainer import PipelinedTrainer
-    trainer = PipelinedTrainer(layer, rows, shapes[0][2])
-    losses_host = torch.empty(max(args.steps, 2), J, dtype=torch.float32).pin_memory()
-    trainer.run([x_host] * 2, losses_host[:2])  # warm the pipeline
-    barrier()
-    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    f0.record(stream)
-    trainer.run([x_host] * args.steps, losses_host[:args.steps])
-    f1.record(stream)
-    barrier()
-    e2e_ms = max_over_ranks(f0.elapsed_time(f1))
-    e2e_value = eff_tokens * args.steps / (e2e_ms / 1e3)
-    losses = losses_host[args.steps - 1].tolist()
 
     # ---------------- roofline of the dominant kernel (base GEMM, forward)
     peaks = load_peaks()
@@ -403,7 +406,7 @@ def main():
         "kernel_ms_per_step": kernel_ms_per_step,
         "profiled_pass_ms_per_step": prof_ms_total / args.steps,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": x_host.numel() * 2,
-                "d2h_bytes_per_step": J * 4, "ms_per_step": e2e_ms / args.steps},
+                "d2h_bytes_per_step": J * 4, "ms_per_step": e2e_ms / args.steps, "clocks": e2e_clocks},
         "gpu_launches": launches,
         "clocks": clocks,
         "losses": losses,
