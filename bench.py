@@ -504,12 +504,15 @@ def run_decoder(args, cfg):
     # tokens / labels / mask / layout) + step + D2H of the per-job losses, every step
     host_loss = torch.empty(J, dtype=torch.float32).pin_memory()
     barrier()
+    e2e_sampler = ClockSampler(dev)
+    e2e_sampler.start()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record(stream)
     for _ in range(args.steps):
         host_loss.copy_(m.step(batch), non_blocking=True)
     f1.record(stream)
     barrier()
+    e2e_clocks = e2e_sampler.stop()
     e2e_ms = PL.max_over_ranks(f0.elapsed_time(f1), device=dev)
     # live per-kernel timing of the base GEMM (dominant kernel), a separate pass
     ctx.profile(reset=True)
@@ -551,7 +554,7 @@ def run_decoder(args, cfg):
         "kernel_ms_per_step": {k: round(v[1] / args.steps, 3) for k, v in prof.items()},
         "e2e": {"value": eff * args.steps / (e2e_ms / 1e3), "unit": UNIT,
                 "h2d_bytes_per_step": 9 * batch.rows + 4 * (2 * len(batch.seq_lens) + 1 + J + 1),
-                "d2h_bytes_per_step": 4 * J, "ms_per_step": e2e_ms / args.steps},
+                "d2h_bytes_per_step": 4 * J, "ms_per_step": e2e_ms / args.steps, "clocks": e2e_clocks},
         "gpu_launches": launches, "clocks": clocks, "losses": host_loss.tolist(),
         "cpu_baseline": None,
         "cpu_baseline_note": "the reference has no model arithmetic; its CPU path is per linear (--config c2)",
