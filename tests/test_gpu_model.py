@@ -12,18 +12,18 @@ def bf16_np(t):
     return t.float().cpu().double().numpy()
 
 
-def test_masked_ce_per_job_mean_and_grad_c4_vocab():
-    """ChatGLM2 vocabulary (V = 65024), padded fused batch with pad rows masked."""
+def _check_masked_ce(V, seg, seed=0):
     from paper_2312_02515_b200 import model_ops as M
     dev = torch.device("cuda", 0)
-    g = torch.Generator().manual_seed(0)
-    V, seg = 65024, [0, 40, 40, 100, 128]
+    g = torch.Generator().manual_seed(seed)
     rows = seg[-1]
     logits = (torch.randn(rows, V, generator=g) * 3).to(torch.bfloat16)
     labels = torch.randint(0, V, (rows,), generator=g, dtype=torch.int32)
     mask = (torch.rand(rows, generator=g) > 0.25).to(torch.uint8)
     loss, dl = M.masked_ce(logits.to(dev), labels.to(dev), seg, mask.to(dev))
+    loss2, dl2 = M.masked_ce(logits.to(dev), labels.to(dev), seg, mask.to(dev))
     torch.cuda.synchronize()
+    assert torch.equal(loss, loss2) and torch.equal(dl, dl2)  # deterministic
     L = bf16_np(logits)
     mx = L.max(1, keepdims=True)
     lse = (mx + np.log(np.exp(L - mx).sum(1, keepdims=True)))[:, 0]
@@ -42,6 +42,18 @@ def test_masked_ce_per_job_mean_and_grad_c4_vocab():
     got = bf16_np(dl)
     assert np.all(got[~m] == 0)
     assert np.linalg.norm(got - want_dl) / np.linalg.norm(want_dl) < 1e-2
+
+
+def test_masked_ce_per_job_mean_and_grad_c4_vocab():
+    """ChatGLM2 vocabulary (V = 65024), padded fused batch with pad rows masked."""
+    _check_masked_ce(65024, [0, 40, 40, 100, 128])
+
+
+@pytest.mark.parametrize("V", [8, 1000, 32000, 1001, 70000])
+def test_masked_ce_vocab_sizes(V):
+    """Vector row pass (V % 8 == 0: 8, 1000, LLaMA's 32000, 70000) and the scalar
+    path (1001: V % 8 != 0)."""
+    _check_masked_ce(V, [0, 17, 17, 50, 64], seed=V)
 
 
 def test_rmsnorm_fwd_bwd():
