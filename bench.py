@@ -36,6 +36,8 @@ sys.path.insert(0, ROOT)
 METRIC = "effective (non-pad) tokens/sec, LLaMA-7B shape, 4 fused LoRA jobs, 1-8 GPU"
 UNIT = "tokens/s"
 
+DEFAULT_STEPS = {"c2": 200, "c5": 30, "c4": 5}  # ~1.0 s, ~1.3 s, ~1.5 s of device time on one B200
+
 CONFIGS = {
     # name: (shape set, ranks, lrs, sequences per job, tokens per sequence)
     "c2": dict(shapes="llama7b", ranks=[16, 16, 16, 16], lrs=[1e-4, 2e-4, 5e-5, 3e-4], seqs=4, seq_len=512,
@@ -76,6 +78,8 @@ class ClockSampler(threading.Thread):
         super().__init__(daemon=True)
         self.period = period
         self.samples = []
+        self.power = []
+        self.power_limit_w = None
         self.reasons = 0
         self.max_mhz = None
         self._halt = threading.Event()
@@ -92,6 +96,10 @@ class ClockSampler(threading.Thread):
             except Exception:
                 self.h = nv.nvmlDeviceGetHandleByIndex(torch_dev.index or 0)
             self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+            try:
+                self.power_limit_w = nv.nvmlDeviceGetEnforcedPowerLimit(self.h) / 1000.0
+            except Exception:
+                pass
             self.ok = True
         except Exception:
             pass
@@ -106,16 +114,35 @@ class ClockSampler(threading.Thread):
             try:
                 self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
                 self.reasons |= get_reasons(self.h)
+                self.power.append(self._power_w())
             except Exception:
                 pass
             time.sleep(self.period)
+
+    def _power_w(self):
+        # instantaneous board power where the driver has it (GetPowerUsage is a ~1 s average)
+        nv = self.nv
+        fi = getattr(nv, "NVML_FI_DEV_POWER_INSTANT", None)
+        if fi is not None:
+            try:
+                v = nv.nvmlDeviceGetFieldValues(self.h, [fi])[0]
+                if v.nvmlReturn == 0:
+                    return v.value.uiVal / 1000.0
+            except Exception:
+                pass
+        return nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0
 
     def stop(self):
         self._halt.set()
         self.join(timeout=2)
         med = statistics.median(self.samples) if self.samples else None
+        # board power (instantaneous) against the enforced limit shows the power cap
+        # directly: the step is power-bound
         return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "samples": len(self.samples),
-                "reasons": [n for b, n in REASONS.items() if self.reasons & b]}
+                "reasons": [n for b, n in REASONS.items() if self.reasons & b],
+                "power_w_median": statistics.median(self.power) if self.power else None,
+                "power_w_max": max(self.power) if self.power else None,
+                "power_limit_w": self.power_limit_w}
 
 
 # ----------------------------------------------------------------------------- reference CPU arm
@@ -211,13 +238,19 @@ def run_reference_arm(args, cfg):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default: about 1 s of device time per config; 30 for --impl reference)")
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
+    if args.steps is None:
+        # NVML refreshes SM clocks / clock-event reasons / power about every 100 ms
+        # (tools/nvml_probe.py), so the timed region defaults to about 1 s of device
+        # time for the clock evidence to describe it
+        args.steps = 30 if args.impl == "reference" else DEFAULT_STEPS[args.config]
     if "decoder" in cfg:
         return run_decoder(args, cfg)
     if args.impl == "reference":
@@ -396,9 +429,11 @@ def main():
                    "flops_per_token": fpt},
         "step_tflops": step_tflops, "step_frac_of_peak": step_tflops / peak,
         "step_frac_of_sustained_peak": step_tflops / peaks["bf16_sustained"],
+        "step_frac_of_burst_peak": step_tflops / peaks["bf16"],
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "frac_of_sustained": (achieved / peaks["bf16_sustained"]) if achieved else None,
+                     "frac_of_burst": (achieved / peaks["bf16"]) if achieved else None,
                      "kernel": "mlora_base_pair_kernel (cta_group::2, 256x256 tile) forward: X W0^T + H B^T",
                      "peak_kind": ("sustained" if use_sustained else "burst") + " bf16, " + peaks["source"],
                      "launches": cnt, "avg_launch_us": 1e3 * ms / cnt if cnt else None},
