@@ -15,7 +15,6 @@ token per projection: 4dk + 6 r (d + k).
 """
 from __future__ import annotations
 
-import ctypes as C
 from dataclasses import dataclass
 
 import torch

@@ -1,5 +1,5 @@
 """Quick numerical probe of the device path vs the fp64 oracle (prints errors)."""
-import os, sys, time
+import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import torch
