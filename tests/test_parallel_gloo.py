@@ -54,7 +54,7 @@ def _worker(rank, world, port, out):
 @pytest.mark.timeout(120)
 def test_world2_broadcast_partition_and_timing():
     world = 2
-    mgr = mp.Manager()
+    mgr = mp.get_context("spawn").Manager()  # no fork() of the multi-threaded test process
     out = mgr.dict()
     mp.spawn(_worker, args=(world, _free_port(), out), nprocs=world, join=True)
     assert set(out.keys()) == {0, 1}
