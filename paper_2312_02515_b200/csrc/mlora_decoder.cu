@@ -751,7 +751,8 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 template <int HD>
-__global__ void __launch_bounds__(128, 1) attn_fwd_tc_kernel(AttnArgs a) {
+__global__ void __launch_bounds__(128, 1) attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tk,
+                                                             const __grid_constant__ CUtensorMap tv, AttnArgs a) {
     using T = TcAttn<HD>;
     pdl_prologue();
     int start, len;
@@ -767,12 +768,15 @@ __global__ void __launch_bounds__(128, 1) attn_fwd_tc_kernel(AttnArgs a) {
     uint8_t* Vs = Ks + T::K_BYTES;  // two buffers: V_kt at Vs + (kt & 1) * V_BYTES
     uint8_t* Ps = Vs + 2 * T::V_BYTES;
     uint64_t* bar = reinterpret_cast<uint64_t*>(Ps + T::P_BYTES);  // [0] S done, [1] P V done
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 2);
+    uint64_t* k_full = bar + 2;                                     // K tile landed (TMA)
+    uint64_t* v_full = bar + 3;                                     // [2] V tile landed (TMA), per buffer
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 5);
     const int warp = threadIdx.x >> 5, row = threadIdx.x;
     if (threadIdx.x == 0) {
-        tc5::mbar_init(bar, 1);
-        tc5::mbar_init(bar + 1, 1);
+        for (int i = 0; i < 5; ++i) tc5::mbar_init(bar + i, 1);
         tc5::fence_barrier_init();
+        tc5::tma_prefetch_desc(&tk);
+        tc5::tma_prefetch_desc(&tv);
     }
     if (warp == 0) {
         tc5::tmem_alloc(tslot, T::TMEM_COLS);
@@ -782,22 +786,42 @@ __global__ void __launch_bounds__(128, 1) attn_fwd_tc_kernel(AttnArgs a) {
     // Software pipeline over the key tiles.  The MMA thread issues S_kt+1 = Q K_kt+1^T
     // ahead of O += P_kt V_kt, so the softmax of tile kt+1 (TMEM load, max, exp2)
     // runs while the tensor pipe still works on P_kt V_kt; only the P store and
-    // the rare O rescale wait for it.  cp.async groups, in issue order: [Q + K_0],
-    // [V_0], then per tile kt [K_kt+1] (once S_kt is done) and [V_kt+1] (once
-    // P_kt-1 V_kt-1 is done, into the other V buffer).
+    // the rare O rescale wait for it.  K / V tiles arrive by TMA (thread 0 issues,
+    // mbarriers complete): K_kt+1 once S_kt is done, V_kt+1 into the other V buffer
+    // once P_kt-1 V_kt-1 is done.  V rows past the sequence are zeroed after the
+    // tile lands (P is 0 there, but 0 * NaN from a neighbouring sequence is not);
+    // K rows past it only reach masked scores.
+    auto load_k = [&](int t) {
+        tc5::mbar_arrive_expect_tx(k_full, T::K_BYTES);
+#pragma unroll
+        for (int blk = 0; blk < T::NB; ++blk)
+            tc5::tma_load_2d(smem_u32(Ks + blk * T::BK * 128), &tk, k_full, kvh * HD + blk * 64, start + t * T::BK);
+    };
+    auto load_v = [&](int t) {
+        uint8_t* Vb = Vs + (t & 1) * T::V_BYTES;
+        tc5::mbar_arrive_expect_tx(v_full + (t & 1), T::V_BYTES);
+#pragma unroll
+        for (int blk = 0; blk < T::NB; ++blk)
+            tc5::tma_load_2d(smem_u32(Vb + blk * T::BK * 128), &tv, v_full + (t & 1), kvh * HD + blk * 64,
+                             start + t * T::BK);
+    };
     stage_sw128<HD>(Qs, T::BQ, a.q, a.ldq, start, q0, len, h * HD);
-    if (nkt > 0) stage_sw128<HD>(Ks, T::BK, a.k, a.ldk, start, 0, len, kvh * HD);
     cp_async_commit();
-    if (nkt > 0) stage_sw128<HD>(Vs, T::BK, a.v, a.ldv, start, 0, len, kvh * HD);
-    cp_async_commit();
-    cp_async_wait<1>();  // Q and K_0
-    fence_proxy_async();
     tc5::tc_fence_before();
-    __syncthreads();
+    __syncthreads();  // barriers initialised
     tc5::tc_fence_after();
+    if (threadIdx.x == 0 && nkt > 0) {
+        load_k(0);
+        load_v(0);
+    }
+    cp_async_wait<0>();  // Q
+    fence_proxy_async();
+    __syncthreads();
     const uint32_t tmem = *tslot;
     const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
-    auto issue_s = [&]() {  // S = Q K^T into TMEM, K-major operands
+    auto issue_s = [&](int t) {  // S = Q K_t^T into TMEM, K-major operands
+        tc5::mbar_wait(k_full, t & 1);
+        tc5::tc_fence_after();
 #pragma unroll
         for (int j = 0; j < HD / 16; ++j) {
             const uint64_t ad = tc5::sdesc_sw128(smem_u32(Qs + (j / 4) * T::BQ * 128 + (j % 4) * 32), 16, 1024);
@@ -806,7 +830,7 @@ __global__ void __launch_bounds__(128, 1) attn_fwd_tc_kernel(AttnArgs a) {
         }
         tc5::tc_commit(bar);
     };
-    if (threadIdx.x == 0 && nkt > 0) issue_s();
+    if (threadIdx.x == 0 && nkt > 0) issue_s(0);
     const float c2 = a.scale * kLog2e;
     const int qi = q0 + row;
     float m = -INFINITY, l = 0.f;  // m: the row's reference max (log2 domain)
@@ -815,8 +839,7 @@ __global__ void __launch_bounds__(128, 1) attn_fwd_tc_kernel(AttnArgs a) {
         tc5::mbar_wait(bar, phase_s);  // S_kt in TMEM (and K_kt consumed)
         phase_s ^= 1u;
         tc5::tc_fence_after();
-        if (kt + 1 < nkt) stage_sw128<HD>(Ks, T::BK, a.k, a.ldk, start, (kt + 1) * T::BK, len, kvh * HD);
-        cp_async_commit();
+        if (threadIdx.x == 0 && kt + 1 < nkt) load_k(kt + 1);
         // ---- softmax of this thread's row (64 keys)
         float s[64];
         {
@@ -871,10 +894,7 @@ __global__ void __launch_bounds__(128, 1) attn_fwd_tc_kernel(AttnArgs a) {
             phase_o ^= 1u;
             tc5::tc_fence_after();
         }
-        if (kt + 1 < nkt)
-            stage_sw128<HD>(Vs + ((kt + 1) & 1) * T::V_BYTES, T::BK, a.v, a.ldv, start, (kt + 1) * T::BK, len,
-                            kvh * HD);
-        cp_async_commit();
+        if (threadIdx.x == 0 && kt + 1 < nkt) load_v(kt + 1);
         // rescale what O holds so far.  tcgen05.ld / st are warp-collective
         // (.sync.aligned): the O read-modify-write runs for the whole warp when any
         // of its rows needs it (alpha = 1 for the others).
@@ -895,14 +915,23 @@ __global__ void __launch_bounds__(128, 1) attn_fwd_tc_kernel(AttnArgs a) {
         for (int ch = 0; ch < 8; ++ch)
             *reinterpret_cast<uint4*>(prow + ((ch ^ (row & 7)) << 4)) =
                 make_uint4(pk[ch * 4], pk[ch * 4 + 1], pk[ch * 4 + 2], pk[ch * 4 + 3]);
-        cp_async_wait<1>();  // V_kt and K_kt+1 landed (V_kt+1 may still be in flight)
+        uint8_t* Vb = Vs + (kt & 1) * T::V_BYTES;
+        if (kt * T::BK + T::BK > len) {  // V_kt holds rows past the sequence: zero them
+            tc5::mbar_wait(v_full + (kt & 1), (kt >> 1) & 1);
+            const int r0 = len - kt * T::BK;
+            for (int e = threadIdx.x; e < (T::BK - r0) * T::NB * 8; e += blockDim.x) {
+                const int ch = e & 7, rb = e >> 3, r = r0 + rb % (T::BK - r0), blk = rb / (T::BK - r0);
+                *reinterpret_cast<uint4*>(Vb + blk * T::BK * 128 + r * 128 + (ch << 4)) = make_uint4(0, 0, 0, 0);
+            }
+        }
         fence_proxy_async();
         tc5::tc_fence_before();
         __syncthreads();
         if (threadIdx.x == 0) {
             tc5::tc_fence_after();
-            if (kt + 1 < nkt) issue_s();  // S_kt+1 first: the next softmax overlaps P_kt V_kt
-            const uint8_t* Vb = Vs + (kt & 1) * T::V_BYTES;
+            if (kt + 1 < nkt) issue_s(kt + 1);  // S_kt+1 first: the next softmax overlaps P_kt V_kt
+            tc5::mbar_wait(v_full + (kt & 1), (kt >> 1) & 1);
+            tc5::tc_fence_after();
 #pragma unroll
             for (int j = 0; j < T::BK / 16; ++j) {  // O += P V, V an MN-major B operand
                 const uint64_t ad = tc5::sdesc_sw128(smem_u32(Ps + j * 32), 16, 1024);
@@ -2240,6 +2269,16 @@ cudaError_t launch_attn_wsq(K kernel, const mlora_attn_desc* d, size_t smem, voi
     return launch(kernel, dim3((d->max_len + 127) / 128, d->num_seqs, d->heads), dim3(288), smem, stream, tk, tv, a);
 }
 
+// The tcgen05 forward: 128-query blocks, 128 threads, K / V tensor maps.
+template <typename K>
+cudaError_t launch_attn_fwd_tc(K kernel, const mlora_attn_desc* d, size_t smem, void* stream, const CUtensorMap& tk,
+                               const CUtensorMap& tv, const AttnArgs& a) {
+    if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
+        cudaSuccess)
+        return cudaErrorInvalidValue;
+    return launch(kernel, dim3((d->max_len + 127) / 128, d->num_seqs, d->heads), dim3(128), smem, stream, tk, tv, a);
+}
+
 // MLORA_ATTN_TC=0 keeps the mma.sync forward / dQ kernels (A/B knob); the
 // tcgen05 ones need pre-rotated Q / K and 16-byte-aligned rows.
 bool attn_tc_enabled() {
@@ -2367,11 +2406,13 @@ mlora_status mlora_attn_fwd(const mlora_attn_desc* d, const void* q, int64_t ldq
     a.lse = lse;
     a.vec = rows16(q, ldq) && rows16(k, ldk) && rows16(v, ldv);
     cudaError_t e;
-    if (attn_tc_enabled() && a.vec && !a.rope_in && (reinterpret_cast<uintptr_t>(o) & 15) == 0 && ldo % 8 == 0) {
-        // the tcgen05 kernel: 128 query rows per CTA, one thread per row
+    CUtensorMap tk, tv;
+    if (attn_tc_enabled() && a.vec && !a.rope_in && (reinterpret_cast<uintptr_t>(o) & 15) == 0 && ldo % 8 == 0 &&
+        encode_rows_map(k, ldk, d->rows, &tk) && encode_rows_map(v, ldv, d->rows, &tv)) {
+        // the tcgen05 kernel: 128 query rows per CTA, one thread per row, K / V by TMA
         const size_t smem = hd == 64 ? TcAttn<64>::SMEM : TcAttn<128>::SMEM;
-        e = hd == 64 ? launch_attn_rows(attn_fwd_tc_kernel<64>, 128, 128, d, d->heads, smem, stream, a)
-                     : launch_attn_rows(attn_fwd_tc_kernel<128>, 128, 128, d, d->heads, smem, stream, a);
+        e = hd == 64 ? launch_attn_fwd_tc(attn_fwd_tc_kernel<64>, d, smem, stream, tk, tv, a)
+                     : launch_attn_fwd_tc(attn_fwd_tc_kernel<128>, d, smem, stream, tk, tv, a);
     } else {
         constexpr int R = kFwdRows;
         e = hd == 64 ? launch_attn(attn_fwd_kernel<64, R>, R, d, d->heads, attn_smem_fwd<64, R>(), stream, a)
