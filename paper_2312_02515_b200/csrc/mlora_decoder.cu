@@ -692,8 +692,9 @@ __global__ void attn_rope_kernel(AttnArgs a, const __nv_bfloat16* __restrict__ s
 // than 2^8: P then stays <= 256 (exact in bf16's range, fp32 sums), and the O
 // read-modify-write happens a handful of times per row instead of every tile.
 // Operand tiles use the 128-byte-swizzle layout (16-byte chunk c of row r at
-// chunk c ^ (r & 7) of a 1024-byte, 8-row atom), written with cp.async (Q, K,
-// V) or st.shared (P), then fence.proxy.async before the MMA reads them.
+// chunk c ^ (r & 7) of a 1024-byte, 8-row atom): Q, K and V land there by TMA
+// (SWIZZLE_128B maps, mbarrier completion), P is written with st.shared and
+// fenced (fence.proxy.async) before the MMA reads it.
 // Q and K must come pre-rotated (mlora_attn_rope); otherwise the mma.sync
 // kernel above runs.
 namespace tc5 = mlora::sm100;
@@ -751,7 +752,8 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 template <int HD>
-__global__ void __launch_bounds__(128, 1) attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tk,
+__global__ void __launch_bounds__(128, 1) attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap tq,
+                                                             const __grid_constant__ CUtensorMap tk,
                                                              const __grid_constant__ CUtensorMap tv, AttnArgs a) {
     using T = TcAttn<HD>;
     pdl_prologue();
@@ -770,11 +772,13 @@ __global__ void __launch_bounds__(128, 1) attn_fwd_tc_kernel(const __grid_consta
     uint64_t* bar = reinterpret_cast<uint64_t*>(Ps + T::P_BYTES);  // [0] S done, [1] P V done
     uint64_t* k_full = bar + 2;                                     // K tile landed (TMA)
     uint64_t* v_full = bar + 3;                                     // [2] V tile landed (TMA), per buffer
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 5);
+    uint64_t* q_full = bar + 5;                                     // Q block landed (TMA)
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 6);
     const int warp = threadIdx.x >> 5, row = threadIdx.x;
     if (threadIdx.x == 0) {
-        for (int i = 0; i < 5; ++i) tc5::mbar_init(bar + i, 1);
+        for (int i = 0; i < 6; ++i) tc5::mbar_init(bar + i, 1);
         tc5::fence_barrier_init();
+        tc5::tma_prefetch_desc(&tq);
         tc5::tma_prefetch_desc(&tk);
         tc5::tma_prefetch_desc(&tv);
     }
@@ -805,21 +809,26 @@ __global__ void __launch_bounds__(128, 1) attn_fwd_tc_kernel(const __grid_consta
             tc5::tma_load_2d(smem_u32(Vb + blk * T::BK * 128), &tv, v_full + (t & 1), kvh * HD + blk * 64,
                              start + t * T::BK);
     };
-    stage_sw128<HD>(Qs, T::BQ, a.q, a.ldq, start, q0, len, h * HD);
-    cp_async_commit();
+    // Q rows past the sequence (the next sequence's, or TMA's zero fill) only reach
+    // rows whose scores are all masked: P = 0 there and the output row is zeroed
     tc5::tc_fence_before();
     __syncthreads();  // barriers initialised
     tc5::tc_fence_after();
     if (threadIdx.x == 0 && nkt > 0) {
+        tc5::mbar_arrive_expect_tx(q_full, T::Q_BYTES);
+#pragma unroll
+        for (int blk = 0; blk < T::NB; ++blk)
+#pragma unroll
+            for (int hf = 0; hf < T::BQ / 64; ++hf)
+                tc5::tma_load_2d(smem_u32(Qs + blk * T::BQ * 128 + hf * 64 * 128), &tq, q_full, h * HD + blk * 64,
+                                 start + q0 + hf * 64);
         load_k(0);
         load_v(0);
     }
-    cp_async_wait<0>();  // Q
-    fence_proxy_async();
-    __syncthreads();
     const uint32_t tmem = *tslot;
     const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
     auto issue_s = [&](int t) {  // S = Q K_t^T into TMEM, K-major operands
+        if (t == 0) tc5::mbar_wait(q_full, 0);
         tc5::mbar_wait(k_full, t & 1);
         tc5::tc_fence_after();
 #pragma unroll
@@ -2271,12 +2280,13 @@ cudaError_t launch_attn_wsq(K kernel, const mlora_attn_desc* d, size_t smem, voi
 
 // The tcgen05 forward: 128-query blocks, 128 threads, K / V tensor maps.
 template <typename K>
-cudaError_t launch_attn_fwd_tc(K kernel, const mlora_attn_desc* d, size_t smem, void* stream, const CUtensorMap& tk,
-                               const CUtensorMap& tv, const AttnArgs& a) {
+cudaError_t launch_attn_fwd_tc(K kernel, const mlora_attn_desc* d, size_t smem, void* stream, const CUtensorMap& tq,
+                               const CUtensorMap& tk, const CUtensorMap& tv, const AttnArgs& a) {
     if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
         cudaSuccess)
         return cudaErrorInvalidValue;
-    return launch(kernel, dim3((d->max_len + 127) / 128, d->num_seqs, d->heads), dim3(128), smem, stream, tk, tv, a);
+    return launch(kernel, dim3((d->max_len + 127) / 128, d->num_seqs, d->heads), dim3(128), smem, stream, tq, tk, tv,
+                  a);
 }
 
 // MLORA_ATTN_TC=0 keeps the mma.sync forward / dQ kernels (A/B knob); the
@@ -2406,13 +2416,14 @@ mlora_status mlora_attn_fwd(const mlora_attn_desc* d, const void* q, int64_t ldq
     a.lse = lse;
     a.vec = rows16(q, ldq) && rows16(k, ldk) && rows16(v, ldv);
     cudaError_t e;
-    CUtensorMap tk, tv;
+    CUtensorMap tq, tk, tv;
     if (attn_tc_enabled() && a.vec && !a.rope_in && (reinterpret_cast<uintptr_t>(o) & 15) == 0 && ldo % 8 == 0 &&
-        encode_rows_map(k, ldk, d->rows, &tk) && encode_rows_map(v, ldv, d->rows, &tv)) {
+        encode_rows_map(q, ldq, d->rows, &tq) && encode_rows_map(k, ldk, d->rows, &tk) &&
+        encode_rows_map(v, ldv, d->rows, &tv)) {
         // the tcgen05 kernel: 128 query rows per CTA, one thread per row, K / V by TMA
         const size_t smem = hd == 64 ? TcAttn<64>::SMEM : TcAttn<128>::SMEM;
-        e = hd == 64 ? launch_attn_fwd_tc(attn_fwd_tc_kernel<64>, d, smem, stream, tk, tv, a)
-                     : launch_attn_fwd_tc(attn_fwd_tc_kernel<128>, d, smem, stream, tk, tv, a);
+        e = hd == 64 ? launch_attn_fwd_tc(attn_fwd_tc_kernel<64>, d, smem, stream, tq, tk, tv, a)
+                     : launch_attn_fwd_tc(attn_fwd_tc_kernel<128>, d, smem, stream, tq, tk, tv, a);
     } else {
         constexpr int R = kFwdRows;
         e = hd == 64 ? launch_attn(attn_fwd_kernel<64, R>, R, d, d->heads, attn_smem_fwd<64, R>(), stream, a)
