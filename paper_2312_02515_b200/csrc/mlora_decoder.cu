@@ -1723,6 +1723,8 @@ struct WsDq {
 template <int HD>
 __global__ void __launch_bounds__(288, 1) attn_bwd_dq_ws_kernel(const __grid_constant__ CUtensorMap tk,
                                                                  const __grid_constant__ CUtensorMap tv,
+                                                                 const __grid_constant__ CUtensorMap tq,
+                                                                 const __grid_constant__ CUtensorMap tdo,
                                                                  AttnArgs a) {
     using T = WsDq<HD>;
     pdl_prologue();
@@ -1778,14 +1780,18 @@ __global__ void __launch_bounds__(288, 1) attn_bwd_dq_ws_kernel(const __grid_con
         if (lt == 0) {
             tc5::tma_prefetch_desc(&tk);
             tc5::tma_prefetch_desc(&tv);
+            // Q / dO by TMA; rows past the sequence only reach masked scores (P = 0)
+            // of rows whose dQ the epilogue writes as zero
+            tc5::mbar_arrive_expect_tx(q_full, 2 * T::Q_BYTES);
+#pragma unroll
+            for (int blk = 0; blk < T::NB; ++blk)
+#pragma unroll
+                for (int hf = 0; hf < T::BQ / 64; ++hf) {
+                    const int off = blk * T::BQ * 128 + hf * 64 * 128;
+                    tc5::tma_load_2d(smem_u32(Qs + off), &tq, q_full, h * HD + blk * 64, start + q0 + hf * 64);
+                    tc5::tma_load_2d(smem_u32(dOs + off), &tdo, q_full, h * HD + blk * 64, start + q0 + hf * 64);
+                }
         }
-        stage_sw128_warp<HD>(Qs, T::BQ, a.q, a.ldq, start, q0, len, h * HD, lt);
-        stage_sw128_warp<HD>(dOs, T::BQ, a.dO, a.lddo, start, q0, len, h * HD, lt);
-        cp_async_commit();
-        cp_async_wait<0>();
-        fence_proxy_async();
-        loaders_sync();
-        if (lt == 0) tc5::mbar_arrive(q_full);
         for (int kt = 0; kt < nkt; ++kt) {
             const int st = kt % T::STAGES, k0 = kt * T::BK;
             if (kt >= T::STAGES) tc5::mbar_wait(kv_free + st, ((kt - T::STAGES) / T::STAGES) & 1);
@@ -2271,11 +2277,12 @@ cudaError_t launch_attn_ws(K kernel, const mlora_attn_desc* d, size_t smem, void
 // The warp-specialised dQ kernel: 128-query blocks, 288 threads, one CTA per (block, sequence, head).
 template <typename K>
 cudaError_t launch_attn_wsq(K kernel, const mlora_attn_desc* d, size_t smem, void* stream, const CUtensorMap& tk,
-                            const CUtensorMap& tv, const AttnArgs& a) {
+                            const CUtensorMap& tv, const CUtensorMap& tq, const CUtensorMap& tdo, const AttnArgs& a) {
     if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
         cudaSuccess)
         return cudaErrorInvalidValue;
-    return launch(kernel, dim3((d->max_len + 127) / 128, d->num_seqs, d->heads), dim3(288), smem, stream, tk, tv, a);
+    return launch(kernel, dim3((d->max_len + 127) / 128, d->num_seqs, d->heads), dim3(288), smem, stream, tk, tv, tq,
+                  tdo, a);
 }
 
 // The tcgen05 forward: 128-query blocks, 128 threads, K / V tensor maps.
@@ -2481,16 +2488,15 @@ mlora_status mlora_attn_bwd(const mlora_attn_desc* d, const void* q, int64_t ldq
             const char* e = std::getenv("MLORA_ATTN_WS");
             return !(e && e[0] == '0');
         }();
-        CUtensorMap tk, tv;
-        if (ws && encode_rows_map(k, ldk, d->rows, &tk) && encode_rows_map(v, ldv, d->rows, &tv))
-            e = hd == 64 ? launch_attn_wsq(attn_bwd_dq_ws_kernel<64>, d, WsDq<64>::SMEM, stream, tk, tv, a)
-                         : launch_attn_wsq(attn_bwd_dq_ws_kernel<128>, d, WsDq<128>::SMEM, stream, tk, tv, a);
+        CUtensorMap tk, tv, tq, tdo;
+        const bool maps = ws && encode_rows_map(q, ldq, d->rows, &tq) && encode_rows_map(dout, lddo, d->rows, &tdo);
+        if (maps && encode_rows_map(k, ldk, d->rows, &tk) && encode_rows_map(v, ldv, d->rows, &tv))
+            e = hd == 64 ? launch_attn_wsq(attn_bwd_dq_ws_kernel<64>, d, WsDq<64>::SMEM, stream, tk, tv, tq, tdo, a)
+                         : launch_attn_wsq(attn_bwd_dq_ws_kernel<128>, d, WsDq<128>::SMEM, stream, tk, tv, tq, tdo, a);
         else
             e = hd == 64 ? launch_attn_rows(attn_bwd_dq_tc_kernel<64>, 128, 128, d, d->heads, TcDq<64>::SMEM, stream, a)
                          : launch_attn_rows(attn_bwd_dq_tc_kernel<128>, 128, 128, d, d->heads, TcDq<128>::SMEM, stream,
                                             a);
-        CUtensorMap tq, tdo;
-        const bool maps = ws && encode_rows_map(q, ldq, d->rows, &tq) && encode_rows_map(dout, lddo, d->rows, &tdo);
         if (e == cudaSuccess && maps)
             e = hd == 64 ? launch_attn_ws(attn_bwd_dkv_ws_kernel<64>, d, WsDkv<64>::SMEM, stream, tq, tdo, a)
                          : launch_attn_ws(attn_bwd_dkv_ws_kernel<128>, d, WsDkv<128>::SMEM, stream, tq, tdo, a);
