@@ -639,7 +639,7 @@ __global__ void __launch_bounds__(2 * R, 2) attn_fwd_kernel(AttnArgs a) {
 // rows past len are zeroed): one CTA per (64-row tile, sequence, group of
 // kRopeHeads heads); each thread owns 8 consecutive rotation pairs (16-byte
 // accesses) and applies their angles to the group's heads.
-constexpr int kRopeHeads = 4;
+constexpr int kRopeHeads = 16;  // ncu at C4 (32 query heads): 4 / 8 / 16 / 32 heads -> 42 / 44 / 40 / 58 us
 __global__ void attn_rope_kernel(AttnArgs a, const __nv_bfloat16* __restrict__ src, long long lds, int n_heads, int hd,
                                  __nv_bfloat16* __restrict__ dst, long long ldd) {
     pdl_prologue();
