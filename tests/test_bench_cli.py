@@ -32,3 +32,14 @@ def test_config_table():
 def test_help():
     r = run("--help")
     assert r.returncode == 0 and "--config" in r.stdout
+
+
+def test_default_steps_cover_the_nvml_refresh():
+    """Without --steps each config times about 1 s of device work (NVML refreshes
+    clocks / reasons / power about every 100 ms), and every config has a default."""
+    sys.path.insert(0, ROOT)
+    import bench
+    assert set(bench.DEFAULT_STEPS) == set(bench.CONFIGS)
+    ms_per_step = {"c2": 5.2, "c5": 42.0, "c4": 300.0}  # measured on one B200 (profiles/)
+    for name, steps in bench.DEFAULT_STEPS.items():
+        assert steps * ms_per_step[name] >= 1000.0, name
