@@ -212,6 +212,29 @@ def time_reference(cfg, steps, warmup, seq_len=64, budget_s=None):
                 ms_per_step=1e3 * total / len(times), steps_run=len(times))
 
 
+def time_reference_single_core(cfg, seq_len=16):
+    """The reference's own path as it ships: ONE process, ONE thread
+    (lora.cpp:160-182 is single-threaded).  One fused_forward
+    call per projection of the layer, run back to back on one host thread, on a
+    smaller sample than the all-core leg (J jobs x 1 seq x `seq_len` tokens per
+    projection) so it stays ~15-20 s."""
+    from oracle import ref
+    if not ref.available():
+        ref.build()
+    if not ref.available():
+        return None
+    calls, tokens = reference_sample(cfg, seq_len, seed=2, replicas=1)
+    t0 = time.perf_counter()
+    for c in calls:
+        c()
+    dt = time.perf_counter() - t0
+    return dict(value=tokens / dt, unit=UNIT, cores=1, kind="reference",
+                sample=f"reference fusim::fused_forward (fp64, forward only), one process, one thread: "
+                       f"{len(calls)} projections x {min(4, len(cfg['ranks']))} jobs x 1 seq x {seq_len} tokens "
+                       f"= {tokens} effective tokens in {dt:.1f} s (host nproc = {os.cpu_count()}, "
+                       f"affinity = {host_threads()})")
+
+
 def run_reference_arm(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -235,6 +258,29 @@ def run_reference_arm(args, cfg):
 
 
 # ----------------------------------------------------------------------------- our arm
+def launch_command(gpus: int, argv: list[str], port: int) -> list[str]:
+    """`python bench.py --gpus N ...` without a launcher re-executes itself under
+    torch.distributed.run: one process per GPU, rendezvous on 127.0.0.1."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *argv]
+
+
+def self_launch(gpus: int) -> int:
+    import socket
+    import subprocess
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    # NCCL's init log (rank count, transport) goes to stderr for the record
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    env.setdefault("OMP_NUM_THREADS", "1")
+    cmd = launch_command(gpus, sys.argv[1:], port)
+    print("[bench] " + " ".join(cmd), file=sys.stderr, flush=True)
+    return subprocess.run(cmd, env=env).returncode
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -246,6 +292,17 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is not None and int(env_world) != args.gpus and args.impl != "reference":
+        print(f"[bench] --gpus {args.gpus} but WORLD_SIZE={env_world}: launch one process per GPU "
+              f"(torch.distributed.run --nproc-per-node {args.gpus}) or drop --gpus", file=sys.stderr)
+        return 2
+    if env_world is None and args.gpus > 1 and args.impl != "reference":
+        return self_launch(args.gpus)
+    if os.environ.get("MLORA_BENCH_PROBE_LAUNCH") == "1":  # CPU test of the launcher: report the rank layout
+        print(json.dumps({"rank": int(os.environ.get("RANK", "0")), "world": int(os.environ.get("WORLD_SIZE", "1")),
+                          "local_rank": int(os.environ.get("LOCAL_RANK", "0")), "gpus": args.gpus}), flush=True)
+        return 0
     if args.steps is None:
         # NVML refreshes SM clocks / clock-event reasons / power about every 100 ms
         # (tools/nvml_probe.py), so the timed region defaults to about 1 s of device
@@ -307,8 +364,20 @@ def main():
             comm, replication = PL.NativeComm(ctx), "mlora_broadcast_base (one NCCL group)"
         except Exception as e:  # setup only, never timed: keep the run alive, say so
             print(f"[bench] native communicator unavailable ({e}); W0 via torch.distributed", file=sys.stderr)
+    comm_info = None
+    if comm is not None:
+        import ctypes
+        from paper_2312_02515_b200 import _native as NL
+        v = ctypes.c_int32()
+        NL.lib().mlora_comm_nccl_version(ctypes.byref(v))
+        comm_info = {"impl": "mlora_broadcast_base", "nranks": NL.lib().mlora_comm_size(comm.handle),
+                     "nccl_version": v.value,
+                     "bytes": sum(t.numel() * t.element_size() for t in W0.values())}
+    t_bc = time.perf_counter()
     PL.broadcast_base_weights(W0, src=0, comm=comm)
     torch.cuda.synchronize()
+    if comm_info is not None:
+        comm_info["seconds"] = time.perf_counter() - t_bc
     if comm is not None:
         comm.close()  # the one-off replication is done: the steady state has no collective
 
@@ -348,6 +417,24 @@ def main():
     ms_step = ms_total / args.steps
     eff_tokens = int(PL.sum_over_ranks(rows, device=dev))  # δ = 0: every fused row is a real token
     value = eff_tokens * args.steps / (ms_total / 1e3)
+
+    # ---------------- sustained: the same step for >= 1.2 s of device time, so the
+    # board's power cap (1 kW, engaged within ~100 ms of load) and the capped SM
+    # clock are in force and NVML has refreshed its readings several times
+    sus_steps = max(args.steps, int(1200.0 / max(ms_step, 1e-3)) + 1)
+    sus_sampler = ClockSampler(dev)
+    sus_sampler.start()
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    g0.record(stream)
+    for _ in range(sus_steps):
+        layer.step(x)
+    g1.record(stream)
+    barrier()
+    sus_clocks = sus_sampler.stop()
+    sus_ms = max_over_ranks(g0.elapsed_time(g1))
+    sustained = {"value": eff_tokens * sus_steps / (sus_ms / 1e3), "unit": UNIT, "steps": sus_steps,
+                 "ms_per_step": sus_ms / sus_steps, "clocks": sus_clocks}
 
     # ---------------- end-to-end (right after the headline pass) through the public API with host buffers: every step's
     # 64 MiB hidden-state batch is copied H2D from pinned memory (copy stream, double
@@ -413,6 +500,9 @@ def main():
             r = time_reference(cfg, steps=1, warmup=0)
             if r is not None:
                 cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
+                r1 = time_reference_single_core(cfg)
+                if r1 is not None:
+                    cpu["single_core"] = {k: r1[k] for k in ("value", "unit", "cores", "kind", "sample")}
         except Exception as e:  # the baseline is reported, never the target
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
 
@@ -442,6 +532,8 @@ def main():
         "profiled_pass_ms_per_step": prof_ms_total / args.steps,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": x_host.numel() * 2,
                 "d2h_bytes_per_step": J * 4, "ms_per_step": e2e_ms / args.steps, "clocks": e2e_clocks},
+        "sustained": sustained,
+        "replication": comm_info,
         "gpu_launches": launches,
         "clocks": clocks,
         "losses": losses,

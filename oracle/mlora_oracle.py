@@ -245,6 +245,26 @@ def segmented_backward(dY, X, W0, As, Bs, scales, seg):
     return dX, dAs, dBs
 
 
+def segmented_adapter_grads(dY, X, As, Bs, scales, seg):
+    """The adapter half of segmented_backward (same composed reference
+    primitives, SURVEY.md §8c probe B) without the dense dX = dY W0 term, so
+    full-size layers (8192 x 11008) are checked in seconds:
+       dA_j = transpose(matmul(dY_j, s B_j)) @ X_j,  dB_j = s dY_j^T matmul(X_j, A_j^T).
+    Jobs with an empty segment get exact zeros."""
+    dAs, dBs = [], []
+    for j in range(len(As)):
+        a, b = seg[j], seg[j + 1]
+        A = np.asarray(As[j], np.float64)
+        B = np.asarray(Bs[j], np.float64)
+        s = float(scales[j])
+        dYj = np.asarray(dY[a:b], np.float64)
+        Xj = np.asarray(X[a:b], np.float64)
+        G = (dYj @ B) * s
+        dAs.append(G.T @ Xj)
+        dBs.append(s * (dYj.T @ (Xj @ A.T)))
+    return dAs, dBs
+
+
 # ---------------------------------------------------------------------------
 # batch_select.cpp
 @dataclass

@@ -302,9 +302,18 @@ class FusedLoraLayer(AdapterJobsMixin):
         for p in self.proj:
             states += [p.A, p.B]
             grads += [p.dA, p.dB]
-        F.adam_step(self.ctx, self.plan, states, grads, self.lrs, steps, stream=stream)
+        # loss_gate: a job whose loss this step is not finite keeps p, m, v and its
+        # step count untouched on the device (its gradient was zeroed by the guard,
+        # but stale momentum must not move its adapter either)
+        F.adam_step(self.ctx, self.plan, states, grads, self.lrs, steps, stream=stream, loss_gate=self.loss)
 
     def step(self, x: torch.Tensor, active=None, stream=None) -> torch.Tensor:
+        """One fused training iteration over the installed layout; returns the
+        per-job loss (device fp32 [J]).  Note: when a job's loss is not finite
+        the non-finite guard zeroes that job's rows of every tensor the backward
+        reads, including the caller's `x` (in place) — the rows are already
+        poisoned for this step and a zero row is what keeps the other jobs'
+        fused reductions exact."""
         loss = self.forward_backward(x, stream)
         self.optimizer_step(active, stream)
         return loss
