@@ -349,13 +349,11 @@ def main():
     seg = [j * per_job for j in range(J + 1)]
 
     # frozen base weights: created on rank 0, replicated once (NCCL broadcast over NVLink)
-    g = torch.Generator(device="cpu").manual_seed(1234)
     W0 = {}
-    for name, d, k, _ in shapes:
-        if rank == 0:
-            W0[name] = ((torch.rand(d, k, generator=g) * 2 - 1) / k ** 0.5).to(torch.bfloat16).to(dev)
-        else:
-            W0[name] = torch.empty(d, k, dtype=torch.bfloat16, device=dev)
+    for pi, (name, d, k, _) in enumerate(shapes):
+        W0[name] = torch.empty(d, k, dtype=torch.bfloat16, device=dev)
+        if rank == 0:  # U(-1, 1)/sqrt(k), the device's counter-based fill
+            F.fill_uniform(W0[name], F.mix_seed(1234, 0, pi), -k ** -0.5, k ** -0.5)
     ctx = F.Context(dev)
     # one GPU per rank: the native communicator (libmlora.so -> NCCL), all W0 in one group
     comm, replication = None, "none (1 rank)" if world == 1 else "torch.distributed"

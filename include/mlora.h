@@ -90,6 +90,10 @@ int64_t mlora_free_launch_count(void);
 mlora_status mlora_ctx_set_profiling(mlora_ctx* ctx, int32_t enable);
 mlora_status mlora_ctx_profile_read(mlora_ctx* ctx, int32_t kind, int64_t* count, double* total_ms,
                                     int32_t reset);
+/* A device interval on `stream`: timer_stop records the end event, waits for it
+ * and returns the milliseconds since timer_start (one interval per context). */
+mlora_status mlora_ctx_timer_start(mlora_ctx* ctx, void* stream);
+mlora_status mlora_ctx_timer_stop(mlora_ctx* ctx, void* stream, double* ms);
 
 /* ---------------------------------------------------------------- accounting
  * Replaces fusim::fused_shape (lora.hpp:63, lora.cpp:72-85).  Integer-exact.
@@ -121,6 +125,7 @@ mlora_status mlora_plan_create(mlora_ctx* ctx, int32_t num_jobs, const int64_t* 
 mlora_status mlora_plan_update(mlora_plan* plan, const int64_t* seg_offsets, void* stream);
 mlora_status mlora_plan_destroy(mlora_plan* plan);
 int64_t mlora_plan_rows(const mlora_plan* plan);
+int32_t mlora_plan_num_jobs(const mlora_plan* plan);
 int32_t mlora_plan_rank_padded(const mlora_plan* plan);
 /* host, J+1 entries */
 mlora_status mlora_plan_rank_offsets(const mlora_plan* plan, int32_t* roff_out);
@@ -373,6 +378,93 @@ mlora_status mlora_attn_bwd(const mlora_attn_desc* desc, const void* q, int64_t 
                             const void* v, int64_t ldv, const void* o, int64_t ldo, const void* dout, int64_t lddo,
                             const float* lse, float* dsum, void* dq, int64_t lddq, void* dk, int64_t lddk, void* dv,
                             int64_t lddv, void* stream);
+
+/* ---------------------------------------------------------------- one fused layer step (the trainer hook)
+ * The whole BatchFusion training iteration of one transformer layer's LoRA'd
+ * projections, as ONE call: the runtime counterpart of the reference
+ * simulator's fused iteration (/root/reference/proj/src/sim.cpp:163-191, whose
+ * duration the reference charges analytically at :177-179).  Per call, on
+ * `stream`, in this order (launch count independent of the number of jobs):
+ *   forward, in dependency waves: every projection whose input is ready gets
+ *     its rank-r down-projection in one grouped launch (projections sharing an
+ *     input go through the shared-input kernel), then its base GEMM
+ *     Y = X W0^T + H B_cat^T with the fused per-row sum of bf16(Y)^2;
+ *   loss[j] = 1/2 sum_p ||Y_p[rows of j]||^2 (so dL/dY_p = Y_p, input detached);
+ *   the non-finite guard (mlora_zero_nonfinite_rows over every tensor the
+ *     backward reads: each Y, H and input — a diverged job's rows, x included);
+ *   backward: G = s dY B_cat for every projection (one grouped launch), dX per
+ *     projection (reverse order), dA / dB for every projection (grouped);
+ *   and, in mlora_layer_step, one AdamW over all 2n adapter tensors (per-job lr,
+ *     step[j] = 0 leaves job j untouched, loss-gated: a job whose loss is not
+ *     finite keeps p, m, v).
+ * Every tensor is caller-owned device memory, described once at creation (the
+ * layer object holds only the descriptors); rows = mlora_plan_rows(plan), set
+ * by mlora_plan_update before the call, must not exceed `capacity`. */
+typedef struct mlora_layer_proj {
+    int32_t d;          /* output width (rows of W0) */
+    int32_t k;          /* input width (cols of W0) */
+    int32_t src;        /* -1: the layer input x (rows x k); p >= 0: projection p's Y (p != self, acyclic) */
+    int32_t src_col0;   /* first column of the source's Y that this input starts at */
+    const void* W0;     /* bf16 d x k, frozen */
+    float* A;           /* fp32 master A_cat, R_pad x k */
+    float* B;           /* fp32 master B_cat, d x R_pad */
+    float* mA;          /* AdamW moments, same shapes */
+    float* vA;
+    float* mB;
+    float* vB;
+    void* A_bf16;       /* bf16 operand copies (written by AdamW) */
+    void* B_bf16;
+    float* dA;          /* fp32 gradients */
+    float* dB;
+    void* Y;            /* bf16 capacity x d */
+    void* H;            /* bf16 capacity x R_pad (saved s X A^T) */
+    void* G;            /* bf16 capacity x R_pad (s dY B) */
+    void* dX;           /* bf16 capacity x k */
+    float* row_sq;      /* mlora_rowsq_blocks(d) * capacity floats */
+    void* in_scratch;   /* bf16 capacity x k; needed only when the input is a column slice of a
+                           wider source (src_col0 != 0 or the source's d != k), else NULL */
+} mlora_layer_proj;
+
+typedef struct mlora_adam_hparams {
+    float beta1, beta2, eps, weight_decay;
+} mlora_adam_hparams;
+
+typedef struct mlora_layer mlora_layer;
+/* USAGE on a bad source index / cycle / null tensor, SHAPE on widths that do
+ * not chain (k != the source's d without a scratch buffer); at most 16 projections. */
+mlora_status mlora_layer_create(mlora_ctx* ctx, mlora_plan* plan, int32_t n, const mlora_layer_proj* proj,
+                                int64_t capacity, mlora_layer** out);
+mlora_status mlora_layer_destroy(mlora_layer* layer);
+/* forward + loss + guard + backward (no optimizer); x: bf16 rows x proj[first x-fed].k; loss: device fp32 [J]. */
+mlora_status mlora_layer_forward_backward(mlora_layer* layer, void* x, float* loss, void* stream);
+/* forward_backward + AdamW (lr, step: host arrays of J entries; hp NULL: 0.9, 0.999, 1e-8, 0). */
+mlora_status mlora_layer_step(mlora_layer* layer, void* x, const float* lr, const int32_t* step,
+                              const mlora_adam_hparams* hp, float* loss, void* stream);
+/* mlora_layer_step bracketed by CUDA events on `stream`, then synchronised: returns the step's
+ * device milliseconds and copies the per-job losses to loss_host (J floats) — the measured
+ * duration an executor charges in place of the reference's analytic IterationTimeModel. */
+mlora_status mlora_layer_step_timed(mlora_layer* layer, void* x, const float* lr, const int32_t* step,
+                                    const mlora_adam_hparams* hp, float* loss, float* loss_host,
+                                    double* device_ms, void* stream);
+
+/* ---------------------------------------------------------------- device memory / init helpers
+ * For hosts that do not link the CUDA runtime themselves (the C++ façade, C
+ * programs): everything goes through this library's one runtime instance.
+ * kind: 0 host->device, 1 device->host, 2 device->device. */
+mlora_status mlora_malloc(mlora_ctx* ctx, size_t bytes, void** out);
+mlora_status mlora_free(mlora_ctx* ctx, void* ptr);
+mlora_status mlora_memcpy(mlora_ctx* ctx, void* dst, const void* src, size_t bytes, int32_t kind, void* stream);
+mlora_status mlora_memset(mlora_ctx* ctx, void* dst, int32_t value, size_t bytes, void* stream);
+mlora_status mlora_stream_sync(mlora_ctx* ctx, void* stream);
+/* Free / total device memory of the context's GPU (cudaMemGetInfo): the live
+ * warm-up probes of the memory model (memory_model.cpp:241-259 plans them). */
+mlora_status mlora_mem_info(mlora_ctx* ctx, size_t* free_bytes, size_t* total_bytes);
+/* Deterministic counter-based uniform fill: dst[i] = lo + (hi - lo) * u(seed, i),
+ * u in [0, 1) from a 64-bit mix of (seed, i) — the same values on any device,
+ * launch shape or host language (used to initialise synthetic weights and data
+ * identically from Python and C++).  dtype: 0 fp32, 1 bf16 (round to nearest). */
+mlora_status mlora_fill_uniform(void* dst, int64_t n, int32_t dtype, uint64_t seed, float lo, float hi,
+                                void* stream);
 
 /* ---------------------------------------------------------------- multi-GPU
  * Adapter-parallel: jobs are partitioned across GPUs (one process and one

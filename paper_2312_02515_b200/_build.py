@@ -20,9 +20,11 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 LIB_MLORA = os.path.join(PKG, "libmlora.so")
 LIB_FACADE = os.path.join(PKG, "libfusim_b200.so")
 
-MLORA_SOURCES = ["mlora_capi.cu", "mlora_f64.cu", "mlora_model.cu", "mlora_decoder.cu", "mlora_comm.cpp"]
+MLORA_SOURCES = ["mlora_capi.cu", "mlora_f64.cu", "mlora_model.cu", "mlora_decoder.cu", "mlora_layer.cu", "mlora_comm.cpp"]
 MLORA_HEADERS = ["sm100.cuh", "mlora_gemm.cuh", "mlora_aux.cuh", "mlora_quad.cuh", "mlora_down_multi.cuh"]
-FACADE_SOURCES = ["facade_lora.cpp", "facade_batch_select.cpp", "facade_workload.cpp", "facade_capi.cpp"]
+FACADE_SOURCES = ["facade_lora.cpp", "facade_batch_select.cpp", "facade_workload.cpp", "facade_capi.cpp",
+                  "facade_memory_model.cpp",
+                  "facade_b200.cpp"]
 
 
 def _newer(target: str, deps: list[str]) -> bool:
@@ -37,14 +39,32 @@ def _run(cmd: list[str]) -> None:
     subprocess.run(cmd, check=True)
 
 
+OBJ_DIR = os.path.join(PKG, "build")
+NVCC_FLAGS = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3"]
+
+
+def _compile_one(src: str, deps: list[str], force: bool) -> str:
+    """One translation unit -> build/<name>.o, skipped when newer than its deps."""
+    obj = os.path.join(OBJ_DIR, os.path.basename(src) + ".o")
+    if force or not _newer(obj, [src, *deps]):
+        _run([NVCC, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj])
+    return obj
+
+
 def build_mlora(force: bool = False) -> str:
+    """libmlora.so: every .cu / .cpp compiled in parallel (one nvcc per TU, each
+    object cached by mtime), then one link.  The CUDA runtime is linked
+    statically here and ONLY here: the façade goes through this library's
+    mlora_malloc / mlora_memcpy, so a process holds one runtime instance."""
+    from concurrent.futures import ThreadPoolExecutor
+    os.makedirs(OBJ_DIR, exist_ok=True)
     srcs = [os.path.join(CSRC, s) for s in MLORA_SOURCES if os.path.exists(os.path.join(CSRC, s))]
-    deps = srcs + [os.path.join(CSRC, h) for h in MLORA_HEADERS] + [os.path.join(ROOT, "include", "mlora.h")]
-    if not force and _newer(LIB_MLORA, deps):
+    hdrs = [os.path.join(CSRC, h) for h in MLORA_HEADERS] + [os.path.join(ROOT, "include", "mlora.h")]
+    with ThreadPoolExecutor(len(srcs)) as ex:
+        objs = list(ex.map(lambda s: _compile_one(s, hdrs, force), srcs))
+    if not force and _newer(LIB_MLORA, objs):
         return LIB_MLORA
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-shared",
-           "-cudart", "static", "-I", os.path.join(ROOT, "include"), "-o", LIB_MLORA, *srcs, "-ldl"]
-    _run(cmd)
+    _run([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", LIB_MLORA, *objs, "-ldl"])
     return LIB_MLORA
 
 
@@ -57,10 +77,9 @@ def build_facade(force: bool = False) -> str | None:
     deps = srcs + [LIB_MLORA] + ([os.path.join(fdir, h) for h in os.listdir(fdir)] if os.path.isdir(fdir) else [])
     if not force and _newer(LIB_FACADE, deps):
         return LIB_FACADE
-    cuda = os.path.dirname(os.path.dirname(NVCC))
-    cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-I", inc, "-I", os.path.join(cuda, "include"),
-           "-o", LIB_FACADE, *srcs, "-L", PKG, "-lmlora", "-Wl,-rpath,$ORIGIN",
-           "-L", os.path.join(cuda, "lib64"), "-lcudart_static", "-ldl", "-lrt", "-lpthread"]
+    # no CUDA runtime here: device memory, copies and syncs go through libmlora.so
+    cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-I", inc, "-o", LIB_FACADE, *srcs, "-L", PKG,
+           "-lmlora", "-Wl,-rpath,$ORIGIN", "-lpthread"]
     _run(cmd)
     return LIB_FACADE
 

@@ -39,6 +39,17 @@ class AdamGroupC(C.Structure):
                 ("cols", i64), ("layout", i32), ("_pad", i32)]
 
 
+class LayerProjC(C.Structure):
+    """mlora_layer_proj (include/mlora.h)."""
+    _fields_ = [("d", i32), ("k", i32), ("src", i32), ("src_col0", i32), ("W0", vp), ("A", vp), ("B", vp),
+                ("mA", vp), ("vA", vp), ("mB", vp), ("vB", vp), ("A_bf16", vp), ("B_bf16", vp), ("dA", vp),
+                ("dB", vp), ("Y", vp), ("H", vp), ("G", vp), ("dX", vp), ("row_sq", vp), ("in_scratch", vp)]
+
+
+class AdamHparamsC(C.Structure):
+    _fields_ = [("beta1", f32), ("beta2", f32), ("eps", f32), ("weight_decay", f32)]
+
+
 _SIGS = {
     "mlora_abi_version": (i32, []),
     "mlora_status_string": (C.c_char_p, [i32]),
@@ -57,6 +68,7 @@ _SIGS = {
     "mlora_plan_update": (i32, [vp, C.POINTER(i64), vp]),
     "mlora_plan_rows": (i64, [vp]),
     "mlora_plan_rank_padded": (i32, [vp]),
+    "mlora_plan_num_jobs": (i32, [vp]),
     "mlora_plan_rank_offsets": (i32, [vp, C.POINTER(i32)]),
     "mlora_linear_fwd": (i32, [vp, vp, i32, i32, vp, vp, vp, vp, vp, vp, vp]),
     "mlora_linear_fwd_ex": (i32, [vp, vp, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp]),
@@ -77,6 +89,22 @@ _SIGS = {
                               f32, f32, vp]),
     "mlora_adam_step_ex": (i32, [vp, vp, C.POINTER(AdamGroupC), i32, C.POINTER(f32), C.POINTER(i32), f32, f32,
                                  f32, f32, vp, vp]),
+    # one fused layer step (the trainer hook) and the memory / init helpers
+    "mlora_layer_create": (i32, [vp, vp, i32, C.POINTER(LayerProjC), i64, C.POINTER(vp)]),
+    "mlora_layer_destroy": (i32, [vp]),
+    "mlora_layer_forward_backward": (i32, [vp, vp, vp, vp]),
+    "mlora_layer_step": (i32, [vp, vp, C.POINTER(f32), C.POINTER(i32), C.POINTER(AdamHparamsC), vp, vp]),
+    "mlora_layer_step_timed": (i32, [vp, vp, C.POINTER(f32), C.POINTER(i32), C.POINTER(AdamHparamsC), vp, vp,
+                                     C.POINTER(C.c_double), vp]),
+    "mlora_malloc": (i32, [vp, C.c_size_t, C.POINTER(vp)]),
+    "mlora_free": (i32, [vp, vp]),
+    "mlora_memcpy": (i32, [vp, vp, vp, C.c_size_t, i32, vp]),
+    "mlora_memset": (i32, [vp, vp, i32, C.c_size_t, vp]),
+    "mlora_stream_sync": (i32, [vp, vp]),
+    "mlora_mem_info": (i32, [vp, C.POINTER(C.c_size_t), C.POINTER(C.c_size_t)]),
+    "mlora_fill_uniform": (i32, [vp, i64, i32, C.c_uint64, f32, f32, vp]),
+    "mlora_ctx_timer_start": (i32, [vp, vp]),
+    "mlora_ctx_timer_stop": (i32, [vp, vp, C.POINTER(C.c_double)]),
 }
 
 # Optional groups (present once the corresponding kernels are built).

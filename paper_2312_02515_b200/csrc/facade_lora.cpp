@@ -6,20 +6,15 @@
 // mlora_f64_add) with the reference's per-element operation order.
 #include "fusim/lora.hpp"
 
-#include <cuda_runtime.h>
-
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <mutex>
 
 #include "mlora.h"
 
 namespace fusim {
 namespace {
-
-[[noreturn]] void device_fail(const char* what, cudaError_t e) {
-    throw DeviceError(std::string(what) + ": " + cudaGetErrorString(e));
-}
 
 void check_status(mlora_status st, const char* what) {
     switch (st) {
@@ -33,30 +28,49 @@ void check_status(mlora_status st, const char* what) {
     }
 }
 
+}  // namespace
+
+namespace detail {
+// The façade's device context (GPU 0, created on first use).  The façade links
+// no CUDA runtime of its own: every allocation, copy and sync goes through
+// libmlora.so (mlora_malloc / mlora_memcpy / mlora_stream_sync), so a process
+// using both holds ONE runtime instance and one error state.
+mlora_ctx* facade_ctx() {
+    static std::once_flag once;
+    static mlora_ctx* ctx = nullptr;
+    static mlora_status st = MLORA_OK;
+    std::call_once(once, [] { st = mlora_ctx_create(0, &ctx); });
+    if (st != MLORA_OK || !ctx) throw DeviceError(std::string("mlora_ctx_create: ") + mlora_last_error(nullptr));
+    return ctx;
+}
+}  // namespace detail
+
+namespace {
+
 // A device fp64 buffer (RAII); the façade's only allocation is per call.
 class DevBuf {
 public:
     explicit DevBuf(std::size_t n) : n_(n) {
         if (n_ == 0) return;
-        cudaError_t e = cudaMalloc(&p_, n_ * sizeof(double));
-        if (e != cudaSuccess) device_fail("cudaMalloc", e);
+        if (mlora_malloc(detail::facade_ctx(), n_ * sizeof(double), &p_) != MLORA_OK)
+            throw DeviceError(std::string("mlora_malloc: ") + mlora_last_error(detail::facade_ctx()));
     }
     DevBuf(const double* host, std::size_t n) : DevBuf(n) { upload(host, n, 0); }
     ~DevBuf() {
-        if (p_) cudaFree(p_);
+        if (p_) mlora_free(detail::facade_ctx(), p_);
     }
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
     double* get() const { return static_cast<double*>(p_); }
     void upload(const double* host, std::size_t n, std::size_t off) {
         if (n == 0) return;
-        cudaError_t e = cudaMemcpy(get() + off, host, n * sizeof(double), cudaMemcpyHostToDevice);
-        if (e != cudaSuccess) device_fail("cudaMemcpy H2D", e);
+        if (mlora_memcpy(detail::facade_ctx(), get() + off, host, n * sizeof(double), 0, nullptr) != MLORA_OK)
+            throw DeviceError(std::string("H2D copy: ") + mlora_last_error(detail::facade_ctx()));
     }
     void download(double* host, std::size_t n, std::size_t off) const {
         if (n == 0) return;
-        cudaError_t e = cudaMemcpy(host, get() + off, n * sizeof(double), cudaMemcpyDeviceToHost);
-        if (e != cudaSuccess) device_fail("cudaMemcpy D2H", e);
+        if (mlora_memcpy(detail::facade_ctx(), host, get() + off, n * sizeof(double), 1, nullptr) != MLORA_OK)
+            throw DeviceError(std::string("D2H copy: ") + mlora_last_error(detail::facade_ctx()));
     }
 
 private:
@@ -72,8 +86,8 @@ void gemm(long M, long N, long K, const double* A, long lda, bool tA, const doub
 }
 
 void sync() {
-    cudaError_t e = cudaDeviceSynchronize();
-    if (e != cudaSuccess) device_fail("device execution", e);
+    if (mlora_stream_sync(detail::facade_ctx(), nullptr) != MLORA_OK)
+        throw DeviceError(std::string("device execution: ") + mlora_last_error(detail::facade_ctx()));
 }
 
 }  // namespace

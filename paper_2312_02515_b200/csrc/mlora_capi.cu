@@ -60,6 +60,7 @@ struct mlora_ctx {
     std::vector<cudaEvent_t> event_pool;
     double prof_ms[8] = {0};
     long long prof_count[8] = {0};
+    cudaEvent_t timer[2] = {nullptr, nullptr};  // mlora_ctx_timer_start / _stop
 };
 
 struct mlora_plan {
@@ -744,6 +745,8 @@ mlora_status mlora_ctx_destroy(mlora_ctx* ctx) {
         cudaEventDestroy(std::get<2>(t));
     }
     for (auto e : ctx->event_pool) cudaEventDestroy(e);
+    for (auto e : ctx->timer)
+        if (e) cudaEventDestroy(e);
     delete ctx;
     return MLORA_OK;
 }
@@ -778,6 +781,29 @@ mlora_status mlora_ctx_profile_read(mlora_ctx* ctx, int32_t kind, int64_t* count
     return MLORA_OK;
 }
 int64_t mlora_ctx_launch_count(const mlora_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+mlora_status mlora_ctx_timer_start(mlora_ctx* ctx, void* stream) {
+    if (!ctx) return fail(nullptr, MLORA_USAGE, "null context");
+    DeviceGuard g(ctx->device);
+    if (!ctx->timer[0]) {
+        MLORA_CUDA_TRY(ctx, cudaEventCreate(&ctx->timer[0]));
+        MLORA_CUDA_TRY(ctx, cudaEventCreate(&ctx->timer[1]));
+    }
+    MLORA_CUDA_TRY(ctx, cudaEventRecord(ctx->timer[0], static_cast<cudaStream_t>(stream)));
+    return MLORA_OK;
+}
+
+mlora_status mlora_ctx_timer_stop(mlora_ctx* ctx, void* stream, double* ms) {
+    if (!ctx || !ms) return fail(ctx, MLORA_USAGE, "null argument");
+    if (!ctx->timer[0]) return fail(ctx, MLORA_STATE, "timer not started");
+    DeviceGuard g(ctx->device);
+    MLORA_CUDA_TRY(ctx, cudaEventRecord(ctx->timer[1], static_cast<cudaStream_t>(stream)));
+    MLORA_CUDA_TRY(ctx, cudaEventSynchronize(ctx->timer[1]));
+    float f = 0.f;
+    MLORA_CUDA_TRY(ctx, cudaEventElapsedTime(&f, ctx->timer[0], ctx->timer[1]));
+    *ms = f;
+    return MLORA_OK;
+}
 
 // lora.cpp:72-85: max_len over all lengths, sequences = count,
 // total = sequences * max_len, padding = total - Σ len.
@@ -1022,6 +1048,7 @@ mlora_status mlora_plan_destroy(mlora_plan* plan) {
 }
 
 int64_t mlora_plan_rows(const mlora_plan* plan) { return plan ? plan->rows : 0; }
+int32_t mlora_plan_num_jobs(const mlora_plan* plan) { return plan ? plan->J : 0; }
 int32_t mlora_plan_rank_padded(const mlora_plan* plan) { return plan ? plan->R_pad : 0; }
 mlora_status mlora_plan_rank_offsets(const mlora_plan* plan, int32_t* roff_out) {
     if (!plan || !roff_out) return fail(nullptr, MLORA_USAGE, "null argument");

@@ -16,8 +16,20 @@ and emits the reference's `iteration_done{ξ, ξ_p, jobs_in_batch}` event
 (sim.cpp:185-191) with the MEASURED device time and the per-job losses (what
 the reference's detect_stop consumes, progress.cpp:90-124).  Metrics follow
 compute_metrics (sim.cpp:258-265): δ = Σξ_p / Σξ, T_tot = Σξ / makespan,
-T_e = (1 − δ)·T_tot.  Admission under a memory budget (scheduler.cpp) is policy
-outside the hot path and is not reproduced here.
+T_e = (1 − δ)·T_tot.
+
+Memory-budget admission (`memory_budget_gb`): each live job's footprint is
+estimated by the measured memory model (memory.MemoryModel — live cudaMemGetInfo
+probes of the real step fitted to PAPER Eq. 6; predict_memory_clamped at the
+job's batch size and longest item, as estimate_job_memory, scheduler.cpp:36-42)
+or, without a model, by JobConfig.memory_gb.  Admission then follows the
+reference's schedule() (scheduler.cpp:74-130): fifo / priority order the live
+jobs by arrival / urgency and admit greedily (greedy_admit :61-72: up to
+max_concurrent, running estimate within the budget); minpad keeps the jobs that
+fit alone, runs select_minpad and admits its choice greedily.  admission="pack"
+first reduces the ordered list to its max_packing subset (the M4 pack_admission
+path, :153-164).  An iteration whose admission is empty ends the run with
+`Trace.truncated = "budget_exhausted"` (sim.cpp:140-147).
 
 Early stopping (`early_stopping=True`) applies the reference's rule,
 detect_stop (progress.cpp:90-124, restated below), to the REAL per-job losses
@@ -104,6 +116,7 @@ class JobConfig:
     submit_time: float = 0.0
     iterations: int = 10           # true_iterations
     tokens: list | None = None     # decoder backend: token ids of each dataset item (len == lengths[i])
+    memory_gb: float = 0.0         # static footprint used without a memory model (JobSpec::memory_gb)
 
 
 @dataclass
@@ -140,6 +153,7 @@ class Trace:
     stops: list = field(default_factory=list)       # job_stopped records (early stopping)
     checkpoints: list = field(default_factory=list)  # {job, path, iterations, cause} per saved adapter
     busy_time: float = 0.0
+    truncated: str | None = None                    # "budget_exhausted" when admission came back empty
 
     def metrics(self) -> dict:
         xi = sum(e["total_tokens"] for e in self.events)
@@ -158,7 +172,15 @@ class FusedExecutor:
     def __init__(self, ctx: F.Context, shapes, jobs: list[JobConfig], max_concurrent: int,
                  strategy: str = "minpad", padded: bool = False, seed: int = 0, W0: dict | None = None,
                  pipelined: bool = True, early_stopping: bool = False, patience: int = 3,
-                 accuracy_fn=None, checkpoint_dir: str | None = None, model=None):
+                 accuracy_fn=None, checkpoint_dir: str | None = None, model=None,
+                 memory_budget_gb: float | None = None, memory_model=None, memory_floor_gb: float = 0.1,
+                 admission: str = "greedy"):
+        if admission not in ("greedy", "pack"):
+            raise ValueError("admission must be 'greedy' or 'pack'")
+        self.memory_budget_gb = memory_budget_gb
+        self.memory_model = memory_model
+        self.memory_floor_gb = memory_floor_gb
+        self.admission = admission
         self.ctx = ctx
         self.checkpoint_dir = checkpoint_dir  # a job's adapter is saved when it completes or stops
         self.early_stopping = early_stopping
@@ -178,9 +200,11 @@ class FusedExecutor:
             self.layer = FusedLoraLayer(ctx, shapes, [j.rank for j in jobs], [j.scale for j in jobs],
                                         [j.lr for j in jobs], rows=capacity, seed=seed, W0=W0)
             self.k_in = shapes[0][2]
-            gen = torch.Generator(device=ctx.device).manual_seed(seed + 1)
-            self.data = [[(torch.rand(n, self.k_in, generator=gen, device=ctx.device) * 2 - 1).to(torch.bfloat16)
-                          for n in j.lengths] for j in jobs]  # each job's dataset, resident in HBM
+            # each job's dataset, resident in HBM: item `it` of job i is the counter-based
+            # fill with seed mix_seed(seed, 3, i, it) (the C++ executor builds the same bytes)
+            self.data = [[F.fill_uniform(torch.empty(n, self.k_in, dtype=torch.bfloat16, device=ctx.device),
+                                         F.mix_seed(seed, 3, i, it), -1.0, 1.0)
+                          for it, n in enumerate(j.lengths)] for i, j in enumerate(jobs)]
             self._x = torch.empty(capacity, self.k_in, dtype=torch.bfloat16, device=ctx.device)
             self._mask = torch.empty(capacity, dtype=torch.uint8, device=ctx.device)
         else:
@@ -206,6 +230,24 @@ class FusedExecutor:
 
     def active(self) -> list[int]:
         return [i for i, js in enumerate(self.jobs) if not js.finished]
+
+    def job_memory_gb(self, i: int) -> float:
+        """estimate_job_memory (scheduler.cpp:36-42): the fitted model at the job's
+        batch size and longest item, clamped to the floor; else its static size."""
+        cfg = self.jobs[i].cfg
+        if self.memory_model is not None:
+            return self.memory_model.predict_clamped(cfg.batch_size, max(cfg.lengths), self.memory_floor_gb)
+        return float(cfg.memory_gb)
+
+    def _admit(self, live: list[int]) -> tuple[list[int], dict]:
+        """schedule() (scheduler.cpp:74-130) under the memory budget -> admitted job
+        indices in admission order, and their estimates (memory.admit)."""
+        from . import memory as MM
+        est = {i: self.job_memory_gb(i) for i in live}
+        queue = [MM.QueuedJob(self.jobs[i].cfg.id, self.jobs[i].cfg.priority, self.jobs[i].cfg.submit_time,
+                              self.jobs[i].peek(), est[i]) for i in live]
+        picked = MM.admit(queue, self.strategy, float(self.memory_budget_gb), self.M, self.admission)
+        return [live[q] for q in picked], est
 
     def _collect(self) -> dict | None:
         """Finish the pending step: wait for its end event, read its device time and
@@ -256,12 +298,21 @@ class FusedExecutor:
         returns the PREVIOUS iteration's event, so the host packing of step t+1
         overlaps the device executing step t; `flush()` collects the last one."""
         live = self.active()
-        if not live:
+        if not live or self.trace.truncated:
             return self._collect()
-        cands = [P.Candidate(i, self.jobs[i].peek(), self.jobs[i].cfg.priority, self.jobs[i].cfg.submit_time)
-                 for i in live]
-        sel = P.select(cands, self.M, self.strategy)
-        chosen = [cands[c].job for c in sel.chosen]          # job indices, urgency (routing) order
+        mem_meta = {}
+        if self.memory_budget_gb is None:
+            cands = [P.Candidate(i, self.jobs[i].peek(), self.jobs[i].cfg.priority, self.jobs[i].cfg.submit_time,
+                                 id=self.jobs[i].cfg.id) for i in live]
+            sel = P.select(cands, self.M, self.strategy)
+            chosen = [cands[c].job for c in sel.chosen]      # job indices, urgency (routing) order
+        else:
+            chosen, est = self._admit(live)                  # admission order
+            if not chosen:
+                self.trace.truncated = "budget_exhausted"
+                return self._collect()
+            mem_meta = {"estimated_memory_gb": sum(est[i] for i in chosen),
+                        "per_job_memory_gb": {self.jobs[i].cfg.id: est[i] for i in chosen}}
         batches = {i: self.jobs[i].peek() for i in chosen}
         in_batch = sorted(chosen)                            # row order: job-index order
         lay = P.layout([batches[i] for i in in_batch], padded=self.padded)
@@ -305,7 +356,8 @@ class FusedExecutor:
         self._pending = {"e0": e0, "e1": e1, "loss": slot, "chosen": chosen,
                          "meta": {"total_tokens": lay.total_tokens, "padding_tokens": lay.padding_tokens,
                                   "effective_tokens": lay.effective_tokens, "rows": lay.rows,
-                                  "jobs_in_batch": len(chosen), "routing": [self.jobs[i].cfg.id for i in chosen]}}
+                                  "jobs_in_batch": len(chosen), "routing": [self.jobs[i].cfg.id for i in chosen],
+                                  **mem_meta}}
         if not self.pipelined:
             return self._collect()
         return prev
@@ -315,7 +367,7 @@ class FusedExecutor:
 
     def run(self, max_iterations: int | None = None) -> Trace:
         n = 0
-        while (max_iterations is None or n < max_iterations) and self.active():
+        while (max_iterations is None or n < max_iterations) and self.active() and not self.trace.truncated:
             self.step()
             n += 1
         self.flush()

@@ -203,18 +203,26 @@ def linear_bwd(ctx: Context, plan: Plan, dY: torch.Tensor, X: torch.Tensor, H: t
     return (dX if need_dX else None), dA_cat, dB_cat
 
 
-def pack_adapters(ctx: Context, plan: Plan, d: int, k: int, As, Bs, stream=None):
+def pack_adapters(ctx: Context, plan: Plan, d: int, k: int, As, Bs, stream=None, out=None):
     """Per-job fp32 device adapters (A_j r_j x k, B_j d x r_j) -> cat layout.
-    Returns (A_cat_f32, B_cat_f32, A_cat_bf16, B_cat_bf16)."""
+    Returns (A_cat_f32, B_cat_f32, A_cat_bf16, B_cat_bf16), written into `out`
+    (the same 4-tuple of tensors) when given."""
     J = plan.num_jobs
     if len(As) != J or len(Bs) != J:
         raise errors.RoutingError("need one adapter per job")
     R = plan.rank_padded
     dev = ctx.device
-    A32 = torch.empty((R, k), dtype=torch.float32, device=dev)
-    B32 = torch.empty((d, R), dtype=torch.float32, device=dev)
-    A16 = torch.empty((R, k), dtype=torch.bfloat16, device=dev)
-    B16 = torch.empty((d, R), dtype=torch.bfloat16, device=dev)
+    if out is not None:
+        A32, B32, A16, B16 = out
+        for t, name, dt, shp in ((A32, "A_cat_f32", torch.float32, (R, k)), (B32, "B_cat_f32", torch.float32, (d, R)),
+                                 (A16, "A_cat_bf16", torch.bfloat16, (R, k)),
+                                 (B16, "B_cat_bf16", torch.bfloat16, (d, R))):
+            _require_cuda(t, name, dt, shp)
+    else:
+        A32 = torch.empty((R, k), dtype=torch.float32, device=dev)
+        B32 = torch.empty((d, R), dtype=torch.float32, device=dev)
+        A16 = torch.empty((R, k), dtype=torch.bfloat16, device=dev)
+        B16 = torch.empty((d, R), dtype=torch.bfloat16, device=dev)
     for j in range(J):
         _require_cuda(As[j], f"A[{j}]", torch.float32, (plan.ranks[j], k))
         _require_cuda(Bs[j], f"B[{j}]", torch.float32, (d, plan.ranks[j]))
@@ -280,3 +288,27 @@ def fuse_rows(ctx: Context, seqs, padded: bool = False, out: torch.Tensor | None
                                     1 if padded else 0, out.data_ptr(), mask.data_ptr(), offs,
                                     _stream_handle(stream)), ctx.handle)
     return out, mask, list(offs)
+
+
+_MASK64 = (1 << 64) - 1
+
+
+def mix_seed(*parts: int) -> int:
+    """64-bit FNV-1a over the parts: the per-tensor seed of the synthetic
+    weights / data (the C++ façade's fusim::b200::mix_seed is the same), so a
+    Python and a C++ host initialise bit-identical tensors."""
+    h = 0xCBF29CE484222325
+    for v in parts:
+        h = ((h ^ (int(v) & _MASK64)) * 0x100000001B3) & _MASK64
+    return h
+
+
+def fill_uniform(t: torch.Tensor, seed: int, lo: float = -1.0, hi: float = 1.0, stream=None) -> torch.Tensor:
+    """In place: t[i] = lo + (hi - lo) * u(seed, i) on the device (mlora_fill_uniform:
+    counter-based, independent of launch shape and host language).  fp32 or bf16."""
+    if not t.is_cuda or not t.is_contiguous() or t.dtype not in (torch.float32, torch.bfloat16):
+        raise errors.UsageError("fill_uniform needs a contiguous fp32 / bf16 CUDA tensor")
+    with torch.cuda.device(t.device):
+        N.check(N.lib().mlora_fill_uniform(t.data_ptr(), t.numel(), 0 if t.dtype == torch.float32 else 1,
+                                           int(seed) & _MASK64, float(lo), float(hi), _stream_handle(stream)))
+    return t

@@ -15,11 +15,13 @@ token per projection: 4dk + 6 r (d + k).
 """
 from __future__ import annotations
 
+import ctypes as C
 from dataclasses import dataclass
 
 import torch
 
 from . import _native as N
+from . import errors as E
 from . import fused as F
 
 # (name, d_out, k_in, input source)
@@ -130,6 +132,36 @@ class AdapterJobsMixin:
         self.step_count[job] = int(st["step"])
 
 
+class _Arena:
+    """Tensors carved from one device allocation (256-byte aligned views)."""
+    ALIGN = 256
+
+    def __init__(self, device, nbytes: int):
+        self.buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        self.off = 0
+
+    @staticmethod
+    def size(shape, itemsize: int) -> int:
+        n = itemsize
+        for s in shape:
+            n *= s
+        return (n + _Arena.ALIGN - 1) // _Arena.ALIGN * _Arena.ALIGN
+
+    def take(self, shape, dtype, zero: bool = False) -> torch.Tensor:
+        itemsize = torch.empty((), dtype=dtype).element_size()
+        n = self.size(shape, itemsize)
+        if self.off + n > self.buf.numel():
+            raise MemoryError("layer arena exhausted (size computation out of date)")
+        count = 1
+        for s in shape:
+            count *= s
+        t = self.buf[self.off:self.off + count * itemsize].view(dtype).view(*shape)
+        self.off += n
+        if zero:
+            t.zero_()
+        return t
+
+
 @dataclass
 class Projection:
     name: str
@@ -149,7 +181,14 @@ class Projection:
 
 
 class FusedLoraLayer(AdapterJobsMixin):
-    """All adapters of J jobs on one layer's projections, cat layout, on one GPU."""
+    """All adapters of J jobs on one layer's projections, cat layout, on one GPU.
+
+    The step itself is native: the tensors are described once to
+    mlora_layer_create (include/mlora.h) and every iteration is ONE C-ABI call,
+    mlora_layer_step (forward waves, loss, guard, backward, AdamW).  Synthetic
+    weights come from the device's counter-based fill (fused.fill_uniform with
+    fused.mix_seed per tensor), so the C++ façade's executor
+    (fusim::b200::FusedIterationExecutor) builds the bit-identical layer."""
 
     def __init__(self, ctx: F.Context, shapes, ranks, scales, lrs, rows: int, seed: int = 0,
                  W0: dict | None = None, lora_init: str = "random"):
@@ -165,31 +204,88 @@ class FusedLoraLayer(AdapterJobsMixin):
         # plan with a placeholder layout; set_layout() installs the real one
         self.plan = F.Plan(ctx, [0] * self.J + [rows], ranks, scales)
         R = self.plan.rank_padded
-        g = torch.Generator(device="cpu").manual_seed(seed)
+        names = [name for name, _, _, _ in shapes]
+        # every per-layer tensor (adapters, moments, gradients, activations, the
+        # loss) is carved from ONE device allocation: no allocator fragmentation,
+        # and the layer's footprint is exactly its bytes (what the memory model's
+        # cudaMemGetInfo probes measure, memory.py)
+        arena = _Arena(dev, self._arena_bytes(shapes, names, self.J, R, rows))
+        self._arena = arena
         self.proj: list[Projection] = []
-        for name, d, k, src in shapes:
+        for pi, (name, d, k, src) in enumerate(shapes):
             if W0 is not None and name in W0:
                 w = W0[name]
             else:
-                w = ((torch.rand(d, k, generator=g) * 2 - 1) / k ** 0.5).to(torch.bfloat16).to(dev)
+                w = F.fill_uniform(torch.empty(d, k, dtype=torch.bfloat16, device=dev), F.mix_seed(seed, 0, pi),
+                                   -k ** -0.5, k ** -0.5)
             As, Bs = [], []
-            for r in ranks:
-                As.append(((torch.rand(r, k, generator=g) * 2 - 1) / k ** 0.5).to(dev))
+            for j, r in enumerate(ranks):
+                As.append(F.fill_uniform(torch.empty(r, k, device=dev), F.mix_seed(seed, 1, pi, j), -k ** -0.5,
+                                         k ** -0.5))
                 if lora_init == "zero_b":   # standard LoRA init: B = 0
                     Bs.append(torch.zeros(d, r, device=dev))
                 else:
-                    Bs.append(((torch.rand(d, r, generator=g) * 2 - 1) / r ** 0.5).to(dev))
-            A32, B32, A16, B16 = F.pack_adapters(ctx, self.plan, d, k, As, Bs)
+                    Bs.append(F.fill_uniform(torch.empty(d, r, device=dev), F.mix_seed(seed, 2, pi, j), -r ** -0.5,
+                                             r ** -0.5))
+            f32, b16 = torch.float32, torch.bfloat16
+            A32, B32, A16, B16 = F.pack_adapters(ctx, self.plan, d, k, As, Bs,
+                                                 out=(arena.take((R, k), f32), arena.take((d, R), f32),
+                                                      arena.take((R, k), b16), arena.take((d, R), b16)))
+            del As, Bs
+            sA = F.AdamState(A32, arena.take((R, k), f32, zero=True), arena.take((R, k), f32, zero=True), A16, 0)
+            sB = F.AdamState(B32, arena.take((d, R), f32, zero=True), arena.take((d, R), f32, zero=True), B16, 1)
             self.proj.append(Projection(
-                name, d, k, src, w, F.AdamState.of(A32, A16, 0), F.AdamState.of(B32, B16, 1),
-                torch.zeros(R, k, device=dev), torch.zeros(d, R, device=dev),
-                torch.empty(rows, d, dtype=torch.bfloat16, device=dev),
-                torch.empty(rows, R, dtype=torch.bfloat16, device=dev),
-                torch.empty(rows, R, dtype=torch.bfloat16, device=dev),
-                torch.empty(rows, k, dtype=torch.bfloat16, device=dev),
-                torch.empty(N.lib().mlora_rowsq_blocks(d), rows, dtype=torch.float32, device=dev)))
-        self.loss = torch.zeros(self.J, dtype=torch.float32, device=dev)
-        self._rowsq_d = (N.i32 * len(self.proj))(*[p.d for p in self.proj])
+                name, d, k, src, w, sA, sB, arena.take((R, k), f32, zero=True), arena.take((d, R), f32, zero=True),
+                arena.take((rows, d), b16), arena.take((rows, R), b16), arena.take((rows, R), b16),
+                arena.take((rows, k), b16), arena.take((N.lib().mlora_rowsq_blocks(d), rows), f32)))
+        self.loss = arena.take((self.J,), torch.float32, zero=True)
+        # ---- the native layer: one descriptor per projection (pointers into the tensors above)
+        self._scratch = {}
+        desc = (N.LayerProjC * len(self.proj))()
+        for i, p in enumerate(self.proj):
+            if p.src == "x":
+                src, col0 = -1, 0
+            else:
+                base = "h_to_4h" if p.src == "h_to_4h_half" else p.src
+                src, col0 = names.index(base), 0
+            scratch = None
+            if src >= 0 and self.proj[src].d != p.k:  # column slice of a wider source (ChatGLM2 4h_to_h)
+                scratch = self._scratch[p.name] = arena.take((rows, p.k), torch.bfloat16)
+            desc[i] = N.LayerProjC(p.d, p.k, src, col0, p.W0.data_ptr(), p.A.p.data_ptr(), p.B.p.data_ptr(),
+                                   p.A.m.data_ptr(), p.A.v.data_ptr(), p.B.m.data_ptr(), p.B.v.data_ptr(),
+                                   p.A.p_bf16.data_ptr(), p.B.p_bf16.data_ptr(), p.dA.data_ptr(), p.dB.data_ptr(),
+                                   p.Y.data_ptr(), p.H.data_ptr(), p.G.data_ptr(), p.dX.data_ptr(),
+                                   p.row_sq.data_ptr(), None if scratch is None else scratch.data_ptr())
+        h = N.vp()
+        N.check(N.lib().mlora_layer_create(ctx.handle, self.plan.handle, len(self.proj), desc, rows, C.byref(h)),
+                ctx.handle)
+        self._layer = h
+        self._hp = N.AdamHparamsC(0.9, 0.999, 1e-8, 0.0)
+
+    @staticmethod
+    def _arena_bytes(shapes, names, J: int, R: int, rows: int) -> int:
+        total = _Arena.size((J,), 4)  # the per-job loss
+        for name, d, k, src in shapes:
+            total += 4 * _Arena.size((R, k), 4) + _Arena.size((R, k), 2)      # A_cat: p, m, v, grad; bf16 copy
+            total += 4 * _Arena.size((d, R), 4) + _Arena.size((d, R), 2)      # B_cat: the same
+            total += _Arena.size((rows, d), 2) + 2 * _Arena.size((rows, R), 2) + _Arena.size((rows, k), 2)
+            total += _Arena.size((N.lib().mlora_rowsq_blocks(d), rows), 4)
+            if src != "x":
+                base = "h_to_4h" if src == "h_to_4h_half" else src
+                if shapes[names.index(base)][1] != k:
+                    total += _Arena.size((rows, k), 2)
+        return total
+
+    def close(self) -> None:
+        if getattr(self, "_layer", None):
+            N.lib().mlora_layer_destroy(self._layer)
+            self._layer = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
     def set_layout(self, seg_offsets) -> None:
         """Install the segment layout of the next fused batch: job j owns rows
@@ -203,117 +299,60 @@ class FusedLoraLayer(AdapterJobsMixin):
     def named_projections(self):
         return [(p.name, p) for p in self.proj]
 
-    def _views(self, p: Projection, rows: int):
-        nblk = p.row_sq.shape[0]
-        return (p.Y[:rows], p.H[:rows], p.G[:rows], p.dX[:rows],
-                p.row_sq.view(-1)[: nblk * rows].view(nblk, rows))
+    def input_of(self, p: Projection, x: torch.Tensor) -> torch.Tensor:
+        """The tensor projection p read in the last step (x, or its source's Y / slice)."""
+        rows = getattr(self, "cur_rows", self.rows)
+        if p.src == "x":
+            return x[:rows]
+        if p.name in self._scratch:
+            return self._scratch[p.name][:rows]
+        return next(q for q in self.proj if q.name == p.src).Y[:rows]
 
-    def _input(self, src: str, x: torch.Tensor, rows: int) -> torch.Tensor:
-        if src == "x":
-            return x
-        if src == "h_to_4h_half":
-            p = next(q for q in self.proj if q.name == "h_to_4h")
-            # first half of the fused gate/up output (stand-in for the gated act.)
-            return p.Y[:rows, : p.d // 2].contiguous()
-        return next(q for q in self.proj if q.name == src).Y[:rows]
+    def _check_x(self, x: torch.Tensor) -> None:
+        rows = getattr(self, "cur_rows", self.rows)
+        k0 = next((p.k for p in self.proj if p.src == "x"), None)
+        if not (x.is_cuda and x.dtype == torch.bfloat16 and x.is_contiguous() and x.dim() == 2
+                and x.shape[0] >= rows and x.shape[1] == k0):
+            raise E.ShapeError(f"x must be a contiguous bf16 CUDA tensor of >= {rows} x {k0}")
 
     def forward_backward(self, x: torch.Tensor, stream=None) -> torch.Tensor:
-        """Grouped schedule: every HBM-bound op is issued once for all projections
-        whose inputs are ready (mlora_down_group / mlora_grad_group), the tensor-
-        bound base GEMMs once per projection.  LLaMA layer: 2 forward down-group
-        launches, 7 base GEMMs, loss, non-finite guard, 1 backward down-group, 7 dX GEMMs,
-        1 grad group."""
-        ctx, plan = self.ctx, self.plan
-        L, s = N.lib(), F._stream_handle(stream)
-        rows = getattr(self, "cur_rows", self.rows)
-        views = [self._views(p, rows) for p in self.proj]
-        inputs: dict[int, torch.Tensor] = {}
-        done: set[str] = set()
-        # ---- forward, in dependency waves
-        while len(done) < len(self.proj):
-            source = lambda src: None if src == "x" else ("h_to_4h" if src == "h_to_4h_half" else src)
-            wave = [i for i, p in enumerate(self.proj)
-                    if p.name not in done and (source(p.src) is None or source(p.src) in done)]
-            if not wave:
-                raise RuntimeError("projection inputs form a cycle")
-            for i in wave:
-                inputs[i] = self._input(self.proj[i].src, x, rows)
-            n = len(wave)
-            N.check(L.mlora_down_group(ctx.handle, plan.handle, n, 0,
-                                       (N.i32 * n)(*[self.proj[i].k for i in wave]),
-                                       (N.vp * n)(*[inputs[i].data_ptr() for i in wave]),
-                                       (N.vp * n)(*[self.proj[i].A.p_bf16.data_ptr() for i in wave]),
-                                       (N.vp * n)(*[views[i][1].data_ptr() for i in wave]), s), ctx.handle)
-            for i in wave:
-                p = self.proj[i]
-                Y, H, _, _, rsq = views[i]
-                N.check(L.mlora_base_fwd(ctx.handle, plan.handle, p.d, p.k, inputs[i].data_ptr(), p.W0.data_ptr(),
-                                         H.data_ptr(), p.B.p_bf16.data_ptr(), Y.data_ptr(), rsq.data_ptr(), s),
-                        ctx.handle)
-                done.add(p.name)
-        # ---- per-job loss from the row sums the forward GEMM epilogues produced (no re-read of Y)
-        n = len(self.proj)
-        ptrs = (N.vp * n)(*[v[4].data_ptr() for v in views])
-        N.check(L.mlora_loss_from_rowsq(ctx.handle, plan.handle, ptrs, self._rowsq_d, n, self.loss.data_ptr(), s),
-                ctx.handle)
-        # ---- a job whose loss is not finite contributes a zero gradient: its rows of
-        # every tensor the backward reads — dY (= Y here), the saved H and every
-        # projection input X — are zeroed.  No inf/NaN then meets the structural
-        # zeros of other jobs' columns (dB = dY^T H, dA = G^T X), and the job's own
-        # gradient is exactly 0, so its adapter stays finite and cannot leak into
-        # its neighbours' forward tiles either.  (The caller's x rows of that job
-        # are zeroed in place.)
-        guard = {}
-        for i, v in enumerate(views):
-            guard[v[0].data_ptr()] = self.proj[i].d
-            guard[v[1].data_ptr()] = self.plan.rank_padded
-            guard[inputs[i].data_ptr()] = inputs[i].shape[1]
-        ng = len(guard)
-        N.check(L.mlora_zero_nonfinite_rows(ctx.handle, plan.handle, self.loss.data_ptr(),
-                                            (N.vp * ng)(*guard.keys()), (N.i32 * ng)(*guard.values()), ng, s),
-                ctx.handle)
-        # ---- backward: dL/dY_p = Y_p for every projection
-        N.check(L.mlora_down_group(ctx.handle, plan.handle, n, 1, (N.i32 * n)(*[p.d for p in self.proj]),
-                                   (N.vp * n)(*[v[0].data_ptr() for v in views]),
-                                   (N.vp * n)(*[p.B.p_bf16.data_ptr() for p in self.proj]),
-                                   (N.vp * n)(*[v[2].data_ptr() for v in views]), s), ctx.handle)
-        for i in reversed(range(n)):
-            p = self.proj[i]
-            Y, _, G, dX, _ = views[i]
-            N.check(L.mlora_base_dx(ctx.handle, plan.handle, p.d, p.k, Y.data_ptr(), p.W0.data_ptr(), G.data_ptr(),
-                                    p.A.p_bf16.data_ptr(), dX.data_ptr(), s), ctx.handle)
-        N.check(L.mlora_grad_group(ctx.handle, plan.handle, n, (N.i32 * n)(*[p.d for p in self.proj]),
-                                   (N.i32 * n)(*[p.k for p in self.proj]),
-                                   (N.vp * n)(*[inputs[i].data_ptr() for i in range(n)]),
-                                   (N.vp * n)(*[v[0].data_ptr() for v in views]),
-                                   (N.vp * n)(*[v[1].data_ptr() for v in views]),
-                                   (N.vp * n)(*[v[2].data_ptr() for v in views]),
-                                   (N.vp * n)(*[p.dA.data_ptr() for p in self.proj]),
-                                   (N.vp * n)(*[p.dB.data_ptr() for p in self.proj]), s), ctx.handle)
+        """Forward (dependency waves: shared-input and grouped down-projections,
+        base GEMMs with fused row sums), per-job loss, non-finite guard, backward
+        (G group, dX GEMMs, grouped dA / dB): mlora_layer_forward_backward."""
+        self._check_x(x)
+        N.check(N.lib().mlora_layer_forward_backward(self._layer, x.data_ptr(), self.loss.data_ptr(),
+                                                     F._stream_handle(stream)), self.ctx.handle)
         return self.loss
+
+    def _steps(self, active):
+        active = [True] * self.J if active is None else list(active)
+        self.step_count = [s + (1 if a else 0) for s, a in zip(self.step_count, active)]
+        return [s if a else 0 for s, a in zip(self.step_count, active)]
 
     def optimizer_step(self, active=None, stream=None) -> None:
         """AdamW on every adapter; jobs not in `active` (bool per job) keep p, m, v
-        untouched this step (their rows were absent from the fused batch)."""
-        active = [True] * self.J if active is None else list(active)
-        self.step_count = [s + (1 if a else 0) for s, a in zip(self.step_count, active)]
-        steps = [s if a else 0 for s, a in zip(self.step_count, active)]
+        untouched this step (their rows were absent from the fused batch).
+        loss_gate: a job whose loss this step is not finite keeps p, m, v
+        untouched on the device (its gradient was zeroed by the guard, but
+        stale momentum must not move its adapter either)."""
+        steps = self._steps(active)
         states, grads = [], []
         for p in self.proj:
             states += [p.A, p.B]
             grads += [p.dA, p.dB]
-        # loss_gate: a job whose loss this step is not finite keeps p, m, v and its
-        # step count untouched on the device (its gradient was zeroed by the guard,
-        # but stale momentum must not move its adapter either)
         F.adam_step(self.ctx, self.plan, states, grads, self.lrs, steps, stream=stream, loss_gate=self.loss)
 
     def step(self, x: torch.Tensor, active=None, stream=None) -> torch.Tensor:
-        """One fused training iteration over the installed layout; returns the
-        per-job loss (device fp32 [J]).  Note: when a job's loss is not finite
-        the non-finite guard zeroes that job's rows of every tensor the backward
-        reads, including the caller's `x` (in place) — the rows are already
-        poisoned for this step and a zero row is what keeps the other jobs'
-        fused reductions exact."""
-        loss = self.forward_backward(x, stream)
-        self.optimizer_step(active, stream)
-        return loss
+        """One fused training iteration over the installed layout, ONE native call
+        (mlora_layer_step); returns the per-job loss (device fp32 [J]).  Note: when
+        a job's loss is not finite the non-finite guard zeroes that job's rows of
+        every tensor the backward reads, including the caller's `x` (in place) —
+        the rows are already poisoned for this step and a zero row is what keeps
+        the other jobs' fused reductions exact."""
+        self._check_x(x)
+        steps = self._steps(active)
+        lr_c = (N.f32 * self.J)(*[float(v) for v in self.lrs])
+        st_c = (N.i32 * self.J)(*steps)
+        N.check(N.lib().mlora_layer_step(self._layer, x.data_ptr(), lr_c, st_c, C.byref(self._hp),
+                                         self.loss.data_ptr(), F._stream_handle(stream)), self.ctx.handle)
+        return self.loss

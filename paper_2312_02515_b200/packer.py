@@ -38,6 +38,15 @@ def lib() -> C.CDLL:
         L.fusim_c_select.argtypes = [C.c_int32, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                      C.POINTER(C.c_int32), C.POINTER(C.c_double), C.c_int32,
                                      C.POINTER(C.c_int32), C.POINTER(C.c_int64)]
+        L.fusim_c_select_ids.argtypes = [C.c_int32, C.c_int32, C.POINTER(C.c_char_p), C.POINTER(C.c_int32),
+                                         C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_double),
+                                         C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int64)]
+        L.fusim_c_fit_memory_model.argtypes = [C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                               C.POINTER(C.c_double), C.c_int32, C.POINTER(C.c_double)]
+        L.fusim_c_max_packing.argtypes = [C.c_int32, C.POINTER(C.c_double), C.c_double, C.c_int32,
+                                          C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
+        L.fusim_c_warmup_plan.argtypes = [C.c_int32, C.POINTER(C.c_int32), C.c_int32, C.POINTER(C.c_int32),
+                                          C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
         L.fusim_c_sample_lengths.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_int32,
                                              C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.c_int32, C.c_uint64,
                                              C.POINTER(C.c_int32)]
@@ -49,7 +58,7 @@ def _chk(rc: int) -> None:
     if rc == 0:
         return
     msg = lib().fusim_c_last_error().decode()
-    raise {1: errors.UsageError, 7: errors.ConfigError}.get(rc, errors.Error)(msg)
+    raise {1: errors.UsageError, 7: errors.ConfigError, 8: errors.FitError}.get(rc, errors.Error)(msg)
 
 
 @dataclass
@@ -59,6 +68,7 @@ class Candidate:
     lengths: list
     priority: int = 1
     submit_time: float = 0.0
+    id: str | None = None             # the job id the reference's tie-breaks compare (default "c<index>")
 
 
 @dataclass
@@ -87,7 +97,11 @@ def select(candidates: list[Candidate], m: int, strategy: str = "minpad") -> Sel
     sub = (C.c_double * max(n, 1))(*[float(c.submit_time) for c in candidates])
     chosen = (C.c_int32 * max(n, 1))()
     meta = (C.c_int64 * 4)()
-    _chk(lib().fusim_c_select(STRATEGIES[strategy], n, counts, lengths, pri, sub, m, chosen, meta))
+    if all(c.id is not None for c in candidates) and n:
+        ids = (C.c_char_p * n)(*[str(c.id).encode() for c in candidates])
+        _chk(lib().fusim_c_select_ids(STRATEGIES[strategy], n, ids, counts, lengths, pri, sub, m, chosen, meta))
+    else:
+        _chk(lib().fusim_c_select(STRATEGIES[strategy], n, counts, lengths, pri, sub, m, chosen, meta))
     return Selection([int(chosen[i]) for i in range(meta[0])], int(meta[1]), int(meta[2]), int(meta[3]))
 
 

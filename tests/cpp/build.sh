@@ -11,7 +11,7 @@ PKG="$ROOT/paper_2312_02515_b200"
 OUT="$HERE/build"
 mkdir -p "$OUT"
 if [ -d "$REF" ]; then
-for t in test_lora test_batch_select test_workload; do
+for t in test_lora test_batch_select test_workload test_memory_model; do
   g++ -std=c++20 -O1 -I "$HERE" -I "$ROOT/include" -o "$OUT/$t" "$REF/$t.cpp" "$HERE/main.cpp" \
       -L "$PKG" -lfusim_b200 -lmlora -Wl,-rpath,"$PKG"
 done
@@ -20,5 +20,8 @@ else
 fi
 # façade-only driver (no reference sources needed)
 g++ -std=c++20 -O1 -I "$ROOT/include" -o "$OUT/facade_forward_io" "$HERE/facade_forward_io.cpp" \
+    -L "$PKG" -lfusim_b200 -lmlora -Wl,-rpath,"$PKG"
+# the B200 executor behind the fused iteration, driven by a simulator-shaped loop
+g++ -std=c++20 -O1 -I "$ROOT/include" -o "$OUT/executor_loop" "$HERE/executor_loop.cpp" \
     -L "$PKG" -lfusim_b200 -lmlora -Wl,-rpath,"$PKG"
 echo "built: $(ls "$OUT")"

@@ -3,12 +3,16 @@
 // compare them BIT FOR BIT with the reference's own outputs (tests/golden/).
 // Input per case (little-endian): int32 d, k, J, ranks[J], nseq, seq_job[nseq],
 // seq_len[nseq]; then float64 W0[d*k], A_all, B_all, X_all.  Output per case:
-// float64 out[S * max_len * d].
+// float64 out[S * max_len * d].  With --bf16 the cases run through
+// fusim::b200::fused_forward_bf16 (the tcgen05 path behind the same signature).
 #include <cstdint>
 #include <cstdio>
 #include <map>
 #include <vector>
 
+#include <cstring>
+
+#include "fusim/b200.hpp"
 #include "fusim/lora.hpp"
 
 using namespace fusim;
@@ -16,7 +20,8 @@ using namespace fusim;
 template <class T>
 static bool rd(T* p, size_t n) { return std::fread(p, sizeof(T), n, stdin) == n; }
 
-int main() {
+int main(int argc, char** argv) {
+    const bool bf16 = argc > 1 && std::strcmp(argv[1], "--bf16") == 0;
     int32_t ncases = 0;
     if (!rd(&ncases, 1)) return 2;
     for (int c = 0; c < ncases; ++c) {
@@ -47,7 +52,8 @@ int main() {
             rd(x.data.data(), x.data.size());
             batches.back().sequences.push_back(std::move(x));
         }
-        const auto outs = fused_forward(W0, adapters, fuse(batches));
+        const auto fb = fuse(batches);
+        const auto outs = bf16 ? b200::fused_forward_bf16(W0, adapters, fb) : fused_forward(W0, adapters, fb);
         for (const auto& o : outs) std::fwrite(o.data.data(), sizeof(double), o.data.size(), stdout);
     }
     return 0;

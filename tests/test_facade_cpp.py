@@ -77,3 +77,9 @@ def test_reference_lora_suite_on_facade_gpu():
     # forward on real tokens" (100 trials, < 1e-9) and the BITWISE padding-
     # neutrality check, with the arithmetic on the device
     assert "15 passed" in _run("test_lora")
+
+
+def test_reference_memory_model_suite_on_facade():
+    # the reference's own test_memory_model.cpp (fit, NNLS, clamping, packing,
+    # warm-up plan) against the product's memory model (facade_memory_model.cpp)
+    assert "16 passed" in _run("test_memory_model")

@@ -45,14 +45,16 @@ def test_executor_replays_reference_selection(padded):
         if not live:
             assert ex.step() is None
             break
-        cands = [O.BatchCandidate(f"c{n}", O.next_candidate_batch(jobs[i].lengths, cursors[i], jobs[i].batch_size),
-                                  jobs[i].priority, jobs[i].submit_time) for n, i in enumerate(live)]
+        # candidates carry the real job ids: the reference's tie-breaks compare them
+        cands = [O.BatchCandidate(jobs[i].id, O.next_candidate_batch(jobs[i].lengths, cursors[i], jobs[i].batch_size),
+                                  jobs[i].priority, jobs[i].submit_time) for i in live]
         want = O.select_minpad(cands, 3)
-        chosen = [live[int(c[1:])] for c in want.chosen]
+        pos = {jobs[i].id: n for n, i in enumerate(live)}
+        chosen = [live[pos[c]] for c in want.chosen]
         before = {j: (ex.layer.proj[0].A.p.clone(), ex.layer.proj[0].A.m.clone()) for j in range(len(jobs))}
         ev = ex.step()
         assert ev["routing"] == [jobs[i].id for i in chosen]
-        shape = O.fused_shape([c.item_lengths for c in (cands[int(c[1:])] for c in want.chosen)])
+        shape = O.fused_shape([cands[pos[c]].item_lengths for c in want.chosen])
         assert (ev["total_tokens"], ev["padding_tokens"]) == (shape.total_tokens, shape.padding_tokens)
         assert ev["effective_tokens"] == shape.total_tokens - shape.padding_tokens
         assert ev["rows"] == (shape.total_tokens if padded else ev["effective_tokens"])
