@@ -21,7 +21,7 @@ LIB_MLORA = os.path.join(PKG, "libmlora.so")
 LIB_FACADE = os.path.join(PKG, "libfusim_b200.so")
 
 MLORA_SOURCES = ["mlora_capi.cu", "mlora_f64.cu", "mlora_model.cu", "mlora_decoder.cu", "mlora_layer.cu", "mlora_comm.cpp"]
-MLORA_HEADERS = ["sm100.cuh", "mlora_gemm.cuh", "mlora_aux.cuh", "mlora_quad.cuh", "mlora_down_multi.cuh"]
+MLORA_HEADERS = ["sm100.cuh", "mlora_gemm.cuh", "mlora_aux.cuh", "mlora_down_multi.cuh"]
 FACADE_SOURCES = ["facade_lora.cpp", "facade_batch_select.cpp", "facade_workload.cpp", "facade_capi.cpp",
                   "facade_memory_model.cpp",
                   "facade_b200.cpp"]

@@ -16,6 +16,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <set>
 #include <string>
 #include <tuple>
 #include <utility>
@@ -26,7 +27,6 @@
 
 #include "mlora_aux.cuh"
 #include "mlora_gemm.cuh"
-#include "mlora_quad.cuh"
 #include "mlora_down_multi.cuh"
 
 using namespace mlora;
@@ -75,8 +75,6 @@ struct mlora_plan {
     std::vector<int> ext;                 // [n_mblk][2]   (128-row m-blocks)
     std::vector<int> ext256;              // [n_mblk256][2] (256-row m-blocks of the CTA-pair kernel)
     int n_mblk256 = 0;
-    std::vector<int> ext512;              // [n_mblk512][2] (512-row m-blocks of the 4-CTA kernel)
-    int n_mblk512 = 0;
     std::vector<int> down;                // [n_down][3]
     int n_down = 0;
     std::vector<int> chunk_kb;            // [n_chunks][2] token k-block range
@@ -92,7 +90,6 @@ struct mlora_plan {
     float* d_scale = nullptr;
     int* d_ext = nullptr;
     int* d_ext256 = nullptr;
-    int* d_ext512 = nullptr;
     int* d_down = nullptr;
     int* d_grad = nullptr;
 };
@@ -168,14 +165,6 @@ mlora_status ensure_workspace(mlora_ctx* ctx, size_t bytes) {
     return MLORA_OK;
 }
 
-bool pdl_enabled() {
-    static const bool on = [] {
-        const char* e = std::getenv("MLORA_PDL");
-        return !(e && std::string(e) == "0");
-    }();
-    return on;
-}
-
 // Every kernel goes through cudaLaunchKernelEx with programmatic stream
 // serialisation (PDL): the next kernel's prologue overlaps this one's tail; the
 // kernels themselves griddepcontrol.wait before their first global access.
@@ -190,7 +179,7 @@ cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
     cudaLaunchAttribute attr[2];
     unsigned n = 0;
     attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[n].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
     ++n;
     if (cluster_x > 1) {
         attr[n].id = cudaLaunchAttributeClusterDimension;
@@ -244,6 +233,19 @@ struct ProfScope {
     }
 };
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize is per (kernel, device): opt in
+// once per pair, under a lock (contexts on several devices / threads share the
+// process's kernels).
+mlora_status ensure_smem_attr(mlora_ctx* ctx, const void* kern, int bytes) {
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> done;
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.count({kern, ctx->device})) return MLORA_OK;
+    MLORA_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    done.insert({kern, ctx->device});
+    return MLORA_OK;
+}
+
 constexpr int kGroupMax = 8;  // problems per grouped launch (a transformer layer has <= 7 LoRA'd projections)
 
 // Accumulates the problems of one (possibly grouped) launch.
@@ -271,74 +273,15 @@ mlora_status launch_gemm(mlora_ctx* ctx, const ProblemSet<NP>& set, int ctas_per
     if (set.ps.total_tiles <= 0) return MLORA_OK;
     using L = GemmSmem<BN, STAGES, KSPLIT>;
     auto kern = mlora_gemm_kernel<MODE, BN, STAGES, A_MN, B_MN, KSPLIT, NP>;
-    static bool attr_done = false;  // per instantiation
-    if (!attr_done) {
-        MLORA_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 L::kDynBytes));
-        attr_done = true;
-    }
+    mlora_status st = ensure_smem_attr(ctx, reinterpret_cast<const void*>(kern), L::kDynBytes);
+    if (st != MLORA_OK) return st;
     const int units = std::min(set.ps.total_tiles, ctx->num_sms * ctas_per_sm / KSPLIT);
-    ProfScope ps(ctx, MODE == MODE_BASE ? (B_MN ? 1 : 0) : MODE == MODE_DOWN ? 2 : 3, stream);
+    ProfScope ps(ctx, MODE == MODE_DOWN ? 2 : 3, stream);
     MLORA_CUDA_TRY(ctx, launch_k(kern, dim3(units * KSPLIT), dim3(kNumThreads), L::kDynBytes, stream, KSPLIT,
                                  set.ps));
     ++ctx->launches;
     return MLORA_OK;
 }
-
-// MLORA_BASE_KERNEL: "pair" (default, CTA pair), "quad" (two pairs sharing the
-// weight tile by TMA multicast), "single" (1-CTA variant) — A/B measurement knob.
-int base_kernel_variant() {
-    static const int v = [] {
-        const char* e = std::getenv("MLORA_BASE_KERNEL");
-        if (!e) return 1;
-        const std::string s(e);
-        return s == "single" ? 0 : s == "quad" ? 2 : 1;
-    }();
-    return v;
-}
-
-constexpr int kQuadStages = 6;
-
-template <bool B_MN>
-mlora_status launch_base_quad(mlora_ctx* ctx, const CUtensorMap& a0, const CUtensorMap& b0,
-                              const CUtensorMap& a1, const CUtensorMap& b1, const GemmParams& p,
-                              cudaStream_t stream) {
-    if (p.num_tiles <= 0) return MLORA_OK;
-    using L = PairSmem<kQuadStages>;
-    auto kern = mlora_base_quad_kernel<kQuadStages, B_MN>;
-    static bool attr_done = false;
-    if (!attr_done) {
-        MLORA_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 L::kDynBytes));
-        attr_done = true;
-    }
-    // clusters of 4 pack into fewer SMs than pairs do (GPC granularity): size the
-    // persistent grid by the hardware's co-resident cluster count, not num_sms / 4
-    static int max_clusters = 0;
-    if (!max_clusters) {
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(4 * (ctx->num_sms / 4));
-        cfg.blockDim = dim3(kNumThreads);
-        cfg.dynamicSmemBytes = L::kDynBytes;
-        cudaLaunchAttribute attr;
-        attr.id = cudaLaunchAttributeClusterDimension;
-        attr.val.clusterDim.x = 4;
-        attr.val.clusterDim.y = 1;
-        attr.val.clusterDim.z = 1;
-        cfg.attrs = &attr;
-        cfg.numAttrs = 1;
-        MLORA_CUDA_TRY(ctx, cudaOccupancyMaxActiveClusters(&max_clusters, kern, &cfg));
-        if (max_clusters < 1) max_clusters = 1;
-    }
-    const int clusters = std::min(p.num_tiles, max_clusters);
-    ProfScope ps(ctx, B_MN ? 1 : 0, stream);
-    MLORA_CUDA_TRY(ctx, launch_k(kern, dim3(4 * clusters), dim3(kNumThreads), L::kDynBytes, stream, 4, a0, b0,
-                                 a1, b1, p));
-    ++ctx->launches;
-    return MLORA_OK;
-}
-
-bool use_pair_kernel() { return base_kernel_variant() != 0; }
 
 constexpr int kPairStages = 6;
 
@@ -349,12 +292,8 @@ mlora_status launch_base_pair(mlora_ctx* ctx, const CUtensorMap& a0, const CUten
     if (p.num_tiles <= 0) return MLORA_OK;
     using L = PairSmem<kPairStages>;
     auto kern = mlora_base_pair_kernel<kPairStages, B_MN>;
-    static bool attr_done = false;
-    if (!attr_done) {
-        MLORA_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 L::kDynBytes));
-        attr_done = true;
-    }
+    mlora_status st = ensure_smem_attr(ctx, reinterpret_cast<const void*>(kern), L::kDynBytes);
+    if (st != MLORA_OK) return st;
     const int clusters = std::min(p.num_tiles, ctx->num_sms / 2);
     ProfScope ps(ctx, B_MN ? 1 : 0, stream);
     MLORA_CUDA_TRY(ctx, launch_k(kern, dim3(2 * clusters), dim3(kNumThreads), L::kDynBytes, stream, 1, a0, b0,
@@ -363,20 +302,17 @@ mlora_status launch_base_pair(mlora_ctx* ctx, const CUtensorMap& a0, const CUten
     return MLORA_OK;
 }
 
-// Frozen-base GEMM + LoRA k-blocks (forward: B_MN=false; dX: B_MN=true).
+// Frozen-base GEMM + LoRA k-blocks (forward: B_MN=false; dX: B_MN=true), on
+// the CTA-pair kernel.
 template <bool B_MN>
 mlora_status run_base(mlora_ctx* ctx, const mlora_plan* plan, const void* A0, int64_t lda0, int K0,
                       const void* B0, const void* A1, const void* B1, int R, int N, void* out,
                       cudaStream_t s, float* row_sq = nullptr) {
-    const bool pair = use_pair_kernel();
-    const bool quad = base_kernel_variant() == 2;
     const int M = plan->rows;
-    const uint32_t bbox = quad ? 64 : pair ? 128 : 256;  // K-major B rows staged per TMA box
-    // A1 == B1 == NULL: no LoRA term (frozen GEMM, e.g. an LM head): the CTA-pair
-    // kernel then runs no extra k-blocks (ext_tab == NULL) and never reads tA1/tB1.
+    constexpr uint32_t bbox = 128;  // K-major B rows staged per TMA box (one CTA's half of the pair's 256)
+    // A1 == B1 == NULL: no LoRA term (frozen GEMM, e.g. an LM head): no extra
+    // k-blocks (ext_tab == NULL), tA1/tB1 are never read.
     const bool lora = A1 != nullptr;
-    if (!lora && (!pair || quad))
-        return fail(ctx, MLORA_USAGE, "a GEMM without a LoRA term needs the CTA-pair base kernel");
     CUtensorMap tA0, tB0, tA1, tB1;
     mlora_status st;
     if ((st = get_tmap(ctx, A0, K0, M, lda0, 64, 128, &tA0)) != MLORA_OK) return st;
@@ -405,49 +341,19 @@ mlora_status run_base(mlora_ctx* ctx, const mlora_plan* plan, const void* A0, in
     pb.scale = plan->d_scale;
     pb.num_jobs = plan->J;
     pb.row_sq = row_sq;
-    if (row_sq && !pair) return fail(ctx, MLORA_USAGE, "fused row sums need the CTA-pair base kernel");
-    if (pair) {
-        // super-row of m-blocks whose A slab (~32 MB) stays L2-resident while all of B streams past it
-        static const int raster_env = [] {
-            const char* e = std::getenv("MLORA_RASTER");
-            return e ? std::atoi(e) : -1;
-        }();
-        const long long slab = (long long)(quad ? kQuadBM : kPairBM) * K0 * 2;
-        pb.raster_group = raster_env >= 0 ? raster_env
-                                          : static_cast<int>(std::max<long long>(1, (32LL << 20) / slab));
-        if (quad) {
-            pb.n_mblk = plan->n_mblk512;
-            pb.n_nblk = cdiv(N, kPairBN);
-            pb.num_tiles = pb.n_mblk * pb.n_nblk;
-            pb.ext_tab = plan->d_ext512;
-            return launch_base_quad<B_MN>(ctx, tA0, tB0, tA1, tB1, pb, s);
-        }
-        pb.n_mblk = plan->n_mblk256;
-        pb.n_nblk = cdiv(N, kPairBN);
-        pb.num_tiles = pb.n_mblk * pb.n_nblk;
-        pb.ext_tab = lora ? plan->d_ext256 : nullptr;
-        return launch_base_pair<B_MN>(ctx, tA0, tB0, tA1, tB1, pb, s);
-    }
-    pb.n_mblk = plan->n_mblk;
-    pb.n_nblk = cdiv(N, 256);
+    // super-row of m-blocks whose A slab (~32 MB) stays L2-resident while all of B
+    // streams past it (a sweep of 2-16 moved neither time nor energy by > 1%,
+    // profiles/r01_raster_energy.log)
+    const long long slab = (long long)kPairBM * K0 * 2;
+    pb.raster_group = static_cast<int>(std::max<long long>(1, (32LL << 20) / slab));
+    pb.n_mblk = plan->n_mblk256;
+    pb.n_nblk = cdiv(N, kPairBN);
     pb.num_tiles = pb.n_mblk * pb.n_nblk;
-    pb.ext_tab = plan->d_ext;
-    ProblemSet<1> set;
-    set.add(tA0, tB0, tA1, tB1, pb);
-    return launch_gemm<MODE_BASE, 256, kBaseStages, false, B_MN, 1, 1>(ctx, set, 1, s);
+    pb.ext_tab = lora ? plan->d_ext256 : nullptr;
+    return launch_base_pair<B_MN>(ctx, tA0, tB0, tA1, tB1, pb, s);
 }
 
 constexpr int kDownStages = 6;
-
-// MLORA_DOWN_MULTI=0 sends shared-input forward down-projections through the
-// grouped per-projection kernel instead (A/B measurement knob).
-bool down_multi_enabled() {
-    static const bool v = [] {
-        const char* e = std::getenv("MLORA_DOWN_MULTI");
-        return !(e && std::string(e) == "0");
-    }();
-    return v;
-}
 
 // Pipeline depth of the shared-input kernel: as deep as 227 KB of shared memory
 // allows (stage = x tile + NB adapter tiles; the K-split partials reuse the ring).
@@ -482,11 +388,7 @@ mlora_status launch_down_multi(mlora_ctx* ctx, const mlora_plan* plan, int K, co
     p.num_jobs = plan->J;
     if (p.num_tiles <= 0) return MLORA_OK;
     auto kern = mlora_down_multi_kernel<NB, STAGES>;
-    static bool attr_done = false;
-    if (!attr_done) {
-        MLORA_CUDA_TRY(ctx, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::kDynBytes));
-        attr_done = true;
-    }
+    if ((st = ensure_smem_attr(ctx, reinterpret_cast<const void*>(kern), L::kDynBytes)) != MLORA_OK) return st;
     const int clusters = std::min(p.num_tiles, ctx->num_sms / 2);
     ProfScope ps(ctx, 2, s);
     MLORA_CUDA_TRY(ctx, launch_k(kern, dim3(2 * clusters), dim3(kNumThreads), L::kDynBytes, s, 2, a));
@@ -525,7 +427,7 @@ mlora_status run_down_group(mlora_ctx* ctx, const mlora_plan* plan, int n, const
     for (int i = 0; i < n; ++i) {
         if (taken[i]) continue;
         std::vector<int> same{i};
-        if (!B_MN && down_multi_enabled())
+        if (!B_MN)
             for (int j = i + 1; j < n; ++j)
                 if (!taken[j] && in[j] == in[i] && K[j] == K[i]) same.push_back(j);
         if (same.size() < 2) {
@@ -850,7 +752,7 @@ mlora_status check_segments(mlora_ctx* ctx, int32_t num_jobs, const int64_t* seg
 
 // Host tables of a segment layout (ranks/roff/scale already set) -> one blob:
 // seg | roff | scale | ext | ext256 | down | grad, with the section offsets.
-std::vector<int> build_tables(mlora_plan* p, const int64_t* seg_offsets, size_t off[8]) {
+std::vector<int> build_tables(mlora_plan* p, const int64_t* seg_offsets, size_t off[7]) {
     const int J = p->J;
     const long long rows = seg_offsets[J];
     p->rows = static_cast<int>(rows);
@@ -886,15 +788,6 @@ std::vector<int> build_tables(mlora_plan* p, const int64_t* seg_offsets, size_t 
         const int ja = job_of_row(r0), jb = job_of_row(r1);
         p->ext256[2 * mb] = p->roff[ja] / kBK;
         p->ext256[2 * mb + 1] = cdiv(p->roff[jb + 1], kBK);
-    }
-    p->n_mblk512 = cdiv(rows, kQuadBM);
-    p->ext512.assign(2 * p->n_mblk512, 0);
-    for (int mb = 0; mb < p->n_mblk512; ++mb) {
-        const int r0 = mb * kQuadBM;
-        const int r1 = std::min<int>(r0 + kQuadBM, p->rows) - 1;
-        const int ja = job_of_row(r0), jb = job_of_row(r1);
-        p->ext512[2 * mb] = p->roff[ja] / kBK;
-        p->ext512[2 * mb + 1] = cdiv(p->roff[jb + 1], kBK);
     }
     // per chunk: union of the token segments of the jobs owning its columns
     p->chunk_kb.assign(2 * p->n_chunks, 0);
@@ -938,14 +831,13 @@ std::vector<int> build_tables(mlora_plan* p, const int64_t* seg_offsets, size_t 
     off[4] = append(p->ext256);
     off[5] = append(p->down);
     off[6] = append(grad);
-    off[7] = append(p->ext512);
     return blob;
 }
 
 // Stream-ordered upload: pinned staging + cudaMemcpyAsync, device buffer grown with
 // cudaMallocAsync/cudaFreeAsync.  Kernels already enqueued on `stream` still see the
 // old tables (the copy runs after them); nothing blocks the host.
-mlora_status upload_tables(mlora_plan* p, const std::vector<int>& blob, const size_t off[8], cudaStream_t s) {
+mlora_status upload_tables(mlora_plan* p, const std::vector<int>& blob, const size_t off[7], cudaStream_t s) {
     mlora_ctx* ctx = p->ctx;
     const size_t bytes = blob.size() * sizeof(int);
     if (p->staging_done) MLORA_CUDA_TRY(ctx, cudaEventSynchronize(p->staging_done));  // staging reusable
@@ -973,7 +865,6 @@ mlora_status upload_tables(mlora_plan* p, const std::vector<int>& blob, const si
     p->d_ext256 = base + off[4];
     p->d_down = base + off[5];
     p->d_grad = base + off[6];
-    p->d_ext512 = base + off[7];
     return MLORA_OK;
 }
 
@@ -1016,7 +907,7 @@ mlora_status mlora_plan_create(mlora_ctx* ctx, int32_t num_jobs, const int64_t* 
         p->scale[j] = scales ? scales[j] : 1.0f;
     }
     p->R_pad = p->roff[num_jobs];
-    size_t off[8];
+    size_t off[7];
     const std::vector<int> blob = build_tables(p, seg_offsets, off);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     st = upload_tables(p, blob, off, s);
@@ -1035,7 +926,7 @@ mlora_status mlora_plan_update(mlora_plan* plan, const int64_t* seg_offsets, voi
     mlora_status st = check_segments(ctx, plan->J, seg_offsets);
     if (st != MLORA_OK) return st;
     DeviceGuard g(ctx->device);
-    size_t off[8];
+    size_t off[7];
     const std::vector<int> blob = build_tables(plan, seg_offsets, off);
     return upload_tables(plan, blob, off, static_cast<cudaStream_t>(stream));
 }

@@ -21,15 +21,13 @@
 //   * elementwise: embed, add_rmsnorm, rmsnorm_bwd_sum, swiglu_{fwd,bwd},
 //     attn_rope (RoPE applied once into separate Q/K buffers);
 //   * mma.sync attention (attn_fwd_kernel / attn_bwd_dq_kernel /
-//     attn_bwd_dkv_kernel, 64-128 row tiles): the fallback for un-rotated
-//     inputs, unaligned row strides and MLORA_ATTN_TC=0;
+//     attn_bwd_dkv_kernel, 64-128 row tiles): RoPE fused into the Q/K loads
+//     (un-rotated inputs) and unaligned row strides;
 //   * tcgen05 attention, the default on pre-rotated inputs: attn_fwd_tc_kernel
 //     (S and O accumulators in TMEM, one query row per thread, lazy rescale),
 //     attn_bwd_dq_ws_kernel and attn_bwd_dkv_ws_kernel (warp-specialised:
 //     TMA loader warps, one MMA-issuing warp, four elementwise warps; dK/dV of
 //     a GQA/MQA group reduced over a thread-block cluster in DSMEM rank order).
-//     The phase-serial *_tc_kernel backwards stay as the MLORA_ATTN_WS=0
-//     fallback.
 // Every kernel launched here bumps the native launch counter
 // (mlora_free_launch_count) so bench.py's gpu_launches is counted, not claimed.
 #include <cooperative_groups.h>
@@ -1018,393 +1016,11 @@ __device__ __forceinline__ void load_stats(const AttnArgs& a, int h, int start, 
     }
 }
 
-// dQ on the 5th-generation tensor cores: one CTA of 4 warps per (128-query
-// block, sequence, head); thread t owns query row t = TMEM lane t.  Per 64-key
-// tile:  S = Q K^T and dP = dO V^T (tcgen05.mma, M=128 N=64, K-major operands),
-// dS = P (dP - D) with P = exp2(S c2 - lse2) computed by each row's thread and
-// written (bf16) as the swizzled A operand, dQ += dS K (M=128 N=HD, K as an
-// MN-major operand) accumulating in TMEM.  No online softmax: the forward's lse
-// fixes P, so dQ needs no rescaling.  V_kt+1 streams in once dP_kt is computed,
-// K_kt+1 once dQ_kt's product is.  Deterministic (no atomics).
-template <int HD>
-struct TcDq {
-    static constexpr int BQ = 128, BK = 64, NB = HD / 64;
-    static constexpr int Q_BYTES = BQ * 128 * NB, K_BYTES = BK * 128 * NB, DS_BYTES = BQ * 128;
-    static constexpr int SMEM = 2 * Q_BYTES + 2 * K_BYTES + DS_BYTES + 64;  // two CTAs per SM at HD = 128
-    static constexpr uint32_t S_COL = 0, DP_COL = 64, DQ_COL = 128, TMEM_COLS = 256;
-    static constexpr uint32_t IDESC_S = tc5::idesc_bf16_f32(128, BK, false, false);
-    static constexpr uint32_t IDESC_Q = tc5::idesc_bf16_f32(128, HD, false, true);
-};
 
-template <int HD>
-__global__ void __launch_bounds__(128, 1) attn_bwd_dq_tc_kernel(AttnArgs a) {
-    using T = TcDq<HD>;
-    pdl_prologue();
-    int start, len;
-    seq_range(a, blockIdx.y, start, len);
-    const int slot = a.seq_off[blockIdx.y + 1] - start;
-    const int q0 = blockIdx.x * T::BQ;
-    if (q0 >= slot) return;
-    const int h = blockIdx.z, kvh = h / (a.heads / a.kv_heads);
-    extern __shared__ __align__(1024) uint8_t smq[];
-    if ((smem_u32(smq) & 1023) != 0) __trap();  // the swizzled operand tiles need 1 KB alignment
-    uint8_t* Qs = smq;
-    uint8_t* dOs = Qs + T::Q_BYTES;
-    uint8_t* Ks = dOs + T::Q_BYTES;
-    uint8_t* Vs = Ks + T::K_BYTES;
-    uint8_t* dSs = Vs + T::K_BYTES;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(dSs + T::DS_BYTES);
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
-    const int warp = threadIdx.x >> 5, row = threadIdx.x;
-    if (threadIdx.x == 0) {
-        tc5::mbar_init(bar, 1);
-        tc5::fence_barrier_init();
-    }
-    if (warp == 0) {
-        tc5::tmem_alloc(tslot, T::TMEM_COLS);
-        tc5::tmem_relinquish();
-    }
-    const int nkt = q0 < len ? (min(q0 + T::BQ, len) + T::BK - 1) / T::BK : 0;
-    // cp.async groups in issue order: [Q, dO, K_0], [V_0], then per tile [V_kt+1], [K_kt+1]
-    stage_sw128<HD>(Qs, T::BQ, a.q, a.ldq, start, q0, len, h * HD);
-    stage_sw128<HD>(dOs, T::BQ, a.dO, a.lddo, start, q0, len, h * HD);
-    if (nkt > 0) stage_sw128<HD>(Ks, T::BK, a.k, a.ldk, start, 0, len, kvh * HD);
-    cp_async_commit();
-    if (nkt > 0) stage_sw128<HD>(Vs, T::BK, a.v, a.ldv, start, 0, len, kvh * HD);
-    cp_async_commit();
-    tc5::tc_fence_before();
-    __syncthreads();
-    tc5::tc_fence_after();
-    const uint32_t tmem = *tslot;
-    const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
-    const float c2 = a.scale * kLog2e;
-    const int qi = q0 + row;
-    const bool real = qi < len;  // this row's lse (log2 units), in a register
-    const float nl = real ? -a.lse[(long long)h * a.rows + start + qi] * kLog2e : 0.f;
-    // D = rowsum(dO * O) of this row, published for the dK/dV kernel that runs next
-    float dr = 0.f;
-    if (real) {
-        const __nv_bfloat16* orow = a.o + (long long)(start + qi) * a.ldo + h * HD;
-        const __nv_bfloat16* drow = a.dO + (long long)(start + qi) * a.lddo + h * HD;
-        for (int c = 0; c < HD; c += 8) {
-            float ov[8], dv[8];
-            ld8(orow + c, ov);
-            ld8(drow + c, dv);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) dr = fmaf(ov[e], dv[e], dr);
-        }
-    }
-    if (qi < slot) a.dsum[(long long)h * a.rows + start + qi] = dr;
-    uint32_t phase = 0;
-    for (int kt = 0; kt < nkt; ++kt) {
-        cp_async_wait<0>();  // K_kt and V_kt (and Q, dO) landed
-        fence_proxy_async();
-        __syncthreads();
-        if (threadIdx.x == 0) {  // S = Q K^T, dP = dO V^T
-            tc5::tc_fence_after();
-#pragma unroll
-            for (int j = 0; j < HD / 16; ++j) {
-                const uint32_t qo = (j / 4) * T::BQ * 128 + (j % 4) * 32, ko = (j / 4) * T::BK * 128 + (j % 4) * 32;
-                tc5::mma_bf16(tmem + T::S_COL, tc5::sdesc_sw128(smem_u32(Qs + qo), 16, 1024),
-                              tc5::sdesc_sw128(smem_u32(Ks + ko), 16, 1024), T::IDESC_S, j > 0 ? 1u : 0u);
-                tc5::mma_bf16(tmem + T::DP_COL, tc5::sdesc_sw128(smem_u32(dOs + qo), 16, 1024),
-                              tc5::sdesc_sw128(smem_u32(Vs + ko), 16, 1024), T::IDESC_S, j > 0 ? 1u : 0u);
-            }
-            tc5::tc_commit(bar);
-        }
-        tc5::mbar_wait(bar, phase);
-        phase ^= 1u;
-        tc5::tc_fence_after();
-        // V_kt is consumed: prefetch V_kt+1 under dS and the dQ product
-        if (kt + 1 < nkt) stage_sw128<HD>(Vs, T::BK, a.v, a.ldv, start, (kt + 1) * T::BK, len, kvh * HD);
-        cp_async_commit();
-        const bool interior = kt * T::BK + T::BK - 1 <= q0 && q0 + T::BQ <= len;
-        uint8_t* drow = dSs + row * 128;
-#pragma unroll
-        for (int half = 0; half < 2; ++half) {
-            uint32_t sv[32], pv[32];
-            tc5::tmem_ld32(tmem + lane_base + T::S_COL + half * 32, sv);
-            tc5::tmem_ld32(tmem + lane_base + T::DP_COL + half * 32, pv);
-            tc5::tmem_wait_ld();
-#pragma unroll
-            for (int ch = 0; ch < 4; ++ch) {
-                float d[8];
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    const int c = ch * 8 + e, kj = kt * T::BK + half * 32 + c;
-                    float p = ex2_ftz(fmaf(__uint_as_float(sv[c]), c2, nl));
-                    if (!interior) p = (kj <= qi && qi < len) ? p : 0.f;
-                    d[e] = p * (__uint_as_float(pv[c]) - dr);
-                }
-                uint4 w;
-                w.x = pack2(d[0], d[1]);
-                w.y = pack2(d[2], d[3]);
-                w.z = pack2(d[4], d[5]);
-                w.w = pack2(d[6], d[7]);
-                const int chunk = half * 4 + ch;
-                *reinterpret_cast<uint4*>(drow + ((chunk ^ (row & 7)) << 4)) = w;
-            }
-        }
-        fence_proxy_async();
-        tc5::tc_fence_before();
-        __syncthreads();
-        if (threadIdx.x == 0) {  // dQ += dS K
-            tc5::tc_fence_after();
-#pragma unroll
-            for (int j = 0; j < T::BK / 16; ++j) {
-                const uint64_t ad = tc5::sdesc_sw128(smem_u32(dSs + j * 32), 16, 1024);
-                const uint64_t bd = tc5::sdesc_sw128(smem_u32(Ks + j * 2048), T::BK * 128, 1024);
-                tc5::mma_bf16(tmem + T::DQ_COL, ad, bd, T::IDESC_Q, (kt > 0 || j > 0) ? 1u : 0u);
-            }
-            tc5::tc_commit(bar);
-        }
-        tc5::mbar_wait(bar, phase);
-        phase ^= 1u;
-        tc5::tc_fence_after();
-        // K_kt is consumed: prefetch K_kt+1
-        if (kt + 1 < nkt) stage_sw128<HD>(Ks, T::BK, a.k, a.ldk, start, (kt + 1) * T::BK, len, kvh * HD);
-        cp_async_commit();
-        tc5::tc_fence_before();
-        __syncthreads();  // S, dP and dS are reused by the next tile
-    }
-    cp_async_wait<0>();
-    // ---- epilogue: dQ (scaled, un-rotated) through an fp32 stage in the Q / dO tiles
-    float* st = reinterpret_cast<float*>(Qs);  // 128 x (HD + 4) fp32 over the (free) Q, dO, K, V tiles
-    __syncthreads();
-    if (nkt > 0) {
-#pragma unroll
-        for (int c0 = 0; c0 < HD; c0 += 32) {
-            uint32_t v[32];
-            tc5::tmem_ld32(tmem + lane_base + T::DQ_COL + c0, v);
-            tc5::tmem_wait_ld();
-#pragma unroll
-            for (int c = 0; c < 32; ++c) st[row * Tile<HD>::LDF + c0 + c] = a.scale * __uint_as_float(v[c]);
-        }
-    } else {
-        for (int c = 0; c < HD; ++c) st[row * Tile<HD>::LDF + c] = 0.f;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int hlf = 0; hlf < 2; ++hlf)
-        store_tile<HD>(st + hlf * kBM * Tile<HD>::LDF, a.dq, a.lddq, start, q0 + hlf * kBM, len, h * HD, slot,
-                       a.rope_base, a.rope_base > 0.f);
-    tc5::tc_fence_before();
-    __syncthreads();
-    if (warp == 0) {
-        tc5::tc_fence_after();
-        tc5::tmem_dealloc(tmem, T::TMEM_COLS);
-    }
-}
-static_assert(2 * TcDq<128>::Q_BYTES + 2 * TcDq<128>::K_BYTES >= 128 * Tile<128>::LDF * 4, "dQ stage fits");
-static_assert(2 * TcDq<64>::Q_BYTES + 2 * TcDq<64>::K_BYTES >= 128 * Tile<64>::LDF * 4, "dQ stage fits");
-
-// dK, dV on the 5th-generation tensor cores: one CTA of 4 warps per (128-key
-// block, sequence, K/V head, head part); thread t owns key row t = TMEM lane t.
-// Per (query head, 64-query tile) the CTA computes the transposed products
-//   S^T = K Q^T and dP^T = V dO^T     (tcgen05.mma, M=128 N=64, K-major),
-// each key's thread forms P^T = exp2(S^T c2 - lse2) (causal-masked) and
-// dS^T = P^T (dP^T - D), writes both (bf16) as swizzled A operands, and
-//   dV += P^T dO,  dK += dS^T Q        (M=128 N=HD, dO / Q as MN-major operands)
-// accumulate in TMEM over the group's query heads and the query tiles.  Q / dO
-// tiles are double-buffered (the next pair streams in under the current MMAs).
-// A GQA / MQA group's heads are split over a cluster as in attn_bwd_dkv_kernel;
-// the partials meet in DSMEM, summed in rank order (deterministic).
-template <int HD>
-struct TcDkv {
-    static constexpr int BK = 128, BQ = 64, NB = HD / 64;
-    static constexpr int K_BYTES = BK * 128 * NB, Q_BYTES = BQ * 128 * NB, P_BYTES = BK * 128;
-    static constexpr int SMEM = 2 * K_BYTES + 4 * Q_BYTES + 2 * P_BYTES + 4 * BQ * 4 + 64;
-    static constexpr uint32_t ST_COL = 0, DPT_COL = 64, DV_COL = 128, DK_COL = 128 + HD, TMEM_COLS = 512;
-    static constexpr uint32_t IDESC_S = tc5::idesc_bf16_f32(128, BQ, false, false);
-    static constexpr uint32_t IDESC_G = tc5::idesc_bf16_f32(128, HD, false, true);
-};
-
-template <int HD>
-__global__ void __launch_bounds__(128, 1) attn_bwd_dkv_tc_kernel(AttnArgs a) {
-    using T = TcDkv<HD>;
-    pdl_prologue();
-    int start, len;
-    seq_range(a, blockIdx.y, start, len);
-    const int slot = a.seq_off[blockIdx.y + 1] - start;
-    const int k0 = blockIdx.x * T::BK;
-    if (k0 >= slot) return;
-    const int kvh = blockIdx.z / a.hsplit, part = blockIdx.z % a.hsplit;
-    const int gh = a.heads / a.kv_heads / a.hsplit;
-    const int h0 = kvh * (a.heads / a.kv_heads) + part * gh;
-    extern __shared__ __align__(1024) uint8_t smk[];
-    if ((smem_u32(smk) & 1023) != 0) __trap();
-    uint8_t* Ks = smk;
-    uint8_t* Vs = Ks + T::K_BYTES;
-    uint8_t* QD = Vs + T::K_BYTES;          // (Q, dO) x 2 buffers
-    uint8_t* Pt = QD + 4 * T::Q_BYTES;
-    uint8_t* dSt = Pt + T::P_BYTES;
-    float* stats = reinterpret_cast<float*>(dSt + T::P_BYTES);  // (lse2, dsum) x 2 buffers
-    uint64_t* bar = reinterpret_cast<uint64_t*>(stats + 4 * T::BQ);
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(bar + 1);
-    const int warp = threadIdx.x >> 5, row = threadIdx.x;
-    if (threadIdx.x == 0) {
-        tc5::mbar_init(bar, 1);
-        tc5::fence_barrier_init();
-    }
-    if (warp == 0) {
-        tc5::tmem_alloc(tslot, T::TMEM_COLS);
-        tc5::tmem_relinquish();
-    }
-    const int qt0 = k0 / T::BQ, nq = (len + T::BQ - 1) / T::BQ - qt0;
-    const int nit = nq > 0 ? gh * nq : 0;
-    auto fetch = [&](int it) {
-        const int h = h0 + it / nq, q0 = (qt0 + it % nq) * T::BQ, b = it & 1;
-        uint8_t* Qb = QD + 2 * T::Q_BYTES * b;
-        stage_sw128<HD>(Qb, T::BQ, a.q, a.ldq, start, q0, len, h * HD);
-        stage_sw128<HD>(Qb + T::Q_BYTES, T::BQ, a.dO, a.lddo, start, q0, len, h * HD);
-        load_stats(a, h, start, q0, T::BQ, len, stats + b * 2 * T::BQ, stats + b * 2 * T::BQ + T::BQ);
-        cp_async_commit();
-    };
-    stage_sw128<HD>(Ks, T::BK, a.k, a.ldk, start, k0, len, kvh * HD);
-    stage_sw128<HD>(Vs, T::BK, a.v, a.ldv, start, k0, len, kvh * HD);
-    cp_async_commit();
-    if (nit > 0) fetch(0);
-    tc5::tc_fence_before();
-    __syncthreads();
-    tc5::tc_fence_after();
-    const uint32_t tmem = *tslot;
-    const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
-    const float c2 = a.scale * kLog2e;
-    const int kj = k0 + row;
-    uint32_t phase = 0;
-    for (int it = 0; it < nit; ++it) {
-        const int q0 = (qt0 + it % nq) * T::BQ, b = it & 1;
-        cp_async_wait<0>();  // K, V and this iteration's (Q, dO, stats) landed
-        fence_proxy_async();
-        __syncthreads();
-        const uint8_t* Qb = QD + 2 * T::Q_BYTES * b;
-        const uint8_t* dOb = Qb + T::Q_BYTES;
-        const float* lse2 = stats + b * 2 * T::BQ;
-        const float* dsm = lse2 + T::BQ;
-        if (threadIdx.x == 0) {  // S^T = K Q^T, dP^T = V dO^T
-            tc5::tc_fence_after();
-#pragma unroll
-            for (int j = 0; j < HD / 16; ++j) {
-                const uint32_t ko = (j / 4) * T::BK * 128 + (j % 4) * 32, qo = (j / 4) * T::BQ * 128 + (j % 4) * 32;
-                tc5::mma_bf16(tmem + T::ST_COL, tc5::sdesc_sw128(smem_u32(Ks + ko), 16, 1024),
-                              tc5::sdesc_sw128(smem_u32(Qb + qo), 16, 1024), T::IDESC_S, j > 0 ? 1u : 0u);
-                tc5::mma_bf16(tmem + T::DPT_COL, tc5::sdesc_sw128(smem_u32(Vs + ko), 16, 1024),
-                              tc5::sdesc_sw128(smem_u32(dOb + qo), 16, 1024), T::IDESC_S, j > 0 ? 1u : 0u);
-            }
-            tc5::tc_commit(bar);
-        }
-        if (it + 1 < nit) fetch(it + 1);  // the other buffer's previous readers finished last iteration
-        tc5::mbar_wait(bar, phase);
-        phase ^= 1u;
-        tc5::tc_fence_after();
-        const bool interior = k0 + T::BK - 1 <= q0 && q0 + T::BQ <= len;
-        uint8_t* prow = Pt + row * 128;
-        uint8_t* drow = dSt + row * 128;
-#pragma unroll
-        for (int half = 0; half < 2; ++half) {
-            uint32_t sv[32], pv[32];
-            tc5::tmem_ld32(tmem + lane_base + T::ST_COL + half * 32, sv);
-            tc5::tmem_ld32(tmem + lane_base + T::DPT_COL + half * 32, pv);
-            tc5::tmem_wait_ld();
-#pragma unroll
-            for (int ch = 0; ch < 4; ++ch) {
-                float p[8], d[8];
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    const int cq = half * 32 + ch * 8 + e, qi = q0 + cq;
-                    float pe = ex2_ftz(fmaf(__uint_as_float(sv[ch * 8 + e]), c2, -lse2[cq]));
-                    if (!interior) pe = (kj <= qi && qi < len) ? pe : 0.f;
-                    p[e] = pe;
-                    d[e] = pe * (__uint_as_float(pv[ch * 8 + e]) - dsm[cq]);
-                }
-                const int chunk = half * 4 + ch, off = (chunk ^ (row & 7)) << 4;
-                uint4 w;
-                w.x = pack2(p[0], p[1]), w.y = pack2(p[2], p[3]), w.z = pack2(p[4], p[5]), w.w = pack2(p[6], p[7]);
-                *reinterpret_cast<uint4*>(prow + off) = w;
-                w.x = pack2(d[0], d[1]), w.y = pack2(d[2], d[3]), w.z = pack2(d[4], d[5]), w.w = pack2(d[6], d[7]);
-                *reinterpret_cast<uint4*>(drow + off) = w;
-            }
-        }
-        fence_proxy_async();
-        tc5::tc_fence_before();
-        __syncthreads();
-        if (threadIdx.x == 0) {  // dV += P^T dO, dK += dS^T Q
-            tc5::tc_fence_after();
-#pragma unroll
-            for (int j = 0; j < T::BQ / 16; ++j) {
-                const uint32_t acc = (it > 0 || j > 0) ? 1u : 0u;
-                tc5::mma_bf16(tmem + T::DV_COL, tc5::sdesc_sw128(smem_u32(Pt + j * 32), 16, 1024),
-                              tc5::sdesc_sw128(smem_u32(dOb + j * 2048), T::BQ * 128, 1024), T::IDESC_G, acc);
-                tc5::mma_bf16(tmem + T::DK_COL, tc5::sdesc_sw128(smem_u32(dSt + j * 32), 16, 1024),
-                              tc5::sdesc_sw128(smem_u32(Qb + j * 2048), T::BQ * 128, 1024), T::IDESC_G, acc);
-            }
-            tc5::tc_commit(bar);
-        }
-        tc5::mbar_wait(bar, phase);
-        phase ^= 1u;
-        tc5::tc_fence_after();
-        tc5::tc_fence_before();
-        __syncthreads();  // P^T, dS^T, S^T / dP^T and this (Q, dO) buffer are reused
-    }
-    cp_async_wait<0>();
-    __syncthreads();
-    // ---- epilogue: dK (scaled, un-rotated) then dV, through an fp32 stage over K / V / Q / dO
-    float* st = reinterpret_cast<float*>(smk);
-    const bool rope_out = a.rope_base > 0.f;
-    namespace cg = cooperative_groups;
-    for (int which = 0; which < 2; ++which) {  // 0: dK, 1: dV
-        const uint32_t col = which == 0 ? T::DK_COL : T::DV_COL;
-        const float sc = which == 0 ? a.scale : 1.f;
-        if (nit > 0) {
-#pragma unroll
-            for (int c0 = 0; c0 < HD; c0 += 32) {
-                uint32_t v[32];
-                tc5::tmem_ld32(tmem + lane_base + col + c0, v);
-                tc5::tmem_wait_ld();
-#pragma unroll
-                for (int c = 0; c < 32; ++c) st[row * Tile<HD>::LDF + c0 + c] = sc * __uint_as_float(v[c]);
-            }
-        } else {
-            for (int c = 0; c < HD; ++c) st[row * Tile<HD>::LDF + c] = 0.f;
-        }
-        __nv_bfloat16* dst = which == 0 ? a.dk : a.dv;
-        const long long ld = which == 0 ? a.lddk : a.lddv;
-        const bool rope = which == 0 && rope_out;
-        if (a.hsplit > 1) {
-            cg::cluster_group cluster = cg::this_cluster();
-            cluster.sync();
-            const float* parts[8];
-            for (int k = 0; k < a.hsplit; ++k) parts[k] = cluster.map_shared_rank(st, k);
-            const int lo = part * T::BK / a.hsplit, hi = (part + 1) * T::BK / a.hsplit;
-            for (int hlf = 0; hlf < 2; ++hlf) {  // store_tile_sum covers 64-row tiles
-                const int l0 = max(lo, hlf * kBM), h1 = min(hi, hlf * kBM + kBM);
-                if (l0 >= h1) continue;
-                const float* ph[8];
-                for (int k = 0; k < a.hsplit; ++k) ph[k] = parts[k] + hlf * kBM * Tile<HD>::LDF;
-                store_tile_sum<HD>(ph, a.hsplit, dst, ld, start, k0 + hlf * kBM, l0 - hlf * kBM, h1 - hlf * kBM, len,
-                                   kvh * HD, slot, a.rope_base, rope);
-            }
-            cluster.sync();
-        } else {
-            __syncthreads();
-            for (int hlf = 0; hlf < 2; ++hlf)
-                store_tile<HD>(st + hlf * kBM * Tile<HD>::LDF, dst, ld, start, k0 + hlf * kBM, len, kvh * HD, slot,
-                               a.rope_base, rope);
-            __syncthreads();
-        }
-    }
-    tc5::tc_fence_before();
-    __syncthreads();
-    if (warp == 0) {
-        tc5::tc_fence_after();
-        tc5::tmem_dealloc(tmem, T::TMEM_COLS);
-    }
-}
-static_assert(2 * TcDkv<128>::K_BYTES + 4 * TcDkv<128>::Q_BYTES >= 128 * Tile<128>::LDF * 4, "dK/dV stage fits");
-static_assert(2 * TcDkv<64>::K_BYTES + 4 * TcDkv<64>::Q_BYTES >= 128 * Tile<64>::LDF * 4, "dK/dV stage fits");
-
-// Warp-specialised dK / dV (tcgen05): the same products as attn_bwd_dkv_tc_kernel,
-// pipelined across three roles of one CTA (288 threads):
+// Warp-specialised dK / dV (tcgen05): per 128-key block, the transposed products
+// S^T = K Q^T and dP^T = V dO^T into TMEM, P^T / dS^T formed per key row as
+// swizzled A operands, dV += P^T dO and dK += dS^T Q accumulated in TMEM over the
+// group's query heads and tiles, pipelined across three roles of one CTA (288 threads):
 //   warps 0-3  elementwise: key row t = TMEM lane t forms P^T, dS^T of pair `it`
 //   warps 4-7  loaders: cp.async of K / V once, then (Q, dO, lse, D) per pair into
 //              two buffers, each refilled once the dV / dK product reading it is done
@@ -2296,38 +1912,13 @@ cudaError_t launch_attn_fwd_tc(K kernel, const mlora_attn_desc* d, size_t smem, 
                   a);
 }
 
-// MLORA_ATTN_TC=0 keeps the mma.sync forward / dQ kernels (A/B knob); the
-// tcgen05 ones need pre-rotated Q / K and 16-byte-aligned rows.
-bool attn_tc_enabled() {
-    static const bool tc = [] {
-        const char* e = std::getenv("MLORA_ATTN_TC");
-        return !(e && e[0] == '0');
-    }();
-    return tc;
-}
-
-// Grid (rows_per_cta-row blocks, sequences, heads_z) with an explicit block size.
-template <typename K>
-cudaError_t launch_attn_rows(K kernel, int rows_per_cta, int threads, const mlora_attn_desc* d, int heads_z,
-                             size_t smem, void* stream, const AttnArgs& a) {
-    if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) !=
-        cudaSuccess)
-        return cudaErrorInvalidValue;
-    const dim3 grid((d->max_len + rows_per_cta - 1) / rows_per_cta, d->num_seqs, heads_z);
-    return launch(kernel, grid, dim3(threads), smem, stream, a);
-}
-
 // Query-head split of the dK/dV kernel for grouped / multi-query attention: the
-// largest divisor of the group size up to the cap (cluster size; default 2,
-// MLORA_ATTN_HSPLIT overrides), none for multi-head attention.  ncu at C4
-// (ChatGLM2, 16 query heads per K/V head), dK/dV per layer: 687 us unsplit,
-// 580 / 594 / 643 us with 2 / 4 / 8-CTA clusters.
+// largest divisor of the group size up to 2 (a 2-CTA cluster), none for
+// multi-head attention.  ncu at C4 (ChatGLM2, 16 query heads per K/V head),
+// dK/dV per layer: 687 us unsplit, 580 / 594 / 643 us with 2 / 4 / 8-CTA clusters.
 int attn_hsplit(const mlora_attn_desc* d) {
     const int group = d->heads / d->kv_heads;
-    static const int cap = [] {
-        const char* e = std::getenv("MLORA_ATTN_HSPLIT");
-        return e ? std::max(1, std::min(8, std::atoi(e))) : 2;
-    }();
+    constexpr int cap = 2;
     int best = 1;
     for (int s = 2; s <= cap; ++s)
         if (group % s == 0) best = s;
@@ -2424,7 +2015,7 @@ mlora_status mlora_attn_fwd(const mlora_attn_desc* d, const void* q, int64_t ldq
     a.vec = rows16(q, ldq) && rows16(k, ldk) && rows16(v, ldv);
     cudaError_t e;
     CUtensorMap tq, tk, tv;
-    if (attn_tc_enabled() && a.vec && !a.rope_in && (reinterpret_cast<uintptr_t>(o) & 15) == 0 && ldo % 8 == 0 &&
+    if (a.vec && !a.rope_in && (reinterpret_cast<uintptr_t>(o) & 15) == 0 && ldo % 8 == 0 &&
         encode_rows_map(q, ldq, d->rows, &tq) && encode_rows_map(k, ldk, d->rows, &tk) &&
         encode_rows_map(v, ldv, d->rows, &tv)) {
         // the tcgen05 kernel: 128 query rows per CTA, one thread per row, K / V by TMA
@@ -2478,33 +2069,21 @@ mlora_status mlora_attn_bwd(const mlora_attn_desc* d, const void* q, int64_t ldq
     a.hsplit = attn_hsplit(d);
     cudaError_t e;
     constexpr int R = kBwdRows;
-    const bool tc = attn_tc_enabled() && a.vec && !a.rope_in && (reinterpret_cast<uintptr_t>(dq) & 3) == 0 &&
-                    (reinterpret_cast<uintptr_t>(o) & 15) == 0 && ldo % 8 == 0;
+    // tcgen05 (default): pre-rotated Q / K, 16-byte rows, TMA-describable operands.
+    // dQ first — its CTAs also compute D = rowsum(dO O) for their rows — then dK / dV,
+    // both warp-specialised and TMA-fed.  Otherwise (fused RoPE, unaligned rows):
+    // the mma.sync kernels below.
+    CUtensorMap tk, tv, tq, tdo;
+    const bool tc = a.vec && !a.rope_in && (reinterpret_cast<uintptr_t>(dq) & 3) == 0 &&
+                    (reinterpret_cast<uintptr_t>(o) & 15) == 0 && ldo % 8 == 0 &&
+                    encode_rows_map(q, ldq, d->rows, &tq) && encode_rows_map(dout, lddo, d->rows, &tdo) &&
+                    encode_rows_map(k, ldk, d->rows, &tk) && encode_rows_map(v, ldv, d->rows, &tv);
     if (tc) {
-        // dQ first: its CTAs also compute D = rowsum(dO O) for their rows (no separate pass);
-        // then dK / dV.  Both warp-specialised and TMA-fed unless MLORA_ATTN_WS=0 (A/B knob:
-        // the phase-serial tcgen05 kernels)
-        static const bool ws = [] {
-            const char* e = std::getenv("MLORA_ATTN_WS");
-            return !(e && e[0] == '0');
-        }();
-        CUtensorMap tk, tv, tq, tdo;
-        const bool maps = ws && encode_rows_map(q, ldq, d->rows, &tq) && encode_rows_map(dout, lddo, d->rows, &tdo);
-        if (maps && encode_rows_map(k, ldk, d->rows, &tk) && encode_rows_map(v, ldv, d->rows, &tv))
-            e = hd == 64 ? launch_attn_wsq(attn_bwd_dq_ws_kernel<64>, d, WsDq<64>::SMEM, stream, tk, tv, tq, tdo, a)
-                         : launch_attn_wsq(attn_bwd_dq_ws_kernel<128>, d, WsDq<128>::SMEM, stream, tk, tv, tq, tdo, a);
-        else
-            e = hd == 64 ? launch_attn_rows(attn_bwd_dq_tc_kernel<64>, 128, 128, d, d->heads, TcDq<64>::SMEM, stream, a)
-                         : launch_attn_rows(attn_bwd_dq_tc_kernel<128>, 128, 128, d, d->heads, TcDq<128>::SMEM, stream,
-                                            a);
-        if (e == cudaSuccess && maps)
+        e = hd == 64 ? launch_attn_wsq(attn_bwd_dq_ws_kernel<64>, d, WsDq<64>::SMEM, stream, tk, tv, tq, tdo, a)
+                     : launch_attn_wsq(attn_bwd_dq_ws_kernel<128>, d, WsDq<128>::SMEM, stream, tk, tv, tq, tdo, a);
+        if (e == cudaSuccess)
             e = hd == 64 ? launch_attn_ws(attn_bwd_dkv_ws_kernel<64>, d, WsDkv<64>::SMEM, stream, tq, tdo, a)
                          : launch_attn_ws(attn_bwd_dkv_ws_kernel<128>, d, WsDkv<128>::SMEM, stream, tq, tdo, a);
-        else if (e == cudaSuccess)
-            e = hd == 64 ? launch_attn(attn_bwd_dkv_tc_kernel<64>, 128, d, d->kv_heads * a.hsplit, TcDkv<64>::SMEM,
-                                       stream, a, a.hsplit, 128)
-                         : launch_attn(attn_bwd_dkv_tc_kernel<128>, 128, d, d->kv_heads * a.hsplit, TcDkv<128>::SMEM,
-                                       stream, a, a.hsplit, 128);
         return e == cudaSuccess ? MLORA_OK : MLORA_CUDA;
     }
     const long long warps = d->rows * d->heads;
@@ -2515,14 +2094,12 @@ mlora_status mlora_attn_bwd(const mlora_attn_desc* d, const void* q, int64_t ldq
         e = launch_attn(attn_bwd_dkv_kernel<64, R>, R, d, d->kv_heads * a.hsplit, attn_smem_bwd<64, R>(), stream, a,
                         a.hsplit);
         if (e == cudaSuccess)
-            e = tc ? launch_attn_rows(attn_bwd_dq_tc_kernel<64>, 128, 128, d, d->heads, TcDq<64>::SMEM, stream, a)
-                   : launch_attn(attn_bwd_dq_kernel<64, R>, R, d, d->heads, attn_smem_dq1<64, R>(), stream, a);
+            e = launch_attn(attn_bwd_dq_kernel<64, R>, R, d, d->heads, attn_smem_dq1<64, R>(), stream, a);
     } else {
         e = launch_attn(attn_bwd_dkv_kernel<128, R>, R, d, d->kv_heads * a.hsplit, attn_smem_bwd<128, R>(), stream,
                         a, a.hsplit);
         if (e == cudaSuccess)
-            e = tc ? launch_attn_rows(attn_bwd_dq_tc_kernel<128>, 128, 128, d, d->heads, TcDq<128>::SMEM, stream, a)
-                   : launch_attn(attn_bwd_dq_kernel<128, R>, R, d, d->heads, attn_smem_dq1<128, R>(), stream, a);
+            e = launch_attn(attn_bwd_dq_kernel<128, R>, R, d, d->heads, attn_smem_dq1<128, R>(), stream, a);
     }
     return e == cudaSuccess ? MLORA_OK : MLORA_CUDA;
 }

@@ -10,6 +10,7 @@
 //               k-blocks of the jobs present in the m-tile)       -> bf16 C
 //               forward:  A0=X,  B0=W0 (K-major), A1=H_cat, B1=B_cat
 //               dX:       A0=dY, B0=W0 (MN-major), A1=G_cat, B1=A_cat (MN)
+//               — on a CTA pair, mlora_base_pair_kernel (below)
 //   MODE_DOWN : H_cat[M, 64-col chunk] = s_j * A0 B0^T, masked block-diagonal
 //               H = s X A_cat^T  (B0 = A_cat K-major)
 //               G = s dY B_cat   (B0 = B_cat MN-major)
@@ -17,7 +18,8 @@
 //               chunk's token range, stored transposed ([R_pad, F], fp32)
 //   MODE_GRAD : dB_cat partials    [F, 64-col chunk] = dY^T H_cat  ([F, R_pad])
 //
-// Roles (192 threads, 1 CTA per SM for BASE): warp 0 = TMA producer,
+// mlora_gemm_kernel runs DOWN / GRADT / GRAD.
+// Roles (192 threads): warp 0 = TMA producer,
 // warp 1 = TMEM allocator + single-thread tcgen05.mma issuer, warps 2..5 =
 // epilogue (TMEM -> registers -> HBM).  Accumulators are double-buffered in
 // TMEM so the epilogue of tile i overlaps the MMAs of tile i+1.  Operands are
@@ -67,18 +69,9 @@ struct TileInfo {
 
 template <int MODE, int BN>
 __device__ __forceinline__ TileInfo decode_tile(const GemmParams& p, int t) {
+    static_assert(MODE != MODE_BASE, "the base GEMM runs on the CTA-pair kernel");
     TileInfo ti;
-    if constexpr (MODE == MODE_BASE) {
-        const int mb = t % p.n_mblk;
-        const int nb = t / p.n_mblk;
-        ti.m0 = mb * kBM;
-        ti.n0 = nb * BN;
-        ti.kb0 = 0;
-        ti.kb1 = p.num_kb;
-        ti.xb0 = __ldg(p.ext_tab + 2 * mb);
-        ti.xb1 = __ldg(p.ext_tab + 2 * mb + 1);
-        ti.aux = 0;
-    } else if constexpr (MODE == MODE_DOWN) {
+    if constexpr (MODE == MODE_DOWN) {
         const int mb = __ldg(p.down_tab + 3 * t);
         const int c = __ldg(p.down_tab + 3 * t + 1);
         ti.aux = __ldg(p.down_tab + 3 * t + 2);
@@ -244,10 +237,6 @@ mlora_gemm_kernel(const __grid_constant__ GemmProblemSet<NP> ps) {
         for (int pi = 0; pi < ps.nprobs; ++pi) {
             tma_prefetch_desc(&ps.prob[pi].tmA0);
             tma_prefetch_desc(&ps.prob[pi].tmB0);
-            if constexpr (MODE == MODE_BASE) {
-                tma_prefetch_desc(&ps.prob[pi].tmA1);
-                tma_prefetch_desc(&ps.prob[pi].tmB1);
-            }
         }
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(full_bar + s, 1);
@@ -364,30 +353,7 @@ mlora_gemm_kernel(const __grid_constant__ GemmProblemSet<NP> ps) {
             const int row = ti.m0 + rloc;
             const bool row_ok = row < p.M;
 
-            if constexpr (MODE == MODE_BASE) {
-                __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out);
-#pragma unroll 1
-                for (int c = 0; c < BN / 32; ++c) {
-                    uint32_t v[32];
-                    tmem_ld32(t_row + c * 32, v);
-                    tmem_wait_ld();
-                    const int col = ti.n0 + c * 32;
-                    if (row_ok && col < p.N) {
-                        uint4* dst = reinterpret_cast<uint4*>(out + (long long)row * p.ldo + col);
-#pragma unroll
-                        for (int g = 0; g < 4; ++g) {
-                            if (col + 8 * g + 8 <= p.N) {
-                                uint4 w;
-                                w.x = pack_bf16x2(__uint_as_float(v[8 * g + 0]), __uint_as_float(v[8 * g + 1]));
-                                w.y = pack_bf16x2(__uint_as_float(v[8 * g + 2]), __uint_as_float(v[8 * g + 3]));
-                                w.z = pack_bf16x2(__uint_as_float(v[8 * g + 4]), __uint_as_float(v[8 * g + 5]));
-                                w.w = pack_bf16x2(__uint_as_float(v[8 * g + 6]), __uint_as_float(v[8 * g + 7]));
-                                dst[g] = w;
-                            }
-                        }
-                    }
-                }
-            } else if constexpr (MODE == MODE_DOWN) {
+            if constexpr (MODE == MODE_DOWN) {
                 __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out);
                 float accv[BN];
 #pragma unroll

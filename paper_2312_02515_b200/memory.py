@@ -95,8 +95,10 @@ def measure_step_gb(device, shapes, ranks, rows: int, W0: dict, seed: int = 0) -
     so the reading is its bytes to the driver's 2 MB page."""
     from . import fused as F
     from .layer import FusedLoraLayer
+    import gc
     dev = torch.device(device)
     torch.cuda.synchronize(dev)
+    gc.collect()  # a previous probe's layer must really be gone before the baseline
     torch.cuda.empty_cache()
     probe = F.Context(dev)
     free0 = device_free_bytes(probe)
@@ -115,6 +117,7 @@ def measure_step_gb(device, shapes, ranks, rows: int, W0: dict, seed: int = 0) -
     del layer
     ctx.close()
     torch.cuda.synchronize(dev)
+    gc.collect()
     torch.cuda.empty_cache()
     probe.close()
     return used / 2 ** 30
