@@ -185,17 +185,6 @@ mlora_status mlora_base_fwd(mlora_ctx* ctx, const mlora_plan* plan, int32_t d, i
 /* dX = dY W0 + G A_cat  (G == A_cat == NULL: dX = dY W0). */
 mlora_status mlora_base_dx(mlora_ctx* ctx, const mlora_plan* plan, int32_t d, int32_t k, const void* dY,
                            const void* W0, const void* G, const void* A_cat, void* dX, void* stream);
-/* The same GEMMs for n projections at once: ONE persistent CTA-pair launch per 8
- * problems (their tiles walked as one tile space), e.g. a forward dependency wave
- * (q, k, v, gate, up <- x) or every dX of a layer.  H / B_cat (G / A_cat) may be
- * NULL arrays (no LoRA term for any problem) or hold NULL pairs; row_sq may be NULL. */
-mlora_status mlora_base_fwd_group(mlora_ctx* ctx, const mlora_plan* plan, int32_t n, const int32_t* d,
-                                  const int32_t* k, const void* const* X, const void* const* W0,
-                                  const void* const* H, const void* const* B_cat, void* const* Y,
-                                  float* const* row_sq, void* stream);
-mlora_status mlora_base_dx_group(mlora_ctx* ctx, const mlora_plan* plan, int32_t n, const int32_t* d,
-                                 const int32_t* k, const void* const* dY, const void* const* W0,
-                                 const void* const* G, const void* const* A_cat, void* const* dX, void* stream);
 /* dA_cat_i = G_i^T X_i and dB_cat_i = dY_i^T H_i for n projections (two grouped launches + at most one
  * grouped fixed-order split reduction). */
 mlora_status mlora_grad_group(mlora_ctx* ctx, const mlora_plan* plan, int32_t n, const int32_t* d,

@@ -77,10 +77,6 @@ _SIGS = {
     "mlora_down_group": (i32, [vp, vp, i32, i32, C.POINTER(i32), C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), vp]),
     "mlora_base_fwd": (i32, [vp, vp, i32, i32, vp, vp, vp, vp, vp, vp, vp]),
     "mlora_base_dx": (i32, [vp, vp, i32, i32, vp, vp, vp, vp, vp, vp]),
-    "mlora_base_fwd_group": (i32, [vp, vp, i32, C.POINTER(i32), C.POINTER(i32), C.POINTER(vp), C.POINTER(vp),
-                                   C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), vp]),
-    "mlora_base_dx_group": (i32, [vp, vp, i32, C.POINTER(i32), C.POINTER(i32), C.POINTER(vp), C.POINTER(vp),
-                                  C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), vp]),
     "mlora_grad_group": (i32, [vp, vp, i32, C.POINTER(i32), C.POINTER(i32), C.POINTER(vp), C.POINTER(vp),
                                C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), C.POINTER(vp), vp]),
     "mlora_linear_bwd": (i32, [vp, vp, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),

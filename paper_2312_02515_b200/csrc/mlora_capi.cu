@@ -285,54 +285,52 @@ mlora_status launch_gemm(mlora_ctx* ctx, const ProblemSet<NP>& set, int ctas_per
 
 constexpr int kPairStages = 6;
 
-using BaseSet = PairProblemSet<kPairGroupMax>;
-
-// One launch of the CTA-pair base GEMM over a problem set (a wave of projections).
 template <bool B_MN>
-mlora_status launch_base_pair(mlora_ctx* ctx, const BaseSet& set, cudaStream_t stream) {
-    if (set.total_tiles <= 0) return MLORA_OK;
+mlora_status launch_base_pair(mlora_ctx* ctx, const CUtensorMap& a0, const CUtensorMap& b0,
+                              const CUtensorMap& a1, const CUtensorMap& b1, const GemmParams& p,
+                              cudaStream_t stream) {
+    if (p.num_tiles <= 0) return MLORA_OK;
     using L = PairSmem<kPairStages>;
-    auto kern = mlora_base_pair_kernel<kPairStages, B_MN, kPairGroupMax>;
+    auto kern = mlora_base_pair_kernel<kPairStages, B_MN>;
     mlora_status st = ensure_smem_attr(ctx, reinterpret_cast<const void*>(kern), L::kDynBytes);
     if (st != MLORA_OK) return st;
-    const int clusters = std::min(set.total_tiles, ctx->num_sms / 2);
+    const int clusters = std::min(p.num_tiles, ctx->num_sms / 2);
     ProfScope ps(ctx, B_MN ? 1 : 0, stream);
-    MLORA_CUDA_TRY(ctx, launch_k(kern, dim3(2 * clusters), dim3(kNumThreads), L::kDynBytes, stream, 1, set));
+    MLORA_CUDA_TRY(ctx, launch_k(kern, dim3(2 * clusters), dim3(kNumThreads), L::kDynBytes, stream, 1, a0, b0,
+                                 a1, b1, p));
     ++ctx->launches;
     return MLORA_OK;
 }
 
-// One base GEMM problem: frozen-base GEMM + LoRA k-blocks (forward: B_MN=false;
-// dX: B_MN=true), appended to `set`.
-//   forward: A0 = X [M, K0=k], B0 = W0 [N=d, K0] K-major, A1 = H_cat [M, R], B1 = B_cat [N, R]
-//   dX:      A0 = dY [M, K0=d], B0 = W0 [K0, N=k] MN-major, A1 = G_cat [M, R], B1 = A_cat [R, N]
-// A1 == B1 == NULL: no LoRA term (frozen GEMM, e.g. an LM head): no extra
-// k-blocks (ext_tab == NULL), tA1/tB1 are never read.
+// Frozen-base GEMM + LoRA k-blocks (forward: B_MN=false; dX: B_MN=true), on
+// the CTA-pair kernel.
 template <bool B_MN>
-mlora_status add_base_problem(mlora_ctx* ctx, const mlora_plan* plan, const void* A0, int64_t lda0, int K0,
-                              const void* B0, const void* A1, const void* B1, int R, int N, void* out,
-                              float* row_sq, BaseSet& set) {
-    if (set.nprobs >= kPairGroupMax) return fail(ctx, MLORA_USAGE, "too many problems in one base launch");
+mlora_status run_base(mlora_ctx* ctx, const mlora_plan* plan, const void* A0, int64_t lda0, int K0,
+                      const void* B0, const void* A1, const void* B1, int R, int N, void* out,
+                      cudaStream_t s, float* row_sq = nullptr) {
     const int M = plan->rows;
     constexpr uint32_t bbox = 128;  // K-major B rows staged per TMA box (one CTA's half of the pair's 256)
+    // A1 == B1 == NULL: no LoRA term (frozen GEMM, e.g. an LM head): no extra
+    // k-blocks (ext_tab == NULL), tA1/tB1 are never read.
     const bool lora = A1 != nullptr;
-    PairProblem& pr = set.prob[set.nprobs];
+    CUtensorMap tA0, tB0, tA1, tB1;
     mlora_status st;
-    if ((st = get_tmap(ctx, A0, K0, M, lda0, 64, 128, &pr.tmA0)) != MLORA_OK) return st;
-    if (lora && (st = get_tmap(ctx, A1, R, M, R, 64, 128, &pr.tmA1)) != MLORA_OK) return st;
+    if ((st = get_tmap(ctx, A0, K0, M, lda0, 64, 128, &tA0)) != MLORA_OK) return st;
+    if (lora && (st = get_tmap(ctx, A1, R, M, R, 64, 128, &tA1)) != MLORA_OK) return st;
     if (!B_MN) {
-        if ((st = get_tmap(ctx, B0, K0, N, K0, 64, bbox, &pr.tmB0)) != MLORA_OK) return st;
-        if (lora && (st = get_tmap(ctx, B1, R, N, R, 64, bbox, &pr.tmB1)) != MLORA_OK) return st;
+        // B0 = W0 [N=d, K0=k], B1 = B_cat [N=d, R]
+        if ((st = get_tmap(ctx, B0, K0, N, K0, 64, bbox, &tB0)) != MLORA_OK) return st;
+        if (lora && (st = get_tmap(ctx, B1, R, N, R, 64, bbox, &tB1)) != MLORA_OK) return st;
     } else {
-        if ((st = get_tmap(ctx, B0, N, K0, N, 64, 64, &pr.tmB0)) != MLORA_OK) return st;
-        if (lora && (st = get_tmap(ctx, B1, N, R, N, 64, 64, &pr.tmB1)) != MLORA_OK) return st;
+        // B0 = W0 [K0=d, N=k] (n contiguous), B1 = A_cat [R, N=k]
+        if ((st = get_tmap(ctx, B0, N, K0, N, 64, 64, &tB0)) != MLORA_OK) return st;
+        if (lora && (st = get_tmap(ctx, B1, N, R, N, 64, 64, &tB1)) != MLORA_OK) return st;
     }
     if (!lora) {
-        pr.tmA1 = pr.tmA0;
-        pr.tmB1 = pr.tmB0;
+        tA1 = tA0;
+        tB1 = tB0;
     }
-    GemmParams& pb = pr.p;
-    pb = GemmParams{};
+    GemmParams pb{};
     pb.M = M;
     pb.N = N;
     pb.num_kb = cdiv(K0, kBK);
@@ -352,20 +350,7 @@ mlora_status add_base_problem(mlora_ctx* ctx, const mlora_plan* plan, const void
     pb.n_nblk = cdiv(N, kPairBN);
     pb.num_tiles = pb.n_mblk * pb.n_nblk;
     pb.ext_tab = lora ? plan->d_ext256 : nullptr;
-    pr.tile_begin = set.total_tiles;
-    set.total_tiles += pb.num_tiles;
-    ++set.nprobs;
-    return MLORA_OK;
-}
-
-template <bool B_MN>
-mlora_status run_base(mlora_ctx* ctx, const mlora_plan* plan, const void* A0, int64_t lda0, int K0,
-                      const void* B0, const void* A1, const void* B1, int R, int N, void* out,
-                      cudaStream_t s, float* row_sq = nullptr) {
-    BaseSet set{};
-    mlora_status st = add_base_problem<B_MN>(ctx, plan, A0, lda0, K0, B0, A1, B1, R, N, out, row_sq, set);
-    if (st != MLORA_OK) return st;
-    return launch_base_pair<B_MN>(ctx, set, s);
+    return launch_base_pair<B_MN>(ctx, tA0, tB0, tA1, tB1, pb, s);
 }
 
 constexpr int kDownStages = 6;
@@ -1078,65 +1063,6 @@ mlora_status mlora_base_dx(mlora_ctx* ctx, const mlora_plan* plan, int32_t d, in
     if (!dY || !W0 || !dX || (!G != !A_cat)) return fail(ctx, MLORA_USAGE, "null tensor pointer");
     DeviceGuard g(ctx->device);
     return run_base<true>(ctx, plan, dY, d, d, W0, G, A_cat, plan->R_pad, k, dX, static_cast<cudaStream_t>(stream));
-}
-
-// Every problem of a forward dependency wave (or every dX of a layer) in ONE
-// persistent CTA-pair launch per 8 problems.
-mlora_status mlora_base_fwd_group(mlora_ctx* ctx, const mlora_plan* plan, int32_t n, const int32_t* d,
-                                  const int32_t* k, const void* const* X, const void* const* W0,
-                                  const void* const* H, const void* const* B_cat, void* const* Y,
-                                  float* const* row_sq, void* stream) {
-    if (!ctx || !plan || n < 0 || (n > 0 && (!d || !k || !X || !W0 || !Y)))
-        return fail(ctx, MLORA_USAGE, "null argument");
-    for (int i = 0; i < n; ++i) {
-        mlora_status st = check_dims(ctx, plan, d[i], k[i]);
-        if (st != MLORA_OK) return st;
-        const void* h = H ? H[i] : nullptr;
-        const void* b = B_cat ? B_cat[i] : nullptr;
-        if (!X[i] || !W0[i] || !Y[i] || (!h != !b)) return fail(ctx, MLORA_USAGE, "null tensor pointer");
-    }
-    DeviceGuard g(ctx->device);
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    for (int i0 = 0; i0 < n; i0 += kPairGroupMax) {
-        BaseSet set{};
-        for (int i = i0; i < std::min<int>(n, i0 + kPairGroupMax); ++i) {
-            mlora_status st = add_base_problem<false>(ctx, plan, X[i], k[i], k[i], W0[i], H ? H[i] : nullptr,
-                                                      B_cat ? B_cat[i] : nullptr, plan->R_pad, d[i], Y[i],
-                                                      row_sq ? row_sq[i] : nullptr, set);
-            if (st != MLORA_OK) return st;
-        }
-        mlora_status st = launch_base_pair<false>(ctx, set, s);
-        if (st != MLORA_OK) return st;
-    }
-    return MLORA_OK;
-}
-
-mlora_status mlora_base_dx_group(mlora_ctx* ctx, const mlora_plan* plan, int32_t n, const int32_t* d,
-                                 const int32_t* k, const void* const* dY, const void* const* W0,
-                                 const void* const* G, const void* const* A_cat, void* const* dX, void* stream) {
-    if (!ctx || !plan || n < 0 || (n > 0 && (!d || !k || !dY || !W0 || !dX)))
-        return fail(ctx, MLORA_USAGE, "null argument");
-    for (int i = 0; i < n; ++i) {
-        mlora_status st = check_dims(ctx, plan, d[i], k[i]);
-        if (st != MLORA_OK) return st;
-        const void* g = G ? G[i] : nullptr;
-        const void* a = A_cat ? A_cat[i] : nullptr;
-        if (!dY[i] || !W0[i] || !dX[i] || (!g != !a)) return fail(ctx, MLORA_USAGE, "null tensor pointer");
-    }
-    DeviceGuard g(ctx->device);
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    for (int i0 = 0; i0 < n; i0 += kPairGroupMax) {
-        BaseSet set{};
-        for (int i = i0; i < std::min<int>(n, i0 + kPairGroupMax); ++i) {
-            mlora_status st = add_base_problem<true>(ctx, plan, dY[i], d[i], d[i], W0[i], G ? G[i] : nullptr,
-                                                     A_cat ? A_cat[i] : nullptr, plan->R_pad, k[i], dX[i], nullptr,
-                                                     set);
-            if (st != MLORA_OK) return st;
-        }
-        mlora_status st = launch_base_pair<true>(ctx, set, s);
-        if (st != MLORA_OK) return st;
-    }
-    return MLORA_OK;
 }
 
 mlora_status mlora_grad_group(mlora_ctx* ctx, const mlora_plan* plan, int32_t n, const int32_t* d,

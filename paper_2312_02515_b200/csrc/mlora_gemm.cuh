@@ -479,29 +479,11 @@ struct PairSmem {
     static constexpr int kDynBytes = kBytes + 1024;
 };
 
-// One persistent launch may carry up to NP independent base GEMMs (e.g. every
-// projection of a forward dependency wave, or every dX of a layer): their tiles
-// form one global tile space, problem after problem, walked round-robin by the
-// clusters, so the launch's pipeline fill and drain are paid once per wave
-// instead of once per projection.
-constexpr int kPairGroupMax = 8;
-
-struct alignas(64) PairProblem {
-    CUtensorMap tmA0, tmB0, tmA1, tmB1;
-    GemmParams p;
-    int tile_begin;
-};
-
-template <int NP>
-struct PairProblemSet {
-    PairProblem prob[NP];
-    int nprobs;
-    int total_tiles;
-};
-
-template <int STAGES, bool B_MN, int NP>
+template <int STAGES, bool B_MN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
-mlora_base_pair_kernel(const __grid_constant__ PairProblemSet<NP> ps) {
+mlora_base_pair_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmB0,
+                       const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1,
+                       const GemmParams p) {
     using namespace sm100;
     using L = PairSmem<STAGES>;
     constexpr uint32_t kTmemCols = 512;  // 2 x 256 fp32 accumulator columns
@@ -524,23 +506,11 @@ mlora_base_pair_kernel(const __grid_constant__ PairProblemSet<NP> ps) {
     const int cluster_id = blockIdx.x >> 1;
     const int nclusters = gridDim.x >> 1;
 
-    // problem owning global tile t, and t's index inside it
-    auto locate = [&](int t, int& pi) {
-        pi = 0;
-        while (pi + 1 < ps.nprobs && ps.prob[pi + 1].tile_begin <= t) ++pi;
-        return t - ps.prob[pi].tile_begin;
-    };
-    const int num_tiles = ps.total_tiles;
-
     if (warp == 0 && elect_one()) {
-        for (int pi = 0; pi < ps.nprobs; ++pi) {
-            tma_prefetch_desc(&ps.prob[pi].tmA0);
-            tma_prefetch_desc(&ps.prob[pi].tmB0);
-            if (ps.prob[pi].p.ext_tab) {
-                tma_prefetch_desc(&ps.prob[pi].tmA1);
-                tma_prefetch_desc(&ps.prob[pi].tmB1);
-            }
-        }
+        tma_prefetch_desc(&tmA0);
+        tma_prefetch_desc(&tmB0);
+        tma_prefetch_desc(&tmA1);
+        tma_prefetch_desc(&tmB1);
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(full_bar + s, 1);    // leader producer's arrive.expect_tx
             mbar_init(empty_bar + s, 1);   // leader MMA's multicast commit
@@ -567,12 +537,9 @@ mlora_base_pair_kernel(const __grid_constant__ PairProblemSet<NP> ps) {
         if (elect_one()) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = cluster_id; t < num_tiles; t += nclusters) {
-                int pi, mb, nb;
-                const int lt = locate(t, pi);
-                const PairProblem& P = ps.prob[pi];
-                const GemmParams& p = P.p;
-                pair_tile_coords(p, lt, mb, nb);
+            for (int t = cluster_id; t < p.num_tiles; t += nclusters) {
+                int mb, nb;
+                pair_tile_coords(p, t, mb, nb);
                 const int m0 = mb * kPairBM + static_cast<int>(cta) * 128;
                 const int n0 = nb * kPairBN + static_cast<int>(cta) * 128;
                 const int xb0 = p.ext_tab ? __ldg(p.ext_tab + 2 * mb) : 0;
@@ -582,8 +549,8 @@ mlora_base_pair_kernel(const __grid_constant__ PairProblemSet<NP> ps) {
                 for (int it = 0; it < nk; ++it) {
                     mbar_wait(empty_bar + stage, phase ^ 1u);
                     const bool ext = it >= nmain;
-                    const CUtensorMap* mA = ext ? &P.tmA1 : &P.tmA0;
-                    const CUtensorMap* mB = ext ? &P.tmB1 : &P.tmB0;
+                    const CUtensorMap* mA = ext ? &tmA1 : &tmA0;
+                    const CUtensorMap* mB = ext ? &tmB1 : &tmB0;
                     const int kc = (ext ? (xb0 + it - nmain) : it) * kBK;
                     const uint32_t sA = base_addr + stage * L::kStageBytes;
                     const uint32_t sB = sA + L::kABytes;
@@ -606,11 +573,9 @@ mlora_base_pair_kernel(const __grid_constant__ PairProblemSet<NP> ps) {
             int stage = 0;
             uint32_t phase = 0;
             int local = 0;
-            for (int t = cluster_id; t < num_tiles; t += nclusters, ++local) {
-                int pi, mb, nb;
-                const int lt = locate(t, pi);
-                const GemmParams& p = ps.prob[pi].p;
-                pair_tile_coords(p, lt, mb, nb);
+            for (int t = cluster_id; t < p.num_tiles; t += nclusters, ++local) {
+                int mb, nb;
+                pair_tile_coords(p, t, mb, nb);
                 const int nk = p.num_kb + (p.ext_tab ? __ldg(p.ext_tab + 2 * mb + 1) - __ldg(p.ext_tab + 2 * mb) : 0);
                 const int acc = local & 1;
                 const uint32_t use = static_cast<uint32_t>(local >> 1);
@@ -643,13 +608,11 @@ mlora_base_pair_kernel(const __grid_constant__ PairProblemSet<NP> ps) {
         // ------------------------------------------------ epilogue (warps 2..5, both CTAs)
         const uint32_t q = warp & 3;
         const int rloc = static_cast<int>(cta * 128 + q * 32 + lane);
+        __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out);
         int local = 0;
-        for (int t = cluster_id; t < num_tiles; t += nclusters, ++local) {
-            int pi, mb, nb;
-            const int lt = locate(t, pi);
-            const GemmParams& p = ps.prob[pi].p;
-            __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out);
-            pair_tile_coords(p, lt, mb, nb);
+        for (int t = cluster_id; t < p.num_tiles; t += nclusters, ++local) {
+            int mb, nb;
+            pair_tile_coords(p, t, mb, nb);
             const int acc = local & 1;
             const uint32_t use = static_cast<uint32_t>(local >> 1);
             mbar_wait(tfull_bar + acc, use & 1u);
