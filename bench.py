@@ -416,6 +416,27 @@ def main():
     eff_tokens = int(PL.sum_over_ranks(rows, device=dev))  # δ = 0: every fused row is a real token
     value = eff_tokens * args.steps / (ms_total / 1e3)
 
+    # ---------------- end-to-end (after the headline pass) through the public API with host buffers: every step's
+    # 64 MiB hidden-state batch is copied H2D from pinned memory (copy stream, double
+    # buffered so step i+1's upload overlaps step i) and its per-job losses D2H.
+    from paper_2312_02515_b200.trainer import PipelinedTrainer
+    trainer = PipelinedTrainer(layer, rows, shapes[0][2])
+    losses_host = torch.empty(max(args.steps, 2), J, dtype=torch.float32).pin_memory()
+    trainer.run([x_host] * 2, losses_host[:2])  # warm the pipeline
+    barrier()
+    time.sleep(1.5)  # the same rested-GPU regime as the headline pass (the power limiter relaxes)
+    e2e_sampler = ClockSampler(dev)
+    e2e_sampler.start()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    trainer.run([x_host] * args.steps, losses_host[:args.steps])
+    f1.record(stream)
+    barrier()
+    e2e_clocks = e2e_sampler.stop()
+    e2e_ms = max_over_ranks(f0.elapsed_time(f1))
+    e2e_value = eff_tokens * args.steps / (e2e_ms / 1e3)
+    losses = losses_host[args.steps - 1].tolist()
+
     # ---------------- sustained: the same step for >= 1.2 s of device time, so the
     # board's power cap (1 kW, engaged within ~100 ms of load) and the capped SM
     # clock are in force and NVML has refreshed its readings several times
@@ -434,38 +455,25 @@ def main():
     sustained = {"value": eff_tokens * sus_steps / (sus_ms / 1e3), "unit": UNIT, "steps": sus_steps,
                  "ms_per_step": sus_ms / sus_steps, "clocks": sus_clocks}
 
-    # ---------------- end-to-end (right after the headline pass) through the public API with host buffers: every step's
-    # 64 MiB hidden-state batch is copied H2D from pinned memory (copy stream, double
-    # buffered so step i+1's upload overlaps step i) and its per-job losses D2H.
-    from paper_2312_02515_b200.trainer import PipelinedTrainer
-    trainer = PipelinedTrainer(layer, rows, shapes[0][2])
-    losses_host = torch.empty(max(args.steps, 2), J, dtype=torch.float32).pin_memory()
-    trainer.run([x_host] * 2, losses_host[:2])  # warm the pipeline
-    barrier()
-    e2e_sampler = ClockSampler(dev)
-    e2e_sampler.start()
-    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    f0.record(stream)
-    trainer.run([x_host] * args.steps, losses_host[:args.steps])
-    f1.record(stream)
-    barrier()
-    e2e_clocks = e2e_sampler.stop()
-    e2e_ms = max_over_ranks(f0.elapsed_time(f1))
-    e2e_value = eff_tokens * args.steps / (e2e_ms / 1e3)
-    losses = losses_host[args.steps - 1].tolist()
-
     # ---------------- per-kernel live timing: the same K steps again with every launch
     # bracketed by CUDA events on its own stream (mlora_ctx_set_profiling).  Kept out of
     # the headline pass because events between launches defeat the PDL prologue overlap.
+    # The board's power limiter needs ~1 s without load to lift the clock back to its
+    # boost value; the pass then sees the same regime as the headline (a short burst
+    # from a rested GPU) instead of the capped clock the sustained pass left behind.
+    barrier()
+    time.sleep(1.5)
     ctx.profile(reset=True)
     ctx.set_profiling(True)
-    barrier()
+    prof_sampler = ClockSampler(dev)
+    prof_sampler.start()
     p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     p0.record(stream)
     for _ in range(args.steps):
         layer.step(x)
     p1.record(stream)
     barrier()
+    prof_clocks = prof_sampler.stop()
     ctx.set_profiling(False)
     prof = ctx.profile(reset=True)
     prof_ms_total = p0.elapsed_time(p1)
@@ -524,7 +532,9 @@ def main():
                      "frac_of_burst": (achieved / peaks["bf16"]) if achieved else None,
                      "kernel": "mlora_base_pair_kernel (cta_group::2, 256x256 tile) forward: X W0^T + H B^T",
                      "peak_kind": ("sustained" if use_sustained else "burst") + " bf16, " + peaks["source"],
-                     "launches": cnt, "avg_launch_us": 1e3 * ms / cnt if cnt else None},
+                     "launches": cnt, "avg_launch_us": 1e3 * ms / cnt if cnt else None,
+                     "timed_in": "a separate pass of the same K steps after a 1.5 s rest, every launch bracketed "
+                                 "by CUDA events on its stream", "clocks": prof_clocks},
         "kernel_time_share": kernel_share,
         "kernel_ms_per_step": kernel_ms_per_step,
         "profiled_pass_ms_per_step": prof_ms_total / args.steps,

@@ -346,6 +346,10 @@ mlora_status run_base(mlora_ctx* ctx, const mlora_plan* plan, const void* A0, in
     // profiles/r01_raster_energy.log)
     const long long slab = (long long)kPairBM * K0 * 2;
     pb.raster_group = static_cast<int>(std::max<long long>(1, (32LL << 20) / slab));
+    // W0 with an L2 evict_last policy: measured on one B200 (profiles/r02_l2_policy.md,
+    // tools/step_probe.py, interleaved A/B): C2 step 4.93 -> 4.79 ms rested, 5.23 -> 5.07
+    // ms in a 20-step burst, 5.69 -> 5.42 J per step sustained
+    pb.keep_b_in_l2 = 1;
     pb.n_mblk = plan->n_mblk256;
     pb.n_nblk = cdiv(N, kPairBN);
     pb.num_tiles = pb.n_mblk * pb.n_nblk;

@@ -54,6 +54,7 @@ struct GemmParams {
     const int* grad_tab;  // [nchunks*nsplit][2] token k-block range
     float* row_sq;        // BASE (pair) optional: [n_nblk][M] sum over the tile's columns of bf16(Y)^2
     int raster_group;     // BASE (pair): m-blocks per raster super-row (<= 0: plain m-fastest)
+    int keep_b_in_l2;     // BASE (pair): load the main B operand (W0) with an L2 evict_last policy
     const int* seg;       // [J+1] row offsets of job segments
     const int* roff;      // [J+1] padded rank column offsets
     const float* scale;   // [J] per-job LoRA scale s_j
@@ -537,6 +538,9 @@ mlora_base_pair_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_co
         if (elect_one()) {
             int stage = 0;
             uint32_t phase = 0;
+            // W0 is re-read by every super-row of m-blocks; when asked, its lines are
+            // kept in L2 (evict_last) while the streamed A rows age out normally
+            const uint64_t pol_b = p.keep_b_in_l2 ? l2_policy_evict_last() : l2_policy_evict_normal();
             for (int t = cluster_id; t < p.num_tiles; t += nclusters) {
                 int mb, nb;
                 pair_tile_coords(p, t, mb, nb);
@@ -558,10 +562,10 @@ mlora_base_pair_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_co
                     if (leader) mbar_arrive_expect_tx(full_bar + stage, 2 * L::kStageBytes);
                     tma_load_2d_2sm(sA, mA, lbar, kc, m0);
                     if constexpr (!B_MN) {
-                        tma_load_2d_2sm(sB, mB, lbar, kc, n0);
+                        tma_load_2d_2sm_hint(sB, mB, lbar, kc, n0, pol_b);
                     } else {
-                        tma_load_2d_2sm(sB, mB, lbar, n0, kc);
-                        tma_load_2d_2sm(sB + 8192, mB, lbar, n0 + 64, kc);
+                        tma_load_2d_2sm_hint(sB, mB, lbar, n0, kc, pol_b);
+                        tma_load_2d_2sm_hint(sB + 8192, mB, lbar, n0 + 64, kc, pol_b);
                     }
                     if (++stage == STAGES) { stage = 0; phase ^= 1u; }
                 }

@@ -132,12 +132,39 @@ class AdapterJobsMixin:
         self.step_count[job] = int(st["step"])
 
 
+class _DeviceBlock:
+    """One cudaMalloc'd block owned through the C ABI (mlora_malloc / mlora_free),
+    exposed to torch by the CUDA array interface (no copy).  Outside torch's
+    caching allocator, so the layer's footprint on the device is exactly its bytes."""
+
+    def __init__(self, ctx, nbytes: int):
+        self.ctx = ctx
+        p = N.vp()
+        N.check(N.lib().mlora_malloc(ctx.handle, max(int(nbytes), 1), C.byref(p)), ctx.handle)
+        self.ptr, self.nbytes = p.value, int(nbytes)
+        self.__cuda_array_interface__ = {"shape": (self.nbytes,), "typestr": "|u1", "data": (self.ptr, False),
+                                         "version": 3, "strides": None}
+
+    def free(self) -> None:
+        if self.ptr:
+            N.lib().mlora_free(self.ctx.handle, self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
 class _Arena:
     """Tensors carved from one device allocation (256-byte aligned views)."""
     ALIGN = 256
 
-    def __init__(self, device, nbytes: int):
-        self.buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+    def __init__(self, ctx, nbytes: int):
+        self.block = _DeviceBlock(ctx, nbytes)
+        self.buf = torch.as_tensor(self.block, device=ctx.device)
+        assert self.buf.data_ptr() == self.block.ptr and self.buf.numel() == nbytes
         self.off = 0
 
     @staticmethod
@@ -209,7 +236,7 @@ class FusedLoraLayer(AdapterJobsMixin):
         # loss) is carved from ONE device allocation: no allocator fragmentation,
         # and the layer's footprint is exactly its bytes (what the memory model's
         # cudaMemGetInfo probes measure, memory.py)
-        arena = _Arena(dev, self._arena_bytes(shapes, names, self.J, R, rows))
+        arena = _Arena(ctx, self._arena_bytes(shapes, names, self.J, R, rows))
         self._arena = arena
         self.proj: list[Projection] = []
         for pi, (name, d, k, src) in enumerate(shapes):
