@@ -13,7 +13,8 @@ import re
 from . import errors
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libmlora.so")
+# MLORA_LIBRARY points the binding at another build of the same ABI (A/B runs of two builds)
+LIB_PATH = os.environ.get("MLORA_LIBRARY") or os.path.join(_PKG, "libmlora.so")
 HEADER = os.path.join(os.path.dirname(_PKG), "include", "mlora.h")
 
 _lib: C.CDLL | None = None

@@ -287,8 +287,8 @@ constexpr int kPairStages = 6;
 
 template <bool B_MN>
 mlora_status launch_base_pair(mlora_ctx* ctx, const CUtensorMap& a0, const CUtensorMap& b0,
-                              const CUtensorMap& a1, const CUtensorMap& b1, const GemmParams& p,
-                              cudaStream_t stream) {
+                              const CUtensorMap& a1, const CUtensorMap& b1, const CUtensorMap& o,
+                              const GemmParams& p, cudaStream_t stream) {
     if (p.num_tiles <= 0) return MLORA_OK;
     using L = PairSmem<kPairStages>;
     auto kern = mlora_base_pair_kernel<kPairStages, B_MN>;
@@ -297,7 +297,7 @@ mlora_status launch_base_pair(mlora_ctx* ctx, const CUtensorMap& a0, const CUten
     const int clusters = std::min(p.num_tiles, ctx->num_sms / 2);
     ProfScope ps(ctx, B_MN ? 1 : 0, stream);
     MLORA_CUDA_TRY(ctx, launch_k(kern, dim3(2 * clusters), dim3(kNumThreads), L::kDynBytes, stream, 1, a0, b0,
-                                 a1, b1, p));
+                                 a1, b1, o, p));
     ++ctx->launches;
     return MLORA_OK;
 }
@@ -330,6 +330,8 @@ mlora_status run_base(mlora_ctx* ctx, const mlora_plan* plan, const void* A0, in
         tA1 = tA0;
         tB1 = tB0;
     }
+    CUtensorMap tOut;  // the epilogue's TMA store: 64-column x 32-row boxes of C [M, N]
+    if ((st = get_tmap(ctx, out, N, M, N, 64, 32, &tOut)) != MLORA_OK) return st;
     GemmParams pb{};
     pb.M = M;
     pb.N = N;
@@ -356,7 +358,7 @@ mlora_status run_base(mlora_ctx* ctx, const mlora_plan* plan, const void* A0, in
     pb.n_nblk = cdiv(N, kPairBN);
     pb.num_tiles = pb.n_mblk * pb.n_nblk;
     pb.ext_tab = lora ? plan->d_ext256 : nullptr;
-    return launch_base_pair<B_MN>(ctx, tA0, tB0, tA1, tB1, pb, s);
+    return launch_base_pair<B_MN>(ctx, tA0, tB0, tA1, tB1, tOut, pb, s);
 }
 
 constexpr int kDownStages = 6;

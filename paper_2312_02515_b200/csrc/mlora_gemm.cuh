@@ -475,7 +475,12 @@ struct PairSmem {
     static constexpr int kABytes = 128 * kBK * 2;   // this CTA's A rows
     static constexpr int kBBytes = 128 * kBK * 2;   // this CTA's half of the B tile
     static constexpr int kStageBytes = kABytes + kBBytes;
-    static constexpr int kBarOffset = STAGES * kStageBytes;
+    // output staging of the TMA-store epilogue: per epilogue warp two 32-row x
+    // 64-column bf16 boxes (128-byte swizzled rows), written by the warp and stored
+    // by one TMA each while the warp converts the next 64 columns
+    static constexpr int kOutBufBytes = 32 * 64 * 2;
+    static constexpr int kOutOffset = STAGES * kStageBytes;
+    static constexpr int kBarOffset = kOutOffset + 4 * 2 * kOutBufBytes;
     static constexpr int kBytes = kBarOffset + (2 * STAGES + 4) * 8 + 16;
     static constexpr int kDynBytes = kBytes + 1024;
 };
@@ -484,7 +489,7 @@ template <int STAGES, bool B_MN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kNumThreads, 1)
 mlora_base_pair_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmB0,
                        const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1,
-                       const GemmParams p) {
+                       const __grid_constant__ CUtensorMap tmOut, const GemmParams p) {
     using namespace sm100;
     using L = PairSmem<STAGES>;
     constexpr uint32_t kTmemCols = 512;  // 2 x 256 fp32 accumulator columns
@@ -512,6 +517,7 @@ mlora_base_pair_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_co
         tma_prefetch_desc(&tmB0);
         tma_prefetch_desc(&tmA1);
         tma_prefetch_desc(&tmB1);
+        tma_prefetch_desc(&tmOut);
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(full_bar + s, 1);    // leader producer's arrive.expect_tx
             mbar_init(empty_bar + s, 1);   // leader MMA's multicast commit
@@ -610,10 +616,13 @@ mlora_base_pair_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_co
         }
     } else {
         // ------------------------------------------------ epilogue (warps 2..5, both CTAs)
+        // TMEM -> registers -> bf16 -> a 128-byte-swizzled staging box -> TMA store:
+        // each warp owns 32 rows (its TMEM lane quarter) and stores them 64 columns at
+        // a time, double-buffered, so the stores run under the next chunk's loads
         const uint32_t q = warp & 3;
         const int rloc = static_cast<int>(cta * 128 + q * 32 + lane);
-        __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out);
-        int local = 0;
+        const uint32_t out_stage = base_addr + L::kOutOffset + q * 2 * L::kOutBufBytes;
+        int local = 0, nstore = 0;
         for (int t = cluster_id; t < p.num_tiles; t += nclusters, ++local) {
             int mb, nb;
             pair_tile_coords(p, t, mb, nb);
@@ -623,37 +632,51 @@ mlora_base_pair_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_co
             tc_fence_after();
             const uint32_t t_row = tmem_base + ((q * 32u) << 16) + acc * kPairBN;
             const int row = mb * kPairBM + rloc;
+            const int row0 = mb * kPairBM + static_cast<int>(cta * 128 + q * 32);
             const bool row_ok = row < p.M;
             float sq = 0.f;  // fused loss: sum of squares of the stored (bf16-rounded) outputs
 #pragma unroll 1
-            for (int c = 0; c < kPairBN / 32; ++c) {
-                uint32_t v[32];
-                tmem_ld32(t_row + c * 32, v);
+            for (int c = 0; c < kPairBN / 64; ++c) {
+                const int col0 = nb * kPairBN + c * 64;
+                if (col0 >= p.N) break;
+                uint32_t v[64];
+                tmem_ld32(t_row + c * 64, *reinterpret_cast<uint32_t(*)[32]>(v));
+                tmem_ld32(t_row + c * 64 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
                 tmem_wait_ld();
-                const int col = nb * kPairBN + c * 32;
-                if (row_ok && col < p.N) {
-                    uint4* dst = reinterpret_cast<uint4*>(out + (long long)row * p.ldo + col);
+                const uint32_t buf = out_stage + static_cast<uint32_t>(nstore & 1) * L::kOutBufBytes;
+                if (lane == 0) bulk_wait_group_read<1>();  // the store issued from `buf` two chunks ago has read it
+                __syncwarp();
 #pragma unroll
-                    for (int g = 0; g < 4; ++g) {
-                        if (col + 8 * g + 8 <= p.N) {
-                            uint32_t w[4];
+                for (int j = 0; j < 8; ++j) {  // 16-byte chunk j: columns col0 + 8j .. col0 + 8j + 7
+                    uint32_t w[4];
 #pragma unroll
-                            for (int h = 0; h < 4; ++h) {
-                                w[h] = pack_bf16x2(__uint_as_float(v[8 * g + 2 * h]), __uint_as_float(v[8 * g + 2 * h + 1]));
-                                const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[h]));
-                                sq = fmaf(f.x, f.x, sq);
-                                sq = fmaf(f.y, f.y, sq);
-                            }
-                            dst[g] = make_uint4(w[0], w[1], w[2], w[3]);
+                    for (int h = 0; h < 4; ++h) {
+                        w[h] = pack_bf16x2(__uint_as_float(v[8 * j + 2 * h]), __uint_as_float(v[8 * j + 2 * h + 1]));
+                        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[h]));
+                        if (col0 + 8 * j < p.N) {
+                            sq = fmaf(f.x, f.x, sq);
+                            sq = fmaf(f.y, f.y, sq);
                         }
                     }
+                    const uint32_t dst = buf + lane * 128u + ((static_cast<uint32_t>(j) ^ (lane & 7u)) << 4);
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "r"(w[0]), "r"(w[1]),
+                                 "r"(w[2]), "r"(w[3])
+                                 : "memory");
                 }
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store_2d(&tmOut, buf, col0, row0);  // rows past M / columns past N are clipped
+                    bulk_commit_group();
+                }
+                ++nstore;
             }
             if (p.row_sq && row_ok) p.row_sq[(long long)nb * p.M + row] = sq;
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(tempty_bar + acc), 0));
         }
+        if (lane == 0) bulk_wait_group_read<0>();  // the staging must outlive every store's read
     }
 
     __syncthreads();
