@@ -77,6 +77,7 @@ struct mlora_plan {
     int n_mblk256 = 0;
     std::vector<int> down;                // [n_down][3]
     int n_down = 0;
+    int down_groups_max = 1;              // widest down tile, in 16-row rank groups
     std::vector<int> chunk_kb;            // [n_chunks][2] token k-block range
     int grad_off[kMaxSplit + 1] = {0};    // offset (ints) of the split-ns table
     // device copies (one allocation, grow-only) and the pinned staging of their upload
@@ -363,24 +364,22 @@ mlora_status run_base(mlora_ctx* ctx, const mlora_plan* plan, const void* A0, in
 
 constexpr int kDownStages = 6;
 
-// Pipeline depth of the shared-input kernel: as deep as 227 KB of shared memory
-// allows (stage = x tile + NB adapter tiles; the K-split partials reuse the ring).
-constexpr int down_multi_stages(int nb) { return nb <= 2 ? 6 : nb == 3 ? 5 : 4; }
-
 template <int NB>
 mlora_status launch_down_multi(mlora_ctx* ctx, const mlora_plan* plan, int K, const void* x,
                                const void* const* bop, void* const* out, cudaStream_t s) {
-    constexpr int STAGES = down_multi_stages(NB);
-    using L = DownMultiSmem<NB, STAGES>;
+    using L = DownMultiSmem;
     static_assert(L::kDynBytes <= 232448, "shared memory budget");
     const int M = plan->rows, R = plan->R_pad;
     DownMultiArgs<NB> a{};
     mlora_status st;
     if ((st = get_tmap(ctx, x, K, M, K, 64, 128, &a.tmA)) != MLORA_OK) return st;
     for (int b = 0; b < NB; ++b) {
-        if ((st = get_tmap(ctx, bop[b], K, R, K, 64, 64, &a.tmB[b])) != MLORA_OK) return st;
+        if ((st = get_tmap(ctx, bop[b], K, R, K, 64, 16, &a.tmB[b])) != MLORA_OK) return st;
         a.out[b] = out[b];
     }
+    // ring sized for the plan's widest tile (16-row rank groups of the jobs present)
+    a.stage_bytes = L::stage_bytes(NB, plan->down_groups_max);
+    a.stages = L::stages_for(a.stage_bytes);
     GemmParams& p = a.p;
     p.M = M;
     p.N = R;
@@ -395,7 +394,7 @@ mlora_status launch_down_multi(mlora_ctx* ctx, const mlora_plan* plan, int K, co
     p.scale = plan->d_scale;
     p.num_jobs = plan->J;
     if (p.num_tiles <= 0) return MLORA_OK;
-    auto kern = mlora_down_multi_kernel<NB, STAGES>;
+    auto kern = mlora_down_multi_kernel<NB>;
     if ((st = ensure_smem_attr(ctx, reinterpret_cast<const void*>(kern), L::kDynBytes)) != MLORA_OK) return st;
     const int clusters = std::min(p.num_tiles, ctx->num_sms / 2);
     ProfScope ps(ctx, 2, s);
@@ -474,12 +473,15 @@ mlora_status run_down_group(mlora_ctx* ctx, const mlora_plan* plan, int n, const
         ProblemSet<kGroupMax> set;
         for (int oi = i0; oi < std::min(nrest, i0 + kGroupMax); ++oi) {
             const int i = order[oi];
-            CUtensorMap tA, tB;
+            CUtensorMap tA, tB, tB16;
             mlora_status st;
             if ((st = get_tmap(ctx, in[i], K[i], M, K[i], 64, 128, &tA)) != MLORA_OK) return st;
             if (!B_MN) st = get_tmap(ctx, bop[i], K[i], R, K[i], 64, 64, &tB);   // A_cat [R, K] K-major
             else st = get_tmap(ctx, bop[i], R, K[i], R, 64, 64, &tB);            // B_cat [K, R] MN-major
             if (st != MLORA_OK) return st;
+            // forward: A_cat loaded by 16-row rank groups (only the m-block's jobs', down_group_lo/hi)
+            tB16 = tB;
+            if (!B_MN && (st = get_tmap(ctx, bop[i], K[i], R, K[i], 64, 16, &tB16)) != MLORA_OK) return st;
             GemmParams p{};
             p.M = M;
             p.N = R;
@@ -494,7 +496,7 @@ mlora_status run_down_group(mlora_ctx* ctx, const mlora_plan* plan, int n, const
             p.roff = plan->d_roff;
             p.scale = plan->d_scale;
             p.num_jobs = plan->J;
-            set.add(tA, tB, tA, tB, p);
+            set.add(tA, tB, tA, tB16, p);
         }
         set.ps.interleave = same_k ? 1 : 0;
         mlora_status st = launch_gemm<MODE_DOWN, 64, kDownStages, false, B_MN, 2, kGroupMax>(ctx, set, 1, s);
@@ -781,13 +783,21 @@ std::vector<int> build_tables(mlora_plan* p, const int64_t* seg_offsets, size_t 
         const int ja = job_of_row(r0), jb = job_of_row(r1);
         p->ext[2 * mb] = p->roff[ja] / kBK;
         p->ext[2 * mb + 1] = cdiv(p->roff[jb + 1], kBK);
+        // flags: bit 0 = first chunk (zero-fill duty), bits 1-3 / 4-6 = the chunk's 16-row rank
+        // groups [lo, hi) held by the jobs present (roff is a multiple of 16: exact)
+        const int c_lo = p->roff[ja], c_hi = p->roff[jb + 1];
         for (int c = p->ext[2 * mb]; c < p->ext[2 * mb + 1]; ++c) {
+            const int lo = (std::max(c_lo, c * kBK) - c * kBK) / 16;
+            const int hi = (std::min(c_hi, (c + 1) * kBK) - c * kBK + 15) / 16;
             p->down.push_back(mb);
             p->down.push_back(c);
-            p->down.push_back(c == p->ext[2 * mb] ? 1 : 0);
+            p->down.push_back((c == p->ext[2 * mb] ? 1 : 0) | (lo << 1) | (hi << 4));
         }
     }
     p->n_down = static_cast<int>(p->down.size() / 3);
+    p->down_groups_max = 1;
+    for (int t = 0; t < p->n_down; ++t)
+        p->down_groups_max = std::max(p->down_groups_max, down_group_hi(p->down[3 * t + 2]) - down_group_lo(p->down[3 * t + 2]));
     p->n_mblk256 = cdiv(rows, kPairBM);
     p->ext256.assign(2 * p->n_mblk256, 0);
     for (int mb = 0; mb < p->n_mblk256; ++mb) {

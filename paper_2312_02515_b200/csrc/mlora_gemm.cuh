@@ -50,7 +50,7 @@ struct GemmParams {
     long long ldo;     // output leading dimension (elements)
     long long split_stride;  // elements between split partials (GRAD*)
     const int* ext_tab;   // [n_mblk][2]  extra (LoRA) k-block range per m-block
-    const int* down_tab;  // [num_tiles][3] (m_blk, chunk, flags) for MODE_DOWN
+    const int* down_tab;  // [num_tiles][3] (m_blk, chunk, flags) for MODE_DOWN (flags: down_group_lo/hi)
     const int* grad_tab;  // [nchunks*nsplit][2] token k-block range
     float* row_sq;        // BASE (pair) optional: [n_nblk][M] sum over the tile's columns of bf16(Y)^2
     int raster_group;     // BASE (pair): m-blocks per raster super-row (<= 0: plain m-fastest)
@@ -94,6 +94,13 @@ __device__ __forceinline__ TileInfo decode_tile(const GemmParams& p, int t) {
     return ti;
 }
 
+// MODE_DOWN tile flags: bit 0 = first chunk of the m-block (zero-fill duty);
+// bits 1-3 / 4-6 = [lo, hi) of the 16-row rank groups of the chunk that belong
+// to the jobs present in the m-block (mlora_capi.cu build_tables).  Only those
+// rank rows of the K-major adapter operand are loaded and multiplied.
+__host__ __device__ __forceinline__ int down_group_lo(int flags) { return (flags >> 1) & 7; }
+__host__ __device__ __forceinline__ int down_group_hi(int flags) { return (flags >> 4) & 7; }
+
 __device__ __forceinline__ int job_of_row(const int* seg, int num_jobs, int row) {
     // largest j with seg[j] <= row (segments partition [0, M))
     int lo = 0, hi = num_jobs - 1;
@@ -110,12 +117,43 @@ __device__ __forceinline__ int job_of_row(const int* seg, int num_jobs, int row)
 // The first chunk tile of an m-block (aux & 1) also zero-fills the row's
 // columns outside the m-block's LoRA k-block range, so H/G are fully
 // block-diagonal in HBM.
+//
+// The row's job lookup (a dependent chain of table loads) is split off into
+// down_row_info so the epilogue can issue it before it waits for the
+// mainloop, and a multi-projection epilogue does it once per row, not once
+// per projection.
+struct DownRow {
+    int c_lo, c_hi;  // the row's job's columns
+    float s;         // its scale
+    int z0, z1;      // first chunk tile: columns kept (LoRA k-block range); z0 = z1 = -1 otherwise
+};
+
+__device__ __forceinline__ DownRow down_row_info(const GemmParams& p, int row, int m0, int aux) {
+    DownRow r;
+    const int jr = job_of_row(p.seg, p.num_jobs, row < p.M ? row : p.M - 1);
+    r.c_lo = __ldg(p.roff + jr);
+    r.c_hi = __ldg(p.roff + jr + 1);
+    r.s = __ldg(p.scale + jr);
+    r.z0 = r.z1 = -1;
+    if (aux & 1) {
+        const int mb = m0 / kBM;
+        r.z0 = __ldg(p.ext_tab + 2 * mb) * kBK;
+        r.z1 = __ldg(p.ext_tab + 2 * mb + 1) * kBK;
+    }
+    return r;
+}
+
+// First chunk tile of an m-block: zero the row's columns outside its LoRA k-block range.
+__device__ __forceinline__ void down_zero_outside(const GemmParams& p, const DownRow& r, __nv_bfloat16* out, int row) {
+    uint4* rowp = reinterpret_cast<uint4*>(out + (long long)row * p.ldo);
+    const uint4 zero = make_uint4(0, 0, 0, 0);
+    for (int cc = 0; cc < p.N; cc += 8)
+        if (cc < r.z0 || cc >= r.z1) rowp[cc / 8] = zero;
+}
+
 template <int BN>
-__device__ __forceinline__ void down_store_row(const GemmParams& p, __nv_bfloat16* out, int row, int m0, int n0,
-                                               int aux, const float* accv) {
-    const int jr = job_of_row(p.seg, p.num_jobs, row);
-    const int c_lo = __ldg(p.roff + jr), c_hi = __ldg(p.roff + jr + 1);
-    const float s = __ldg(p.scale + jr);
+__device__ __forceinline__ void down_store_row(const GemmParams& p, const DownRow& r, __nv_bfloat16* out, int row,
+                                               int n0, const float* accv) {
     uint4* dst = reinterpret_cast<uint4*>(out + (long long)row * p.ldo + n0);
 #pragma unroll
     for (int g = 0; g < BN / 8; ++g) {
@@ -124,7 +162,7 @@ __device__ __forceinline__ void down_store_row(const GemmParams& p, __nv_bfloat1
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
             const int cc = n0 + 8 * g + e;
-            f[e] = (cc >= c_lo && cc < c_hi) ? s * accv[8 * g + e] : 0.f;
+            f[e] = (cc >= r.c_lo && cc < r.c_hi) ? r.s * accv[8 * g + e] : 0.f;
         }
         uint4 w;
         w.x = sm100::pack_bf16x2(f[0], f[1]);
@@ -133,15 +171,7 @@ __device__ __forceinline__ void down_store_row(const GemmParams& p, __nv_bfloat1
         w.w = sm100::pack_bf16x2(f[6], f[7]);
         dst[g] = w;
     }
-    if (aux & 1) {
-        const int mb = m0 / kBM;
-        const int z0 = __ldg(p.ext_tab + 2 * mb) * kBK;
-        const int z1 = __ldg(p.ext_tab + 2 * mb + 1) * kBK;
-        uint4* rowp = reinterpret_cast<uint4*>(out + (long long)row * p.ldo);
-        const uint4 zero = make_uint4(0, 0, 0, 0);
-        for (int cc = 0; cc < p.N; cc += 8)
-            if (cc < z0 || cc >= z1) rowp[cc / 8] = zero;
-    }
+    if (r.z0 >= 0) down_zero_outside(p, r, out, row);
 }
 
 template <int BN, int STAGES, int KSPLIT = 1>
@@ -273,6 +303,12 @@ mlora_gemm_kernel(const __grid_constant__ GemmProblemSet<NP> ps) {
                 const TileInfo ti = tile_of(pi, t);
                 const int nmain = ti.kb1 - ti.kb0;
                 const int nk = nmain + (ti.xb1 - ti.xb0);
+                // forward down-projection: only the present jobs' 16-row rank groups of A_cat
+                // (tmB1 = the same tensor, 16-row box); everything else loads whole tiles
+                constexpr bool kNarrow = MODE == MODE_DOWN && !B_MN;
+                const int glo = kNarrow ? down_group_lo(ti.aux) : 0, ghi = kNarrow ? down_group_hi(ti.aux) : 0;
+                const uint32_t tx = kNarrow ? static_cast<uint32_t>(L::kABytes + (ghi - glo) * 16 * kBK * 2)
+                                            : static_cast<uint32_t>(L::kStageBytes);
                 for (int it = 0; it < nk; ++it) {
                     mbar_wait(empty_bar + stage, phase ^ 1u);
                     const bool ext = it >= nmain;
@@ -282,7 +318,7 @@ mlora_gemm_kernel(const __grid_constant__ GemmProblemSet<NP> ps) {
                     const uint32_t sA = base_addr + stage * L::kStageBytes;
                     const uint32_t sB = sA + L::kABytes;
                     uint64_t* bar = full_bar + stage;
-                    mbar_arrive_expect_tx(bar, L::kStageBytes);
+                    mbar_arrive_expect_tx(bar, tx);
                     if constexpr (!A_MN) {
                         tma_load_2d(sA, mA, bar, kc, ti.m0);
                     } else {
@@ -290,7 +326,10 @@ mlora_gemm_kernel(const __grid_constant__ GemmProblemSet<NP> ps) {
                         for (int h = 0; h < kBM / 64; ++h)
                             tma_load_2d(sA + h * 8192, mA, bar, ti.m0 + 64 * h, kc);
                     }
-                    if constexpr (!B_MN) {
+                    if constexpr (kNarrow) {
+                        for (int g = glo; g < ghi; ++g)
+                            tma_load_2d(sB + g * 16 * kBK * 2, &P.tmB1, bar, kc, ti.n0 + 16 * g);
+                    } else if constexpr (!B_MN) {
                         tma_load_2d(sB, mB, bar, kc, ti.n0);
                     } else {
 #pragma unroll
@@ -313,7 +352,15 @@ mlora_gemm_kernel(const __grid_constant__ GemmProblemSet<NP> ps) {
             const uint32_t use = static_cast<uint32_t>(local >> 1);
             mbar_wait(tempty_bar + acc, (use & 1u) ^ 1u);
             tc_fence_after();
-            const uint32_t d_tmem = tmem_base + acc * BN;
+            uint32_t d_tmem = tmem_base + acc * BN;
+            uint32_t idesc = kIdesc;
+            uint32_t b_off = 0;
+            if constexpr (MODE == MODE_DOWN && !B_MN) {
+                const int glo = down_group_lo(ti.aux), ghi = down_group_hi(ti.aux);
+                idesc = idesc_bf16_f32(kBM, 16 * (ghi - glo), A_MN, B_MN);
+                d_tmem += 16 * glo;
+                b_off = glo * 16 * kBK * 2;
+            }
             for (int it = 0; it < nk; ++it) {
                 mbar_wait(full_bar + stage, phase);
                 tc_fence_after();
@@ -325,8 +372,8 @@ mlora_gemm_kernel(const __grid_constant__ GemmProblemSet<NP> ps) {
                         const uint64_t ad = A_MN ? sdesc_sw128(sA + j * 2048, 8192, 1024)
                                                  : sdesc_sw128(sA + j * 32, 16, 1024);
                         const uint64_t bd = B_MN ? sdesc_sw128(sB + j * 2048, 8192, 1024)
-                                                 : sdesc_sw128(sB + j * 32, 16, 1024);
-                        mma_bf16(d_tmem, ad, bd, kIdesc, (it | j) != 0 ? 1u : 0u);
+                                                 : sdesc_sw128(sB + b_off + j * 32, 16, 1024);
+                        mma_bf16(d_tmem, ad, bd, idesc, (it | j) != 0 ? 1u : 0u);
                     }
                     tc_commit(empty_bar + stage);
                 }
@@ -348,21 +395,26 @@ mlora_gemm_kernel(const __grid_constant__ GemmProblemSet<NP> ps) {
             const bool empty = (ti.kb1 - ti.kb0) + (ti.xb1 - ti.xb0) == 0;
             const int acc = local & 1;
             const uint32_t use = static_cast<uint32_t>(local >> 1);
+            const int row = ti.m0 + rloc;
+            const bool row_ok = row < p.M;
+            DownRow dr{};
+            if constexpr (MODE == MODE_DOWN) dr = down_row_info(p, row, ti.m0, ti.aux);  // overlaps the mainloop
             mbar_wait(tfull_bar + acc, use & 1u);
             tc_fence_after();
             const uint32_t t_row = tmem_base + ((q * 32u) << 16) + acc * BN;
-            const int row = ti.m0 + rloc;
-            const bool row_ok = row < p.M;
 
             if constexpr (MODE == MODE_DOWN) {
                 __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out);
+                // 16-column groups holding written accumulators (narrowed forward: the present jobs')
+                const int glo = B_MN ? 0 : down_group_lo(ti.aux), ghi = B_MN ? BN / 16 : down_group_hi(ti.aux);
                 float accv[BN];
 #pragma unroll
                 for (int c = 0; c < BN / 32; ++c) {
+                    const bool live = !empty && 2 * c < ghi && 2 * c + 2 > glo;
                     uint32_t v[32];
-                    if (!empty) { tmem_ld32(t_row + c * 32, v); tmem_wait_ld(); }
+                    if (live) { tmem_ld32(t_row + c * 32, v); tmem_wait_ld(); }
 #pragma unroll
-                    for (int e = 0; e < 32; ++e) accv[c * 32 + e] = empty ? 0.f : __uint_as_float(v[e]);
+                    for (int e = 0; e < 32; ++e) accv[c * 32 + e] = live ? __uint_as_float(v[e]) : 0.f;
                 }
                 bool store = true;
                 if constexpr (KSPLIT == 2) {
@@ -372,8 +424,9 @@ mlora_gemm_kernel(const __grid_constant__ GemmProblemSet<NP> ps) {
                         mbar_wait(pempty_bar, (static_cast<uint32_t>(local) & 1u) ^ 1u);
 #pragma unroll
                         for (int g = 0; g < BN / 4; ++g)
-                            st_cluster_v4(mapa_shared(smem_u32(part + g * kBM + rloc), 0),
-                                          make_float4(accv[4 * g], accv[4 * g + 1], accv[4 * g + 2], accv[4 * g + 3]));
+                            if (g >= 4 * glo && g < 4 * ghi)
+                                st_cluster_v4(mapa_shared(smem_u32(part + g * kBM + rloc), 0),
+                                              make_float4(accv[4 * g], accv[4 * g + 1], accv[4 * g + 2], accv[4 * g + 3]));
                         // every lane orders its DSMEM stores at cluster scope before lane 0's release-arrive
                         asm volatile("fence.acq_rel.cluster;" ::: "memory");
                         __syncwarp();
@@ -383,6 +436,7 @@ mlora_gemm_kernel(const __grid_constant__ GemmProblemSet<NP> ps) {
                         mbar_wait_cluster(pfull_bar, static_cast<uint32_t>(local) & 1u);
 #pragma unroll
                         for (int g = 0; g < BN / 4; ++g) {
+                            if (g < 4 * glo || g >= 4 * ghi) continue;
                             const float4 q4 = part[g * kBM + rloc];
                             accv[4 * g] += q4.x;
                             accv[4 * g + 1] += q4.y;
@@ -395,7 +449,7 @@ mlora_gemm_kernel(const __grid_constant__ GemmProblemSet<NP> ps) {
                         if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(pempty_bar), 1));
                     }
                 }
-                if (store && row_ok) down_store_row<BN>(p, out, row, ti.m0, ti.n0, ti.aux, accv);
+                if (store && row_ok) down_store_row<BN>(p, dr, out, row, ti.n0, accv);
             } else if constexpr (MODE == MODE_GRADT) {
                 float* out = static_cast<float*>(p.out) + (long long)ti.aux * p.split_stride;
 #pragma unroll 1
