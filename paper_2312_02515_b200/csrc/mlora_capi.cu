@@ -344,13 +344,14 @@ mlora_status run_base(mlora_ctx* ctx, const mlora_plan* plan, const void* A0, in
     pb.scale = plan->d_scale;
     pb.num_jobs = plan->J;
     pb.row_sq = row_sq;
-    // super-row of m-blocks whose A slab (~32 MB) stays L2-resident while all of B
-    // streams past it, and at least a square wave (8 m-blocks x ~9 n-blocks for the 74
-    // concurrent tiles): for K = 11008 (5.6 MB slabs) 8 instead of 5 cuts the launch's
-    // DRAM reads 964 -> 838 MB (ncu sweep of 2 / 5 / 8 / 16 / 32: 876 / 964 / 838 /
-    // 927 / 1380 MB, profiles/r02_raster_k11008.md)
+    // Raster.  K <= 8192: super-rows of m-blocks whose A slab (~32 MB) stays L2-resident
+    // while all of B streams past it, at least a square wave (8 m-blocks x ~9 n-blocks for
+    // the 74 concurrent tiles).  K > 8192 (5.6 MB slabs at K = 11008: the 74 tiles in
+    // flight span ~100 MB): super-columns of 8 n-blocks, n fastest — the W0 slabs (kept
+    // with evict_last) stay resident while the A slabs stream past them, which cuts the
+    // launch's DRAM reads 839 -> 740 MB (ncu sweeps, profiles/r02_raster_k11008.md)
     const long long slab = (long long)kPairBM * K0 * 2;
-    pb.raster_group = static_cast<int>(std::max<long long>(8, (32LL << 20) / slab));
+    pb.raster_group = K0 > 8192 ? -8 : static_cast<int>(std::max<long long>(8, (32LL << 20) / slab));
     // W0 with an L2 evict_last policy: measured on one B200 (profiles/r02_l2_policy.md,
     // tools/step_probe.py, interleaved A/B): C2 step 4.93 -> 4.79 ms rested, 5.23 -> 5.07
     // ms in a 20-step burst, 5.69 -> 5.42 J per step sustained

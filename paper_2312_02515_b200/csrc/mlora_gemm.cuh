@@ -53,7 +53,7 @@ struct GemmParams {
     const int* down_tab;  // [num_tiles][3] (m_blk, chunk, flags) for MODE_DOWN (flags: down_group_lo/hi)
     const int* grad_tab;  // [nchunks*nsplit][2] token k-block range
     float* row_sq;        // BASE (pair) optional: [n_nblk][M] sum over the tile's columns of bf16(Y)^2
-    int raster_group;     // BASE (pair): m-blocks per raster super-row (<= 0: plain m-fastest)
+    int raster_group;     // BASE (pair): > 0 m-blocks per super-row (m fastest); < 0 n-blocks per super-column (n fastest); 0 plain m-fastest
     int keep_b_in_l2;     // BASE (pair): load the main B operand (W0) with an L2 evict_last policy
     const int* seg;       // [J+1] row offsets of job segments
     const int* roff;      // [J+1] padded rank column offsets
@@ -516,6 +516,16 @@ constexpr int kPairBN = 256;
 // super-row) so the A rows of a super-row stay L2-resident while every n-block
 // of B streams past them; group_m <= 0 means plain m-fastest order.
 __device__ __forceinline__ void pair_tile_coords(const GemmParams& p, int t, int& mb, int& nb) {
+    if (p.raster_group < 0) {
+        // super-columns of -raster_group n-blocks: n fastest inside, m walks
+        const int gn = -p.raster_group;
+        const int per_group = gn * p.n_mblk;
+        const int g = t / per_group, r = t - g * per_group;
+        const int cols_in_group = min(gn, p.n_nblk - g * gn);
+        nb = g * gn + r % cols_in_group;
+        mb = r / cols_in_group;
+        return;
+    }
     const int gm = p.raster_group > 0 ? p.raster_group : p.n_mblk;
     const int per_group = gm * p.n_nblk;
     const int g = t / per_group, r = t - g * per_group;
