@@ -74,6 +74,7 @@ struct mlora_plan {
     std::vector<float> scale;
     std::vector<int> ext;                 // [n_mblk][2]   (128-row m-blocks)
     std::vector<int> ext256;              // [n_mblk256][2] (256-row m-blocks of the CTA-pair kernel)
+    std::vector<int> grp256;              // [n_mblk256][2] 16-column rank groups [lo, hi) of the jobs present
     int n_mblk256 = 0;
     std::vector<int> down;                // [n_down][3]
     int n_down = 0;
@@ -91,6 +92,7 @@ struct mlora_plan {
     float* d_scale = nullptr;
     int* d_ext = nullptr;
     int* d_ext256 = nullptr;
+    int* d_grp256 = nullptr;
     int* d_down = nullptr;
     int* d_grad = nullptr;
 };
@@ -360,6 +362,7 @@ mlora_status run_base(mlora_ctx* ctx, const mlora_plan* plan, const void* A0, in
     pb.n_nblk = cdiv(N, kPairBN);
     pb.num_tiles = pb.n_mblk * pb.n_nblk;
     pb.ext_tab = lora ? plan->d_ext256 : nullptr;
+    pb.ext_grp = lora ? plan->d_grp256 : nullptr;
     return launch_base_pair<B_MN>(ctx, tA0, tB0, tA1, tB1, tOut, pb, s);
 }
 
@@ -763,7 +766,7 @@ mlora_status check_segments(mlora_ctx* ctx, int32_t num_jobs, const int64_t* seg
 
 // Host tables of a segment layout (ranks/roff/scale already set) -> one blob:
 // seg | roff | scale | ext | ext256 | down | grad, with the section offsets.
-std::vector<int> build_tables(mlora_plan* p, const int64_t* seg_offsets, size_t off[7]) {
+std::vector<int> build_tables(mlora_plan* p, const int64_t* seg_offsets, size_t off[8]) {
     const int J = p->J;
     const long long rows = seg_offsets[J];
     p->rows = static_cast<int>(rows);
@@ -801,12 +804,15 @@ std::vector<int> build_tables(mlora_plan* p, const int64_t* seg_offsets, size_t 
         p->down_groups_max = std::max(p->down_groups_max, down_group_hi(p->down[3 * t + 2]) - down_group_lo(p->down[3 * t + 2]));
     p->n_mblk256 = cdiv(rows, kPairBM);
     p->ext256.assign(2 * p->n_mblk256, 0);
+    p->grp256.assign(2 * p->n_mblk256, 0);
     for (int mb = 0; mb < p->n_mblk256; ++mb) {
         const int r0 = mb * kPairBM;
         const int r1 = std::min<int>(r0 + kPairBM, p->rows) - 1;
         const int ja = job_of_row(r0), jb = job_of_row(r1);
         p->ext256[2 * mb] = p->roff[ja] / kBK;
         p->ext256[2 * mb + 1] = cdiv(p->roff[jb + 1], kBK);
+        p->grp256[2 * mb] = p->roff[ja] / 16;       // roff is a multiple of 16: exact
+        p->grp256[2 * mb + 1] = p->roff[jb + 1] / 16;
     }
     // per chunk: union of the token segments of the jobs owning its columns
     p->chunk_kb.assign(2 * p->n_chunks, 0);
@@ -850,13 +856,14 @@ std::vector<int> build_tables(mlora_plan* p, const int64_t* seg_offsets, size_t 
     off[4] = append(p->ext256);
     off[5] = append(p->down);
     off[6] = append(grad);
+    off[7] = append(p->grp256);
     return blob;
 }
 
 // Stream-ordered upload: pinned staging + cudaMemcpyAsync, device buffer grown with
 // cudaMallocAsync/cudaFreeAsync.  Kernels already enqueued on `stream` still see the
 // old tables (the copy runs after them); nothing blocks the host.
-mlora_status upload_tables(mlora_plan* p, const std::vector<int>& blob, const size_t off[7], cudaStream_t s) {
+mlora_status upload_tables(mlora_plan* p, const std::vector<int>& blob, const size_t off[8], cudaStream_t s) {
     mlora_ctx* ctx = p->ctx;
     const size_t bytes = blob.size() * sizeof(int);
     if (p->staging_done) MLORA_CUDA_TRY(ctx, cudaEventSynchronize(p->staging_done));  // staging reusable
@@ -884,6 +891,7 @@ mlora_status upload_tables(mlora_plan* p, const std::vector<int>& blob, const si
     p->d_ext256 = base + off[4];
     p->d_down = base + off[5];
     p->d_grad = base + off[6];
+    p->d_grp256 = base + off[7];
     return MLORA_OK;
 }
 
@@ -926,7 +934,7 @@ mlora_status mlora_plan_create(mlora_ctx* ctx, int32_t num_jobs, const int64_t* 
         p->scale[j] = scales ? scales[j] : 1.0f;
     }
     p->R_pad = p->roff[num_jobs];
-    size_t off[7];
+    size_t off[8];
     const std::vector<int> blob = build_tables(p, seg_offsets, off);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     st = upload_tables(p, blob, off, s);
@@ -945,7 +953,7 @@ mlora_status mlora_plan_update(mlora_plan* plan, const int64_t* seg_offsets, voi
     mlora_status st = check_segments(ctx, plan->J, seg_offsets);
     if (st != MLORA_OK) return st;
     DeviceGuard g(ctx->device);
-    size_t off[7];
+    size_t off[8];
     const std::vector<int> blob = build_tables(plan, seg_offsets, off);
     return upload_tables(plan, blob, off, static_cast<cudaStream_t>(stream));
 }

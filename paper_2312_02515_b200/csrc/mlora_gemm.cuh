@@ -50,6 +50,7 @@ struct GemmParams {
     long long ldo;     // output leading dimension (elements)
     long long split_stride;  // elements between split partials (GRAD*)
     const int* ext_tab;   // [n_mblk][2]  extra (LoRA) k-block range per m-block
+    const int* ext_grp;   // BASE (pair): [n_mblk][2] 16-column rank groups [lo, hi) of the m-block's jobs
     const int* down_tab;  // [num_tiles][3] (m_blk, chunk, flags) for MODE_DOWN (flags: down_group_lo/hi)
     const int* grad_tab;  // [nchunks*nsplit][2] token k-block range
     float* row_sq;        // BASE (pair) optional: [n_nblk][M] sum over the tile's columns of bf16(Y)^2
@@ -650,7 +651,12 @@ mlora_base_pair_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_co
             for (int t = cluster_id; t < p.num_tiles; t += nclusters, ++local) {
                 int mb, nb;
                 pair_tile_coords(p, t, mb, nb);
-                const int nk = p.num_kb + (p.ext_tab ? __ldg(p.ext_tab + 2 * mb + 1) - __ldg(p.ext_tab + 2 * mb) : 0);
+                const int xb0 = p.ext_tab ? __ldg(p.ext_tab + 2 * mb) : 0;
+                const int nk = p.num_kb + (p.ext_tab ? __ldg(p.ext_tab + 2 * mb + 1) - xb0 : 0);
+                // LoRA k-blocks: only the UMMA k-steps of the rank groups of the jobs present
+                // (H / G are block-diagonal: the other groups' columns are exact zeros there)
+                const int glo = p.ext_grp ? __ldg(p.ext_grp + 2 * mb) : 0;
+                const int ghi = p.ext_grp ? __ldg(p.ext_grp + 2 * mb + 1) : 0x7fffffff;
                 const int acc = local & 1;
                 const uint32_t use = static_cast<uint32_t>(local >> 1);
                 mbar_wait(tempty_bar + acc, (use & 1u) ^ 1u);
@@ -664,6 +670,10 @@ mlora_base_pair_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_co
                         const uint32_t sB = sA + L::kABytes;
 #pragma unroll
                         for (int j = 0; j < kBK / kUmmaK; ++j) {
+                            if (it >= p.num_kb) {
+                                const int g = (xb0 + it - p.num_kb) * (kBK / kUmmaK) + j;
+                                if (g < glo || g >= ghi) continue;
+                            }
                             const uint64_t ad = sdesc_sw128(sA + j * 32, 16, 1024);
                             const uint64_t bd = B_MN ? sdesc_sw128(sB + j * 2048, 8192, 1024)
                                                      : sdesc_sw128(sB + j * 32, 16, 1024);
