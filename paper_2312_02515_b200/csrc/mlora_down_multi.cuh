@@ -21,11 +21,14 @@
 // 56 KB — what keeps enough x bytes in flight per SM for HBM.
 //
 // As in the grouped kernel (mlora_gemm.cuh, KSPLIT = 2) a CTA pair splits the
-// K range.  Once both mainloops are over, the follower ships its NB fp32
-// partials (only the live 16-column groups) over DSMEM into the leader's then
-// idle stage ring in one go; the leader adds them in a fixed order
-// (deterministic) and applies the per-job select/scale store
-// (down_store_row).  Accumulator columns outside [lo, hi) do not exist; the
+// K range.  Once both mainloops are over the pair splits the epilogue too: CTA r
+// finalises the projections b with b % 2 == r, so each CTA ships its fp32
+// partials of the partner's projections (only the live 16-column groups) over
+// DSMEM into the partner's then idle stage ring in one go, then adds the
+// partner's partials of its own projections (one IEEE addition: deterministic,
+// bitwise equal to the grouped kernel) and applies the per-job select/scale
+// store (down_store_row).  Both CTAs' epilogue warps work, so the exposed
+// epilogue of a tile is about half of a one-sided hand-over.  Accumulator columns outside [lo, hi) do not exist; the
 // epilogue feeds zeros there and the per-row job select (a select, not a
 // multiply) keeps them out of every stored value.  One TMEM buffer: at C2
 // every cluster owns at most one tile, so there is nothing to double-buffer.
@@ -86,9 +89,9 @@ mlora_down_multi_kernel(const __grid_constant__ DownMultiArgs<NB> a) {
     uint64_t* empty_bar = full_bar + kDownMultiMaxStages;
     uint64_t* tfull_bar = empty_bar + kDownMultiMaxStages;
     uint64_t* tempty_bar = tfull_bar + 1;
-    uint64_t* pfull_bar = tempty_bar + 1;   // leader: the follower's partials have landed
-    uint64_t* ready_bar = pfull_bar + 1;    // follower: the leader's ring may take them
-    uint64_t* free_bar = ready_bar + 1;     // leader: partials consumed, ring reusable by TMA
+    uint64_t* pfull_bar = tempty_bar + 1;   // the partner's partials have landed in this CTA's ring
+    uint64_t* ready_bar = pfull_bar + 1;    // the partner's ring may take this CTA's partials
+    uint64_t* free_bar = ready_bar + 1;     // partials consumed, this CTA's ring reusable by TMA
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(free_bar + 1);
 
     const uint32_t warp = warp_id();
@@ -112,9 +115,9 @@ mlora_down_multi_kernel(const __grid_constant__ DownMultiArgs<NB> a) {
         }
         mbar_init(tfull_bar, 1);
         mbar_init(tempty_bar, 128);
-        mbar_init(pfull_bar, 4);  // follower's 4 epilogue warps (remote)
-        mbar_init(ready_bar, 4);  // leader's 4 epilogue warps (remote)
-        mbar_init(free_bar, 4);   // leader's 4 epilogue warps
+        mbar_init(pfull_bar, 4);  // the partner's 4 epilogue warps (remote)
+        mbar_init(ready_bar, 4);  // the partner's 4 epilogue warps (remote)
+        mbar_init(free_bar, 4);   // this CTA's 4 epilogue warps
         fence_barrier_init();
     }
     if (warp == 1) {
@@ -140,8 +143,8 @@ mlora_down_multi_kernel(const __grid_constant__ DownMultiArgs<NB> a) {
                 const int fl = __ldg(p.down_tab + 3 * t + 2);
                 const int glo = down_group_lo(fl), ng = down_group_hi(fl) - glo;
                 const uint32_t tx = L::kABytes + static_cast<uint32_t>(NB * ng * L::kGroupBytes);
-                // the leader's ring held the previous tile's partials until its epilogue read them
-                if (krank == 0 && local > 0) mbar_wait(free_bar, static_cast<uint32_t>(local - 1) & 1u);
+                // the ring held the previous tile's partials until this CTA's epilogue read them
+                if (local > 0) mbar_wait(free_bar, static_cast<uint32_t>(local - 1) & 1u);
                 for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(empty_bar + stage, phase ^ 1u);
                     const uint32_t sA = base_addr + stage * stage_bytes;
@@ -227,56 +230,60 @@ mlora_down_multi_kernel(const __grid_constant__ DownMultiArgs<NB> a) {
                 }
             };
             auto part_at = [&](int b, int g, int f) { return part + ((4 * b + g) * 4 + f) * kBM + rloc; };
-            if (krank == 1) {
-                // ship the live groups of all NB partials into the leader's ring in one go
-                mbar_wait_cluster(ready_bar, par);
-                for (int b = 0; b < NB; ++b) {
-                    float accv[64];
-                    load_acc(b, accv);
+            // Symmetric hand-over: CTA r finalises the projections b with b % 2 == r and ships
+            // its partials of the others into the partner's ring, so both CTAs' epilogue warps
+            // share the work (the partner's ring must be idle first: `ready`).
+            const uint32_t partner = krank ^ 1u;
+            // this CTA's ring: its TMA data were all consumed by the MMAs behind tfull
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(ready_bar), partner));
+            mbar_wait_cluster(ready_bar, par);  // the partner's ring may take this CTA's partials
+            for (int b = 0; b < NB; ++b) {
+                if ((b & 1) == static_cast<int>(krank)) continue;
+                float accv[64];
+                load_acc(b, accv);
 #pragma unroll
-                    for (int g = 0; g < 4; ++g) {
-                        if (g < glo || g >= ghi) continue;
+                for (int g = 0; g < 4; ++g) {
+                    if (g < glo || g >= ghi) continue;
 #pragma unroll
-                        for (int f = 0; f < 4; ++f) {
-                            const float* v = accv + 16 * g + 4 * f;
-                            st_cluster_v4(mapa_shared(smem_u32(part_at(b, g, f)), 0), make_float4(v[0], v[1], v[2], v[3]));
-                        }
+                    for (int f = 0; f < 4; ++f) {
+                        const float* v = accv + 16 * g + 4 * f;
+                        st_cluster_v4(mapa_shared(smem_u32(part_at(b, g, f)), partner), make_float4(v[0], v[1], v[2], v[3]));
                     }
                 }
-                // every lane orders its DSMEM stores at cluster scope before lane 0's release-arrive
-                asm volatile("fence.acq_rel.cluster;" ::: "memory");
-                __syncwarp();
-                if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(pfull_bar), 0));
-            } else {
-                // the ring's TMA data were all consumed by the MMAs behind tfull
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                __syncwarp();
-                if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(ready_bar), 1));
-                mbar_wait_cluster(pfull_bar, par);
-                for (int b = 0; b < NB; ++b) {
-                    float accv[64];
-                    load_acc(b, accv);
-#pragma unroll
-                    for (int g = 0; g < 4; ++g) {
-                        if (g < glo || g >= ghi) continue;
-#pragma unroll
-                        for (int f = 0; f < 4; ++f) {
-                            const float4 q4 = *part_at(b, g, f);
-                            float* v = accv + 16 * g + 4 * f;
-                            v[0] += q4.x;
-                            v[1] += q4.y;
-                            v[2] += q4.z;
-                            v[3] += q4.w;
-                        }
-                    }
-                    if (row_ok)
-                        down_store_row<64>(p, dr, static_cast<__nv_bfloat16*>(a.out[b]), row, n0, accv);
-                }
-                // partial reads complete before the producer's TMA may refill the ring
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                __syncwarp();
-                if (lane == 0) mbar_arrive(free_bar);
             }
+            // every lane orders its DSMEM stores at cluster scope before lane 0's release-arrive
+            asm volatile("fence.acq_rel.cluster;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(mapa_shared(smem_u32(pfull_bar), partner));
+            mbar_wait_cluster(pfull_bar, par);  // the partner's partials of this CTA's projections
+            for (int b = 0; b < NB; ++b) {
+                if ((b & 1) != static_cast<int>(krank)) continue;
+                float accv[64];
+                load_acc(b, accv);
+                // K-half 0 + K-half 1: one IEEE addition, commutative, so the result is the
+                // same bits whichever CTA finalises (bitwise equal to the grouped kernel)
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    if (g < glo || g >= ghi) continue;
+#pragma unroll
+                    for (int f = 0; f < 4; ++f) {
+                        const float4 q4 = *part_at(b, g, f);
+                        float* v = accv + 16 * g + 4 * f;
+                        v[0] += q4.x;
+                        v[1] += q4.y;
+                        v[2] += q4.z;
+                        v[3] += q4.w;
+                    }
+                }
+                if (row_ok)
+                    down_store_row<64>(p, dr, static_cast<__nv_bfloat16*>(a.out[b]), row, n0, accv);
+            }
+            // partial reads complete before this CTA's producer may refill its ring
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(free_bar);
             tc_fence_before();
             mbar_arrive(tempty_bar);
         }
