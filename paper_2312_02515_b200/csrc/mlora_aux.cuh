@@ -358,4 +358,43 @@ rowsq_rows_kernel(const __grid_constant__ RowSqArgs a, float* __restrict__ row_a
 }
 // step 2: segment_loss_kernel (fixed-order per-job block sum of row_acc)
 
+// The layer step's step 2 fused with the non-finite guard: grid (J, ysplit).
+// Every CTA of job j sums the job's row_acc in the same fixed order (8 KB per
+// job at C2: the redundancy is cheaper than a cross-CTA hand-over), CTA y = 0
+// stores loss[j], and when the loss is not finite all ysplit CTAs zero the
+// job's rows of the guarded tensors (as zero_nonfinite_rows_kernel).  One
+// launch instead of two between the forward and the backward.
+__global__ void __launch_bounds__(256) loss_guard_kernel(const float* __restrict__ row_acc,
+                                                          float* __restrict__ loss, const __grid_constant__ GuardArgs a) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    __shared__ float red[8];
+    __shared__ float total;
+    const int j = blockIdx.x;
+    const int r0 = a.seg[j], r1 = a.seg[j + 1];
+    float acc = 0.f;
+    for (int r = r0 + threadIdx.x; r < r1; r += blockDim.x) acc += row_acc[r];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x / 32] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float t = 0.f;
+        for (int w = 0; w < static_cast<int>(blockDim.x / 32); ++w) t += red[w];
+        total = 0.5f * t;
+        if (blockIdx.y == 0) loss[j] = total;
+    }
+    __syncthreads();
+    if (isfinite(total)) return;
+    const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+    for (int t = 0; t < a.ntensors; ++t) {
+        const int n8 = a.cols[t] / 8;
+        const long long cnt = (long long)(r1 - r0) * n8;
+        uint4* base = reinterpret_cast<uint4*>(a.t[t] + (long long)r0 * a.cols[t]);
+        for (long long i = (long long)blockIdx.y * blockDim.x + threadIdx.x; i < cnt;
+             i += (long long)gridDim.y * blockDim.x)
+            base[i] = z;
+    }
+}
+
 }  // namespace mlora

@@ -1269,6 +1269,50 @@ mlora_status mlora_fuse_rows(mlora_ctx* ctx, int32_t num_seqs, const void* const
     return MLORA_OK;
 }
 
+}  // extern "C"
+
+namespace mlora {
+// Internal (layer step): per-job loss from the forward epilogues' row sums fused with
+// the non-finite guard over `tensors` — rowsq_rows_kernel + loss_guard_kernel.
+mlora_status layer_loss_guard(mlora_ctx* ctx, const mlora_plan* plan, const float* const* row_sq, const int32_t* d,
+                              int32_t num_rowsq, float* loss, void* const* tensors, const int32_t* cols,
+                              int32_t num_tensors, cudaStream_t s) {
+    if (num_rowsq < 1 || num_rowsq > kMaxLossTensors) return fail(ctx, MLORA_USAGE, "num_tensors out of range");
+    if (num_tensors < 1 || num_tensors > kMaxGuardTensors) return fail(ctx, MLORA_USAGE, "too many guarded tensors");
+    RowSqArgs ra{};
+    for (int t = 0; t < num_rowsq; ++t) {
+        if (!row_sq[t] || d[t] <= 0) return fail(ctx, MLORA_USAGE, "bad row-sum tensor");
+        ra.part[t] = row_sq[t];
+        ra.nblk[t] = cdiv(d[t], kPairBN);
+    }
+    ra.ntensors = num_rowsq;
+    ra.rows = plan->rows;
+    GuardArgs ga{};
+    for (int t = 0; t < num_tensors; ++t) {
+        if (!tensors[t] || cols[t] <= 0 || cols[t] % 8 != 0 || reinterpret_cast<uintptr_t>(tensors[t]) % 16 != 0)
+            return fail(ctx, MLORA_SHAPE, "guarded tensors need 16-byte aligned rows of a multiple of 8 columns");
+        ga.t[t] = static_cast<__nv_bfloat16*>(tensors[t]);
+        ga.cols[t] = cols[t];
+    }
+    ga.ntensors = num_tensors;
+    ga.seg = plan->d_seg;
+    ga.loss = loss;
+    DeviceGuard g(ctx->device);
+    mlora_status st = ensure_workspace(ctx, sizeof(float) * plan->rows);
+    if (st != MLORA_OK) return st;
+    float* row_acc = static_cast<float*>(ctx->workspace);
+    ProfScope ps(ctx, 4, s);
+    MLORA_CUDA_TRY(ctx, launch_k(rowsq_rows_kernel, dim3(cdiv(plan->rows, 32)), dim3(32, kRowSqSlices), 0, s, 1, ra,
+                                 row_acc));
+    MLORA_CUDA_TRY(ctx, launch_k(loss_guard_kernel, dim3(plan->J, 16), dim3(256), 0, s, 1,
+                                 static_cast<const float*>(row_acc), loss, ga));
+    ctx->launches += 2;
+    return MLORA_OK;
+}
+}  // namespace mlora
+
+extern "C" {
+
 mlora_status mlora_zero_nonfinite_rows(mlora_ctx* ctx, const mlora_plan* plan, const float* loss,
                                        void* const* tensors, const int32_t* cols, int32_t num_tensors,
                                        void* stream) {

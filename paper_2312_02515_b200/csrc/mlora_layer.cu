@@ -74,6 +74,12 @@ struct mlora_layer {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
 };
 
+namespace mlora {
+mlora_status layer_loss_guard(mlora_ctx* ctx, const mlora_plan* plan, const float* const* row_sq, const int32_t* d,
+                              int32_t num_rowsq, float* loss, void* const* tensors, const int32_t* cols,
+                              int32_t num_tensors, cudaStream_t s);  // mlora_capi.cu
+}
+
 namespace {
 
 mlora_status forward_backward(mlora_layer* L, void* x, float* loss, cudaStream_t s) {
@@ -131,8 +137,9 @@ mlora_status forward_backward(mlora_layer* L, void* x, float* loss, cudaStream_t
         dd[i] = L->proj[i].d;
         kk[i] = L->proj[i].k;
     }
-    if ((st = mlora_loss_from_rowsq(ctx, plan, rsq.data(), dd.data(), n, loss, s)) != MLORA_OK) return st;
-    // ---- non-finite guard over every tensor the backward reads (deduplicated)
+    // ---- non-finite guard over every tensor the backward reads (deduplicated), fused
+    // with the per-job loss reduction: a job whose loss is not finite has its rows of
+    // these tensors zeroed before any backward kernel reads them
     std::vector<void*> gt;
     std::vector<int32_t> gc;
     auto guard = [&](const void* t, int cols) {
@@ -145,7 +152,11 @@ mlora_status forward_backward(mlora_layer* L, void* x, float* loss, cudaStream_t
         guard(L->proj[i].H, R);
         guard(in[i], L->proj[i].k);
     }
-    for (size_t t0 = 0; t0 < gt.size(); t0 += 32) {
+    const int nt0 = static_cast<int>(std::min<size_t>(32, gt.size()));
+    if ((st = mlora::layer_loss_guard(ctx, plan, rsq.data(), dd.data(), n, loss, gt.data(), gc.data(), nt0, s)) !=
+        MLORA_OK)
+        return st;
+    for (size_t t0 = 32; t0 < gt.size(); t0 += 32) {
         const int nt = static_cast<int>(std::min<size_t>(32, gt.size() - t0));
         if ((st = mlora_zero_nonfinite_rows(ctx, plan, loss, gt.data() + t0, gc.data() + t0, nt, s)) != MLORA_OK)
             return st;
