@@ -100,6 +100,8 @@ def main():
         ("shared-input down (5 projections)", down_multi, None, rows * 4096 * 2),
         ("dA + dB groups (+ reduce)", grads, None, sum(rows * (p.d + p.k) * 2 for p in projs)),
     ]
+    if os.environ.get("ENERGY_AB"):  # interleaved A/B of the forward and dX GEMM on one shape
+        cases = [c for c in cases if c[0] in ("base fwd 4096x4096 (q)", "base dX 4096x4096 (q)")] * 4
     for name, fn, flops, byts in cases:
         for _ in range(3):
             fn()
