@@ -14,6 +14,7 @@
 #include <string>
 
 #include "../../include/mlora.h"
+#include "sm100.cuh"
 
 namespace {
 
@@ -181,6 +182,179 @@ __global__ void __launch_bounds__(256) ce_rows_kernel(const __nv_bfloat16* __res
     }
 }
 
+// Row pass on a cluster of kCeCl CTAs (V % 8 == 0, 32 <= V <= kCeClusterMaxV): CTA r of
+// the cluster owns a quarter of every row it visits.  The quarter row (32.5 KB at
+// V = 65024) arrives in shared memory by ONE bulk TMA copy, double-buffered (the next
+// row's copy is in flight while this one is reduced), so the row is read from HBM once
+// and re-read from shared memory, never from L2.  Three clusters' CTAs share an SM, so
+// one CTA's reductions overlap another's loads (the grid is as many clusters as are
+// co-resident: a second wave would double the time).  Each CTA reduces its quarter to
+// (max, sum 2^((x - max) log2 e)); the partials go to every CTA of the cluster by
+// st.async into their shared memory, completing on their mbarrier (no per-row cluster
+// barrier, whose release would wait for the previous row's dlogits stores to drain),
+// and are merged in rank order (all CTAs compute the same lse: deterministic).  The
+// dlogits pass re-reads the quarter from shared memory.  C4 (12 288 rows x V = 65 024):
+// 1.07 ms -> 0.78 ms, DRAM 3.57 -> 3.15 GB.  Pad rows (mask 0)
+// are never loaded: their dlogits are written as zeros.  DRAM: 2V read (real rows)
+// + 2V written per row.
+constexpr int kCeCl = 4;
+constexpr int kCeThreads = 256;
+constexpr int kCeClusterMaxV = 74 * 1024;
+constexpr float kLog2e = 1.4426950408889634f;
+__host__ __device__ __forceinline__ int ce_part(int V) { return (V / (8 * kCeCl)) * 8; }  // ranks 0..CL-2
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__global__ void __cluster_dims__(kCeCl, 1, 1) __launch_bounds__(kCeThreads, 3)
+ce_rows_cluster_kernel(const __nv_bfloat16* __restrict__ logits, int V, const int* __restrict__ labels,
+                       const uint8_t* __restrict__ mask, const int* __restrict__ seg, int J,
+                       const float* __restrict__ inv_count, long long rows, float* __restrict__ row_loss,
+                       __nv_bfloat16* __restrict__ dlogits) {
+    using namespace mlora::sm100;
+    extern __shared__ __align__(128) uint8_t ce_smem[];
+    __shared__ float red[kCeThreads / 32];
+    __shared__ float2 xch[2][kCeCl];   // every rank's (max, sum) of the row, by iteration parity
+    __shared__ float lse_s;
+    __shared__ __align__(8) uint64_t full[2];
+    __shared__ __align__(8) uint64_t xbar[2];  // the other ranks' partials of the row have landed
+    const uint32_t rank = cluster_ctarank();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int part = ce_part(V);
+    const int off = static_cast<int>(rank) * part;
+    const int n = rank + 1 == kCeCl ? V - (kCeCl - 1) * part : part;   // this CTA's columns [off, off + n)
+    const int slot_bytes = ((((V - (kCeCl - 1) * part) > part ? V - (kCeCl - 1) * part : part) * 2 + 127) / 128) * 128;
+    const long long cl = blockIdx.x / kCeCl, ncl = gridDim.x / kCeCl;
+    if (threadIdx.x == 0) {
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+        mbar_init(&xbar[0], 1);
+        mbar_init(&xbar[1], 1);
+        fence_barrier_init();
+    }
+    cluster_sync();  // barriers initialised, every CTA of the cluster running (DSMEM targets exist)
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const uint64_t read_once = l2_policy_first(), stream_out = l2_policy_first();
+    auto is_real = [&](long long row) { return mask == nullptr || mask[row] != 0; };
+    auto issue = [&](int it, long long row) {
+        if (threadIdx.x == 0 && is_real(row)) {
+            mbar_arrive_expect_tx(&full[it & 1], static_cast<uint32_t>(2 * n));
+            bulk_load_hint(smem_u32(ce_smem + (it & 1) * slot_bytes), logits + row * V + off,
+                           static_cast<uint32_t>(2 * n), &full[it & 1], read_once);
+        }
+    };
+    if (cl < rows) issue(0, cl);
+    int it = 0;
+    uint32_t phase[2] = {0u, 0u};  // completed loads / exchanges per slot (pad rows do neither)
+    for (long long row = cl; row < rows; row += ncl, ++it) {
+        if (row + ncl < rows) issue(it + 1, row + ncl);  // its slot was released by iteration it - 1
+        const bool real = is_real(row);
+        const uint4* buf = reinterpret_cast<const uint4*>(ce_smem + (it & 1) * slot_bytes);
+        if (real) {
+            mbar_wait(&full[it & 1], phase[it & 1] & 1u);
+            // the quarter row is in shared memory: a packed-bf16 max pass, then one exp2
+            // per element against that max (no online rescaling)
+            __nv_bfloat162 mx2 = __float2bfloat162_rn(-INFINITY);
+            for (int i = threadIdx.x; i < n / 8; i += kCeThreads) {
+                const uint4 u = buf[i];
+                const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+                mx2 = __hmax2(mx2, __hmax2(__hmax2(h[0], h[1]), __hmax2(h[2], h[3])));
+            }
+            float m = fmaxf(__low2float(mx2), __high2float(mx2));
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+            if (lane == 0) red[w] = m;
+            __syncthreads();
+            m = red[0];
+#pragma unroll
+            for (int k = 1; k < kCeThreads / 32; ++k) m = fmaxf(m, red[k]);
+            const float mb = m * kLog2e;
+            float sum = 0.f;
+            for (int i = threadIdx.x; i < n / 8; i += kCeThreads) {
+                const uint4 u = buf[i];
+                const uint32_t* q = &u.x;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    sum += ex2_approx(fmaf(__uint_as_float(q[e] << 16), kLog2e, -mb));
+                    sum += ex2_approx(fmaf(__uint_as_float(q[e] & 0xffff0000u), kLog2e, -mb));
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+            __syncthreads();  // every thread has read red[] (the max) before it is reused
+            if (lane == 0) red[w] = sum;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                sum = red[0];
+                for (int k = 1; k < kCeThreads / 32; ++k) sum += red[k];
+                // this rank's partial to every other rank (st.async + their xbar), own slot locally
+                mbar_arrive_expect_tx(&xbar[it & 1], 8u * (kCeCl - 1));
+#pragma unroll
+                for (int r = 0; r < kCeCl; ++r)
+                    if (r != static_cast<int>(rank))
+                        st_async_v2(mapa_shared(smem_u32(&xch[it & 1][rank]), r), m, sum,
+                                    mapa_shared(smem_u32(&xbar[it & 1]), r));
+                xch[it & 1][rank] = make_float2(m, sum);
+                mbar_wait_cluster(&xbar[it & 1], phase[it & 1] & 1u);
+                float mm = xch[it & 1][0].x, ss = xch[it & 1][0].y;  // fixed order: rank 0, 1, ...
+#pragma unroll
+                for (int r = 1; r < kCeCl; ++r) ms_merge(mm, ss, xch[it & 1][r].x, xch[it & 1][r].y);
+                lse_s = mm + __logf(ss);
+            }
+            ++phase[it & 1];
+        }
+        __syncthreads();
+        const float lse = lse_s;
+        const int label = labels[row];
+        if (threadIdx.x == 0) {
+            if (!real) {
+                if (rank == 0) row_loss[row] = 0.f;
+            } else if (label >= off && label < off + n) {
+                row_loss[row] = lse - __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(buf)[label - off]);
+            }
+        }
+        if (dlogits) {
+            int j = 0;
+            for (int t = 1; t < J; ++t)
+                if (seg[t] <= row) j = t;
+            const float sc = real ? inv_count[j] : 0.f;
+            const float lb = lse * kLog2e;
+            const int li = label - off;  // the label's column in this part (may be outside)
+            uint4* d4 = reinterpret_cast<uint4*>(dlogits + row * V + off);
+            for (int i = threadIdx.x; i < n / 8; i += kCeThreads) {
+                uint4 o = make_uint4(0u, 0u, 0u, 0u);
+                if (real) {
+                    const uint4 u = buf[i];
+                    const uint32_t* q = &u.x;
+                    uint32_t* ow = &o.x;
+                    float g[8];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        g[2 * e] = sc * ex2_approx(fmaf(__uint_as_float(q[e] << 16), kLog2e, -lb));
+                        g[2 * e + 1] = sc * ex2_approx(fmaf(__uint_as_float(q[e] & 0xffff0000u), kLog2e, -lb));
+                    }
+                    if (li >= 8 * i && li < 8 * i + 8) {  // the one-hot term, once per row
+#pragma unroll
+                        for (int e = 0; e < 8; ++e)
+                            if (8 * i + e == li) g[e] -= sc;
+                    }
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const __nv_bfloat162 r = __floats2bfloat162_rn(g[2 * e], g[2 * e + 1]);
+                        ow[e] = *reinterpret_cast<const uint32_t*>(&r);
+                    }
+                }
+                st_hint(d4 + i, o, stream_out);
+            }
+        }
+        __syncthreads();  // this slot's reads and lse_s are done before their reuse
+    }
+    cluster_sync();  // no DSMEM write may target an exited CTA
+}
+
 // loss[j] = (sum of row_loss over job j's rows) * inv_count[j]: fixed order.
 __global__ void ce_loss_kernel(const float* __restrict__ row_loss, const int* __restrict__ seg,
                                const float* __restrict__ inv_count, float* __restrict__ loss) {
@@ -311,12 +485,47 @@ mlora_status mlora_masked_ce(int32_t num_jobs, const int32_t* seg_dev, int64_t r
     const int* seg = static_cast<const int*>(seg_dev);
     if (launch(ce_count_kernel, dim3(num_jobs), dim3(1024), 0, stream, mask, seg, inv_count) != cudaSuccess)
         return MLORA_CUDA;
-    const unsigned grid = static_cast<unsigned>(std::min<long long>(rows, 4LL * sms));
-    if (launch(ce_rows_kernel, dim3(grid), dim3(256), 0, stream, static_cast<const __nv_bfloat16*>(logits),
-               static_cast<int>(V), labels, mask, seg, static_cast<int>(num_jobs),
-               static_cast<const float*>(inv_count), static_cast<long long>(rows), row_loss,
-               static_cast<__nv_bfloat16*>(dlogits)) != cudaSuccess)
-        return MLORA_CUDA;
+    if (V % 8 == 0 && V >= 8 * kCeCl && V <= kCeClusterMaxV) {
+        // cluster row pass: each quarter row by one bulk copy into shared memory
+        const int part = ce_part(V);
+        const size_t slot = ((static_cast<size_t>(std::max(part, V - (kCeCl - 1) * part)) * 2 + 127) / 128) * 128;
+        const size_t smem = 2 * slot;
+        if (cudaFuncSetAttribute(ce_rows_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)) != cudaSuccess)
+            return MLORA_CUDA;
+        // as many clusters as can be co-resident (a persistent grid: a second wave would
+        // double the time), from the occupancy calculator, not from smem arithmetic
+        int max_clusters = 0;
+        {
+            cudaLaunchConfig_t oc{};
+            oc.gridDim = dim3(kCeCl * 1024);
+            oc.blockDim = dim3(kCeThreads);
+            oc.dynamicSmemBytes = smem;
+            cudaLaunchAttribute ca;
+            ca.id = cudaLaunchAttributeClusterDimension;
+            ca.val.clusterDim.x = kCeCl;
+            ca.val.clusterDim.y = 1;
+            ca.val.clusterDim.z = 1;
+            oc.attrs = &ca;
+            oc.numAttrs = 1;
+            if (cudaOccupancyMaxActiveClusters(&max_clusters, ce_rows_cluster_kernel, &oc) != cudaSuccess ||
+                max_clusters < 1)
+                max_clusters = sms / kCeCl;
+        }
+        const unsigned clusters = static_cast<unsigned>(std::min<long long>(rows, max_clusters));
+        if (launch(ce_rows_cluster_kernel, dim3(kCeCl * clusters), dim3(kCeThreads), smem, stream,
+                   static_cast<const __nv_bfloat16*>(logits), static_cast<int>(V), labels, mask, seg,
+                   static_cast<int>(num_jobs), static_cast<const float*>(inv_count), static_cast<long long>(rows),
+                   row_loss, static_cast<__nv_bfloat16*>(dlogits)) != cudaSuccess)
+            return MLORA_CUDA;
+    } else {
+        const unsigned grid = static_cast<unsigned>(std::min<long long>(rows, 4LL * sms));
+        if (launch(ce_rows_kernel, dim3(grid), dim3(256), 0, stream, static_cast<const __nv_bfloat16*>(logits),
+                   static_cast<int>(V), labels, mask, seg, static_cast<int>(num_jobs),
+                   static_cast<const float*>(inv_count), static_cast<long long>(rows), row_loss,
+                   static_cast<__nv_bfloat16*>(dlogits)) != cudaSuccess)
+            return MLORA_CUDA;
+    }
     if (launch(ce_loss_kernel, dim3(num_jobs), dim3(1024), 0, stream, static_cast<const float*>(row_loss), seg,
                static_cast<const float*>(inv_count), loss) != cudaSuccess)
         return MLORA_CUDA;

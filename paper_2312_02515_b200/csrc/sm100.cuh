@@ -228,6 +228,26 @@ __device__ __forceinline__ void tma_load_2d_2sm(uint32_t smem_dst, const CUtenso
         "l"(reinterpret_cast<uint64_t>(map)), "r"(leader_bar), "r"(c0), "r"(c1)
         : "memory");
 }
+// Asynchronous 8-byte store into another CTA's shared memory of the cluster whose
+// completion is signalled on that CTA's mbarrier (complete_tx of 8 bytes): a DSMEM
+// hand-over without a release fence, so it does not wait for this thread's earlier
+// global stores to drain.
+__device__ __forceinline__ void st_async_v2(uint32_t cluster_addr, float a, float b, uint32_t remote_bar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(
+                     cluster_addr),
+                 "f"(a), "f"(b), "r"(remote_bar)
+                 : "memory");
+}
+// Contiguous bulk copy global -> this CTA's shared memory (non-tensor TMA), completion
+// counted on `bar` (complete_tx), with an L2 cache-policy hint.  bytes % 16 == 0.
+__device__ __forceinline__ void bulk_load_hint(uint32_t smem_dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                               uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_dst),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
 // TMA store of a 2-D box from shared memory (bulk-group completion): elements
 // outside the tensor's bounds are not written.
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t smem_src, int c0, int c1) {

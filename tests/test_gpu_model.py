@@ -104,3 +104,9 @@ def test_rope_roundtrip_and_reference():
     rel = lambda p, q: np.linalg.norm(p - q) / np.linalg.norm(q)
     assert rel(bf16_np(y), Y) < 1e-2
     assert rel(bf16_np(back), X) < 1e-2  # rotation is orthogonal: backward = inverse rotation
+
+
+def test_masked_ce_many_rows_per_cta_pair():
+    """Several rows per CTA pair of the bulk-copy row pass (double-buffered half rows,
+    pad rows interleaved so the two slots' load counts drift apart) and an empty job."""
+    _check_masked_ce(4096, [0, 700, 700, 1500, 2000], seed=11)
