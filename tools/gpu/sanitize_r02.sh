@@ -9,3 +9,8 @@ for tool in memcheck racecheck synccheck; do
 done
 timeout 1500 compute-sanitizer --tool memcheck --print-limit 10 python -m pytest tests/test_gpu_parity.py -x -q -k "forward_backward_parity or layer_step or fuzz" > gpurun_out/san_r02_parity.log 2>&1
 echo "parity memcheck rc=$? $(grep -E 'ERROR SUMMARY|passed|failed' gpurun_out/san_r02_parity.log | tr '\n' ' ')" >> gpurun_out/san_r02_summary.log
+# the cluster masked-CE row pass (bulk copies, st.async partial exchange)
+for tool in memcheck racecheck synccheck; do
+  timeout 900 compute-sanitizer --tool $tool --print-limit 10 python -m pytest tests/test_gpu_model.py -x -q -k masked_ce > gpurun_out/san_r02_ce_$tool.log 2>&1
+  echo "masked_ce $tool rc=$? $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY|passed|failed' gpurun_out/san_r02_ce_$tool.log | tr '\n' ' ')" >> gpurun_out/san_r02_summary.log
+done
