@@ -326,8 +326,9 @@ struct RowSqArgs {
 // x = one of 32 consecutive rows (128-byte coalesced loads), y = a fixed slice
 // of the (tensor, column-block) list; the slices are combined in a fixed order
 // (deterministic).  One thread per row summing all ~170 partials serially left
-// the launch latency-bound (22 us at C2 for 5.4 MB).
-constexpr int kRowSqSlices = 8;
+// the launch latency-bound (22 us at C2 for 5.4 MB); 8 slices: 12.1 us; 32 slices
+// (~5 loads per thread, one round of memory latency): 8.6 us.
+constexpr int kRowSqSlices = 32;
 __global__ void __launch_bounds__(32 * kRowSqSlices)
 rowsq_rows_kernel(const __grid_constant__ RowSqArgs a, float* __restrict__ row_acc) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
