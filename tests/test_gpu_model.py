@@ -49,9 +49,10 @@ def test_masked_ce_per_job_mean_and_grad_c4_vocab():
     _check_masked_ce(65024, [0, 40, 40, 100, 128])
 
 
-@pytest.mark.parametrize("V", [8, 1000, 32000, 1001, 70000])
+@pytest.mark.parametrize("V", [8, 32, 40, 1000, 32000, 1001, 70000, 75776])
 def test_masked_ce_vocab_sizes(V):
-    """Vector row pass (V % 8 == 0: 8, 1000, LLaMA's 32000, 70000) and the scalar
+    """Cluster row pass (V % 8 == 0, 32 <= V <= 74 K: 32, 40, 1000, LLaMA's 32000, 70000),
+    the one-row-per-CTA vector pass (8, 75776 > 74 K) and the scalar
     path (1001: V % 8 != 0)."""
     _check_masked_ce(V, [0, 17, 17, 50, 64], seed=V)
 
