@@ -389,9 +389,10 @@ mlora_status mlora_attn_bwd(const mlora_attn_desc* desc, const void* q, int64_t 
  *     its rank-r down-projection in one grouped launch (projections sharing an
  *     input go through the shared-input kernel), then its base GEMM
  *     Y = X W0^T + H B_cat^T with the fused per-row sum of bf16(Y)^2;
- *   loss[j] = 1/2 sum_p ||Y_p[rows of j]||^2 (so dL/dY_p = Y_p, input detached);
- *   the non-finite guard (mlora_zero_nonfinite_rows over every tensor the
- *     backward reads: each Y, H and input — a diverged job's rows, x included);
+ *   loss[j] = 1/2 sum_p ||Y_p[rows of j]||^2 (so dL/dY_p = Y_p, input detached)
+ *     fused with the non-finite guard (as mlora_zero_nonfinite_rows, over every
+ *     tensor the backward reads: each Y, H and input — a diverged job's rows, x
+ *     included): one row-sum launch + one loss / guard launch;
  *   backward: G = s dY B_cat for every projection (one grouped launch), dX per
  *     projection (reverse order), dA / dB for every projection (grouped);
  *   and, in mlora_layer_step, one AdamW over all 2n adapter tensors (per-job lr,
