@@ -17,8 +17,7 @@
 // 16-row groups), so a k-step is ONE UMMA 128 x 16 NB (hi - lo) while that is
 // <= 256 (C2: N = 80), and its accumulators are adjacent in TMEM.  The stage
 // size follows the plan's widest tile (host: `stage_bytes`, `stages`), so a
-// narrow plan gets a deeper ring: C2 runs 8 stages of 26 KB instead of 4 of
-// 56 KB — what keeps enough x bytes in flight per SM for HBM.
+// narrow plan gets a deeper ring (C2: 8 stages of 26 KB instead of 4 of 56 KB).
 //
 // As in the grouped kernel (mlora_gemm.cuh, KSPLIT = 2) a CTA pair splits the
 // K range.  Once both mainloops are over the pair splits the epilogue too: CTA r
@@ -28,10 +27,11 @@
 // partner's partials of its own projections (one IEEE addition: deterministic,
 // bitwise equal to the grouped kernel) and applies the per-job select/scale
 // store (down_store_row).  Both CTAs' epilogue warps work, so the exposed
-// epilogue of a tile is about half of a one-sided hand-over.  Accumulator columns outside [lo, hi) do not exist; the
-// epilogue feeds zeros there and the per-row job select (a select, not a
-// multiply) keeps them out of every stored value.  One TMEM buffer: at C2
-// every cluster owns at most one tile, so there is nothing to double-buffer.
+// epilogue of a tile is about half of a one-sided hand-over.  Accumulator
+// columns outside [lo, hi) do not exist; the epilogue feeds zeros there and the
+// per-row job select (a select, not a multiply) keeps them out of every stored
+// value.  One TMEM buffer: at C2 every cluster owns at most one tile, so there
+// is nothing to double-buffer.
 #pragma once
 
 #include "mlora_gemm.cuh"
@@ -56,8 +56,8 @@ struct DownMultiSmem {
     static constexpr int kABytes = kBM * kBK * 2;
     static constexpr int kGroupBytes = 16 * kBK * 2;  // one 16-row rank group (two 1 KB swizzle atoms)
     static constexpr int kRingBytes = 225 * 1024;     // stage ring (runtime stage size and depth)
-    // The follower's partials land in the leader's ring once its mainloop is
-    // over: projection b's 16-column group g at (4 b + g) * kPartGroupBytes.
+    // The partner's partials land in this CTA's ring once its mainloop is over:
+    // projection b's 16-column group g at (4 b + g) * kPartGroupBytes.
     static constexpr int kPartGroupBytes = kBM * 16 * 4;
     static_assert(kDownMultiMax * 4 * kPartGroupBytes <= kRingBytes, "ring too small for the partials");
     static constexpr int kBarOffset = kRingBytes;
