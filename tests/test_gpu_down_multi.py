@@ -71,3 +71,55 @@ def test_shared_input_down_matches_grouped_bitwise(nb, seg, ranks, k):
         assert np.array_equal(got == 0, want == 0) or np.all(got[want == 0] == 0)  # block-diagonal zeros exact
         err = np.linalg.norm(got - want) / max(np.linalg.norm(want), 1e-30)
         assert err < 1e-2, (p, err)
+
+
+def test_shared_input_down_random_layouts_bitwise():
+    """24 random layouts (1-10 jobs, ranks 1-64, empty / 1-row / straddling segments, K
+    tails, NB 2-5): the rank-group narrowing of both the shared-input and the grouped
+    kernel must agree bitwise and be exactly zero off the block diagonal."""
+    from paper_2312_02515_b200 import _native as N
+    from paper_2312_02515_b200 import fused as F
+
+    dev = torch.device("cuda", 0)
+    ctx = F.Context(dev)
+    rng = np.random.default_rng(2024)
+    for case in range(24):
+        J = int(rng.integers(1, 11))
+        ranks = [int(rng.integers(1, 65)) for _ in range(J)]
+        lens = [int(rng.choice([0, 1, int(rng.integers(2, 400))])) for _ in range(J)]
+        if sum(lens) == 0:
+            lens[0] = 37
+        seg = [0]
+        for n in lens:
+            seg.append(seg[-1] + n)
+        k = int(rng.choice([64, 200, 1000]))
+        nb = int(rng.integers(2, 6))
+        scales = [float(rng.uniform(0.25, 2.0)) for _ in range(J)]
+        plan = F.Plan(ctx, seg, ranks, scales)
+        R = plan.rank_padded
+        g = torch.Generator().manual_seed(case)
+        M = seg[-1]
+        X = (torch.rand(M, k, generator=g) * 2 - 1).to(torch.bfloat16).to(dev)
+        A16s = []
+        for _ in range(nb):
+            A = [((torch.rand(r, k, generator=g) * 2 - 1) / k ** 0.5) for r in ranks]
+            B = [torch.zeros(64, r) for r in ranks]
+            _, _, A16, _ = F.pack_adapters(ctx, plan, 64, k, [a.to(dev) for a in A], [b.to(dev) for b in B])
+            A16s.append(A16)
+        multi = _down(F, N, ctx, plan, X, A16s, R, shared=True)
+        single = _down(F, N, ctx, plan, X, A16s, R, shared=False)
+        ro = plan.rank_offsets
+        for p in range(nb):
+            assert torch.equal(multi[p], single[p]), (case, p, seg, ranks)
+            mask = torch.zeros(M, R, dtype=torch.bool)
+            for j in range(J):
+                mask[seg[j]:seg[j + 1], ro[j]:ro[j] + ranks[j]] = True
+            assert torch.all(multi[p].cpu()[~mask] == 0), (case, p)
+            Xd = X.double().cpu().numpy()
+            want = np.zeros((M, R))
+            for j, r in enumerate(ranks):
+                a16 = A16s[p][ro[j]:ro[j] + r].double().cpu().numpy()
+                want[seg[j]:seg[j + 1], ro[j]:ro[j] + r] = scales[j] * Xd[seg[j]:seg[j + 1]] @ a16.T
+            got = multi[p].double().cpu().numpy()
+            err = np.linalg.norm(got - want) / max(np.linalg.norm(want), 1e-30)
+            assert err < 1e-2, (case, p, err)
