@@ -132,8 +132,8 @@ struct AdamArgs {
     int roff[kMaxJobs + 1];
     int J;
     float lr[kMaxJobs];
-    float bc1[kMaxJobs];   // 1 - beta1^t_j
-    float bc2[kMaxJobs];   // 1 - beta2^t_j
+    float bc1[kMaxJobs];   // 1 / (1 - beta1^t_j); 0: job absent this step
+    float bc2[kMaxJobs];   // 1 / (1 - beta2^t_j)
     float beta1, beta2, eps, wd;
     const float* loss_gate;  // device [J] or NULL: a job whose loss is not finite is skipped
 };
@@ -148,12 +148,14 @@ __global__ void adam_kernel(const __grid_constant__ AdamArgs a) {
         int gi = 0;
         while (gi + 1 < a.ngroups && a.grp[gi + 1].start4 <= i4) ++gi;
         const AdamGroupDev& G = a.grp[gi];
-        const long long e = (i4 - G.start4) * 4;  // element index within group
-        const long long row = e / G.cols;
-        const long long col = e % G.cols;
-        const int j = job_of_col(a.roff, a.J, static_cast<int>(G.layout == 0 ? row : col));
-        const float lr = a.lr[j], bc1 = a.bc1[j], bc2 = a.bc2[j];
-        if (bc1 == 0.f) continue;  // step 0: job not in this fused batch -> p, m, v untouched
+        // element index within the group (< 2^31): 32-bit index arithmetic
+        const int e = static_cast<int>(i4 - G.start4) * 4;
+        const int cols = static_cast<int>(G.cols);
+        const int row = e / cols;
+        const int col = e - row * cols;
+        const int j = job_of_col(a.roff, a.J, G.layout == 0 ? row : col);
+        const float lr = a.lr[j], ibc1 = a.bc1[j], ibc2 = a.bc2[j];
+        if (ibc1 == 0.f) continue;  // step 0: job not in this fused batch -> p, m, v untouched
         if (a.loss_gate && !isfinite(__ldg(a.loss_gate + j))) continue;  // skip-on-overflow (diverged job)
         float4 p = reinterpret_cast<float4*>(G.p)[e / 4];
         const float4 g = reinterpret_cast<const float4*>(G.g)[e / 4];
@@ -164,8 +166,8 @@ __global__ void adam_kernel(const __grid_constant__ AdamArgs a) {
         for (int u = 0; u < 4; ++u) {
             mm[u] = a.beta1 * mm[u] + (1.f - a.beta1) * gg[u];
             vv[u] = a.beta2 * vv[u] + (1.f - a.beta2) * gg[u] * gg[u];
-            const float mh = mm[u] / bc1;
-            const float vh = vv[u] / bc2;
+            const float mh = mm[u] * ibc1;  // bias corrections as reciprocals (host, per job)
+            const float vh = vv[u] * ibc2;
             pp[u] -= lr * (mh / (sqrtf(vh) + a.eps) + a.wd * pp[u]);
         }
         reinterpret_cast<float4*>(G.p)[e / 4] = p;

@@ -1174,8 +1174,9 @@ mlora_status mlora_adam_step_ex(mlora_ctx* ctx, const mlora_plan* plan, const ml
         if (step[j] < 0) return fail(ctx, MLORA_USAGE, "Adam step must be >= 0 (0 = job inactive this step)");
         if (!std::isfinite(lr[j])) return fail(ctx, MLORA_NUMERIC, "non-finite learning rate");
         a.lr[j] = lr[j];
-        a.bc1[j] = static_cast<float>(1.0 - std::pow(static_cast<double>(beta1), step[j]));
-        a.bc2[j] = static_cast<float>(1.0 - std::pow(static_cast<double>(beta2), step[j]));
+        // reciprocal bias corrections (0 marks a job absent from this step)
+        a.bc1[j] = step[j] == 0 ? 0.f : static_cast<float>(1.0 / (1.0 - std::pow(static_cast<double>(beta1), step[j])));
+        a.bc2[j] = step[j] == 0 ? 0.f : static_cast<float>(1.0 / (1.0 - std::pow(static_cast<double>(beta2), step[j])));
     }
     a.beta1 = beta1;
     a.beta2 = beta2;
