@@ -4,9 +4,10 @@ bench.py times FusedLoraLayer.step at C2: the seven LLaMA-7B projections of a
 layer over 8192 fused rows (4 jobs x r16, s = 2, four learning rates), i.e. the
 shared-input down-projection over x (q, k, v, gate, up: mlora_down_multi_kernel
 with NB = 5), the grouped o / down down-projection, seven forward base GEMMs
-with the fused row-sum loss, the non-finite guard, the 7-problem G group, seven
-dX GEMMs, the grouped dA / dB reductions (dA token-split, then the fixed-order
-split reduce) and one AdamW.  These tests run exactly that step once and check
+with the fused row-sum loss, the per-job loss fused with the non-finite guard,
+the 7-problem G group, seven dX GEMMs, the grouped dA / dB reductions (balanced
+persistent grids; a token split + fixed-order reduce only when a group has fewer
+tiles than SMs, as in the TINY edge case below) and one AdamW.  These tests run exactly that step once and check
 every output it produces:
 
   * Y and dX of every projection on sampled rows, against the fp64 oracle
@@ -191,3 +192,12 @@ def test_c3_llama13b_minpad_step_end_to_end():
         seg.append(r)
     layer, _ = run_step_and_check(LLAMA13B, ranks, [2.0] * 8, [1e-4, 2e-4, 5e-5, 3e-4] * 2, seg, seed=2000)
     assert layer.plan.rank_padded == 256
+
+
+def test_tiny_step_edge_layout():
+    """TINY shapes with a 1-row job, an empty job and a 129-row job: few tiles, so the
+    dA / dB groups take the token split and the fixed-order reduce; the empty job's
+    adapters must come out bitwise untouched."""
+    from paper_2312_02515_b200.layer import TINY
+    run_step_and_check(TINY, [8, 16, 4], [2.0, 1.0, 0.5], [1e-3, 2e-3, 5e-4], [0, 1, 1, 130], seed=77)
+
