@@ -195,9 +195,9 @@ def test_c3_llama13b_minpad_step_end_to_end():
 
 
 def test_tiny_step_edge_layout():
-    """TINY shapes with a 1-row job, an empty job and a 129-row job: few tiles, so the
-    dA / dB groups take the token split and the fixed-order reduce; the empty job's
-    adapters must come out bitwise untouched."""
+    """TINY shapes with a 1-row job, an empty job and a 1499-row job: few tiles over a
+    long token range, so the dA / dB groups take the token split (6 splits) and the
+    fixed-order reduce; the empty job's adapters must come out bitwise untouched."""
     from paper_2312_02515_b200.layer import TINY
-    run_step_and_check(TINY, [8, 16, 4], [2.0, 1.0, 0.5], [1e-3, 2e-3, 5e-4], [0, 1, 1, 130], seed=77)
+    run_step_and_check(TINY, [8, 16, 4], [2.0, 1.0, 0.5], [1e-3, 2e-3, 5e-4], [0, 1, 1, 1500], seed=77)
 
