@@ -58,6 +58,14 @@ def sample_rows(seg, per_job, rng):
     return np.concatenate(rows)
 
 
+def _source_y(layer, p, rows):
+    """Projection p's input as the oracle sees it: its source's Y (ChatGLM2's 4h_to_h reads
+    the first p.k columns of h_to_4h's output), taken from the source, not from the layer's
+    own column-slice copy."""
+    base = "h_to_4h" if p.src == "h_to_4h_half" else p.src
+    return next(q for q in layer.proj if q.name == base).Y[:rows, :p.k]
+
+
 def run_step_and_check(shapes, ranks, scales, lrs, seg, seed):
     from paper_2312_02515_b200 import fused as F
     from paper_2312_02515_b200.layer import FusedLoraLayer
@@ -89,7 +97,7 @@ def run_step_and_check(shapes, ranks, scales, lrs, seg, seed):
         A16, B16 = f64(pre[p.name]["A16"]), f64(pre[p.name]["B16"])
         As = [A16[ro[j]:ro[j] + r] for j, r in enumerate(ranks)]
         Bs = [B16[:, ro[j]:ro[j] + r] for j, r in enumerate(ranks)]
-        xin = x_host if p.src == "x" else f64(next(q for q in layer.proj if q.name == p.src).Y[:rows])
+        xin = x_host if p.src == "x" else f64(_source_y(layer, p, rows))
         Y = f64(p.Y[:rows])
         # ---- Y and dX on sampled rows (oracle: fused_forward / composed backward)
         Yr = O.segmented_forward(xin[srows], W, As, Bs, scales, sseg)
@@ -115,7 +123,7 @@ def run_step_and_check(shapes, ranks, scales, lrs, seg, seed):
         with torch.no_grad():
             prev = torch.backends.cuda.matmul.allow_tf32
             torch.backends.cuda.matmul.allow_tf32 = False
-            xin_t = x.float() if p.src == "x" else next(q for q in layer.proj if q.name == p.src).Y[:rows].float()
+            xin_t = x.float() if p.src == "x" else _source_y(layer, p, rows).float()
             Yt = xin_t @ p.W0.float().t()
             for j, r in enumerate(ranks):
                 a, b = seg[j], seg[j + 1]
@@ -200,4 +208,12 @@ def test_tiny_step_edge_layout():
     fixed-order reduce; the empty job's adapters must come out bitwise untouched."""
     from paper_2312_02515_b200.layer import TINY
     run_step_and_check(TINY, [8, 16, 4], [2.0, 1.0, 0.5], [1e-3, 2e-3, 5e-4], [0, 1, 1, 1500], seed=77)
+
+
+def test_c4_chatglm2_layer_step_column_slice():
+    """ChatGLM2-6B-shaped layer (fused qkv 4096 -> 4608, dense, fused h_to_4h 4096 -> 27392,
+    4h_to_h reading the first 13 696 columns of h_to_4h's output through the layer's
+    column-slice copy), 3 jobs of ragged lengths: the whole step against the oracle."""
+    from paper_2312_02515_b200.layer import CHATGLM2_6B
+    run_step_and_check(CHATGLM2_6B, [16, 8, 32], [2.0, 1.0, 0.5], [1e-4, 2e-4, 5e-5], [0, 700, 1200, 2100], seed=91)
 
