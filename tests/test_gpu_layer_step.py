@@ -217,3 +217,14 @@ def test_c4_chatglm2_layer_step_column_slice():
     from paper_2312_02515_b200.layer import CHATGLM2_6B
     run_step_and_check(CHATGLM2_6B, [16, 8, 32], [2.0, 1.0, 0.5], [1e-4, 2e-4, 5e-5], [0, 700, 1200, 2100], seed=91)
 
+
+
+def test_c5_thirty_two_jobs_step():
+    """C5's job count on one GPU: 32 rank-16 jobs (R_pad = 512: eight 64-column rank chunks,
+    every down-projection tile narrowed to its job's group) on LLaMA-7B shapes, 64 rows
+    per job: the whole step against the oracle."""
+    from paper_2312_02515_b200.layer import LLAMA7B
+    J = 32
+    seg = [64 * j for j in range(J + 1)]
+    lrs = [1e-4, 2e-4, 5e-5, 3e-4] * (J // 4)
+    run_step_and_check(LLAMA7B, [16] * J, [2.0] * J, lrs, seg, seed=5)
